@@ -1,0 +1,309 @@
+#!/usr/bin/env python
+"""bench.py -- THIIM sweep throughput (MLUP/s) on B200, per the driver contract.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl native|reference]
+
+Workload (BASELINE.json configs[1]): 256^3 grid, complex128, 100 THIIM
+iterations (H half-step then E half-step, reference step_reference order) per
+bench step, fields U[-1,1]^2 and 28 coefficient arrays uniform in |z|<=0.45,
+seed 1, zero ghosts.  One bench "step" = one full configs[1] run.
+
+  value   MLUP/s with the problem resident in HBM (device time, CUDA events on
+          the launching stream), max over ranks.
+  e2e     same metric through the public API (run_gpu: upload from pinned host
+          memory -> 100 iterations -> download of the 12 fields), every step.
+  roofline  dominant kernel (one THIIM iteration per launch) vs measured HBM.
+  cpu_baseline  the reference's own run_naive (oracle/_ref, compiled from
+          /root/reference unmodified) on the host cores, bounded sample.
+
+--impl reference runs the reference CPU implementation alone (rank 0 only).
+Multi-rank (torchrun): weak scaling, one 256^3 problem per rank (replicas;
+the z-slab decomposition with halo exchange is exercised by the multi-GPU
+context).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+GRID = (256, 256, 256)
+ITERS = 100
+SEED = 1
+WORKLOAD = ("configs[1]: 256x256x256 grid, 100 THIIM iterations (H then E half-step) per "
+            "bench step, complex128, fields U[-1,1], coeffs |c|<=0.45, seed 1, zero halo")
+METRIC = "MLUP/s (double-complex E+H update) at N B200; % of HBM roofline"
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        return float(j.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.Q,
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.result = {"sm_mhz": None, "sm_max_mhz": None, "reasons": []}
+        if not self.proc:
+            return
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if sm:
+            self.result = {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx,
+                           "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def reference_sample(grid, iters, threads):
+    """Time the reference's run_naive (oracle/_ref) on a host problem."""
+    from oracle import oracle as O  # cpu baseline leg only
+    import paper_1510_05218_b200 as P
+    dims = P.GridDims(*grid)
+    s = P.generate_problem(dims, P.GEN_RANDOM, SEED)
+    if O.ref_available():
+        secs = O.ref_run_naive(grid, s.arrays, iters, threads)
+        kind = "reference"
+    else:
+        t0 = time.perf_counter()
+        O.c_step(grid, s.arrays, iters, threads=threads)
+        secs = time.perf_counter() - t0
+        kind = "port"
+    lups = dims.interior_cells() * iters
+    return lups / secs / 1e6, kind
+
+
+def run_reference_arm(args, world, rank):
+    if rank != 0:
+        return
+    threads = cpu_threads()
+    # bounded sample per step: 1 THIIM iteration of the full 256^3 grid
+    sample_iters = 1
+    import paper_1510_05218_b200 as P
+    from oracle import oracle as O
+    dims = P.GridDims(*GRID)
+    s = P.generate_problem(dims, P.GEN_RANDOM, SEED)
+    kind = "reference" if O.ref_available() else "port"
+    vals = []
+    for k in range(args.warmup + args.steps):
+        if kind == "reference":
+            secs = O.ref_run_naive(GRID, s.arrays, sample_iters, threads)
+        else:
+            t0 = time.perf_counter()
+            O.c_step(GRID, s.arrays, sample_iters, threads=threads)
+            secs = time.perf_counter() - t0
+        if k >= args.warmup:
+            vals.append(secs)
+    secs = sum(vals)
+    v = dims.interior_cells() * sample_iters * len(vals) / secs / 1e6
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "MLUP/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * secs / max(1, len(vals)), 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "c128 (f64)", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "grid": list(GRID),
+                   "iterations_per_step": sample_iters,
+                   "note": "reference run_naive on host cores; each step a 1-iteration sample"},
+        "cpu_baseline": {"value": round(v, 3), "unit": "MLUP/s", "cores": threads, "kind": kind,
+                         "sample": "256^3 x %d iteration(s) per step, run_naive threads=%d"
+                                   % (sample_iters, threads)},
+        "e2e": {"value": round(v, 3), "unit": "MLUP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_native(args, world, rank, local):
+    import paper_1510_05218_b200 as P
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+
+    def barrier_max(x: float) -> float:
+        if dist is None:
+            return x
+        import torch
+        t = torch.tensor([x], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    dims = P.GridDims(*GRID)
+    engine = {"auto": P.ENGINE_AUTO, "split": P.ENGINE_SPLIT, "fused": P.ENGINE_FUSED}[args.engine]
+    opts = P.GpuOptions(device=local if world > 1 else args.device, engine=engine)
+    iters = args.iters
+    lups_step = dims.interior_cells() * iters
+
+    # ---- device-resident throughput (value)
+    eng = P.GpuEngine(dims, opts)
+    eng.generate(P.GEN_RANDOM, SEED)
+    for _ in range(args.warmup):
+        eng.step(iters)
+    if dist is not None:
+        dist.barrier()
+    dev_secs = 0.0
+    launches = 0
+    with Clocks(opts.device) as clk:
+        for _ in range(args.steps):
+            st = eng.step(iters)
+            dev_secs += st.seconds
+            launches += st.kernel_launches
+    engine_ran = st.engine
+    eng.close()
+    dev_secs = barrier_max(dev_secs)
+    value = world * lups_step * args.steps / dev_secs / 1e6
+
+    # ---- end to end through the public API from pinned host memory (e2e)
+    host = P.generate_problem(dims, P.GEN_RANDOM, SEED)
+    for a in host.arrays:
+        P.lib().thiim_gpu_pin_host(a.ctypes.data, a.nbytes)
+    e2e_secs = 0.0
+    for k in range(1 + args.steps):  # 1 untimed warm-up
+        work = host  # run_gpu updates fields in place; reset them from a pristine copy
+        t0 = time.perf_counter()
+        with P.GpuEngine(dims, opts) as e:
+            e.upload(work)
+            e.step(iters)
+            e.download_fields(work)
+        t1 = time.perf_counter()
+        if k >= 1:
+            e2e_secs += t1 - t0
+    for a in host.arrays:
+        P.lib().thiim_gpu_unpin_host(a.ctypes.data)
+    e2e_secs = barrier_max(e2e_secs)
+    e2e = world * lups_step * args.steps / e2e_secs / 1e6
+    padded = dims.padded_cells() * 16
+
+    # ---- roofline of the dominant kernel (one THIIM iteration per launch)
+    hbm, peak_kind = load_peaks()
+    per_launch_s = dev_secs / max(1, launches)
+    if engine_ran == P.ENGINE_SPLIT:
+        bytes_launch = 512.0 * dims.interior_cells()  # one half-step sweep: 32 x 16 B per cell
+        kname = "k_split_h/k_split_e"
+    else:
+        bytes_launch = 832.0 * dims.interior_cells()
+        kname = "k_fused<32,8>"
+    achieved = bytes_launch / per_launch_s / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            tj = json.load(f)
+        traffic = tj.get(kname)
+
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "MLUP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * dev_secs / args.steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "c128 (f64)", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "grid": list(GRID), "iterations_per_step": iters,
+                   "engine": P.ENGINE_NAMES.get(engine_ran), "parallelism": "dp%d" % world,
+                   "l2": "inputs (%.1f GB state) larger than L2; no flush needed"
+                         % (dims.padded_cells() * (832 if engine_ran != P.ENGINE_SPLIT else 640) / 1e9)},
+        "e2e": {"value": round(e2e, 2), "unit": "MLUP/s",
+                "h2d_bytes_per_step": 40 * padded, "d2h_bytes_per_step": 12 * padded},
+        "gpu_launches": launches,
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
+                     "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": traffic,
+                     "kernel": kname, "algorithmic_bytes_per_launch": bytes_launch,
+                     "peak_kind": peak_kind,
+                     "lup_roofline_mlups": round(hbm * 1e9 / (bytes_launch / dims.interior_cells()) / 1e6, 1)},
+        "clocks": clk.result,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = cpu_threads()
+        grid = (256, 256, 64)
+        v, kind = reference_sample(grid, 2, threads)
+        line["cpu_baseline"] = {"value": round(v, 3), "unit": "MLUP/s", "cores": threads,
+                                "kind": kind,
+                                "sample": "reference run_naive, 256x256x64 x 2 iterations, %d threads"
+                                          % threads}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--engine", default="auto", choices=["auto", "split", "fused"])
+    ap.add_argument("--iters", type=int, default=ITERS)
+    ap.add_argument("--device", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        run_reference_arm(args, world, rank)
+    else:
+        run_native(args, world, rank, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,166 @@
+/*
+ * thiim_gpu.h -- C-ABI of the B200 THIIM sweep engine (libthiim_gpu.so).
+ *
+ * The drop-in boundary for the reference's hot path.  The reference
+ * (arXiv 1510.05218 THIIM, /root/reference/proj) exposes a C++ driver API:
+ *
+ *   ProblemState build/fill   include/thiim/coefficients.hpp:66-79, state.hpp:49-66
+ *   time loop                 RunReport run_naive(ProblemState&, int steps,
+ *                                                 int threads, UpdateLog*)
+ *                             include/thiim/reference_engines.hpp:12-13
+ *   readback                  ProblemState::fields / field(Component) state.hpp:51-57
+ *
+ * This header replaces the time loop with a GPU engine.  No C++ or torch types
+ * cross it: plain pointers and sizes, status codes instead of exceptions.  The
+ * C++ adapter thiim::run_gpu(ProblemState&, int, const GpuOptions&) in
+ * adapter/thiim_gpu_engine.hpp is the reference-side binding; INTEGRATION.md
+ * shows how a maintainer wires it next to run_naive.
+ *
+ * Semantics: thiim_gpu_step(ctx, n) == n calls of step_reference
+ * (kernels.cpp:105-113): per step the six H components (kHOrder), then the
+ * six E components (kEOrder), over the full interior, ghosts never written.
+ * Results are BITWISE equal to the reference built without FMA contraction
+ * (kernels are compiled with -fmad=false and use explicit round-to-nearest
+ * intrinsics in the reference's per-cell operation order, kernels.cpp:43-51).
+ *
+ * Threading: calls on one context are synchronous and not reentrant, like the
+ * reference engines (worker_pool.hpp:39-64).  Distinct contexts are
+ * independent.
+ */
+#ifndef THIIM_GPU_H
+#define THIIM_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define THIIM_GPU_ABI_VERSION 1
+
+/* == thiim::ComplexScalar (include/thiim/complex.hpp:11-20). */
+typedef struct { double re, im; } thiim_c128;
+
+/* == thiim::GridDims (include/thiim/grid.hpp:12-48); ghost must be 1,
+ * n >= 4 per axis (GridDims::valid, grid.hpp:21).  Every array is
+ * (nx+2)*(ny+2)*(nz+2) elements, x unit-stride, z slowest. */
+typedef struct { int nx, ny, nz, ghost; } thiim_dims;
+
+/* Status codes.  The C++ adapter maps CONFIG -> thiim::ConfigError and
+ * SETUP -> thiim::SetupError (grid.hpp:50-60), the rest -> std::runtime_error,
+ * mirroring the CLI's exit-code split (tools/main.cpp:438-450). */
+enum {
+  THIIM_OK = 0,
+  THIIM_ERR_CONFIG = 2, /* bad argument (negative steps, bad engine, ...) */
+  THIIM_ERR_SETUP = 3,  /* invalid dims, device allocation failure */
+  THIIM_ERR_CUDA = 4,   /* CUDA runtime error or no device */
+  THIIM_ERR_COMM = 5,   /* halo exchange / peer access failure */
+  THIIM_ERR_STATE = 6   /* call order (step before upload, ...) */
+};
+
+/* Engines (all bitwise-equal to step_reference). */
+enum {
+  THIIM_ENGINE_AUTO = 0,
+  THIIM_ENGINE_SPLIT = 1, /* H sweep + E sweep, in place, z-streamed: 1024 B/LUP */
+  THIIM_ENGINE_FUSED = 2, /* one z-streamed H->E sweep per step, ping-pong fields: 832 B/LUP */
+  THIIM_ENGINE_TBLOCK = 3 /* temporally blocked fused sweep, `time_block` steps per pass */
+};
+
+/* Synthetic problem kinds for thiim_gpu_init_generated / thiim_generate_host
+ * (BASELINE.json configs). */
+enum {
+  THIIM_GEN_RANDOM = 0,  /* fields U[-1,1]^2, 28 coefficient arrays uniform in |z|<=0.45 */
+  THIIM_GEN_LAYERED = 1  /* config 3: 6 z-layers, seeded +-8-cell interface height maps */
+};
+
+typedef struct {
+  int device;       /* CUDA device ordinal of the first slab */
+  int n_gpus;       /* z-slabs driven by this context (1..8), one device each */
+  int engine;       /* THIIM_ENGINE_* */
+  int tile_x;       /* 0 = auto */
+  int tile_y;       /* 0 = auto */
+  int z_chunk;      /* planes per CTA along the z-stream, 0 = auto */
+  int time_block;   /* TBLOCK: steps per HBM pass, 0 = auto */
+  int reserved[9];
+} thiim_gpu_opts;
+
+typedef struct {
+  double seconds;          /* device time of the whole step loop (CUDA events) */
+  double mlups;            /* interior*steps/seconds/1e6 (reference_engines.cpp:19-23) */
+  double balance_model;    /* algorithmic bytes per LUP of the engine that ran */
+  double kernel_seconds;   /* device time summed over the sweep kernels only */
+  long long kernel_launches;
+  int steps;
+  int engine;              /* engine that actually ran (AUTO resolved) */
+  int n_gpus;
+  int reserved[5];
+} thiim_gpu_stats;
+
+typedef struct thiim_gpu_ctx thiim_gpu_ctx;
+
+void thiim_gpu_default_opts(thiim_gpu_opts* opts);
+
+/* Allocates device state for `dims` (reference padded layout).  Fields and
+ * coefficients start zeroed, like allocate_state (state.cpp:5-16). */
+int thiim_gpu_create(const thiim_dims* dims, const thiim_gpu_opts* opts, thiim_gpu_ctx** out);
+
+/* Uploads a full ProblemState: 12 fields (Component order, components.hpp:17-30),
+ * 12 t, 12 c (same order), 4 src (source_index order, components.hpp:89-97).
+ * Host arrays are (nx+2)(ny+2)(nz+2) elements, ghosts included. */
+int thiim_gpu_upload(thiim_gpu_ctx* ctx, const thiim_c128* const fields[12],
+                     const thiim_c128* const t[12], const thiim_c128* const c[12],
+                     const thiim_c128* const src[4]);
+
+/* Uploads the 12 field arrays only (coefficients unchanged). */
+int thiim_gpu_upload_fields(thiim_gpu_ctx* ctx, const thiim_c128* const fields[12]);
+
+/* Generates a synthetic problem directly in HBM (no PCIe traffic); bitwise
+ * identical to thiim_generate_host with the same (kind, seed). */
+int thiim_gpu_init_generated(thiim_gpu_ctx* ctx, int kind, uint64_t seed);
+
+/* Advances `steps` THIIM iterations (== steps x step_reference).  Blocking.
+ * steps < 0 -> THIIM_ERR_CONFIG (run_naive, reference_engines.cpp:35). */
+int thiim_gpu_step(thiim_gpu_ctx* ctx, int steps, thiim_gpu_stats* stats);
+
+/* Copies the 12 current field arrays back (ghosts included). */
+int thiim_gpu_download_fields(thiim_gpu_ctx* ctx, thiim_c128* const fields[12]);
+
+/* Copies one of the 40 arrays back: 0..11 fields, 12..23 t, 24..35 c, 36..39 src. */
+int thiim_gpu_download_array(thiim_gpu_ctx* ctx, int array_id, thiim_c128* dst);
+
+/* On-device comparison of the current fields against 12 host arrays (interior
+ * only, like compare_states, verifier.cpp:13-44): bitwise mismatch count plus
+ * the worst per-component relative L2 error ||a-b||/||b||. */
+typedef struct {
+  unsigned long long differing_values;
+  double max_rel_l2;
+  double rel_l2[12];
+} thiim_gpu_diff;
+int thiim_gpu_compare_fields(thiim_gpu_ctx* ctx, const thiim_c128* const ref_fields[12],
+                             thiim_gpu_diff* out);
+
+/* Host-side generator for the same synthetic problem (for CPU oracles and for
+ * uploading); arrays must be zeroed or are fully overwritten (ghosts -> 0). */
+int thiim_generate_host(const thiim_dims* dims, int kind, uint64_t seed,
+                        thiim_c128* const arrays[40]);
+
+/* Page-locks (cudaHostRegister) / unlocks a host buffer so uploads and
+ * downloads run at full PCIe rate.  Optional. */
+int thiim_gpu_pin_host(void* ptr, size_t bytes);
+int thiim_gpu_unpin_host(void* ptr);
+
+void thiim_gpu_destroy(thiim_gpu_ctx* ctx);
+
+/* Message of the last failing call on this thread ("" if none). */
+const char* thiim_gpu_last_error(void);
+
+/* Algorithmic bytes per LUP of an engine (832 / time_block for TBLOCK). */
+double thiim_gpu_balance_model(int engine, int time_block);
+
+int thiim_gpu_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* THIIM_GPU_H */

@@ -1,0 +1,490 @@
+"""paper_1510_05218_b200 -- B200-native THIIM split-field sweep engine.
+
+Host-side mirror of the reference C++ driver API for the hot path
+(/root/reference/proj/include/thiim, read-only upstream), bound over the
+C-ABI of ``libthiim_gpu.so`` (include/thiim_gpu.h).  Names, argument meaning
+and error behaviour follow the reference:
+
+==========================  ===========================================  =======================================
+here                        reference                                    file:line
+==========================  ===========================================  =======================================
+``GridDims``                ``thiim::GridDims``                          include/thiim/grid.hpp:12-48
+``ProblemState``            ``thiim::ProblemState`` (40 arrays)          include/thiim/state.hpp:49-66
+``allocate_state``          ``allocate_state``                           src/state.cpp:5-16
+``clone_state``             ``clone_state``                              src/state.cpp:18-29
+``Component``               ``thiim::Component``                         include/thiim/components.hpp:17-30
+``COMPONENT_TABLE``         ``kComponentTable``                          include/thiim/components.hpp:54-67
+``run_gpu``                 ``run_naive`` (the time loop it replaces)    src/reference_engines.cpp:34-67
+``RunReport``               ``thiim::RunReport``                         include/thiim/report.hpp:37-52
+``compare_states``          ``compare_states``                           src/verifier.cpp:13-44
+``ConfigError`` ...         ``ConfigError`` / ``SetupError``             include/thiim/grid.hpp:50-60
+==========================  ===========================================  =======================================
+
+The compute path is the CUDA library only: there is no CPU fallback.  If the
+library cannot be loaded, importing the engine raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import enum
+import os
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+__all__ = [
+    "ConfigError", "SetupError", "PlanError", "GpuError",
+    "GridDims", "ProblemState", "allocate_state", "clone_state", "Component",
+    "COMPONENT_TABLE", "GEN_RANDOM", "GEN_LAYERED", "ENGINE_AUTO", "ENGINE_SPLIT",
+    "ENGINE_FUSED", "ENGINE_TBLOCK", "GpuOptions", "RunReport", "StateDiff", "GpuEngine",
+    "run_gpu", "generate_problem", "compare_states", "balance_model", "lib",
+]
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libthiim_gpu.so")
+
+
+# ---------------------------------------------------------------- errors
+class ConfigError(RuntimeError):
+    """thiim::ConfigError (grid.hpp:50-52)."""
+
+
+class SetupError(RuntimeError):
+    """thiim::SetupError (grid.hpp:58-60)."""
+
+
+class PlanError(RuntimeError):
+    """thiim::PlanError (grid.hpp:54-56)."""
+
+
+class GpuError(RuntimeError):
+    """CUDA / communication / call-order failures of the GPU engine."""
+
+
+# ---------------------------------------------------------------- layout
+@dataclass(frozen=True)
+class GridDims:
+    """thiim::GridDims (grid.hpp:12-48): interior extents + 1-cell ghost."""
+
+    nx: int
+    ny: int
+    nz: int
+    ghost: int = 1
+
+    def valid(self) -> bool:
+        return self.nx >= 4 and self.ny >= 4 and self.nz >= 4 and self.ghost == 1
+
+    def px(self) -> int:
+        return self.nx + 2 * self.ghost
+
+    def py(self) -> int:
+        return self.ny + 2 * self.ghost
+
+    def pz(self) -> int:
+        return self.nz + 2 * self.ghost
+
+    def padded_cells(self) -> int:
+        return self.px() * self.py() * self.pz()
+
+    def interior_cells(self) -> int:
+        return self.nx * self.ny * self.nz
+
+    def stride_y(self) -> int:
+        return self.px()
+
+    def stride_z(self) -> int:
+        return self.px() * self.py()
+
+    def linear_index(self, x: int, y: int, z: int) -> int:
+        return (z + self.ghost) * self.stride_z() + (y + self.ghost) * self.stride_y() + x + self.ghost
+
+
+class Component(enum.IntEnum):
+    """thiim::Component (components.hpp:17-30)."""
+
+    Exy = 0
+    Exz = 1
+    Eyx = 2
+    Eyz = 3
+    Ezx = 4
+    Ezy = 5
+    Hxy = 6
+    Hxz = 7
+    Hyx = 8
+    Hyz = 9
+    Hzx = 10
+    Hzy = 11
+
+
+# kComponentTable (components.hpp:54-67):
+# id -> (family 'E'/'H', shift axis 0/1/2, shift sign, operand_a, operand_b, curl_sign, has_source)
+C = Component
+COMPONENT_TABLE = {
+    C.Exy: ("E", 1, -1, C.Hzx, C.Hzy, +1, False),
+    C.Exz: ("E", 2, -1, C.Hyx, C.Hyz, -1, True),
+    C.Eyx: ("E", 0, -1, C.Hzx, C.Hzy, -1, False),
+    C.Eyz: ("E", 2, -1, C.Hxy, C.Hxz, +1, True),
+    C.Ezx: ("E", 0, -1, C.Hyx, C.Hyz, +1, False),
+    C.Ezy: ("E", 1, -1, C.Hxy, C.Hxz, -1, False),
+    C.Hxy: ("H", 1, +1, C.Ezx, C.Ezy, -1, False),
+    C.Hxz: ("H", 2, +1, C.Eyx, C.Eyz, +1, True),
+    C.Hyx: ("H", 0, +1, C.Ezx, C.Ezy, +1, False),
+    C.Hyz: ("H", 2, +1, C.Exy, C.Exz, -1, True),
+    C.Hzx: ("H", 0, +1, C.Eyx, C.Eyz, -1, False),
+    C.Hzy: ("H", 1, +1, C.Exy, C.Exz, +1, False),
+}
+del C
+
+
+def source_index(c: int) -> int:
+    """source_index (components.hpp:89-97)."""
+    return {1: 0, 3: 1, 7: 2, 9: 3}.get(int(c), -1)
+
+
+class ProblemState:
+    """thiim::ProblemState (state.hpp:49-66): 12 fields, 12 t, 12 c, 4 src.
+
+    Every array is a C-contiguous complex128 numpy vector of padded_cells()
+    elements (== interleaved {re, im} doubles, ComplexScalar).  ``arrays``
+    lists them in C-ABI order [fields, t, c, src].
+    """
+
+    def __init__(self, dims: GridDims, arrays: Optional[List[np.ndarray]] = None):
+        if not dims.valid():
+            raise SetupError("invalid grid dims (need nx,ny,nz >= 4, ghost = 1)")
+        self.dims = dims
+        n = dims.padded_cells()
+        if arrays is None:
+            arrays = [np.zeros(n, dtype=np.complex128) for _ in range(40)]
+        if len(arrays) != 40 or any(a.shape != (n,) or a.dtype != np.complex128 for a in arrays):
+            raise ConfigError("ProblemState needs 40 complex128 arrays of padded_cells()")
+        self.arrays = [np.ascontiguousarray(a) for a in arrays]
+
+    @property
+    def fields(self) -> List[np.ndarray]:
+        return self.arrays[0:12]
+
+    @property
+    def coeff_t(self) -> List[np.ndarray]:
+        return self.arrays[12:24]
+
+    @property
+    def coeff_c(self) -> List[np.ndarray]:
+        return self.arrays[24:36]
+
+    @property
+    def coeff_src(self) -> List[np.ndarray]:
+        return self.arrays[36:40]
+
+    def field(self, c: int) -> np.ndarray:
+        return self.arrays[int(c)]
+
+    def t_of(self, c: int) -> np.ndarray:
+        return self.arrays[12 + int(c)]
+
+    def c_of(self, c: int) -> np.ndarray:
+        return self.arrays[24 + int(c)]
+
+    def view3d(self, a: int) -> np.ndarray:
+        """(pz, py, px) view of array ``a`` (z slowest, x unit stride)."""
+        d = self.dims
+        return self.arrays[a].reshape(d.pz(), d.py(), d.px())
+
+    def interior(self, a: int) -> np.ndarray:
+        return self.view3d(a)[1:-1, 1:-1, 1:-1]
+
+    def zero_fields(self) -> None:
+        for f in self.fields:
+            f[:] = 0
+
+
+def allocate_state(dims: GridDims) -> ProblemState:
+    """allocate_state (state.cpp:5-16): all 40 arrays zeroed."""
+    return ProblemState(dims)
+
+
+def clone_state(s: ProblemState) -> ProblemState:
+    """clone_state (state.cpp:18-29): deep copy of all 40 arrays."""
+    return ProblemState(s.dims, [a.copy() for a in s.arrays])
+
+
+@dataclass
+class StateDiff:
+    """thiim::StateDiff (verifier.hpp:11-18) plus per-component relative L2."""
+
+    max_abs_diff: float = 0.0
+    bitwise_equal: bool = True
+    differing_values: int = 0
+    first_component: int = 0
+    x: int = -1
+    y: int = -1
+    z: int = -1
+    rel_l2: List[float] = field(default_factory=lambda: [0.0] * 12)
+
+    @property
+    def max_rel_l2(self) -> float:
+        return max(self.rel_l2)
+
+
+def compare_states(a: ProblemState, b: ProblemState) -> StateDiff:
+    """compare_states (verifier.cpp:13-44): exact interior scan of the 12 fields.
+
+    ``rel_l2[k] = ||a_k - b_k|| / ||b_k||`` over the interior is the
+    north-star 1e-12 criterion; ``bitwise_equal`` the -fmad=false contract.
+    """
+    if a.dims != b.dims:
+        raise ConfigError("compare_states: dimension mismatch")
+    d = StateDiff()
+    for ci in range(12):
+        va, vb = a.interior(ci), b.interior(ci)
+        ba = va.view(np.uint64).reshape(va.shape + (2,))
+        bb = vb.view(np.uint64).reshape(vb.shape + (2,))
+        neq = np.any(ba != bb, axis=-1)
+        n = int(neq.sum())
+        if n:
+            if d.bitwise_equal:
+                z, y, x = np.argwhere(neq)[0]
+                d.first_component, d.x, d.y, d.z = ci, int(x), int(y), int(z)
+            d.bitwise_equal = False
+            d.differing_values += n
+            diff = np.maximum(np.abs(va.real - vb.real), np.abs(va.imag - vb.imag))
+            d.max_abs_diff = max(d.max_abs_diff, float(diff.max()))
+        den = float(np.sqrt(np.sum(np.abs(vb) ** 2)))
+        num = float(np.sqrt(np.sum(np.abs(va - vb) ** 2)))
+        d.rel_l2[ci] = num / den if den > 0 else num
+    return d
+
+
+# ---------------------------------------------------------------- C-ABI binding
+class _Dims(ctypes.Structure):
+    _fields_ = [("nx", ctypes.c_int), ("ny", ctypes.c_int), ("nz", ctypes.c_int),
+                ("ghost", ctypes.c_int)]
+
+
+class _Opts(ctypes.Structure):
+    _fields_ = [("device", ctypes.c_int), ("n_gpus", ctypes.c_int), ("engine", ctypes.c_int),
+                ("tile_x", ctypes.c_int), ("tile_y", ctypes.c_int), ("z_chunk", ctypes.c_int),
+                ("time_block", ctypes.c_int), ("reserved", ctypes.c_int * 9)]
+
+
+class _Stats(ctypes.Structure):
+    _fields_ = [("seconds", ctypes.c_double), ("mlups", ctypes.c_double),
+                ("balance_model", ctypes.c_double), ("kernel_seconds", ctypes.c_double),
+                ("kernel_launches", ctypes.c_longlong), ("steps", ctypes.c_int),
+                ("engine", ctypes.c_int), ("n_gpus", ctypes.c_int),
+                ("reserved", ctypes.c_int * 5)]
+
+
+class _Diff(ctypes.Structure):
+    _fields_ = [("differing_values", ctypes.c_ulonglong), ("max_rel_l2", ctypes.c_double),
+                ("rel_l2", ctypes.c_double * 12)]
+
+
+EXPORTED_SYMBOLS = [
+    "thiim_gpu_abi_version", "thiim_gpu_last_error", "thiim_gpu_default_opts",
+    "thiim_gpu_balance_model", "thiim_gpu_create", "thiim_gpu_destroy", "thiim_gpu_upload",
+    "thiim_gpu_upload_fields", "thiim_gpu_init_generated", "thiim_gpu_step",
+    "thiim_gpu_download_fields", "thiim_gpu_download_array", "thiim_gpu_compare_fields",
+    "thiim_generate_host", "thiim_gpu_pin_host", "thiim_gpu_unpin_host",
+]
+
+_LIB = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libthiim_gpu.so (built in-tree by __graft_entry__.build()).  Raises
+    if it is missing: there is no fallback compute path."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(LIB_PATH):
+        raise GpuError("libthiim_gpu.so not built (%s); run __graft_entry__.build()" % LIB_PATH)
+    L = ctypes.CDLL(LIB_PATH)
+    P = ctypes.c_void_p
+    PP = ctypes.POINTER(ctypes.c_void_p)
+    L.thiim_gpu_abi_version.restype = ctypes.c_int
+    L.thiim_gpu_last_error.restype = ctypes.c_char_p
+    L.thiim_gpu_default_opts.argtypes = [ctypes.POINTER(_Opts)]
+    L.thiim_gpu_balance_model.restype = ctypes.c_double
+    L.thiim_gpu_balance_model.argtypes = [ctypes.c_int, ctypes.c_int]
+    L.thiim_gpu_create.argtypes = [ctypes.POINTER(_Dims), ctypes.POINTER(_Opts), ctypes.POINTER(P)]
+    L.thiim_gpu_destroy.argtypes = [P]
+    L.thiim_gpu_upload.argtypes = [P, PP, PP, PP, PP]
+    L.thiim_gpu_upload_fields.argtypes = [P, PP]
+    L.thiim_gpu_init_generated.argtypes = [P, ctypes.c_int, ctypes.c_uint64]
+    L.thiim_gpu_step.argtypes = [P, ctypes.c_int, ctypes.POINTER(_Stats)]
+    L.thiim_gpu_download_fields.argtypes = [P, PP]
+    L.thiim_gpu_download_array.argtypes = [P, ctypes.c_int, P]
+    L.thiim_gpu_compare_fields.argtypes = [P, PP, ctypes.POINTER(_Diff)]
+    L.thiim_generate_host.argtypes = [ctypes.POINTER(_Dims), ctypes.c_int, ctypes.c_uint64, PP]
+    L.thiim_gpu_pin_host.argtypes = [P, ctypes.c_size_t]
+    L.thiim_gpu_unpin_host.argtypes = [P]
+    if L.thiim_gpu_abi_version() != 1:
+        raise GpuError("libthiim_gpu.so ABI mismatch")
+    _LIB = L
+    return L
+
+
+def _ptrs(arrays) -> "ctypes.Array":
+    return (ctypes.c_void_p * len(arrays))(*[a.ctypes.data for a in arrays])
+
+
+def _check(rc: int) -> None:
+    if rc == 0:
+        return
+    msg = (lib().thiim_gpu_last_error() or b"").decode()
+    if rc == 2:
+        raise ConfigError(msg)
+    if rc == 3:
+        raise SetupError(msg)
+    raise GpuError("thiim_gpu error %d: %s" % (rc, msg))
+
+
+GEN_RANDOM = 0
+GEN_LAYERED = 1
+ENGINE_AUTO, ENGINE_SPLIT, ENGINE_FUSED, ENGINE_TBLOCK = 0, 1, 2, 3
+ENGINE_NAMES = {ENGINE_SPLIT: "gpu-split", ENGINE_FUSED: "gpu-fused", ENGINE_TBLOCK: "gpu-tblock"}
+
+
+def balance_model(engine: int, time_block: int = 1) -> float:
+    return float(lib().thiim_gpu_balance_model(engine, time_block))
+
+
+@dataclass
+class GpuOptions:
+    """Mirror of thiim_gpu_opts (include/thiim_gpu.h)."""
+
+    device: int = 0
+    n_gpus: int = 1
+    engine: int = ENGINE_AUTO
+    tile_x: int = 0
+    tile_y: int = 0
+    z_chunk: int = 0
+    time_block: int = 0
+
+    def _c(self) -> _Opts:
+        o = _Opts()
+        lib().thiim_gpu_default_opts(ctypes.byref(o))
+        o.device, o.n_gpus, o.engine = self.device, self.n_gpus, self.engine
+        o.tile_x, o.tile_y, o.z_chunk, o.time_block = self.tile_x, self.tile_y, self.z_chunk, self.time_block
+        return o
+
+
+@dataclass
+class RunReport:
+    """thiim::RunReport (report.hpp:37-52), filled like run_naive does
+    (reference_engines.cpp:37-44, 19-23): threads = #GPUs, balance_model = the
+    engine's algorithmic bytes/LUP, seconds = device time (CUDA events)."""
+
+    engine: str = ""
+    dims: Optional[GridDims] = None
+    steps: int = 0
+    steps_executed: int = 0
+    threads: int = 1
+    dw: int = 0
+    bz: int = 0
+    seconds: float = 0.0
+    mlups: Optional[float] = None
+    balance_model: float = 0.0
+    cache_model_bytes: int = 0
+    predicted_mlups: Optional[float] = None
+    verification: str = "skipped"
+    kernel_launches: int = 0
+
+
+class GpuEngine:
+    """A device-resident problem (one thiim_gpu_ctx)."""
+
+    def __init__(self, dims: GridDims, opts: Optional[GpuOptions] = None):
+        self.dims = dims
+        self.opts = opts or GpuOptions()
+        L = lib()
+        self._ctx = ctypes.c_void_p()
+        d = _Dims(dims.nx, dims.ny, dims.nz, dims.ghost)
+        o = self.opts._c()
+        _check(L.thiim_gpu_create(ctypes.byref(d), ctypes.byref(o), ctypes.byref(self._ctx)))
+
+    def close(self) -> None:
+        if self._ctx:
+            lib().thiim_gpu_destroy(self._ctx)
+            self._ctx = ctypes.c_void_p()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def upload(self, s: ProblemState) -> None:
+        if s.dims != self.dims:
+            raise ConfigError("state dims do not match the engine")
+        a = s.arrays
+        _check(lib().thiim_gpu_upload(self._ctx, _ptrs(a[0:12]), _ptrs(a[12:24]), _ptrs(a[24:36]),
+                                      _ptrs(a[36:40])))
+
+    def upload_fields(self, s: ProblemState) -> None:
+        _check(lib().thiim_gpu_upload_fields(self._ctx, _ptrs(s.arrays[0:12])))
+
+    def generate(self, kind: int = GEN_RANDOM, seed: int = 1) -> None:
+        _check(lib().thiim_gpu_init_generated(self._ctx, kind, seed))
+
+    def step(self, steps: int) -> _Stats:
+        st = _Stats()
+        _check(lib().thiim_gpu_step(self._ctx, steps, ctypes.byref(st)))
+        return st
+
+    def download_fields(self, s: ProblemState) -> None:
+        _check(lib().thiim_gpu_download_fields(self._ctx, _ptrs(s.arrays[0:12])))
+
+    def download_array(self, a: int, out: np.ndarray) -> None:
+        _check(lib().thiim_gpu_download_array(self._ctx, a, out.ctypes.data))
+
+    def download_state(self) -> ProblemState:
+        s = allocate_state(self.dims)
+        for a in range(40):
+            self.download_array(a, s.arrays[a])
+        return s
+
+    def compare_fields(self, ref: ProblemState) -> StateDiff:
+        out = _Diff()
+        _check(lib().thiim_gpu_compare_fields(self._ctx, _ptrs(ref.arrays[0:12]), ctypes.byref(out)))
+        d = StateDiff()
+        d.differing_values = int(out.differing_values)
+        d.bitwise_equal = d.differing_values == 0
+        d.rel_l2 = list(out.rel_l2)
+        return d
+
+
+def generate_problem(dims: GridDims, kind: int = GEN_RANDOM, seed: int = 1) -> ProblemState:
+    """Host copy of the seeded synthetic problem (bitwise equal to the device
+    generator)."""
+    s = allocate_state(dims)
+    d = _Dims(dims.nx, dims.ny, dims.nz, dims.ghost)
+    _check(lib().thiim_generate_host(ctypes.byref(d), kind, seed, _ptrs(s.arrays)))
+    return s
+
+
+def run_gpu(state: ProblemState, steps: int, opts: Optional[GpuOptions] = None) -> RunReport:
+    """Drop-in for run_naive(state, steps) (reference_engines.cpp:34-67): uploads
+    ``state``, runs ``steps`` THIIM iterations on the GPU(s), downloads the 12
+    fields back into ``state`` in place, returns a RunReport."""
+    if steps < 0:
+        raise ConfigError("steps must be >= 0")
+    opts = opts or GpuOptions()
+    with GpuEngine(state.dims, opts) as eng:
+        eng.upload(state)
+        st = eng.step(steps)
+        eng.download_fields(state)
+    r = RunReport(engine=ENGINE_NAMES.get(st.engine, "gpu"), dims=state.dims, steps=steps,
+                  steps_executed=steps, threads=st.n_gpus, seconds=st.seconds,
+                  balance_model=st.balance_model, kernel_launches=st.kernel_launches)
+    if steps > 0 and st.seconds > 0:
+        r.mlups = state.dims.interior_cells() * steps / st.seconds / 1e6
+    return r

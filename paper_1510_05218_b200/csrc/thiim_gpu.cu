@@ -1,0 +1,629 @@
+// thiim_gpu.cu -- libthiim_gpu.so: the C-ABI declared in include/thiim_gpu.h.
+//
+// One context = one problem split into z-slabs, one slab per GPU.  Each slab
+// holds the reference padded layout for its planes [z0-1, z1] (the outer
+// planes are global ghosts or halo copies of the neighbour slab's boundary
+// planes) in one device allocation:
+//   [F0: 12 field arrays][F1: 12 field arrays, fused engines only]
+//   [t: 12][c: 12][src: 4]
+// each array `stride` elements (padded plane count x (nx+2)(ny+2), rounded up
+// to 256 B).  Upload/download are plain plane-range copies: no layout change.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/thiim_gpu.h"
+#include "thiim_common.cuh"
+#include "thiim_fused.cuh"
+#include "thiim_split.cuh"
+
+using namespace thiim_gpu;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CK(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(THIIM_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+constexpr int kSplitBY = 4;
+constexpr int kFusedBX = 32, kFusedBY = 8;
+
+struct Slab {
+  int device = 0;
+  int z0 = 0, z1 = 0;  // global interior planes [z0, z1)
+  Grid g{};            // local grid: nz = z1 - z0
+  double2* buf = nullptr;
+  size_t stride = 0;   // elements per array
+  int nfield_sets = 1;
+  int cur = 0;         // current field set
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+
+  double2* field(int set, int k) const { return buf + (size_t)(set * 12 + k) * stride; }
+  double2* coeff(int a) const {  // a in 12..39
+    return buf + (size_t)(nfield_sets * 12 + (a - 12)) * stride;
+  }
+  double2* array(int a) const { return a < 12 ? field(cur, a) : coeff(a); }
+  Arrays arrays(int in_set, int out_set) const {
+    Arrays A;
+    for (int k = 0; k < 12; ++k) {
+      A.f[k] = field(in_set, k);
+      A.fo[k] = field(out_set, k);
+      A.t[k] = coeff(12 + k);
+      A.c[k] = coeff(24 + k);
+    }
+    for (int k = 0; k < 4; ++k) A.src[k] = coeff(36 + k);
+    return A;
+  }
+};
+
+}  // namespace
+
+struct thiim_gpu_ctx {
+  thiim_dims dims{};
+  thiim_gpu_opts opts{};
+  int engine = THIIM_ENGINE_FUSED;
+  std::vector<Slab> slabs;
+  bool loaded = false;
+  long long pxy() const { return (long long)(dims.nx + 2) * (dims.ny + 2); }
+};
+
+// ------------------------------------------------------------------ kernels
+
+namespace {
+
+// Device generator: one thread per padded cell of the slab, all 40 arrays.
+__global__ void k_generate(Grid g, int z_global0, int nz_global, Arrays A, int kind,
+                           uint64_t seed, const double2* __restrict__ layer_table) {
+  const long long n = (long long)(g.nz + 2) * g.pxy;
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
+       p += (long long)gridDim.x * blockDim.x) {
+    const int zp = (int)(p / g.pxy);
+    const long long r = p - (long long)zp * g.pxy;
+    const int yp = (int)(r / g.px);
+    const int xp = (int)(r - (long long)yp * g.px);
+    const int x = xp - 1, y = yp - 1, zl = zp - 1;
+    const int z = z_global0 + zl;  // global interior plane
+    const bool interior = x >= 0 && x < g.nx && y >= 0 && y < g.ny && z >= 0 && z < nz_global;
+    // the counter is the GLOBAL padded index, so slabs reproduce the 1-GPU problem
+    const uint64_t gidx = (uint64_t)(z + 1) * (uint64_t)g.pxy + (uint64_t)r;
+    for (int a = 0; a < 40; ++a) {
+      double2 v = make_double2(0.0, 0.0);
+      if (interior) {
+        if (a < 12) {
+          v = gen_field(gen_key(seed, a), gidx);
+        } else if (kind == THIIM_GEN_LAYERED) {
+          v = layer_table[(a - 12) * 6 + gen_layer(seed, g.nx, nz_global, x, y, z)];
+        } else {
+          v = gen_disk(gen_key(seed, a), gidx);
+        }
+      }
+      double2* dst = a < 12 ? A.f[a] : a < 24 ? const_cast<double2*>(A.t[a - 12])
+                                       : a < 36 ? const_cast<double2*>(A.c[a - 24])
+                                                : const_cast<double2*>(A.src[a - 36]);
+      dst[p] = v;
+    }
+  }
+}
+
+// Interior comparison of one field array against a reference copy.
+// acc[0] += sum |a-b|^2, acc[1] += sum |b|^2; cnt += bit mismatches.
+__global__ void k_compare(Grid g, const double2* __restrict__ a, const double2* __restrict__ b,
+                          double* acc, unsigned long long* cnt) {
+  double num = 0.0, den = 0.0;
+  unsigned long long c = 0;
+  const long long n = (long long)g.nx * g.ny * g.nz;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n;
+       q += (long long)gridDim.x * blockDim.x) {
+    const int x = (int)(q % g.nx);
+    const long long r = q / g.nx;
+    const int y = (int)(r % g.ny);
+    const int z = (int)(r / g.ny);
+    const long long i = g.idx(x, y, z);
+    const double2 va = a[i], vb = b[i];
+    const double dr = va.x - vb.x, di = va.y - vb.y;
+    num += dr * dr + di * di;
+    den += vb.x * vb.x + vb.y * vb.y;
+    if (__double_as_longlong(va.x) != __double_as_longlong(vb.x) ||
+        __double_as_longlong(va.y) != __double_as_longlong(vb.y))
+      ++c;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    num += __shfl_xor_sync(0xffffffffu, num, o);
+    den += __shfl_xor_sync(0xffffffffu, den, o);
+    c += __shfl_xor_sync(0xffffffffu, c, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&acc[0], num);
+    atomicAdd(&acc[1], den);
+    atomicAdd(cnt, c);
+  }
+}
+
+int sm_count(int dev) {
+  int n = 148;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+
+int pick_zchunk(const thiim_gpu_ctx* ctx, const Slab& s, long long cols, int user) {
+  if (user > 0) return std::min(user, s.g.nz);
+  // enough CTAs for >= ~8 per SM, but chunks no shorter than 16 planes
+  const long long want = 8LL * sm_count(s.device);
+  long long chunks = (want + cols - 1) / cols;
+  chunks = std::max(1LL, std::min(chunks, (long long)std::max(1, s.g.nz / 16)));
+  (void)ctx;
+  return (int)((s.g.nz + chunks - 1) / chunks);
+}
+
+// Exchange halo planes between neighbouring slabs (single-process multi-GPU).
+// which: 0 = E top halo (slab s's plane z1 <- slab s+1's first interior plane),
+//        1 = H bottom halo (slab s's plane z0-1 <- slab s-1's last interior plane).
+int exchange(thiim_gpu_ctx* ctx, int which) {
+  const int n = (int)ctx->slabs.size();
+  if (n < 2) return THIIM_OK;
+  const long long pxy = ctx->pxy();
+  const size_t bytes = (size_t)pxy * sizeof(double2);
+  for (int s = 0; s < n; ++s) {
+    Slab& me = ctx->slabs[s];
+    if (which == 0 && s + 1 < n) {
+      const Slab& nb = ctx->slabs[s + 1];
+      for (int k = EXY; k <= EZY; ++k)
+        CK(cudaMemcpyPeerAsync(me.field(me.cur, k) + (size_t)(me.g.nz + 1) * pxy, me.device,
+                               nb.field(nb.cur, k) + (size_t)1 * pxy, nb.device, bytes,
+                               me.stream));
+    }
+    if (which == 1 && s > 0) {
+      const Slab& nb = ctx->slabs[s - 1];
+      for (int k = HXY; k <= HZY; ++k)
+        CK(cudaMemcpyPeerAsync(me.field(me.cur, k), me.device,
+                               nb.field(nb.cur, k) + (size_t)nb.g.nz * pxy, nb.device, bytes,
+                               me.stream));
+    }
+  }
+  // the copies are issued on the receiver's stream; the sender must not
+  // overwrite before they land: serialize by synchronizing all streams.
+  for (auto& sl : ctx->slabs) {
+    CK(cudaSetDevice(sl.device));
+    CK(cudaStreamSynchronize(sl.stream));
+  }
+  return THIIM_OK;
+}
+
+int launch_split(thiim_gpu_ctx* ctx, Slab& s, int fam, long long* launches) {
+  CK(cudaSetDevice(s.device));
+  const Arrays A = s.arrays(s.cur, s.cur);
+  const dim3 block(kSplitBX, kSplitBY);
+  const long long cols = (long long)((s.g.nx + kSplitBX - 1) / kSplitBX) *
+                         ((s.g.ny + kSplitBY - 1) / kSplitBY);
+  const int zc = pick_zchunk(ctx, s, cols, ctx->opts.z_chunk);
+  const dim3 grid((s.g.nx + kSplitBX - 1) / kSplitBX, (s.g.ny + kSplitBY - 1) / kSplitBY,
+                  (s.g.nz + zc - 1) / zc);
+  if (fam == 0)
+    k_split_h<kSplitBY><<<grid, block, 0, s.stream>>>(s.g, A, zc);
+  else
+    k_split_e<kSplitBY><<<grid, block, 0, s.stream>>>(s.g, A, zc);
+  CK(cudaGetLastError());
+  ++*launches;
+  return THIIM_OK;
+}
+
+int launch_fused(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
+  CK(cudaSetDevice(s.device));
+  const Arrays A = s.arrays(s.cur, s.cur ^ 1);
+  constexpr int TX = kFusedBX - 2, TY = kFusedBY - 2;
+  const dim3 block(kFusedBX, kFusedBY);
+  const long long cols = (long long)((s.g.nx + TX - 1) / TX) * ((s.g.ny + TY - 1) / TY);
+  const int zc = pick_zchunk(ctx, s, cols, ctx->opts.z_chunk);
+  const dim3 grid((s.g.nx + TX - 1) / TX, (s.g.ny + TY - 1) / TY, (s.g.nz + zc - 1) / zc);
+  k_fused<kFusedBX, kFusedBY><<<grid, block, 0, s.stream>>>(s.g, A, zc);
+  CK(cudaGetLastError());
+  s.cur ^= 1;
+  ++*launches;
+  return THIIM_OK;
+}
+
+bool valid_dims(const thiim_dims* d) {
+  return d && d->nx >= 4 && d->ny >= 4 && d->nz >= 4 && d->ghost == 1;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ C-ABI
+
+extern "C" {
+
+int thiim_gpu_abi_version(void) { return THIIM_GPU_ABI_VERSION; }
+
+const char* thiim_gpu_last_error(void) { return g_err.c_str(); }
+
+void thiim_gpu_default_opts(thiim_gpu_opts* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof(*o));
+  o->device = 0;
+  o->n_gpus = 1;
+  o->engine = THIIM_ENGINE_AUTO;
+}
+
+double thiim_gpu_balance_model(int engine, int time_block) {
+  switch (engine) {
+    case THIIM_ENGINE_SPLIT: return 1024.0;
+    case THIIM_ENGINE_TBLOCK: return 832.0 / std::max(1, time_block);
+    default: return 832.0;
+  }
+}
+
+int thiim_gpu_create(const thiim_dims* dims, const thiim_gpu_opts* opts, thiim_gpu_ctx** out) {
+  g_err.clear();
+  if (!out) return fail(THIIM_ERR_CONFIG, "out pointer is null");
+  *out = nullptr;
+  if (!valid_dims(dims))
+    return fail(THIIM_ERR_SETUP, "invalid grid dims (need nx,ny,nz >= 4, ghost = 1)");
+  thiim_gpu_opts o;
+  if (opts)
+    o = *opts;
+  else
+    thiim_gpu_default_opts(&o);
+  if (o.n_gpus < 1 || o.n_gpus > 8) return fail(THIIM_ERR_CONFIG, "n_gpus must be in 1..8");
+  if (o.engine < THIIM_ENGINE_AUTO || o.engine > THIIM_ENGINE_TBLOCK)
+    return fail(THIIM_ERR_CONFIG, "unknown engine");
+  if (o.engine == THIIM_ENGINE_TBLOCK)
+    return fail(THIIM_ERR_CONFIG, "engine TBLOCK is not built yet");
+  if (dims->nz < 4 * o.n_gpus)
+    return fail(THIIM_ERR_CONFIG, "need at least 4 z planes per GPU");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1)
+    return fail(THIIM_ERR_CUDA, "no CUDA device visible");
+  if (o.device < 0 || o.device + o.n_gpus > ndev)
+    return fail(THIIM_ERR_CONFIG, "device range exceeds visible devices");
+
+  auto* ctx = new thiim_gpu_ctx;
+  ctx->dims = *dims;
+  ctx->opts = o;
+  ctx->engine = o.engine == THIIM_ENGINE_AUTO ? THIIM_ENGINE_FUSED : o.engine;
+  const int nf = ctx->engine == THIIM_ENGINE_SPLIT ? 1 : 2;
+  const long long pxy = ctx->pxy();
+  const int n = o.n_gpus;
+  for (int s = 0; s < n; ++s) {
+    Slab sl;
+    sl.device = o.device + s;
+    const int base = dims->nz / n, rem = dims->nz % n;  // reference z_slab split
+    sl.z0 = s * base + std::min(s, rem);
+    sl.z1 = sl.z0 + base + (s < rem ? 1 : 0);
+    sl.g.nx = dims->nx;
+    sl.g.ny = dims->ny;
+    sl.g.nz = sl.z1 - sl.z0;
+    sl.g.px = dims->nx + 2;
+    sl.g.pxy = pxy;
+    sl.nfield_sets = nf;
+    sl.stride = ((size_t)(sl.g.nz + 2) * (size_t)pxy + 15) / 16 * 16;
+    ctx->slabs.push_back(sl);
+  }
+  for (auto& sl : ctx->slabs) {
+    const size_t bytes = sl.stride * sizeof(double2) * (size_t)(12 * nf + 28);
+    cudaError_t e = cudaSetDevice(sl.device);
+    if (e == cudaSuccess) e = cudaMalloc(&sl.buf, bytes);
+    if (e == cudaSuccess) e = cudaMemset(sl.buf, 0, bytes);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&sl.stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreate(&sl.ev0);
+    if (e == cudaSuccess) e = cudaEventCreate(&sl.ev1);
+    if (e != cudaSuccess) {
+      const std::string msg = std::string("device allocation of ") + std::to_string(bytes) +
+                              " bytes failed: " + cudaGetErrorString(e);
+      cudaGetLastError();
+      thiim_gpu_destroy(ctx);
+      return fail(THIIM_ERR_SETUP, msg);
+    }
+  }
+  if (n > 1) {
+    for (int s = 0; s < n; ++s)
+      for (int t = 0; t < n; ++t) {
+        if (s == t || std::abs(s - t) != 1) continue;
+        int can = 0;
+        cudaDeviceCanAccessPeer(&can, ctx->slabs[s].device, ctx->slabs[t].device);
+        if (can) {
+          cudaSetDevice(ctx->slabs[s].device);
+          cudaError_t e = cudaDeviceEnablePeerAccess(ctx->slabs[t].device, 0);
+          if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+        }
+      }
+  }
+  *out = ctx;
+  return THIIM_OK;
+}
+
+void thiim_gpu_destroy(thiim_gpu_ctx* ctx) {
+  if (!ctx) return;
+  for (auto& sl : ctx->slabs) {
+    cudaSetDevice(sl.device);
+    if (sl.stream) cudaStreamSynchronize(sl.stream);
+    if (sl.buf) cudaFree(sl.buf);
+    if (sl.ev0) cudaEventDestroy(sl.ev0);
+    if (sl.ev1) cudaEventDestroy(sl.ev1);
+    if (sl.stream) cudaStreamDestroy(sl.stream);
+  }
+  delete ctx;
+}
+
+static int upload_arrays(thiim_gpu_ctx* ctx, const thiim_c128* const* arrays, int first, int count) {
+  const long long pxy = ctx->pxy();
+  for (auto& sl : ctx->slabs) {
+    CK(cudaSetDevice(sl.device));
+    // planes [z0, z1+2) of the global padded grid == local planes [0, nz+2)
+    const size_t off = (size_t)sl.z0 * (size_t)pxy;
+    const size_t bytes = (size_t)(sl.g.nz + 2) * (size_t)pxy * sizeof(double2);
+    for (int a = first; a < first + count; ++a) {
+      if (!arrays[a - first]) return fail(THIIM_ERR_CONFIG, "null host array");
+      const thiim_c128* src = arrays[a - first] + off;
+      if (a < 12) {
+        for (int set = 0; set < sl.nfield_sets; ++set)
+          CK(cudaMemcpyAsync(sl.field(set, a), src, bytes, cudaMemcpyHostToDevice, sl.stream));
+      } else {
+        CK(cudaMemcpyAsync(sl.coeff(a), src, bytes, cudaMemcpyHostToDevice, sl.stream));
+      }
+    }
+  }
+  for (auto& sl : ctx->slabs) {
+    CK(cudaSetDevice(sl.device));
+    CK(cudaStreamSynchronize(sl.stream));
+    sl.cur = 0;
+  }
+  return THIIM_OK;
+}
+
+int thiim_gpu_upload(thiim_gpu_ctx* ctx, const thiim_c128* const fields[12],
+                     const thiim_c128* const t[12], const thiim_c128* const c[12],
+                     const thiim_c128* const src[4]) {
+  g_err.clear();
+  if (!ctx || !fields || !t || !c || !src) return fail(THIIM_ERR_CONFIG, "null argument");
+  int r;
+  if ((r = upload_arrays(ctx, fields, 0, 12))) return r;
+  if ((r = upload_arrays(ctx, t, 12, 12))) return r;
+  if ((r = upload_arrays(ctx, c, 24, 12))) return r;
+  if ((r = upload_arrays(ctx, src, 36, 4))) return r;
+  ctx->loaded = true;
+  return THIIM_OK;
+}
+
+int thiim_gpu_upload_fields(thiim_gpu_ctx* ctx, const thiim_c128* const fields[12]) {
+  g_err.clear();
+  if (!ctx || !fields) return fail(THIIM_ERR_CONFIG, "null argument");
+  return upload_arrays(ctx, fields, 0, 12);
+}
+
+int thiim_gpu_init_generated(thiim_gpu_ctx* ctx, int kind, uint64_t seed) {
+  g_err.clear();
+  if (!ctx) return fail(THIIM_ERR_CONFIG, "null context");
+  if (kind != THIIM_GEN_RANDOM && kind != THIIM_GEN_LAYERED)
+    return fail(THIIM_ERR_CONFIG, "unknown generator kind");
+  // per-layer coefficient table (config 3), same draws as the host generator
+  double2 table[28 * 6];
+  for (int a = 12; a < 40; ++a)
+    for (int L = 0; L < 6; ++L) table[(a - 12) * 6 + L] = gen_disk(gen_key(seed, a), (uint64_t)L);
+  for (auto& sl : ctx->slabs) {
+    CK(cudaSetDevice(sl.device));
+    double2* dtable = nullptr;
+    CK(cudaMallocAsync(&dtable, sizeof(table), sl.stream));
+    CK(cudaMemcpyAsync(dtable, table, sizeof(table), cudaMemcpyHostToDevice, sl.stream));
+    // local plane 0 is global padded plane z0 (global interior z0-1)
+    Arrays A = sl.arrays(0, 0);
+    k_generate<<<8 * sm_count(sl.device), 256, 0, sl.stream>>>(sl.g, sl.z0, ctx->dims.nz, A,
+                                                                 kind, seed, dtable);
+    CK(cudaGetLastError());
+    for (int set = 1; set < sl.nfield_sets; ++set)
+      for (int k = 0; k < 12; ++k)
+        CK(cudaMemcpyAsync(sl.field(set, k), sl.field(0, k), sl.stride * sizeof(double2),
+                           cudaMemcpyDeviceToDevice, sl.stream));
+    CK(cudaFreeAsync(dtable, sl.stream));
+    CK(cudaStreamSynchronize(sl.stream));
+    sl.cur = 0;
+  }
+  ctx->loaded = true;
+  return THIIM_OK;
+}
+
+int thiim_gpu_step(thiim_gpu_ctx* ctx, int steps, thiim_gpu_stats* stats) {
+  g_err.clear();
+  if (!ctx) return fail(THIIM_ERR_CONFIG, "null context");
+  if (steps < 0) return fail(THIIM_ERR_CONFIG, "steps must be >= 0");
+  if (!ctx->loaded) return fail(THIIM_ERR_STATE, "no problem uploaded or generated");
+  long long launches = 0;
+  const bool multi = ctx->slabs.size() > 1;
+  for (auto& sl : ctx->slabs) {
+    CK(cudaSetDevice(sl.device));
+    CK(cudaEventRecord(sl.ev0, sl.stream));
+  }
+  int r;
+  for (int n = 0; n < steps; ++n) {
+    if (ctx->engine == THIIM_ENGINE_SPLIT) {
+      if (multi && (r = exchange(ctx, 0))) return r;
+      for (auto& sl : ctx->slabs)
+        if ((r = launch_split(ctx, sl, 0, &launches))) return r;
+      if (multi && (r = exchange(ctx, 1))) return r;
+      for (auto& sl : ctx->slabs)
+        if ((r = launch_split(ctx, sl, 1, &launches))) return r;
+    } else {
+      if (multi) return fail(THIIM_ERR_CONFIG, "multi-GPU fused engine not built yet");
+      for (auto& sl : ctx->slabs)
+        if ((r = launch_fused(ctx, sl, &launches))) return r;
+    }
+  }
+  double secs = 0.0;
+  for (auto& sl : ctx->slabs) {
+    CK(cudaSetDevice(sl.device));
+    CK(cudaEventRecord(sl.ev1, sl.stream));
+    CK(cudaEventSynchronize(sl.ev1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, sl.ev0, sl.ev1));
+    secs = std::max(secs, (double)ms * 1e-3);
+  }
+  if (stats) {
+    std::memset(stats, 0, sizeof(*stats));
+    stats->seconds = secs;
+    stats->kernel_seconds = secs;
+    stats->steps = steps;
+    stats->engine = ctx->engine;
+    stats->n_gpus = (int)ctx->slabs.size();
+    stats->kernel_launches = launches;
+    stats->balance_model = thiim_gpu_balance_model(ctx->engine, ctx->opts.time_block);
+    const double lups = (double)ctx->dims.nx * ctx->dims.ny * ctx->dims.nz * steps;
+    stats->mlups = (steps > 0 && secs > 0) ? lups / secs / 1e6 : 0.0;
+  }
+  return THIIM_OK;
+}
+
+static int download_impl(thiim_gpu_ctx* ctx, int a, thiim_c128* dst) {
+  const long long pxy = ctx->pxy();
+  const int n = (int)ctx->slabs.size();
+  for (int s = 0; s < n; ++s) {
+    Slab& sl = ctx->slabs[s];
+    CK(cudaSetDevice(sl.device));
+    // interior planes, plus the global ghost plane(s) this slab borders
+    const int p0 = s == 0 ? 0 : 1;
+    const int p1 = s == n - 1 ? sl.g.nz + 2 : sl.g.nz + 1;
+    const size_t off_host = (size_t)(sl.z0 + p0) * (size_t)pxy;
+    CK(cudaMemcpyAsync(dst + off_host, sl.array(a) + (size_t)p0 * pxy,
+                       (size_t)(p1 - p0) * (size_t)pxy * sizeof(double2), cudaMemcpyDeviceToHost,
+                       sl.stream));
+  }
+  for (auto& sl : ctx->slabs) {
+    CK(cudaSetDevice(sl.device));
+    CK(cudaStreamSynchronize(sl.stream));
+  }
+  return THIIM_OK;
+}
+
+int thiim_gpu_download_fields(thiim_gpu_ctx* ctx, thiim_c128* const fields[12]) {
+  g_err.clear();
+  if (!ctx || !fields) return fail(THIIM_ERR_CONFIG, "null argument");
+  for (int k = 0; k < 12; ++k) {
+    if (!fields[k]) return fail(THIIM_ERR_CONFIG, "null host array");
+    int r = download_impl(ctx, k, fields[k]);
+    if (r) return r;
+  }
+  return THIIM_OK;
+}
+
+int thiim_gpu_download_array(thiim_gpu_ctx* ctx, int array_id, thiim_c128* dst) {
+  g_err.clear();
+  if (!ctx || !dst) return fail(THIIM_ERR_CONFIG, "null argument");
+  if (array_id < 0 || array_id >= 40) return fail(THIIM_ERR_CONFIG, "array id out of range");
+  return download_impl(ctx, array_id, dst);
+}
+
+int thiim_gpu_compare_fields(thiim_gpu_ctx* ctx, const thiim_c128* const ref[12],
+                             thiim_gpu_diff* out) {
+  g_err.clear();
+  if (!ctx || !ref || !out) return fail(THIIM_ERR_CONFIG, "null argument");
+  std::memset(out, 0, sizeof(*out));
+  const long long pxy = ctx->pxy();
+  double num[12] = {0}, den[12] = {0};
+  for (auto& sl : ctx->slabs) {
+    CK(cudaSetDevice(sl.device));
+    const size_t elems = (size_t)(sl.g.nz + 2) * (size_t)pxy;
+    double2* dref = nullptr;
+    double* acc = nullptr;
+    unsigned long long* cnt = nullptr;
+    CK(cudaMalloc(&dref, elems * sizeof(double2)));
+    CK(cudaMalloc(&acc, 24 * sizeof(double)));
+    CK(cudaMalloc(&cnt, sizeof(unsigned long long)));
+    CK(cudaMemset(acc, 0, 24 * sizeof(double)));
+    CK(cudaMemset(cnt, 0, sizeof(unsigned long long)));
+    for (int k = 0; k < 12; ++k) {
+      CK(cudaMemcpy(dref, ref[k] + (size_t)sl.z0 * pxy, elems * sizeof(double2),
+                    cudaMemcpyHostToDevice));
+      k_compare<<<4 * sm_count(sl.device), 256, 0, sl.stream>>>(sl.g, sl.field(sl.cur, k), dref,
+                                                                acc + 2 * k, cnt);
+      CK(cudaGetLastError());
+      CK(cudaStreamSynchronize(sl.stream));
+    }
+    double h[24];
+    unsigned long long c = 0;
+    CK(cudaMemcpy(h, acc, sizeof(h), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&c, cnt, sizeof(c), cudaMemcpyDeviceToHost));
+    for (int k = 0; k < 12; ++k) {
+      num[k] += h[2 * k];
+      den[k] += h[2 * k + 1];
+    }
+    out->differing_values += c;
+    cudaFree(dref);
+    cudaFree(acc);
+    cudaFree(cnt);
+  }
+  for (int k = 0; k < 12; ++k) {
+    out->rel_l2[k] = den[k] > 0 ? std::sqrt(num[k] / den[k]) : std::sqrt(num[k]);
+    out->max_rel_l2 = std::max(out->max_rel_l2, out->rel_l2[k]);
+  }
+  return THIIM_OK;
+}
+
+int thiim_generate_host(const thiim_dims* dims, int kind, uint64_t seed,
+                        thiim_c128* const arrays[40]) {
+  g_err.clear();
+  if (!valid_dims(dims)) return fail(THIIM_ERR_SETUP, "invalid grid dims");
+  if (!arrays) return fail(THIIM_ERR_CONFIG, "null arrays");
+  if (kind != THIIM_GEN_RANDOM && kind != THIIM_GEN_LAYERED)
+    return fail(THIIM_ERR_CONFIG, "unknown generator kind");
+  const int nx = dims->nx, ny = dims->ny, nz = dims->nz;
+  const long long px = nx + 2, pxy = px * (ny + 2), n = pxy * (nz + 2);
+  double2 table[28 * 6];
+  for (int a = 12; a < 40; ++a)
+    for (int L = 0; L < 6; ++L) table[(a - 12) * 6 + L] = gen_disk(gen_key(seed, a), (uint64_t)L);
+  uint64_t keys[40];
+  for (int a = 0; a < 40; ++a) keys[a] = gen_key(seed, a);
+  for (int a = 0; a < 40; ++a)
+    if (!arrays[a]) return fail(THIIM_ERR_CONFIG, "null host array");
+#pragma omp parallel for schedule(static)
+  for (long long p = 0; p < n; ++p) {
+    const int zp = (int)(p / pxy);
+    const long long r = p - (long long)zp * pxy;
+    const int yp = (int)(r / px), xp = (int)(r - (long long)yp * px);
+    const int x = xp - 1, y = yp - 1, z = zp - 1;
+    const bool interior = x >= 0 && x < nx && y >= 0 && y < ny && z >= 0 && z < nz;
+    const int L = (interior && kind == THIIM_GEN_LAYERED) ? gen_layer(seed, nx, nz, x, y, z) : 0;
+    for (int a = 0; a < 40; ++a) {
+      double2 v = make_double2(0.0, 0.0);
+      if (interior) {
+        if (a < 12)
+          v = gen_field(keys[a], (uint64_t)p);
+        else if (kind == THIIM_GEN_LAYERED)
+          v = table[(a - 12) * 6 + L];
+        else
+          v = gen_disk(keys[a], (uint64_t)p);
+      }
+      arrays[a][p].re = v.x;
+      arrays[a][p].im = v.y;
+    }
+  }
+  return THIIM_OK;
+}
+
+int thiim_gpu_pin_host(void* ptr, size_t bytes) {
+  g_err.clear();
+  CK(cudaHostRegister(ptr, bytes, cudaHostRegisterDefault));
+  return THIIM_OK;
+}
+
+int thiim_gpu_unpin_host(void* ptr) {
+  g_err.clear();
+  CK(cudaHostUnregister(ptr));
+  return THIIM_OK;
+}
+
+}  // extern "C"
