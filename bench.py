@@ -193,7 +193,8 @@ def run_native(args, world, rank, local):
 
     dims = P.GridDims(*GRID)
     engine = {"auto": P.ENGINE_AUTO, "split": P.ENGINE_SPLIT, "fused": P.ENGINE_FUSED}[args.engine]
-    opts = P.GpuOptions(device=local if world > 1 else args.device, engine=engine)
+    opts = P.GpuOptions(device=local if world > 1 else args.device, engine=engine,
+                        tile_y=args.tile_y, z_chunk=args.z_chunk, min_blocks=args.min_blocks)
     iters = args.iters
     lups_step = dims.interior_cells() * iters
 
@@ -217,25 +218,26 @@ def run_native(args, world, rank, local):
     value = world * lups_step * args.steps / dev_secs / 1e6
 
     # ---- end to end through the public API from pinned host memory (e2e)
-    host = P.generate_problem(dims, P.GEN_RANDOM, SEED)
-    for a in host.arrays:
-        P.lib().thiim_gpu_pin_host(a.ctypes.data, a.nbytes)
-    e2e_secs = 0.0
-    for k in range(1 + args.steps):  # 1 untimed warm-up
-        work = host  # run_gpu updates fields in place; reset them from a pristine copy
-        t0 = time.perf_counter()
-        with P.GpuEngine(dims, opts) as e:
-            e.upload(work)
-            e.step(iters)
-            e.download_fields(work)
-        t1 = time.perf_counter()
-        if k >= 1:
-            e2e_secs += t1 - t0
-    for a in host.arrays:
-        P.lib().thiim_gpu_unpin_host(a.ctypes.data)
-    e2e_secs = barrier_max(e2e_secs)
-    e2e = world * lups_step * args.steps / e2e_secs / 1e6
     padded = dims.padded_cells() * 16
+    e2e = None
+    if not args.no_e2e:
+        host = P.generate_problem(dims, P.GEN_RANDOM, SEED)
+        for a in host.arrays:
+            P.lib().thiim_gpu_pin_host(a.ctypes.data, a.nbytes)
+        e2e_secs = 0.0
+        for k in range(1 + args.steps):  # 1 untimed warm-up
+            t0 = time.perf_counter()
+            with P.GpuEngine(dims, opts) as e:
+                e.upload(host)
+                e.step(iters)
+                e.download_fields(host)
+            t1 = time.perf_counter()
+            if k >= 1:
+                e2e_secs += t1 - t0
+        for a in host.arrays:
+            P.lib().thiim_gpu_unpin_host(a.ctypes.data)
+        e2e_secs = barrier_max(e2e_secs)
+        e2e = world * lups_step * args.steps / e2e_secs / 1e6
 
     # ---- roofline of the dominant kernel (one THIIM iteration per launch)
     hbm, peak_kind = load_peaks()
@@ -247,6 +249,7 @@ def run_native(args, world, rank, local):
         bytes_launch = 832.0 * dims.interior_cells()
         kname = "k_fused<32,8>"
     achieved = bytes_launch / per_launch_s / 1e9
+    thiim_balance = P.balance_model(engine_ran)
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
@@ -263,14 +266,14 @@ def run_native(args, world, rank, local):
                    "engine": P.ENGINE_NAMES.get(engine_ran), "parallelism": "dp%d" % world,
                    "l2": "inputs (%.1f GB state) larger than L2; no flush needed"
                          % (dims.padded_cells() * (832 if engine_ran != P.ENGINE_SPLIT else 640) / 1e9)},
-        "e2e": {"value": round(e2e, 2), "unit": "MLUP/s",
+        "e2e": {"value": round(e2e, 2) if e2e else None, "unit": "MLUP/s",
                 "h2d_bytes_per_step": 40 * padded, "d2h_bytes_per_step": 12 * padded},
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
                      "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": traffic,
                      "kernel": kname, "algorithmic_bytes_per_launch": bytes_launch,
                      "peak_kind": peak_kind,
-                     "lup_roofline_mlups": round(hbm * 1e9 / (bytes_launch / dims.interior_cells()) / 1e6, 1)},
+                     "lup_roofline_mlups": round(hbm * 1e3 / thiim_balance, 1)},
         "clocks": clk.result,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -297,6 +300,10 @@ def main():
     ap.add_argument("--iters", type=int, default=ITERS)
     ap.add_argument("--device", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--tile-y", type=int, default=0)
+    ap.add_argument("--z-chunk", type=int, default=0)
+    ap.add_argument("--min-blocks", type=int, default=0)
     args = ap.parse_args()
     world, rank, local = dist_env()
     if args.impl == "reference":

@@ -362,12 +362,16 @@ class GpuOptions:
     tile_y: int = 0
     z_chunk: int = 0
     time_block: int = 0
+    min_blocks: int = 0  # experimental register cap knob (reserved[0])
+    variant: int = 0     # fused kernel variant (reserved[1]): 0 bulk-async staged, 1 register-staged
 
     def _c(self) -> _Opts:
         o = _Opts()
         lib().thiim_gpu_default_opts(ctypes.byref(o))
         o.device, o.n_gpus, o.engine = self.device, self.n_gpus, self.engine
         o.tile_x, o.tile_y, o.z_chunk, o.time_block = self.tile_x, self.tile_y, self.z_chunk, self.time_block
+        o.reserved[0] = self.min_blocks
+        o.reserved[1] = self.variant
         return o
 
 

@@ -32,8 +32,8 @@ struct FusedSmem {
   double2 sH[3][BY][BX];  // H_new sums at plane z
 };
 
-template <int BX, int BY>
-__global__ void __launch_bounds__(BX* BY)
+template <int BX, int BY, int MINB>
+__global__ void __launch_bounds__(BX* BY, MINB)
     k_fused(Grid g, Arrays A, int zc) {
   constexpr int TX = BX - 2, TY = BY - 2;
   __shared__ FusedSmem<BX, BY> sm;

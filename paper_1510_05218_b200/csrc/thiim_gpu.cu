@@ -8,6 +8,8 @@
 //   [t: 12][c: 12][src: 4]
 // each array `stride` elements (padded plane count x (nx+2)(ny+2), rounded up
 // to 256 B).  Upload/download are plain plane-range copies: no layout change.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -21,6 +23,7 @@
 #include "../../include/thiim_gpu.h"
 #include "thiim_common.cuh"
 #include "thiim_fused.cuh"
+#include "thiim_fused_tma.cuh"
 #include "thiim_split.cuh"
 
 using namespace thiim_gpu;
@@ -54,6 +57,10 @@ struct Slab {
   int cur = 0;         // current field set
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // 4-D tensor maps over the allocation {x (doubles), y, plane, array slot},
+  // one per TMA box height (8 / 16 rows), built lazily
+  CUtensorMap tmap[2];
+  bool tmap_ok[2] = {false, false};
 
   double2* field(int set, int k) const { return buf + (size_t)(set * 12 + k) * stride; }
   double2* coeff(int a) const {  // a in 12..39
@@ -224,19 +231,115 @@ int launch_split(thiim_gpu_ctx* ctx, Slab& s, int fam, long long* launches) {
   return THIIM_OK;
 }
 
-int launch_fused(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
-  CK(cudaSetDevice(s.device));
+template <int BX, int BY, int MINB>
+int launch_fused_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
   const Arrays A = s.arrays(s.cur, s.cur ^ 1);
-  constexpr int TX = kFusedBX - 2, TY = kFusedBY - 2;
-  const dim3 block(kFusedBX, kFusedBY);
+  constexpr int TX = BX - 2, TY = BY - 2;
+  const dim3 block(BX, BY);
   const long long cols = (long long)((s.g.nx + TX - 1) / TX) * ((s.g.ny + TY - 1) / TY);
   const int zc = pick_zchunk(ctx, s, cols, ctx->opts.z_chunk);
   const dim3 grid((s.g.nx + TX - 1) / TX, (s.g.ny + TY - 1) / TY, (s.g.nz + zc - 1) / zc);
-  k_fused<kFusedBX, kFusedBY><<<grid, block, 0, s.stream>>>(s.g, A, zc);
+  k_fused<BX, BY, MINB><<<grid, block, 0, s.stream>>>(s.g, A, zc);
   CK(cudaGetLastError());
   s.cur ^= 1;
   ++*launches;
   return THIIM_OK;
+}
+
+// z-chunk count for a grid of `cols` column tiles with `per_sm` resident CTAs
+// per SM: minimise (waves x planes-per-CTA incl. ~1.5 planes of prologue).
+int balanced_zchunk(const Slab& s, long long cols, int per_sm, int user) {
+  if (user > 0) return std::min(user, s.g.nz);
+  const long long slots = (long long)sm_count(s.device) * per_sm;
+  double best = 1e300;
+  int best_c = 1;
+  for (int c = 1; c <= std::max(1, s.g.nz / 4); ++c) {
+    const int planes = (s.g.nz + c - 1) / c;
+    const long long ctas = cols * c;
+    const long long waves = (ctas + slots - 1) / slots;
+    const double t = (double)waves * (planes + 1.5);
+    if (t < best - 1e-9) {
+      best = t;
+      best_c = c;
+    }
+  }
+  return (s.g.nz + best_c - 1) / best_c;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+int ensure_tmap(Slab& s, int by) {
+  const int w = by == 16 ? 1 : 0;
+  if (s.tmap_ok[w]) return THIIM_OK;
+  auto fn = get_encode_fn();
+  if (!fn) return fail(THIIM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[4] = {(cuuint64_t)(2 * s.g.px), (cuuint64_t)(s.g.pxy / s.g.px),
+                              (cuuint64_t)(s.g.nz + 2), (cuuint64_t)(s.nfield_sets * 12 + 28)};
+  const cuuint64_t strides[3] = {(cuuint64_t)s.g.px * 16, (cuuint64_t)s.g.pxy * 16,
+                                 (cuuint64_t)s.stride * 16};
+  const cuuint32_t box[4] = {64, (cuuint32_t)by, 1, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = fn(&s.tmap[w], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, s.buf, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(THIIM_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  s.tmap_ok[w] = true;
+  return THIIM_OK;
+}
+
+template <int BY, int NBUF>
+int launch_fused_tma_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
+  const Arrays A = s.arrays(s.cur, s.cur ^ 1);
+  const int cur = s.cur, nf = s.nfield_sets;
+  const SeqSlots S = make_seq([&](int k) { return cur * 12 + k; },
+                              [&](int a) { return nf * 12 + (a - 12); });
+  int r = ensure_tmap(s, BY);
+  if (r) return r;
+  constexpr int TX = 30, TY = BY - 2;
+  const size_t smem = sizeof(TmaSmem<BY, NBUF>);
+  static bool attr_set = false;  // per process; the attribute is per function
+  if (!attr_set) {
+    CK(cudaFuncSetAttribute(k_fused_tma<BY, NBUF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)smem));
+    attr_set = true;
+  }
+  const long long cols = (long long)((s.g.nx + TX - 1) / TX) * ((s.g.ny + TY - 1) / TY);
+  const int zc = balanced_zchunk(s, cols, 1, ctx->opts.z_chunk);
+  const dim3 grid((s.g.nx + TX - 1) / TX, (s.g.ny + TY - 1) / TY, (s.g.nz + zc - 1) / zc);
+  const dim3 block(32, BY + 1);
+  k_fused_tma<BY, NBUF><<<grid, block, smem, s.stream>>>(s.g, A, s.tmap[BY == 16 ? 1 : 0], S, zc);
+  CK(cudaGetLastError());
+  s.cur ^= 1;
+  ++*launches;
+  return THIIM_OK;
+}
+
+int launch_fused(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
+  CK(cudaSetDevice(s.device));
+  // reserved[1] = 1 selects the register-staged kernel (thiim_fused.cuh);
+  // default is the bulk-async staged one (thiim_fused_tma.cuh).
+  if (ctx->opts.reserved[1] == 1) {
+    // tile_y selects the CTA height (rows incl. the 2-row ring); reserved[0] the
+    // minimum resident CTAs per SM requested from ptxas (register cap).
+    const int by = ctx->opts.tile_y, minb = ctx->opts.reserved[0];
+    if (by == 16) return launch_fused_t<32, 16, 1>(ctx, s, launches);
+    if (by == 4) return launch_fused_t<32, 4, 4>(ctx, s, launches);
+    if (minb == 1) return launch_fused_t<32, 8, 1>(ctx, s, launches);
+    return launch_fused_t<32, 8, 2>(ctx, s, launches);
+  }
+  if (ctx->opts.tile_y == 8) return launch_fused_tma_t<8, 40>(ctx, s, launches);
+  return launch_fused_tma_t<16, 20>(ctx, s, launches);
 }
 
 bool valid_dims(const thiim_dims* d) {
@@ -316,7 +419,9 @@ int thiim_gpu_create(const thiim_dims* dims, const thiim_gpu_opts* opts, thiim_g
     ctx->slabs.push_back(sl);
   }
   for (auto& sl : ctx->slabs) {
-    const size_t bytes = sl.stride * sizeof(double2) * (size_t)(12 * nf + 28);
+    // + tail slack: tile row copies may run past the last padded row
+    const size_t tail = (size_t)(34 * (dims->nx + 2) + 256) * sizeof(double2);
+    const size_t bytes = sl.stride * sizeof(double2) * (size_t)(12 * nf + 28) + tail;
     cudaError_t e = cudaSetDevice(sl.device);
     if (e == cudaSuccess) e = cudaMalloc(&sl.buf, bytes);
     if (e == cudaSuccess) e = cudaMemset(sl.buf, 0, bytes);
