@@ -194,7 +194,9 @@ def run_native(args, world, rank, local):
     dims = P.GridDims(*GRID)
     engine = {"auto": P.ENGINE_AUTO, "split": P.ENGINE_SPLIT, "fused": P.ENGINE_FUSED}[args.engine]
     opts = P.GpuOptions(device=local if world > 1 else args.device, engine=engine,
-                        tile_y=args.tile_y, z_chunk=args.z_chunk, min_blocks=args.min_blocks)
+                        tile_y=args.tile_y, z_chunk=args.z_chunk, min_blocks=args.min_blocks,
+                        variant=args.variant, l2_promotion=args.l2_promotion,
+                        y_fastest=args.y_fastest, full_boxes=args.full_boxes)
     iters = args.iters
     lups_step = dims.interior_cells() * iters
 
@@ -304,6 +306,10 @@ def main():
     ap.add_argument("--tile-y", type=int, default=0)
     ap.add_argument("--z-chunk", type=int, default=0)
     ap.add_argument("--min-blocks", type=int, default=0)
+    ap.add_argument("--variant", type=int, default=0)
+    ap.add_argument("--l2-promotion", type=int, default=0)
+    ap.add_argument("--y-fastest", type=int, default=0)
+    ap.add_argument("--full-boxes", type=int, default=0)
     args = ap.parse_args()
     world, rank, local = dist_env()
     if args.impl == "reference":

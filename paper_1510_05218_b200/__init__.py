@@ -364,6 +364,9 @@ class GpuOptions:
     time_block: int = 0
     min_blocks: int = 0  # experimental register cap knob (reserved[0])
     variant: int = 0     # fused kernel variant (reserved[1]): 0 bulk-async staged, 1 register-staged
+    l2_promotion: int = 0  # TMA L2 promotion (reserved[2]): 0 none, 1 64B, 2 128B, 3 256B
+    y_fastest: int = 0   # CTA order (reserved[3]): 0 x-tiles fastest (default), 1 y-tiles fastest
+    full_boxes: int = 0  # experiment (reserved[4]): fetch the full 32xBY box for every array
 
     def _c(self) -> _Opts:
         o = _Opts()
@@ -372,6 +375,9 @@ class GpuOptions:
         o.tile_x, o.tile_y, o.z_chunk, o.time_block = self.tile_x, self.tile_y, self.z_chunk, self.time_block
         o.reserved[0] = self.min_blocks
         o.reserved[1] = self.variant
+        o.reserved[2] = self.l2_promotion
+        o.reserved[3] = self.y_fastest
+        o.reserved[4] = self.full_boxes
         return o
 
 

@@ -26,11 +26,38 @@
 
 namespace thiim_gpu {
 
-// Array-plane order the producer streams and the consumers take, per z-plane,
-// as array slots of the slab allocation (the 4th coordinate of its tensor
-// map).  Entries 0..5 are read at plane z+1, the rest at plane z.
+// Array-plane order the producer streams and the consumers take, per z-plane:
+// the array slot of the slab allocation (4th tensor-map coordinate) and the
+// box shape.  Entries 0..5 are read at plane z+1, the rest at plane z.
+//
+// Box shapes (thread tile = 32 x BY cells, own cells = [1,30] x [1,BY-2]):
+//   BOX_A  32 x BY     everything (E_old: own, both rings, +x/+y neighbours)
+//   BOX_B  31 x (BY-1) own + ring_x + ring_y        (Hzx, Hzy operands)
+//   BOX_BX 31 x (BY-2) own + ring_x (x0-1 column)   (Hyx, Hyz operands)
+//   BOX_BY 30 x (BY-1) own + ring_y (y0-1 row)      (Hxy, Hxz operands)
+//   BOX_C  30 x (BY-2) own only                     (E-phase coefficients)
+// Fetching only what each group needs keeps the tile overlap (re-read by the
+// neighbouring CTA) at ~7% instead of ~22%.
+enum : int { BOX_A = 0, BOX_B = 1, BOX_BX = 2, BOX_BY = 3, BOX_C = 4, NBOX = 5 };
+
 struct SeqSlots {
   int s[40];
+  int box[40];
+};
+
+struct TmaMaps {
+  CUtensorMap m[NBOX];
+};
+
+// geometry of a box kind: first thread column/row it covers, width, height
+template <int BY>
+struct BoxGeom {
+  __host__ __device__ static constexpr int x0(int b) { return b >= BOX_BY ? 1 : 0; }
+  __host__ __device__ static constexpr int y0(int b) { return (b == BOX_BX || b == BOX_C) ? 1 : 0; }
+  __host__ __device__ static constexpr int w(int b) { return b == BOX_A ? 32 : b <= BOX_BX ? 31 : 30; }
+  __host__ __device__ static constexpr int h(int b) {
+    return b == BOX_A ? BY : (b == BOX_B || b == BOX_BY) ? BY - 1 : BY - 2;
+  }
 };
 
 // field_slot(k): slot of input field k; coeff_slot(a): slot of array a (12..39)
@@ -38,26 +65,31 @@ template <class FS, class CS>
 inline SeqSlots make_seq(FS field_slot, CS coeff_slot) {
   SeqSlots S;
   int k = 0;
-  for (int c = EXY; c <= EZY; ++c) S.s[k++] = field_slot(c);
-  const int hsrc[6] = {-1, SRC_HXZ, -1, SRC_HYZ, -1, -1};
-  for (int c = HXY; c <= HZY; ++c) {
+  for (int c = EXY; c <= EZY; ++c) {
+    S.box[k] = BOX_A;
     S.s[k++] = field_slot(c);
-    S.s[k++] = coeff_slot(12 + c);
-    S.s[k++] = coeff_slot(24 + c);
-    if (hsrc[c - HXY] >= 0) S.s[k++] = coeff_slot(36 + hsrc[c - HXY]);
+  }
+  const int hsrc[6] = {-1, SRC_HXZ, -1, SRC_HYZ, -1, -1};
+  const int hbox[6] = {BOX_BY, BOX_BY, BOX_BX, BOX_BX, BOX_B, BOX_B};
+  for (int c = HXY; c <= HZY; ++c) {
+    const int b = hbox[c - HXY];
+    S.box[k] = b; S.s[k++] = field_slot(c);
+    S.box[k] = b; S.s[k++] = coeff_slot(12 + c);
+    S.box[k] = b; S.s[k++] = coeff_slot(24 + c);
+    if (hsrc[c - HXY] >= 0) { S.box[k] = b; S.s[k++] = coeff_slot(36 + hsrc[c - HXY]); }
   }
   const int esrc[6] = {-1, SRC_EXZ, -1, SRC_EYZ, -1, -1};
   for (int c = EXY; c <= EZY; ++c) {
-    S.s[k++] = coeff_slot(12 + c);
-    S.s[k++] = coeff_slot(24 + c);
-    if (esrc[c] >= 0) S.s[k++] = coeff_slot(36 + esrc[c]);
+    S.box[k] = BOX_C; S.s[k++] = coeff_slot(12 + c);
+    S.box[k] = BOX_C; S.s[k++] = coeff_slot(24 + c);
+    if (esrc[c] >= 0) { S.box[k] = BOX_C; S.s[k++] = coeff_slot(36 + esrc[c]); }
   }
   return S;
 }
 
 template <int BY, int NBUF>
 struct TmaSmem {
-  double2 buf[NBUF][BY][32];
+  double2 buf[NBUF][BY * 32];  // one box per slot, packed with the box's own pitch
   double2 sE[3][BY][32];
   double2 sH[3][BY][32];
   uint64_t full[NBUF];
@@ -66,15 +98,21 @@ struct TmaSmem {
 
 template <int BY, int NBUF>
 __global__ void __launch_bounds__(32 * (BY + 1), 1)
-    k_fused_tma(Grid g, Arrays A, const __grid_constant__ CUtensorMap tmap, SeqSlots S, int zc) {
+    k_fused_tma(Grid g, Arrays A, const __grid_constant__ TmaMaps maps, SeqSlots S, int zc,
+                int tiles_y, int tiles_x, int x_fastest) {
   constexpr int BX = 32, TX = BX - 2, TY = BY - 2, NCOMP = 32 * BY;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   TmaSmem<BY, NBUF>& sm = *reinterpret_cast<TmaSmem<BY, NBUF>*>(smem_raw);
   const int tx = threadIdx.x, ty = threadIdx.y;
-  const int xb = blockIdx.x * TX - 1, yb = blockIdx.y * TY - 1;
+  // x-tiles enumerate fastest by default: x-neighbours share the DRAM blocks
+  // at their (unaligned) box edges, so running them together lets the second
+  // fetch hit in L2 (measured: 5.7% excess DRAM reads vs 19% y-fastest)
+  const int bty = x_fastest ? blockIdx.x / tiles_x : blockIdx.x % tiles_y;
+  const int btx = x_fastest ? blockIdx.x % tiles_x : blockIdx.x / tiles_y;
+  const int xb = btx * TX - 1, yb = bty * TY - 1;
   const int z0 = blockIdx.z * zc;
   const int z1 = min(g.nz, z0 + zc);
-  const long long px = g.px, pxy = g.pxy;
+  const long long pxy = g.pxy;
 
   if (tx == 0 && ty == 0) {
     for (int k = 0; k < NBUF; ++k) {
@@ -89,17 +127,20 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
     // ---------------- producer warp: one elected lane issues one TMA box
     // (32 cells x BY rows = BY*512 B) per array-plane
     if (tx == 0) {
-      tma_prefetch_desc(&tmap);
+#pragma unroll
+      for (int b = 0; b < NBOX; ++b) tma_prefetch_desc(&maps.m[b]);
       int slot = 0;
       uint32_t phase = 0;
-      const int c0 = 2 * (xb + 1), c1 = yb + 1;  // x in doubles, padded y
+      using G = BoxGeom<BY>;
       for (int z = z0; z < z1; ++z) {
 #pragma unroll 1
         for (int s = 0; s < 40; ++s) {
+          const int b = S.box[s];
           mbar_wait(&sm.empty[slot], phase ^ 1);
-          mbar_arrive_expect_tx(&sm.full[slot], BY * BX * 16);
-          tma_load_4d(&sm.buf[slot][0][0], &tmap, c0, c1, z + 1 + (s < 6 ? 1 : 0), S.s[s],
-                      &sm.full[slot]);
+          mbar_arrive_expect_tx(&sm.full[slot], (uint32_t)(G::w(b) * G::h(b) * 16));
+          // x in doubles, padded y / plane coordinates
+          tma_load_4d(&sm.buf[slot][0], &maps.m[b], 2 * (xb + 1 + G::x0(b)), yb + 1 + G::y0(b),
+                      z + 1 + (s < 6 ? 1 : 0), S.s[s], &sm.full[slot]);
           if (++slot == NBUF) {
             slot = 0;
             phase ^= 1;
@@ -168,9 +209,14 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
 
   int slot = 0;
   uint32_t phase = 0;
-  auto take = [&]() -> double2 {
+  // wait for the next slot, read this thread's element if the slot's box
+  // covers it, release the slot
+  auto take = [&](const int b) -> double2 {
+    using G = BoxGeom<BY>;
     mbar_wait(&sm.full[slot], phase);
-    const double2 v = sm.buf[slot][ty][tx];
+    const int cx = tx - G::x0(b), cy = ty - G::y0(b);
+    double2 v = make_double2(0.0, 0.0);
+    if (cx >= 0 && cx < G::w(b) && cy >= 0 && cy < G::h(b)) v = sm.buf[slot][cy * G::w(b) + cx];
     __syncwarp();
     if (tx == 0) mbar_arrive(&sm.empty[slot]);
     if (++slot == NBUF) {
@@ -184,7 +230,7 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
     // (a) E_old(z+1) splits (carried to the next plane); E sums at z to smem
     double2 en[6];
 #pragma unroll
-    for (int k = 0; k < 6; ++k) en[k] = take();
+    for (int k = 0; k < 6; ++k) en[k] = take(BOX_A);
     if (inpad) {
       sm.sE[0][ty][tx] = csum(e[EXY], e[EXZ]);
       sm.sE[1][ty][tx] = csum(e[EYX], e[EYZ]);
@@ -195,34 +241,34 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
     // (b) H half-step at plane z (own cells: all six; ring: the four needed)
     const double2 sEx = sm.sE[0][ty][tx], sEy = sm.sE[1][ty][tx], sEz = sm.sE[2][ty][tx];
     const double2 nEx = csum(en[EXY], en[EXZ]), nEy = csum(en[EYX], en[EYZ]);
-    double2 hxy = take();
+    double2 hxy = take(BOX_BY);
     {
-      const double2 t = take(), c = take();
+      const double2 t = take(BOX_BY), c = take(BOX_BY);
       if (upd_x) hxy = upd(hxy, t, c, sm.sE[2][ty + 1][tx], sEz);
     }
-    double2 hxz = take();
+    double2 hxz = take(BOX_BY);
     {
-      const double2 t = take(), c = take(), s = take();
+      const double2 t = take(BOX_BY), c = take(BOX_BY), s = take(BOX_BY);
       if (upd_x) hxz = upd_src(hxz, t, c, nEy, sEy, s);
     }
-    double2 hyx = take();
+    double2 hyx = take(BOX_BX);
     {
-      const double2 t = take(), c = take();
+      const double2 t = take(BOX_BX), c = take(BOX_BX);
       if (upd_y) hyx = upd(hyx, t, c, sm.sE[2][ty][tx + 1], sEz);
     }
-    double2 hyz = take();
+    double2 hyz = take(BOX_BX);
     {
-      const double2 t = take(), c = take(), s = take();
+      const double2 t = take(BOX_BX), c = take(BOX_BX), s = take(BOX_BX);
       if (upd_y) hyz = upd_src(hyz, t, c, nEx, sEx, s);
     }
-    double2 hzx = take();
+    double2 hzx = take(BOX_B);
     {
-      const double2 t = take(), c = take();
+      const double2 t = take(BOX_B), c = take(BOX_B);
       if (upd_z) hzx = upd(hzx, t, c, sm.sE[1][ty][tx + 1], sEy);
     }
-    double2 hzy = take();
+    double2 hzy = take(BOX_B);
     {
-      const double2 t = take(), c = take();
+      const double2 t = take(BOX_B), c = take(BOX_B);
       if (upd_z) hzy = upd(hzy, t, c, sm.sE[0][ty + 1][tx], sEx);
     }
     if (own) {
@@ -243,27 +289,27 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
     // (c) E half-step at plane z (own cells)
     const double2 sHx = sm.sH[0][ty][tx], sHy = sm.sH[1][ty][tx], sHz = sm.sH[2][ty][tx];
     {
-      const double2 t = take(), c = take();
+      const double2 t = take(BOX_C), c = take(BOX_C);
       if (own) A.fo[EXY][i] = upd(e[EXY], t, c, sm.sH[2][ty - 1][tx], sHz);
     }
     {
-      const double2 t = take(), c = take(), s = take();
+      const double2 t = take(BOX_C), c = take(BOX_C), s = take(BOX_C);
       if (own) A.fo[EXZ][i] = upd_src(e[EXZ], t, c, pHy, sHy, s);
     }
     {
-      const double2 t = take(), c = take();
+      const double2 t = take(BOX_C), c = take(BOX_C);
       if (own) A.fo[EYX][i] = upd(e[EYX], t, c, sm.sH[2][ty][tx - 1], sHz);
     }
     {
-      const double2 t = take(), c = take(), s = take();
+      const double2 t = take(BOX_C), c = take(BOX_C), s = take(BOX_C);
       if (own) A.fo[EYZ][i] = upd_src(e[EYZ], t, c, pHx, sHx, s);
     }
     {
-      const double2 t = take(), c = take();
+      const double2 t = take(BOX_C), c = take(BOX_C);
       if (own) A.fo[EZX][i] = upd(e[EZX], t, c, sm.sH[1][ty][tx - 1], sHy);
     }
     {
-      const double2 t = take(), c = take();
+      const double2 t = take(BOX_C), c = take(BOX_C);
       if (own) A.fo[EZY][i] = upd(e[EZY], t, c, sm.sH[0][ty - 1][tx], sHx);
     }
     pHx = sHx;

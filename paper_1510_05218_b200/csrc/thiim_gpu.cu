@@ -45,7 +45,6 @@ int fail(int code, const std::string& msg) {
   } while (0)
 
 constexpr int kSplitBY = 4;
-constexpr int kFusedBX = 32, kFusedBY = 8;
 
 struct Slab {
   int device = 0;
@@ -58,9 +57,9 @@ struct Slab {
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   // 4-D tensor maps over the allocation {x (doubles), y, plane, array slot},
-  // one per TMA box height (8 / 16 rows), built lazily
-  CUtensorMap tmap[2];
-  bool tmap_ok[2] = {false, false};
+  // one set of box shapes per tile height (8 / 16 rows), built lazily
+  TmaMaps maps[2];
+  bool maps_ok[2] = {false, false};
 
   double2* field(int set, int k) const { return buf + (size_t)(set * 12 + k) * stride; }
   double2* coeff(int a) const {  // a in 12..39
@@ -279,22 +278,30 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
   return fn;
 }
 
-int ensure_tmap(Slab& s, int by) {
+int ensure_tmap(Slab& s, int by, int promo) {
   const int w = by == 16 ? 1 : 0;
-  if (s.tmap_ok[w]) return THIIM_OK;
+  if (s.maps_ok[w]) return THIIM_OK;
+  const CUtensorMapL2promotion pr[4] = {CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_64B,
+                                        CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B};
   auto fn = get_encode_fn();
   if (!fn) return fail(THIIM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   const cuuint64_t dims[4] = {(cuuint64_t)(2 * s.g.px), (cuuint64_t)(s.g.pxy / s.g.px),
                               (cuuint64_t)(s.g.nz + 2), (cuuint64_t)(s.nfield_sets * 12 + 28)};
   const cuuint64_t strides[3] = {(cuuint64_t)s.g.px * 16, (cuuint64_t)s.g.pxy * 16,
                                  (cuuint64_t)s.stride * 16};
-  const cuuint32_t box[4] = {64, (cuuint32_t)by, 1, 1};
-  const cuuint32_t estr[4] = {1, 1, 1, 1};
-  CUresult r = fn(&s.tmap[w], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, s.buf, dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(THIIM_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
-  s.tmap_ok[w] = true;
+  const int bw[NBOX] = {32, 31, 31, 30, 30};
+  const int bh[NBOX] = {by, by - 1, by - 2, by - 1, by - 2};
+  for (int b = 0; b < NBOX; ++b) {
+    const cuuint32_t box[4] = {(cuuint32_t)(2 * bw[b]), (cuuint32_t)bh[b], 1, 1};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = fn(&s.maps[w].m[b], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, s.buf, dims, strides, box,
+                    estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                    pr[promo & 3], CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+      return fail(THIIM_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  }
+  s.maps_ok[w] = true;
   return THIIM_OK;
 }
 
@@ -302,9 +309,12 @@ template <int BY, int NBUF>
 int launch_fused_tma_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
   const Arrays A = s.arrays(s.cur, s.cur ^ 1);
   const int cur = s.cur, nf = s.nfield_sets;
-  const SeqSlots S = make_seq([&](int k) { return cur * 12 + k; },
-                              [&](int a) { return nf * 12 + (a - 12); });
-  int r = ensure_tmap(s, BY);
+  SeqSlots S = make_seq([&](int k) { return cur * 12 + k; },
+                        [&](int a) { return nf * 12 + (a - 12); });
+  if (ctx->opts.reserved[4] == 1)  // experiment: one full box shape for every array
+    for (int k = 0; k < 40; ++k) S.box[k] = BOX_A;
+  // reserved[2]: L2 promotion of the TMA fills (0 none, 1 64B, 2 128B, 3 256B)
+  int r = ensure_tmap(s, BY, ctx->opts.reserved[2]);
   if (r) return r;
   constexpr int TX = 30, TY = BY - 2;
   const size_t smem = sizeof(TmaSmem<BY, NBUF>);
@@ -316,9 +326,12 @@ int launch_fused_tma_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
   }
   const long long cols = (long long)((s.g.nx + TX - 1) / TX) * ((s.g.ny + TY - 1) / TY);
   const int zc = balanced_zchunk(s, cols, 1, ctx->opts.z_chunk);
-  const dim3 grid((s.g.nx + TX - 1) / TX, (s.g.ny + TY - 1) / TY, (s.g.nz + zc - 1) / zc);
+  const int tiles_y = (s.g.ny + TY - 1) / TY;
+  const int tiles_x = (s.g.nx + TX - 1) / TX;
+  const dim3 grid(tiles_x * tiles_y, 1, (s.g.nz + zc - 1) / zc);
   const dim3 block(32, BY + 1);
-  k_fused_tma<BY, NBUF><<<grid, block, smem, s.stream>>>(s.g, A, s.tmap[BY == 16 ? 1 : 0], S, zc);
+  k_fused_tma<BY, NBUF><<<grid, block, smem, s.stream>>>(s.g, A, s.maps[BY == 16 ? 1 : 0], S, zc,
+                                                         tiles_y, tiles_x, ctx->opts.reserved[3] == 0);
   CK(cudaGetLastError());
   s.cur ^= 1;
   ++*launches;
