@@ -1,0 +1,100 @@
+"""CPU tests of the C-ABI boundary (include/thiim_gpu.h): the library loads,
+exports every declared entry point, and validates arguments like the
+reference (ConfigError / SetupError) before touching a device."""
+import ctypes
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+import paper_1510_05218_b200 as P
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "thiim_gpu.h")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(thiim_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_declares_the_boundary():
+    fns = declared_functions()
+    for f in ["thiim_gpu_create", "thiim_gpu_upload", "thiim_gpu_init_generated",
+              "thiim_gpu_step", "thiim_gpu_download_fields", "thiim_gpu_destroy",
+              "thiim_gpu_last_error"]:
+        assert f in fns
+    assert set(fns) == set(P.EXPORTED_SYMBOLS)
+
+
+def test_library_exports_every_declared_symbol():
+    L = P.lib()
+    for f in declared_functions():
+        assert hasattr(L, f), f
+    out = subprocess.run(["nm", "-D", "--defined-only", P.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    for f in declared_functions():
+        assert re.search(r"\bT %s\b" % f, out), f
+
+
+def test_library_is_sm100a_cubin():
+    out = subprocess.run(["cuobjdump", "-lelf", P.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    sass = subprocess.run(["cuobjdump", "-sass", P.LIB_PATH], capture_output=True, text=True).stdout
+    assert "UTMALDG" in sass, "TMA tensor loads expected in the fused sweep"
+    assert "DFMA" not in sass, "-fmad=false: no contracted FP64 multiply-add may appear"
+
+
+def test_abi_version_and_models():
+    assert P.lib().thiim_gpu_abi_version() == 1
+    assert P.balance_model(P.ENGINE_SPLIT) == 1024.0
+    assert P.balance_model(P.ENGINE_FUSED) == 832.0
+    assert P.balance_model(P.ENGINE_TBLOCK, 2) == 416.0
+
+
+def test_argument_validation_without_device():
+    L = P.lib()
+    ctx = ctypes.c_void_p()
+    bad = P._Dims(3, 8, 8, 1)
+    assert L.thiim_gpu_create(ctypes.byref(bad), None, ctypes.byref(ctx)) == 3  # SetupError
+    ghost2 = P._Dims(8, 8, 8, 2)
+    assert L.thiim_gpu_create(ctypes.byref(ghost2), None, ctypes.byref(ctx)) == 3
+    assert b"invalid grid dims" in L.thiim_gpu_last_error()
+    good = P._Dims(8, 8, 8, 1)
+    o = P.GpuOptions(n_gpus=9)._c()
+    assert L.thiim_gpu_create(ctypes.byref(good), ctypes.byref(o), ctypes.byref(ctx)) == 2
+    assert L.thiim_gpu_step(None, 1, None) == 2
+    with pytest.raises(P.SetupError):
+        P.GpuEngine(P.GridDims(8, 8, 3))
+    with pytest.raises(P.ConfigError):
+        P.run_gpu(P.allocate_state(P.GridDims(4, 4, 4)), -1)
+
+
+def test_host_generator_rejects_bad_input():
+    L = P.lib()
+    arrs = (ctypes.c_void_p * 40)()
+    d = P._Dims(8, 8, 8, 1)
+    assert L.thiim_generate_host(ctypes.byref(d), 7, 1, arrs) == 2
+
+
+def test_compare_states_semantics():
+    """compare_states (verifier.cpp:13-44): interior only, first mismatch in
+    component-major, z, y, x order, bitwise (so -0.0 != +0.0)."""
+    d = P.GridDims(5, 4, 6)
+    a = P.generate_problem(d, P.GEN_RANDOM, 1)
+    b = P.clone_state(a)
+    assert P.compare_states(a, b).bitwise_equal
+    b.view3d(3)[0, 0, 0] = 99.0  # ghost: ignored
+    assert P.compare_states(a, b).bitwise_equal
+    b.interior(4)[2, 1, 3] += 1e-12
+    b.interior(7)[0, 0, 0] += 1.0
+    diff = P.compare_states(a, b)
+    assert not diff.bitwise_equal and diff.differing_values == 2
+    assert (diff.first_component, diff.x, diff.y, diff.z) == (4, 3, 1, 2)
+    c = P.allocate_state(d)
+    e = P.allocate_state(d)
+    e.interior(0)[0, 0, 0] = -0.0
+    assert not P.compare_states(c, e).bitwise_equal
