@@ -1,0 +1,105 @@
+// thiim_gpu_engine.cpp -- thiim::run_gpu over the C-ABI (include/thiim_gpu.h).
+#include "thiim_gpu_engine.hpp"
+
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace thiim {
+
+namespace {
+
+void check(int rc, const char* what) {
+  if (rc == THIIM_OK) return;
+  const std::string msg = std::string(what) + ": " + thiim_gpu_last_error();
+  if (rc == THIIM_ERR_CONFIG) throw ConfigError(msg);
+  if (rc == THIIM_ERR_SETUP) throw SetupError(msg);
+  throw std::runtime_error(msg);
+}
+
+const char* engine_name(int e) {
+  switch (e) {
+    case THIIM_ENGINE_SPLIT: return "gpu-split";
+    case THIIM_ENGINE_TBLOCK: return "gpu-tblock";
+    default: return "gpu-fused";
+  }
+}
+
+// RAII over the page-lock of the 40 host arrays.
+struct PinGuard {
+  std::vector<void*> pinned;
+  void pin(void* p, std::size_t bytes) {
+    if (thiim_gpu_pin_host(p, bytes) == THIIM_OK) pinned.push_back(p);
+  }
+  ~PinGuard() {
+    for (void* p : pinned) thiim_gpu_unpin_host(p);
+  }
+};
+
+struct CtxGuard {
+  thiim_gpu_ctx* ctx = nullptr;
+  ~CtxGuard() { thiim_gpu_destroy(ctx); }
+};
+
+}  // namespace
+
+RunReport run_gpu(ProblemState& state, int steps, const GpuOptions& opts) {
+  if (steps < 0) throw ConfigError("steps must be >= 0");  // reference_engines.cpp:35
+  RunReport report;
+  report.dims = state.dims;
+  report.steps = report.steps_executed = steps;
+  report.threads = opts.n_gpus;
+
+  thiim_dims d{state.dims.nx, state.dims.ny, state.dims.nz, state.dims.ghost};
+  thiim_gpu_opts o;
+  thiim_gpu_default_opts(&o);
+  o.device = opts.device;
+  o.n_gpus = opts.n_gpus;
+  o.engine = opts.engine;
+  o.time_block = opts.time_block;
+  o.z_chunk = opts.z_chunk;
+
+  CtxGuard g;
+  check(thiim_gpu_create(&d, &o, &g.ctx), "thiim_gpu_create");
+
+  const std::size_t bytes = state.dims.padded_cells() * sizeof(ComplexScalar);
+  const thiim_c128* f[12];
+  const thiim_c128* t[12];
+  const thiim_c128* c[12];
+  const thiim_c128* s[4];
+  PinGuard pins;
+  for (int i = 0; i < kNumComponents; ++i) {
+    f[i] = reinterpret_cast<const thiim_c128*>(state.fields[i].data());
+    t[i] = reinterpret_cast<const thiim_c128*>(state.coeff_t[i].data());
+    c[i] = reinterpret_cast<const thiim_c128*>(state.coeff_c[i].data());
+    if (opts.pin_host) {
+      pins.pin(state.fields[i].data(), bytes);
+      pins.pin(state.coeff_t[i].data(), bytes);
+      pins.pin(state.coeff_c[i].data(), bytes);
+    }
+  }
+  for (int i = 0; i < kNumSourceComponents; ++i) {
+    s[i] = reinterpret_cast<const thiim_c128*>(state.coeff_src[i].data());
+    if (opts.pin_host) pins.pin(state.coeff_src[i].data(), bytes);
+  }
+  check(thiim_gpu_upload(g.ctx, f, t, c, s), "thiim_gpu_upload");
+
+  thiim_gpu_stats st{};
+  check(thiim_gpu_step(g.ctx, steps, &st), "thiim_gpu_step");
+
+  thiim_c128* out[12];
+  for (int i = 0; i < kNumComponents; ++i)
+    out[i] = reinterpret_cast<thiim_c128*>(state.fields[i].data());
+  check(thiim_gpu_download_fields(g.ctx, out), "thiim_gpu_download_fields");
+
+  report.engine = engine_name(st.engine);
+  report.seconds = st.seconds;
+  report.balance_model = st.balance_model;
+  if (steps > 0 && st.seconds > 0.0)  // reference_engines.cpp:19-23
+    report.mlups = double(state.dims.interior_cells()) * steps / st.seconds / 1e6;
+  if (opts.hbm_gbs > 0.0) report.predicted_mlups = opts.hbm_gbs * 1e3 / st.balance_model;
+  report.verification = "skipped";
+  return report;
+}
+
+}  // namespace thiim

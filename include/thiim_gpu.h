@@ -152,6 +152,44 @@ int thiim_gpu_unpin_host(void* ptr);
 
 void thiim_gpu_destroy(thiim_gpu_ctx* ctx);
 
+/* ---- z-slab decomposition, one process per GPU (multi-rank drivers) ----
+ *
+ * A slab context owns global interior planes [z0, z1) of the grid `global`
+ * on opts->device.  Its local ghost planes are global ghosts at the grid
+ * boundary and HALO copies of the neighbour slab's boundary planes inside.
+ * Uploads and downloads take GLOBAL-size host arrays and touch only the
+ * slab's planes.  Between steps the driver moves, per interface:
+ *   lower rank SEND_UP (E x6 + Hxy,Hxz,Hyx,Hyz of its last plane)
+ *        -> upper rank RECV_DOWN (its plane below z0)
+ *   upper rank SEND_DOWN (E x6 of its first plane)
+ *        -> lower rank RECV_UP (its plane above z1-1)
+ * The upper rank recomputes H_new on the received plane, so a step needs no
+ * mid-step exchange.  Fused engines only. */
+int thiim_gpu_create_slab(const thiim_dims* global, int z0, int z1, const thiim_gpu_opts* opts,
+                          thiim_gpu_ctx** out);
+
+enum {
+  THIIM_HALO_SEND_DOWN = 0,
+  THIIM_HALO_RECV_DOWN = 1,
+  THIIM_HALO_SEND_UP = 2,
+  THIIM_HALO_RECV_UP = 3
+};
+
+/* One halo plane set: n_arrays array-planes of plane_bytes each, the k-th at
+ * base + k*array_stride_bytes (device memory of `device`).  Valid until the
+ * next thiim_gpu_step (the fused engines ping-pong their field buffers). */
+typedef struct {
+  void* base;
+  long long array_stride_bytes;
+  long long plane_bytes;
+  int n_arrays;
+  int device;
+} thiim_halo_view;
+int thiim_gpu_halo_view(thiim_gpu_ctx* ctx, int which, thiim_halo_view* view);
+
+/* Blocks until all work queued on the context's streams has finished. */
+int thiim_gpu_sync(thiim_gpu_ctx* ctx);
+
 /* Message of the last failing call on this thread ("" if none). */
 const char* thiim_gpu_last_error(void);
 

@@ -106,6 +106,12 @@ def c_step(dims, arrays, steps: int = 1, threads: int = 1) -> None:
         c_lib().orc_run_naive(ctypes.byref(s), steps)
 
 
+def c_step_slab(dims, arrays, halo_lo: bool) -> None:
+    """One step of a z-slab (local dims) whose plane below is a halo copy."""
+    s = _st(dims, arrays)
+    c_lib().orc_step_slab(ctypes.byref(s), 1 if halo_lo else 0)
+
+
 def c_update_region(dims, arrays, comp, x0, x1, y0, y1, z0, z1) -> None:
     s = _st(dims, arrays)
     c_lib().orc_update_component_region(ctypes.byref(s), comp, x0, x1, y0, y1, z0, z1)

@@ -99,6 +99,17 @@ void orc_step_reference(orc_state* s) {
     orc_update_component_region(s, kEOrder[k], 0, s->nx, 0, s->ny, 0, s->nz);
 }
 
+/* One step of a z-slab whose plane below z = 0 is a halo copy of the
+ * neighbour's last plane (halo_lo = 1): H is also updated on that plane
+ * (z = -1) so E at z = 0 sees H_new there, exactly as the neighbour computes
+ * it.  Models the decomposition of paper_1510_05218_b200/distributed.py. */
+void orc_step_slab(orc_state* s, int halo_lo) {
+  for (int k = 0; k < 6; ++k)
+    orc_update_component_region(s, kHOrder[k], 0, s->nx, 0, s->ny, halo_lo ? -1 : 0, s->nz);
+  for (int k = 0; k < 6; ++k)
+    orc_update_component_region(s, kEOrder[k], 0, s->nx, 0, s->ny, 0, s->nz);
+}
+
 /* run_naive serial branch, reference_engines.cpp:44-46 */
 void orc_run_naive(orc_state* s, int steps) {
   for (int n = 0; n < steps; ++n) orc_step_reference(s);

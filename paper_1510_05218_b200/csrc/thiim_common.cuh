@@ -76,6 +76,10 @@ enum : int { SRC_EXZ = 0, SRC_EYZ = 1, SRC_HXZ = 2, SRC_HYZ = 3 };
 struct Grid {
   int nx, ny, nz;  // interior extents of this slab
   long long px, pxy;
+  // 1 when the plane below local z = 0 holds a neighbour slab's interior
+  // plane (a halo copy) rather than the global ghost plane: the fused sweep
+  // then recomputes H_new there instead of reading the never-updated ghost.
+  int halo_lo;
   THIIM_HD long long idx(int x, int y, int z) const {
     return (long long)(z + 1) * pxy + (long long)(y + 1) * px + (long long)(x + 1);
   }

@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(BX* BY, MINB)
   double2 pHx = make_double2(0.0, 0.0), pHy = make_double2(0.0, 0.0);
   {
     const long long im = i - pxy;
-    if (z0 == 0) {
+    if (z0 == 0 && !g.halo_lo) {
       // ghost plane below the grid: H never updated there
       if (own) {
         pHx = csum(__ldg(A.f[HXY] + im), __ldg(A.f[HXZ] + im));

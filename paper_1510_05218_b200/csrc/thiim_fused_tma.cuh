@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
   double2 pHx = make_double2(0.0, 0.0), pHy = make_double2(0.0, 0.0);
   {
     const long long im = i - pxy;
-    if (z0 == 0) {
+    if (z0 == 0 && !g.halo_lo) {
       if (own) {
         pHx = csum(__ldg(A.f[HXY] + im), __ldg(A.f[HXZ] + im));
         pHy = csum(__ldg(A.f[HYX] + im), __ldg(A.f[HYZ] + im));

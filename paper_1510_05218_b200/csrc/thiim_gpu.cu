@@ -212,6 +212,34 @@ int exchange(thiim_gpu_ctx* ctx, int which) {
   return THIIM_OK;
 }
 
+// Fused engines (single-process multi-GPU): before a step, each interface gets
+// the lower slab's last plane (E + Hxy,Hxz,Hyx,Hyz: the upper slab recomputes
+// H_new there) and the upper slab's first plane (E) copied into the halo
+// planes, peer to peer over NVLink.  Same data the multi-process path moves
+// with NCCL (thiim_gpu_halo_view).
+int exchange_fused(thiim_gpu_ctx* ctx) {
+  const int n = (int)ctx->slabs.size();
+  const size_t pbytes = (size_t)ctx->pxy() * sizeof(double2);
+  for (auto& sl : ctx->slabs) {  // previous step finished everywhere
+    CK(cudaSetDevice(sl.device));
+    CK(cudaStreamSynchronize(sl.stream));
+  }
+  for (int s = 0; s + 1 < n; ++s) {
+    Slab& lo = ctx->slabs[s];
+    Slab& hi = ctx->slabs[s + 1];
+    CK(cudaSetDevice(hi.device));
+    for (int k = 0; k < 10; ++k)  // lo's plane nz -> hi's plane 0
+      CK(cudaMemcpyPeerAsync(hi.field(hi.cur, k), hi.device,
+                             lo.field(lo.cur, k) + (size_t)lo.g.nz * lo.g.pxy, lo.device, pbytes,
+                             hi.stream));
+    CK(cudaSetDevice(lo.device));
+    for (int k = 0; k < 6; ++k)  // hi's plane 1 -> lo's plane nz+1
+      CK(cudaMemcpyPeerAsync(lo.field(lo.cur, k) + (size_t)(lo.g.nz + 1) * lo.g.pxy, lo.device,
+                             hi.field(hi.cur, k) + (size_t)hi.g.pxy, hi.device, pbytes, lo.stream));
+  }
+  return THIIM_OK;
+}
+
 int launch_split(thiim_gpu_ctx* ctx, Slab& s, int fam, long long* launches) {
   CK(cudaSetDevice(s.device));
   const Arrays A = s.arrays(s.cur, s.cur);
@@ -385,7 +413,10 @@ double thiim_gpu_balance_model(int engine, int time_block) {
   }
 }
 
-int thiim_gpu_create(const thiim_dims* dims, const thiim_gpu_opts* opts, thiim_gpu_ctx** out) {
+// Shared by thiim_gpu_create (n_gpus slabs split like the reference's z_slab,
+// reference_engines.cpp:26-30) and thiim_gpu_create_slab (one explicit slab).
+static int create_impl(const thiim_dims* dims, const thiim_gpu_opts* opts,
+                       const std::vector<std::pair<int, int>>& ranges, thiim_gpu_ctx** out) {
   g_err.clear();
   if (!out) return fail(THIIM_ERR_CONFIG, "out pointer is null");
   *out = nullptr;
@@ -401,12 +432,13 @@ int thiim_gpu_create(const thiim_dims* dims, const thiim_gpu_opts* opts, thiim_g
     return fail(THIIM_ERR_CONFIG, "unknown engine");
   if (o.engine == THIIM_ENGINE_TBLOCK)
     return fail(THIIM_ERR_CONFIG, "engine TBLOCK is not built yet");
-  if (dims->nz < 4 * o.n_gpus)
-    return fail(THIIM_ERR_CONFIG, "need at least 4 z planes per GPU");
+  for (const auto& r : ranges)
+    if (r.first < 0 || r.second > dims->nz || r.second - r.first < 4)
+      return fail(THIIM_ERR_CONFIG, "each z-slab needs at least 4 planes inside the grid");
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1)
     return fail(THIIM_ERR_CUDA, "no CUDA device visible");
-  if (o.device < 0 || o.device + o.n_gpus > ndev)
+  if (o.device < 0 || o.device + (int)ranges.size() > ndev)
     return fail(THIIM_ERR_CONFIG, "device range exceeds visible devices");
 
   auto* ctx = new thiim_gpu_ctx;
@@ -415,18 +447,18 @@ int thiim_gpu_create(const thiim_dims* dims, const thiim_gpu_opts* opts, thiim_g
   ctx->engine = o.engine == THIIM_ENGINE_AUTO ? THIIM_ENGINE_FUSED : o.engine;
   const int nf = ctx->engine == THIIM_ENGINE_SPLIT ? 1 : 2;
   const long long pxy = ctx->pxy();
-  const int n = o.n_gpus;
+  const int n = (int)ranges.size();
   for (int s = 0; s < n; ++s) {
     Slab sl;
     sl.device = o.device + s;
-    const int base = dims->nz / n, rem = dims->nz % n;  // reference z_slab split
-    sl.z0 = s * base + std::min(s, rem);
-    sl.z1 = sl.z0 + base + (s < rem ? 1 : 0);
+    sl.z0 = ranges[s].first;
+    sl.z1 = ranges[s].second;
     sl.g.nx = dims->nx;
     sl.g.ny = dims->ny;
     sl.g.nz = sl.z1 - sl.z0;
     sl.g.px = dims->nx + 2;
     sl.g.pxy = pxy;
+    sl.g.halo_lo = sl.z0 > 0 ? 1 : 0;
     sl.nfield_sets = nf;
     sl.stride = ((size_t)(sl.g.nz + 2) * (size_t)pxy + 15) / 16 * 16;
     ctx->slabs.push_back(sl);
@@ -450,19 +482,78 @@ int thiim_gpu_create(const thiim_dims* dims, const thiim_gpu_opts* opts, thiim_g
     }
   }
   if (n > 1) {
-    for (int s = 0; s < n; ++s)
-      for (int t = 0; t < n; ++t) {
-        if (s == t || std::abs(s - t) != 1) continue;
+    for (int s = 0; s + 1 < n; ++s)
+      for (int d : {0, 1}) {
+        const int a = ctx->slabs[s + d].device, b = ctx->slabs[s + 1 - d].device;
         int can = 0;
-        cudaDeviceCanAccessPeer(&can, ctx->slabs[s].device, ctx->slabs[t].device);
+        cudaDeviceCanAccessPeer(&can, a, b);
         if (can) {
-          cudaSetDevice(ctx->slabs[s].device);
-          cudaError_t e = cudaDeviceEnablePeerAccess(ctx->slabs[t].device, 0);
+          cudaSetDevice(a);
+          cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
           if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
         }
       }
   }
   *out = ctx;
+  return THIIM_OK;
+}
+
+int thiim_gpu_create(const thiim_dims* dims, const thiim_gpu_opts* opts, thiim_gpu_ctx** out) {
+  const int n = opts ? opts->n_gpus : 1;
+  std::vector<std::pair<int, int>> ranges;
+  if (dims && n >= 1 && n <= 8) {
+    const int base = dims->nz / n, rem = dims->nz % n;  // reference z_slab split
+    for (int s = 0; s < n; ++s) {
+      const int z0 = s * base + std::min(s, rem);
+      ranges.push_back({z0, z0 + base + (s < rem ? 1 : 0)});
+    }
+  }
+  return create_impl(dims, opts, ranges, out);
+}
+
+int thiim_gpu_create_slab(const thiim_dims* global, int z0, int z1, const thiim_gpu_opts* opts,
+                          thiim_gpu_ctx** out) {
+  thiim_gpu_opts o;
+  if (opts)
+    o = *opts;
+  else
+    thiim_gpu_default_opts(&o);
+  o.n_gpus = 1;
+  if (o.engine == THIIM_ENGINE_SPLIT && global && (z0 > 0 || z1 < global->nz)) {
+    g_err = "slab contexts with halos need a fused engine (the split engine exchanges mid-step)";
+    return THIIM_ERR_CONFIG;
+  }
+  return create_impl(global, &o, {{z0, z1}}, out);
+}
+
+int thiim_gpu_halo_view(thiim_gpu_ctx* ctx, int which, thiim_halo_view* v) {
+  g_err.clear();
+  if (!ctx || !v) return fail(THIIM_ERR_CONFIG, "null argument");
+  if (ctx->slabs.size() != 1) return fail(THIIM_ERR_CONFIG, "halo views need a slab context");
+  const Slab& sl = ctx->slabs[0];
+  int plane, n;
+  switch (which) {
+    case THIIM_HALO_SEND_DOWN: plane = 1; n = 6; break;             // E of my first plane
+    case THIIM_HALO_RECV_DOWN: plane = 0; n = 10; break;            // E + Hxy..Hyz below me
+    case THIIM_HALO_SEND_UP: plane = sl.g.nz; n = 10; break;        // E + Hxy..Hyz of my last plane
+    case THIIM_HALO_RECV_UP: plane = sl.g.nz + 1; n = 6; break;     // E above me
+    default: return fail(THIIM_ERR_CONFIG, "unknown halo view");
+  }
+  v->base = sl.field(sl.cur, 0) + (size_t)plane * (size_t)sl.g.pxy;
+  v->array_stride_bytes = (long long)(sl.stride * sizeof(double2));
+  v->plane_bytes = (long long)(sl.g.pxy * sizeof(double2));
+  v->n_arrays = n;
+  v->device = sl.device;
+  return THIIM_OK;
+}
+
+int thiim_gpu_sync(thiim_gpu_ctx* ctx) {
+  g_err.clear();
+  if (!ctx) return fail(THIIM_ERR_CONFIG, "null context");
+  for (auto& sl : ctx->slabs) {
+    CK(cudaSetDevice(sl.device));
+    CK(cudaStreamSynchronize(sl.stream));
+  }
   return THIIM_OK;
 }
 
@@ -577,7 +668,7 @@ int thiim_gpu_step(thiim_gpu_ctx* ctx, int steps, thiim_gpu_stats* stats) {
       for (auto& sl : ctx->slabs)
         if ((r = launch_split(ctx, sl, 1, &launches))) return r;
     } else {
-      if (multi) return fail(THIIM_ERR_CONFIG, "multi-GPU fused engine not built yet");
+      if (multi && (r = exchange_fused(ctx))) return r;
       for (auto& sl : ctx->slabs)
         if ((r = launch_fused(ctx, sl, &launches))) return r;
     }
@@ -608,13 +699,11 @@ int thiim_gpu_step(thiim_gpu_ctx* ctx, int steps, thiim_gpu_stats* stats) {
 
 static int download_impl(thiim_gpu_ctx* ctx, int a, thiim_c128* dst) {
   const long long pxy = ctx->pxy();
-  const int n = (int)ctx->slabs.size();
-  for (int s = 0; s < n; ++s) {
-    Slab& sl = ctx->slabs[s];
+  for (auto& sl : ctx->slabs) {
     CK(cudaSetDevice(sl.device));
     // interior planes, plus the global ghost plane(s) this slab borders
-    const int p0 = s == 0 ? 0 : 1;
-    const int p1 = s == n - 1 ? sl.g.nz + 2 : sl.g.nz + 1;
+    const int p0 = sl.z0 == 0 ? 0 : 1;
+    const int p1 = sl.z1 == ctx->dims.nz ? sl.g.nz + 2 : sl.g.nz + 1;
     const size_t off_host = (size_t)(sl.z0 + p0) * (size_t)pxy;
     CK(cudaMemcpyAsync(dst + off_host, sl.array(a) + (size_t)p0 * pxy,
                        (size_t)(p1 - p0) * (size_t)pxy * sizeof(double2), cudaMemcpyDeviceToHost,

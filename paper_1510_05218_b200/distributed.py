@@ -1,0 +1,146 @@
+"""Multi-GPU z-slab decomposition, one process per GPU.
+
+The grid's interior planes are split into contiguous z-slabs exactly like the
+reference's threaded engines split them among workers (z_slab,
+reference_engines.cpp:26-30).  Each rank owns one slab context
+(thiim_gpu_create_slab) whose boundary planes are either global ghosts or
+halo copies of the neighbour's boundary planes.  Before every THIIM step the
+ranks exchange, per interface:
+
+    lower rank  SEND_UP   : E x6 + Hxy,Hxz,Hyx,Hyz of its last plane  -> upper RECV_DOWN
+    upper rank  SEND_DOWN : E x6 of its first plane                   -> lower RECV_UP
+
+The upper rank recomputes H_new on the received plane inside its sweep, so a
+step needs no mid-step exchange.  The exchange is torch.distributed
+point-to-point (batch_isend_irecv: NCCL over NVLink on GPUs, gloo on CPU for
+the tests); the engine object supplies the plane buffers, so the same logic
+drives the CUDA engine and the CPU test double.
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import List, Optional, Tuple
+
+import numpy as np
+
+from . import (GEN_RANDOM, GridDims, GpuOptions, ProblemState, _check, _Dims, _ptrs, _Stats, lib)
+
+SEND_DOWN, RECV_DOWN, SEND_UP, RECV_UP = 0, 1, 2, 3
+N_ARRAYS = {SEND_DOWN: 6, RECV_DOWN: 10, SEND_UP: 10, RECV_UP: 6}
+
+
+def slab_bounds(nz: int, world: int, rank: int) -> Tuple[int, int]:
+    """Static z partition of reference_engines.cpp:26-30."""
+    base, rem = divmod(nz, world)
+    z0 = rank * base + min(rank, rem)
+    return z0, z0 + base + (1 if rank < rem else 0)
+
+
+class _HaloView(ctypes.Structure):
+    _fields_ = [("base", ctypes.c_void_p), ("array_stride_bytes", ctypes.c_longlong),
+                ("plane_bytes", ctypes.c_longlong), ("n_arrays", ctypes.c_int),
+                ("device", ctypes.c_int)]
+
+
+class _CudaPlane:
+    """__cuda_array_interface__ over one device array-plane (float64 view)."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes // 8,), "typestr": "<f8",
+                                         "data": (ptr, False), "version": 3, "strides": None}
+
+
+class SlabGpuEngine:
+    """One rank's slab of the global grid on its GPU (fused engine)."""
+
+    def __init__(self, global_dims: GridDims, z0: int, z1: int, opts: Optional[GpuOptions] = None):
+        self.dims, self.z0, self.z1 = global_dims, z0, z1
+        self.opts = opts or GpuOptions()
+        L = lib()
+        L.thiim_gpu_create_slab.argtypes = [ctypes.POINTER(_Dims), ctypes.c_int, ctypes.c_int,
+                                            ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)]
+        L.thiim_gpu_halo_view.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(_HaloView)]
+        L.thiim_gpu_sync.argtypes = [ctypes.c_void_p]
+        self._ctx = ctypes.c_void_p()
+        d = _Dims(global_dims.nx, global_dims.ny, global_dims.nz, global_dims.ghost)
+        o = self.opts._c()
+        _check(L.thiim_gpu_create_slab(ctypes.byref(d), z0, z1, ctypes.byref(o),
+                                       ctypes.byref(self._ctx)))
+
+    def close(self):
+        if self._ctx:
+            lib().thiim_gpu_destroy(self._ctx)
+            self._ctx = ctypes.c_void_p()
+
+    def generate(self, kind: int = GEN_RANDOM, seed: int = 1):
+        _check(lib().thiim_gpu_init_generated(self._ctx, kind, seed))
+
+    def upload(self, s: ProblemState):
+        a = s.arrays
+        _check(lib().thiim_gpu_upload(self._ctx, _ptrs(a[0:12]), _ptrs(a[12:24]), _ptrs(a[24:36]),
+                                      _ptrs(a[36:40])))
+
+    def download_fields(self, s: ProblemState):
+        _check(lib().thiim_gpu_download_fields(self._ctx, _ptrs(s.arrays[0:12])))
+
+    def step(self, steps: int = 1):
+        st = _Stats()
+        _check(lib().thiim_gpu_step(self._ctx, steps, ctypes.byref(st)))
+        return st
+
+    def halo(self, which: int):
+        """The halo array-planes as torch CUDA tensors aliasing engine memory."""
+        import torch
+        v = _HaloView()
+        _check(lib().thiim_gpu_halo_view(self._ctx, which, ctypes.byref(v)))
+        dev = torch.device("cuda", v.device)
+        return [torch.as_tensor(_CudaPlane(v.base + k * v.array_stride_bytes, v.plane_bytes),
+                                device=dev) for k in range(v.n_arrays)]
+
+    def sync(self):
+        _check(lib().thiim_gpu_sync(self._ctx))
+
+
+class HaloExchanger:
+    """Between-step halo exchange of one rank with its z-neighbours."""
+
+    def __init__(self, rank: int, world: int, group=None):
+        self.rank, self.world, self.group = rank, world, group
+
+    def exchange(self, engine) -> int:
+        """Returns the number of bytes this rank sent."""
+        import torch
+        import torch.distributed as dist
+        ops: List = []
+        sent = 0
+        if self.rank + 1 < self.world:
+            up = self.rank + 1
+            for t in engine.halo(SEND_UP):
+                ops.append(dist.P2POp(dist.isend, t, up, self.group))
+                sent += t.numel() * 8
+            for t in engine.halo(RECV_UP):
+                ops.append(dist.P2POp(dist.irecv, t, up, self.group))
+        if self.rank > 0:
+            down = self.rank - 1
+            for t in engine.halo(SEND_DOWN):
+                ops.append(dist.P2POp(dist.isend, t, down, self.group))
+                sent += t.numel() * 8
+            for t in engine.halo(RECV_DOWN):
+                ops.append(dist.P2POp(dist.irecv, t, down, self.group))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+            if torch.cuda.is_available() and ops[0].tensor.is_cuda:
+                torch.cuda.synchronize()
+        return sent
+
+
+def run_distributed(engine, steps: int, exchanger: HaloExchanger) -> dict:
+    """`steps` THIIM iterations of the decomposed grid: exchange, then step."""
+    sent = 0
+    launches = 0
+    for _ in range(steps):
+        sent += exchanger.exchange(engine)
+        st = engine.step(1)
+        launches += getattr(st, "kernel_launches", 0)
+    return {"halo_bytes_sent": sent, "kernel_launches": launches}

@@ -1,0 +1,84 @@
+"""GPU: the CUDA slab engine (thiim_gpu_create_slab + halo views) decomposes
+a grid bitwise-exactly.  Several slab contexts share cuda:0 and a local
+exchanger copies the halo planes device-to-device between steps (the NCCL
+exchanger moves the same planes between processes), so no kernel ever waits
+on another."""
+import os
+import subprocess
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1510_05218_b200 as P
+from paper_1510_05218_b200 import distributed as D
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def local_exchange(engines):
+    for lo, hi in zip(engines[:-1], engines[1:]):
+        for d, s in zip(hi.halo(D.RECV_DOWN), lo.halo(D.SEND_UP)):
+            d.copy_(s)
+        for d, s in zip(lo.halo(D.RECV_UP), hi.halo(D.SEND_DOWN)):
+            d.copy_(s)
+    torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("nslabs,shape,steps", [(2, (40, 33, 24), 4), (3, (64, 40, 30), 3),
+                                                (4, (31, 29, 17), 2)])
+def test_gpu_slabs_match_single_domain(nslabs, shape, steps):
+    dims = P.GridDims(*shape)
+    host = P.generate_problem(dims, P.GEN_RANDOM, 8)
+    engines = []
+    for r in range(nslabs):
+        z0, z1 = D.slab_bounds(dims.nz, nslabs, r)
+        e = D.SlabGpuEngine(dims, z0, z1, P.GpuOptions(device=0))
+        if r % 2:
+            e.generate(P.GEN_RANDOM, 8)  # device generator == host generator
+        else:
+            e.upload(host)
+        engines.append(e)
+    for _ in range(steps):
+        local_exchange(engines)
+        for e in engines:
+            e.step(1)
+    got = P.allocate_state(dims)
+    for e in engines:
+        e.download_fields(got)
+        e.close()
+    want = P.clone_state(host)
+    O.c_step(shape, want.arrays, steps, threads=8)
+    diff = P.compare_states(got, want)
+    assert diff.bitwise_equal, diff
+
+
+def test_slab_without_exchange_differs():
+    """Fault injection: stale halos must show up as a parity failure."""
+    dims = P.GridDims(24, 20, 16)
+    host = P.generate_problem(dims, P.GEN_RANDOM, 2)
+    engines = [D.SlabGpuEngine(dims, *D.slab_bounds(16, 2, r)) for r in range(2)]
+    for e in engines:
+        e.upload(host)
+        e.step(3)
+    got = P.allocate_state(dims)
+    for e in engines:
+        e.download_fields(got)
+        e.close()
+    want = P.clone_state(host)
+    O.c_step((24, 20, 16), want.arrays, 3)
+    assert not P.compare_states(got, want).bitwise_equal
+
+
+def test_cpp_adapter_binary():
+    """adapter/test_run_gpu.cpp: thiim::run_gpu against the reference engines
+    (run_naive, run_spatial_blocked, run_mwd), bitwise, via compare_states."""
+    exe = os.path.join(ROOT, "build", "test_run_gpu")
+    if not os.path.exists(exe):
+        pytest.skip("build/test_run_gpu not built (needs /root/reference at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 failed" in r.stdout
