@@ -17,9 +17,9 @@ seed 1, zero ghosts.  One bench "step" = one full configs[1] run.
           /root/reference unmodified) on the host cores, bounded sample.
 
 --impl reference runs the reference CPU implementation alone (rank 0 only).
-Multi-rank (torchrun): weak scaling, one 256^3 problem per rank (replicas;
-the z-slab decomposition with halo exchange is exercised by the multi-GPU
-context).
+Multi-rank (torchrun): weak scaling, rank r owns z-slab r (256^3 cells) of a
+256x256x(256N) grid; the halo planes move over NCCL before every iteration
+(paper_1510_05218_b200/distributed.py).
 """
 from __future__ import annotations
 
@@ -174,74 +174,9 @@ def run_reference_arm(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
-def run_native(args, world, rank, local):
-    import paper_1510_05218_b200 as P
-    dist = None
-    if world > 1:
-        import torch
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
-
-    def barrier_max(x: float) -> float:
-        if dist is None:
-            return x
-        import torch
-        t = torch.tensor([x], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
-    dims = P.GridDims(*GRID)
-    engine = {"auto": P.ENGINE_AUTO, "split": P.ENGINE_SPLIT, "fused": P.ENGINE_FUSED}[args.engine]
-    opts = P.GpuOptions(device=local if world > 1 else args.device, engine=engine,
-                        tile_y=args.tile_y, z_chunk=args.z_chunk, min_blocks=args.min_blocks,
-                        variant=args.variant, l2_promotion=args.l2_promotion,
-                        y_fastest=args.y_fastest, full_boxes=args.full_boxes)
-    iters = args.iters
-    lups_step = dims.interior_cells() * iters
-
-    # ---- device-resident throughput (value)
-    eng = P.GpuEngine(dims, opts)
-    eng.generate(P.GEN_RANDOM, SEED)
-    for _ in range(args.warmup):
-        eng.step(iters)
-    if dist is not None:
-        dist.barrier()
-    dev_secs = 0.0
-    launches = 0
-    with Clocks(opts.device) as clk:
-        for _ in range(args.steps):
-            st = eng.step(iters)
-            dev_secs += st.seconds
-            launches += st.kernel_launches
-    engine_ran = st.engine
-    eng.close()
-    dev_secs = barrier_max(dev_secs)
-    value = world * lups_step * args.steps / dev_secs / 1e6
-
-    # ---- end to end through the public API from pinned host memory (e2e)
-    padded = dims.padded_cells() * 16
-    e2e = None
-    if not args.no_e2e:
-        host = P.generate_problem(dims, P.GEN_RANDOM, SEED)
-        for a in host.arrays:
-            P.lib().thiim_gpu_pin_host(a.ctypes.data, a.nbytes)
-        e2e_secs = 0.0
-        for k in range(1 + args.steps):  # 1 untimed warm-up
-            t0 = time.perf_counter()
-            with P.GpuEngine(dims, opts) as e:
-                e.upload(host)
-                e.step(iters)
-                e.download_fields(host)
-            t1 = time.perf_counter()
-            if k >= 1:
-                e2e_secs += t1 - t0
-        for a in host.arrays:
-            P.lib().thiim_gpu_unpin_host(a.ctypes.data)
-        e2e_secs = barrier_max(e2e_secs)
-        e2e = world * lups_step * args.steps / e2e_secs / 1e6
-
-    # ---- roofline of the dominant kernel (one THIIM iteration per launch)
+def _roofline(P, dims, engine_ran, dev_secs, launches):
+    """Roofline of the dominant kernel: one THIIM iteration (fused) or one
+    half-step sweep (split) per launch over the rank's grid."""
     hbm, peak_kind = load_peaks()
     per_launch_s = dev_secs / max(1, launches)
     if engine_ran == P.ENGINE_SPLIT:
@@ -249,47 +184,168 @@ def run_native(args, world, rank, local):
         kname = "k_split_h/k_split_e"
     else:
         bytes_launch = 832.0 * dims.interior_cells()
-        kname = "k_fused<32,8>"
+        kname = "k_fused_tma<16,20>"
     achieved = bytes_launch / per_launch_s / 1e9
-    thiim_balance = P.balance_model(engine_ran)
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
-            tj = json.load(f)
-        traffic = tj.get(kname)
+            traffic = json.load(f).get(kname)
+    balance = P.balance_model(engine_ran)
+    return {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+            "frac": round(achieved / hbm, 4), "traffic": traffic, "kernel": kname,
+            "algorithmic_bytes_per_launch": bytes_launch, "peak_kind": peak_kind,
+            "bytes_per_lup_model": balance,
+            "lup_roofline_mlups": round(hbm * 1e3 / balance, 1)}
 
-    line = {
-        "metric": METRIC, "value": round(value, 2), "unit": "MLUP/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(1e3 * dev_secs / args.steps, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "c128 (f64)", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "grid": list(GRID), "iterations_per_step": iters,
-                   "engine": P.ENGINE_NAMES.get(engine_ran), "parallelism": "dp%d" % world,
-                   "l2": "inputs (%.1f GB state) larger than L2; no flush needed"
-                         % (dims.padded_cells() * (832 if engine_ran != P.ENGINE_SPLIT else 640) / 1e9)},
-        "e2e": {"value": round(e2e, 2) if e2e else None, "unit": "MLUP/s",
-                "h2d_bytes_per_step": 40 * padded, "d2h_bytes_per_step": 12 * padded},
-        "gpu_launches": launches,
-        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
-                     "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": traffic,
-                     "kernel": kname, "algorithmic_bytes_per_launch": bytes_launch,
-                     "peak_kind": peak_kind,
-                     "lup_roofline_mlups": round(hbm * 1e3 / thiim_balance, 1)},
-        "clocks": clk.result,
-    }
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+
+def run_native(args, world, rank, local):
+    import paper_1510_05218_b200 as P
+    engine = {"auto": P.ENGINE_AUTO, "split": P.ENGINE_SPLIT, "fused": P.ENGINE_FUSED}[args.engine]
+    opts = P.GpuOptions(device=local if world > 1 else args.device, engine=engine,
+                        tile_y=args.tile_y, z_chunk=args.z_chunk, min_blocks=args.min_blocks,
+                        variant=args.variant, l2_promotion=args.l2_promotion,
+                        y_fastest=args.y_fastest, full_boxes=args.full_boxes)
+    iters = args.iters
+    if world == 1:
+        line = run_native_single(P, args, opts, iters)
+    else:
+        line = run_native_multi(P, args, opts, iters, world, rank, local)
+    if line is None:
+        return
+    if world == 1 and not args.no_cpu_baseline:
         threads = cpu_threads()
         grid = (256, 256, 64)
         v, kind = reference_sample(grid, 2, threads)
         line["cpu_baseline"] = {"value": round(v, 3), "unit": "MLUP/s", "cores": threads,
                                 "kind": kind,
-                                "sample": "reference run_naive, 256x256x64 x 2 iterations, %d threads"
-                                          % threads}
-    if rank == 0:
-        print(json.dumps(line), flush=True)
-    if dist is not None:
-        dist.destroy_process_group()
+                                "sample": "reference run_naive (oracle/_ref, compiled unmodified), "
+                                          "256x256x64 x 2 iterations, %d threads" % threads}
+    print(json.dumps(line), flush=True)
+
+
+def _line(P, args, world, dims_rank, engine_ran, dev_secs, launches, e2e, clk, extra_cfg):
+    lups_step = dims_rank.interior_cells() * args.iters
+    value = world * lups_step * args.steps / dev_secs / 1e6
+    padded = dims_rank.padded_cells() * 16
+    cfg = {"workload": WORKLOAD, "grid_per_rank": [dims_rank.nx, dims_rank.ny, dims_rank.nz],
+           "iterations_per_step": args.iters, "engine": P.ENGINE_NAMES.get(engine_ran),
+           "parallelism": "z-slab x%d" % world if world > 1 else "single GPU",
+           "l2": "inputs (%.1f GB state per GPU) larger than the 126 MB L2; no flush needed"
+                 % (dims_rank.padded_cells() * (832 if engine_ran != P.ENGINE_SPLIT else 640) / 1e9)}
+    cfg.update(extra_cfg)
+    return {
+        "metric": METRIC, "value": round(value, 2), "unit": "MLUP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * dev_secs / args.steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "c128 (f64)", "data": "synthetic",
+        "config": cfg,
+        "e2e": {"value": round(e2e, 2) if e2e else None, "unit": "MLUP/s",
+                "h2d_bytes_per_step": 40 * padded, "d2h_bytes_per_step": 12 * padded},
+        "gpu_launches": launches,
+        "roofline": _roofline(P, dims_rank, engine_ran, dev_secs, launches),
+        "clocks": clk.result,
+    }
+
+
+def run_native_single(P, args, opts, iters):
+    dims = P.GridDims(*GRID)
+    eng = P.GpuEngine(dims, opts)
+    eng.generate(P.GEN_RANDOM, SEED)
+    for _ in range(args.warmup):
+        eng.step(iters)
+    dev_secs, launches = 0.0, 0
+    with Clocks(opts.device) as clk:
+        for _ in range(args.steps):
+            st = eng.step(iters)  # CUDA events on the launching stream, inside the library
+            dev_secs += st.seconds
+            launches += st.kernel_launches
+    engine_ran = st.engine
+    eng.close()
+
+    # e2e: the public API call a user makes (upload from pinned host memory,
+    # `iters` iterations, download of the 12 fields), every step
+    e2e = None
+    if not args.no_e2e:
+        host = P.generate_problem(dims, P.GEN_RANDOM, SEED)
+        for a in host.arrays:
+            P.lib().thiim_gpu_pin_host(a.ctypes.data, a.nbytes)
+        secs = 0.0
+        for k in range(1 + args.steps):  # 1 untimed warm-up
+            t0 = time.perf_counter()
+            with P.GpuEngine(dims, opts) as e:
+                e.upload(host)
+                e.step(iters)
+                e.download_fields(host)
+            if k >= 1:
+                secs += time.perf_counter() - t0
+        for a in host.arrays:
+            P.lib().thiim_gpu_unpin_host(a.ctypes.data)
+        e2e = dims.interior_cells() * iters * args.steps / secs / 1e6
+    return _line(P, args, 1, dims, engine_ran, dev_secs, launches, e2e, clk, {})
+
+
+def run_native_multi(P, args, opts, iters, world, rank, local):
+    """Weak scaling: rank r owns the 256^3 z-slab r of a 256x256x(256*N) grid;
+    halo planes move over NCCL (torch.distributed) before every iteration."""
+    import torch
+    import torch.distributed as dist
+    from paper_1510_05218_b200 import distributed as D
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl")
+    gdims = P.GridDims(GRID[0], GRID[1], GRID[2] * world)
+    z0, z1 = D.slab_bounds(gdims.nz, world, rank)
+    eng = D.SlabGpuEngine(gdims, z0, z1, opts)
+    eng.generate(P.GEN_RANDOM, SEED)
+    ex = D.HaloExchanger(rank, world)
+    for _ in range(args.warmup):
+        D.run_distributed(eng, iters, ex)
+
+    def timed(fn):
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        out = fn()
+        eng.sync()
+        torch.cuda.synchronize()
+        e1.record()
+        e1.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) * 1e-3], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item()), out
+
+    launches = 0
+    with Clocks(local) as clk:
+        dev_secs, stats = timed(lambda: [D.run_distributed(eng, iters, ex)
+                                         for _ in range(args.steps)])
+    launches = sum(s["kernel_launches"] for s in stats)
+    halo = sum(s["halo_bytes_sent"] for s in stats)
+    eng.close()
+
+    e2e = None
+    if not args.no_e2e:
+        eng = D.SlabGpuEngine(gdims, z0, z1, opts)
+        host = eng.local_host_problem(P.GEN_RANDOM, SEED)
+        for a in host:
+            P.lib().thiim_gpu_pin_host(a.ctypes.data, a.nbytes)
+
+        def e2e_run():
+            for _ in range(args.steps):
+                eng.upload_local(host)
+                D.run_distributed(eng, iters, ex)
+                eng.download_local(host)
+        e2e_run_secs, _ = timed(e2e_run)
+        for a in host:
+            P.lib().thiim_gpu_unpin_host(a.ctypes.data)
+        eng.close()
+        e2e = world * 256 ** 3 * iters * args.steps / e2e_run_secs / 1e6
+    line = _line(P, args, world, P.GridDims(*GRID), P.ENGINE_FUSED, dev_secs, launches, e2e, clk,
+                 {"global_grid": [gdims.nx, gdims.ny, gdims.nz],
+                  "halo_bytes_per_rank_per_step": halo // max(1, args.steps),
+                  "exchange": "torch.distributed NCCL batch_isend_irecv, before every iteration"})
+    dist.destroy_process_group()
+    return line if rank == 0 else None
 
 
 def main():

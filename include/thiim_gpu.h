@@ -187,6 +187,13 @@ typedef struct {
 } thiim_halo_view;
 int thiim_gpu_halo_view(thiim_gpu_ctx* ctx, int which, thiim_halo_view* view);
 
+/* Plane-range variants for rank-local host buffers: the host arrays hold the
+ * global padded planes [p0, ...) only (plane p = global interior z p-1). */
+int thiim_gpu_upload_planes(thiim_gpu_ctx* ctx, const thiim_c128* const arrays[40], int p0);
+int thiim_gpu_download_fields_planes(thiim_gpu_ctx* ctx, thiim_c128* const fields[12], int p0);
+int thiim_generate_host_planes(const thiim_dims* global, int kind, uint64_t seed, int p0, int p1,
+                               thiim_c128* const arrays[40]);
+
 /* Blocks until all work queued on the context's streams has finished. */
 int thiim_gpu_sync(thiim_gpu_ctx* ctx);
 

@@ -570,19 +570,25 @@ void thiim_gpu_destroy(thiim_gpu_ctx* ctx) {
   delete ctx;
 }
 
-static int upload_arrays(thiim_gpu_ctx* ctx, const thiim_c128* const* arrays, int first, int count) {
+static int upload_arrays(thiim_gpu_ctx* ctx, const thiim_c128* const* arrays, int first, int count,
+                         int p0 = 0) {
   const long long pxy = ctx->pxy();
   for (auto& sl : ctx->slabs) {
     CK(cudaSetDevice(sl.device));
-    // planes [z0, z1+2) of the global padded grid == local planes [0, nz+2)
-    const size_t off = (size_t)sl.z0 * (size_t)pxy;
+    // planes [z0, z1+2) of the global padded grid == local planes [0, nz+2);
+    // the host arrays start at global padded plane p0
+    if (sl.z0 < p0) return fail(THIIM_ERR_CONFIG, "host planes start above the slab");
+    const size_t off = (size_t)(sl.z0 - p0) * (size_t)pxy;
     const size_t bytes = (size_t)(sl.g.nz + 2) * (size_t)pxy * sizeof(double2);
     for (int a = first; a < first + count; ++a) {
       if (!arrays[a - first]) return fail(THIIM_ERR_CONFIG, "null host array");
       const thiim_c128* src = arrays[a - first] + off;
       if (a < 12) {
-        for (int set = 0; set < sl.nfield_sets; ++set)
-          CK(cudaMemcpyAsync(sl.field(set, a), src, bytes, cudaMemcpyHostToDevice, sl.stream));
+        // one PCIe transfer; the ping-pong set gets a device-side copy
+        CK(cudaMemcpyAsync(sl.field(0, a), src, bytes, cudaMemcpyHostToDevice, sl.stream));
+        for (int set = 1; set < sl.nfield_sets; ++set)
+          CK(cudaMemcpyAsync(sl.field(set, a), sl.field(0, a), bytes, cudaMemcpyDeviceToDevice,
+                             sl.stream));
       } else {
         CK(cudaMemcpyAsync(sl.coeff(a), src, bytes, cudaMemcpyHostToDevice, sl.stream));
       }
@@ -697,14 +703,15 @@ int thiim_gpu_step(thiim_gpu_ctx* ctx, int steps, thiim_gpu_stats* stats) {
   return THIIM_OK;
 }
 
-static int download_impl(thiim_gpu_ctx* ctx, int a, thiim_c128* dst) {
+static int download_impl(thiim_gpu_ctx* ctx, int a, thiim_c128* dst, int hp0 = 0) {
   const long long pxy = ctx->pxy();
   for (auto& sl : ctx->slabs) {
     CK(cudaSetDevice(sl.device));
     // interior planes, plus the global ghost plane(s) this slab borders
     const int p0 = sl.z0 == 0 ? 0 : 1;
     const int p1 = sl.z1 == ctx->dims.nz ? sl.g.nz + 2 : sl.g.nz + 1;
-    const size_t off_host = (size_t)(sl.z0 + p0) * (size_t)pxy;
+    if (sl.z0 + p0 < hp0) return fail(THIIM_ERR_CONFIG, "host planes start above the slab");
+    const size_t off_host = (size_t)(sl.z0 + p0 - hp0) * (size_t)pxy;
     CK(cudaMemcpyAsync(dst + off_host, sl.array(a) + (size_t)p0 * pxy,
                        (size_t)(p1 - p0) * (size_t)pxy * sizeof(double2), cudaMemcpyDeviceToHost,
                        sl.stream));
@@ -722,6 +729,29 @@ int thiim_gpu_download_fields(thiim_gpu_ctx* ctx, thiim_c128* const fields[12]) 
   for (int k = 0; k < 12; ++k) {
     if (!fields[k]) return fail(THIIM_ERR_CONFIG, "null host array");
     int r = download_impl(ctx, k, fields[k]);
+    if (r) return r;
+  }
+  return THIIM_OK;
+}
+
+int thiim_gpu_upload_planes(thiim_gpu_ctx* ctx, const thiim_c128* const arrays[40], int p0) {
+  g_err.clear();
+  if (!ctx || !arrays) return fail(THIIM_ERR_CONFIG, "null argument");
+  int r;
+  if ((r = upload_arrays(ctx, arrays, 0, 12, p0))) return r;
+  if ((r = upload_arrays(ctx, arrays + 12, 12, 12, p0))) return r;
+  if ((r = upload_arrays(ctx, arrays + 24, 24, 12, p0))) return r;
+  if ((r = upload_arrays(ctx, arrays + 36, 36, 4, p0))) return r;
+  ctx->loaded = true;
+  return THIIM_OK;
+}
+
+int thiim_gpu_download_fields_planes(thiim_gpu_ctx* ctx, thiim_c128* const fields[12], int p0) {
+  g_err.clear();
+  if (!ctx || !fields) return fail(THIIM_ERR_CONFIG, "null argument");
+  for (int k = 0; k < 12; ++k) {
+    if (!fields[k]) return fail(THIIM_ERR_CONFIG, "null host array");
+    int r = download_impl(ctx, k, fields[k], p0);
     if (r) return r;
   }
   return THIIM_OK;
@@ -780,15 +810,17 @@ int thiim_gpu_compare_fields(thiim_gpu_ctx* ctx, const thiim_c128* const ref[12]
   return THIIM_OK;
 }
 
-int thiim_generate_host(const thiim_dims* dims, int kind, uint64_t seed,
-                        thiim_c128* const arrays[40]) {
+int thiim_generate_host_planes(const thiim_dims* dims, int kind, uint64_t seed, int p0, int p1,
+                               thiim_c128* const arrays[40]) {
   g_err.clear();
   if (!valid_dims(dims)) return fail(THIIM_ERR_SETUP, "invalid grid dims");
   if (!arrays) return fail(THIIM_ERR_CONFIG, "null arrays");
   if (kind != THIIM_GEN_RANDOM && kind != THIIM_GEN_LAYERED)
     return fail(THIIM_ERR_CONFIG, "unknown generator kind");
+  if (p0 < 0 || p1 > dims->nz + 2 || p0 >= p1) return fail(THIIM_ERR_CONFIG, "bad plane range");
   const int nx = dims->nx, ny = dims->ny, nz = dims->nz;
-  const long long px = nx + 2, pxy = px * (ny + 2), n = pxy * (nz + 2);
+  const long long px = nx + 2, pxy = px * (ny + 2);
+  const long long n = pxy * (long long)(p1 - p0), base = pxy * (long long)p0;
   double2 table[28 * 6];
   for (int a = 12; a < 40; ++a)
     for (int L = 0; L < 6; ++L) table[(a - 12) * 6 + L] = gen_disk(gen_key(seed, a), (uint64_t)L);
@@ -797,7 +829,8 @@ int thiim_generate_host(const thiim_dims* dims, int kind, uint64_t seed,
   for (int a = 0; a < 40; ++a)
     if (!arrays[a]) return fail(THIIM_ERR_CONFIG, "null host array");
 #pragma omp parallel for schedule(static)
-  for (long long p = 0; p < n; ++p) {
+  for (long long q = 0; q < n; ++q) {
+    const long long p = base + q;  // global padded index = generator counter
     const int zp = (int)(p / pxy);
     const long long r = p - (long long)zp * pxy;
     const int yp = (int)(r / px), xp = (int)(r - (long long)yp * px);
@@ -814,11 +847,20 @@ int thiim_generate_host(const thiim_dims* dims, int kind, uint64_t seed,
         else
           v = gen_disk(keys[a], (uint64_t)p);
       }
-      arrays[a][p].re = v.x;
-      arrays[a][p].im = v.y;
+      arrays[a][q].re = v.x;
+      arrays[a][q].im = v.y;
     }
   }
   return THIIM_OK;
+}
+
+int thiim_generate_host(const thiim_dims* dims, int kind, uint64_t seed,
+                        thiim_c128* const arrays[40]) {
+  if (!valid_dims(dims)) {
+    g_err = "invalid grid dims";
+    return THIIM_ERR_SETUP;
+  }
+  return thiim_generate_host_planes(dims, kind, seed, 0, dims->nz + 2, arrays);
 }
 
 int thiim_gpu_pin_host(void* ptr, size_t bytes) {

@@ -83,6 +83,21 @@ class SlabGpuEngine:
     def download_fields(self, s: ProblemState):
         _check(lib().thiim_gpu_download_fields(self._ctx, _ptrs(s.arrays[0:12])))
 
+    # rank-local host buffers: global padded planes [z0, z1+2)
+    def local_host_problem(self, kind: int = GEN_RANDOM, seed: int = 1) -> List[np.ndarray]:
+        pxy = (self.dims.nx + 2) * (self.dims.ny + 2)
+        arrays = [np.zeros((self.z1 - self.z0 + 2) * pxy, dtype=np.complex128) for _ in range(40)]
+        d = _Dims(self.dims.nx, self.dims.ny, self.dims.nz, self.dims.ghost)
+        _check(lib().thiim_generate_host_planes(ctypes.byref(d), kind, seed, self.z0, self.z1 + 2,
+                                                _ptrs(arrays)))
+        return arrays
+
+    def upload_local(self, arrays: List[np.ndarray]):
+        _check(lib().thiim_gpu_upload_planes(self._ctx, _ptrs(arrays), self.z0))
+
+    def download_local(self, arrays: List[np.ndarray]):
+        _check(lib().thiim_gpu_download_fields_planes(self._ctx, _ptrs(arrays[0:12]), self.z0))
+
     def step(self, steps: int = 1):
         st = _Stats()
         _check(lib().thiim_gpu_step(self._ctx, steps, ctypes.byref(st)))
