@@ -182,9 +182,13 @@ def _roofline(P, dims, engine_ran, dev_secs, launches):
     if engine_ran == P.ENGINE_SPLIT:
         bytes_launch = 512.0 * dims.interior_cells()  # one half-step sweep: 32 x 16 B per cell
         kname = "k_split_h/k_split_e"
+    elif engine_ran == P.ENGINE_TBLOCK:
+        # one launch = two THIIM iterations in one HBM pass: 832 B per cell = 416 B/LUP
+        bytes_launch = 832.0 * dims.interior_cells()
+        kname = "k_tblock2<15,6>"
     else:
         bytes_launch = 832.0 * dims.interior_cells()
-        kname = "k_fused_tma<16,20>"
+        kname = "k_fused_tma<15,6>"
     achieved = bytes_launch / per_launch_s / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
@@ -201,7 +205,8 @@ def _roofline(P, dims, engine_ran, dev_secs, launches):
 
 def run_native(args, world, rank, local):
     import paper_1510_05218_b200 as P
-    engine = {"auto": P.ENGINE_AUTO, "split": P.ENGINE_SPLIT, "fused": P.ENGINE_FUSED}[args.engine]
+    engine = {"auto": P.ENGINE_AUTO, "split": P.ENGINE_SPLIT, "fused": P.ENGINE_FUSED,
+              "tblock": P.ENGINE_TBLOCK}[args.engine]
     opts = P.GpuOptions(device=local if world > 1 else args.device, engine=engine,
                         tile_y=args.tile_y, z_chunk=args.z_chunk, min_blocks=args.min_blocks,
                         variant=args.variant, l2_promotion=args.l2_promotion,
@@ -354,7 +359,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
-    ap.add_argument("--engine", default="auto", choices=["auto", "split", "fused"])
+    ap.add_argument("--engine", default="auto", choices=["auto", "split", "fused", "tblock"])
     ap.add_argument("--iters", type=int, default=ITERS)
     ap.add_argument("--device", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -369,6 +369,7 @@ class GpuOptions:
     l2_promotion: int = 0  # TMA L2 promotion (reserved[2]): 0 none, 1 64B, 2 128B, 3 256B
     y_fastest: int = 0   # CTA order (reserved[3]): 0 x-tiles fastest (default), 1 y-tiles fastest
     full_boxes: int = 0  # experiment (reserved[4]): fetch the full 32xBY box for every array
+    debug: int = 0       # reserved[5]: TBLOCK debug bits (1 heavy fences, 2 scratch per CTA)
 
     def _c(self) -> _Opts:
         o = _Opts()
@@ -380,6 +381,7 @@ class GpuOptions:
         o.reserved[2] = self.l2_promotion
         o.reserved[3] = self.y_fastest
         o.reserved[4] = self.full_boxes
+        o.reserved[5] = self.debug
         return o
 
 

@@ -97,3 +97,36 @@ __device__ __forceinline__ void tma_prefetch_desc(const void* tmap) {
 }
 
 }  // namespace thiim_gpu
+
+namespace thiim_gpu {
+
+// TMA loads with an L2 eviction-priority policy (createpolicy)
+__device__ __forceinline__ void tma_load_4d_hint(void* dst, const void* tmap, int c0, int c1,
+                                                 int c2, int c3, uint64_t* b, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      ".L2::cache_hint [%0], [%1, {%2, %3, %4, %5}], [%6], %7;" ::"r"(smem_u32(dst)),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(b)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_hint(void* dst, const void* tmap, int c0, int c1,
+                                                 int c2, uint64_t* b, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      ".L2::cache_hint [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(b)), "l"(pol)
+      : "memory");
+}
+// 16-B global store with an L2 eviction-priority policy
+__device__ __forceinline__ void st_hint(double2* p, double2 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y),
+               "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+}  // namespace thiim_gpu

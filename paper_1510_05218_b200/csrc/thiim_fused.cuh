@@ -27,7 +27,7 @@
 namespace thiim_gpu {
 
 template <int BX, int BY>
-struct FusedSmem {
+struct RegFusedSmem {
   double2 sE[3][BY][BX];  // E_old sums (x, y, z physical components) at plane z
   double2 sH[3][BY][BX];  // H_new sums at plane z
 };
@@ -36,7 +36,7 @@ template <int BX, int BY, int MINB>
 __global__ void __launch_bounds__(BX* BY, MINB)
     k_fused(Grid g, Arrays A, int zc) {
   constexpr int TX = BX - 2, TY = BY - 2;
-  __shared__ FusedSmem<BX, BY> sm;
+  __shared__ RegFusedSmem<BX, BY> sm;
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int x = blockIdx.x * TX - 1 + tx;
   const int y = blockIdx.y * TY - 1 + ty;

@@ -25,6 +25,7 @@
 #include "thiim_fused.cuh"
 #include "thiim_fused_tma.cuh"
 #include "thiim_split.cuh"
+#include "thiim_tblock.cuh"
 
 using namespace thiim_gpu;
 
@@ -58,8 +59,13 @@ struct Slab {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   // 4-D tensor maps over the allocation {x (doubles), y, plane, array slot},
   // one set of box shapes per tile height (8 / 16 rows), built lazily
-  TmaMaps maps[2];
-  bool maps_ok[2] = {false, false};
+  TmaMaps maps[3];  // tile heights 8, 16, 15
+  bool maps_ok[3] = {false, false, false};
+  // TBLOCK: per-SM scratch ring (3 planes x 12 fields x tile) and its tensor map
+  double2* scratch = nullptr;
+  size_t scratch_bytes = 0;
+  CUtensorMap smap;
+  int smap_by = 0;
 
   double2* field(int set, int k) const { return buf + (size_t)(set * 12 + k) * stride; }
   double2* coeff(int a) const {  // a in 12..39
@@ -306,8 +312,11 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
   return fn;
 }
 
+int map_index(int by) { return by == 16 ? 1 : by == 15 ? 2 : 0; }
+// (tile heights 8, 16 and 15 each get their own set of box shapes)
+
 int ensure_tmap(Slab& s, int by, int promo) {
-  const int w = by == 16 ? 1 : 0;
+  const int w = map_index(by);
   if (s.maps_ok[w]) return THIIM_OK;
   const CUtensorMapL2promotion pr[4] = {CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_64B,
                                         CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
@@ -333,22 +342,20 @@ int ensure_tmap(Slab& s, int by, int promo) {
   return THIIM_OK;
 }
 
-template <int BY, int NBUF>
+template <int BY, int NG>
 int launch_fused_tma_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
   const Arrays A = s.arrays(s.cur, s.cur ^ 1);
   const int cur = s.cur, nf = s.nfield_sets;
-  SeqSlots S = make_seq([&](int k) { return cur * 12 + k; },
-                        [&](int a) { return nf * 12 + (a - 12); });
-  if (ctx->opts.reserved[4] == 1)  // experiment: one full box shape for every array
-    for (int k = 0; k < 40; ++k) S.box[k] = BOX_A;
+  GroupSeq S;
+  seq_plane(S, [&](int k) { return cur * 12 + k; }, [&](int a) { return nf * 12 + (a - 12); });
   // reserved[2]: L2 promotion of the TMA fills (0 none, 1 64B, 2 128B, 3 256B)
   int r = ensure_tmap(s, BY, ctx->opts.reserved[2]);
   if (r) return r;
   constexpr int TX = 30, TY = BY - 2;
-  const size_t smem = sizeof(TmaSmem<BY, NBUF>);
+  const size_t smem = sizeof(FusedSmem<BY, NG>);
   static bool attr_set = false;  // per process; the attribute is per function
   if (!attr_set) {
-    CK(cudaFuncSetAttribute(k_fused_tma<BY, NBUF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CK(cudaFuncSetAttribute(k_fused_tma<BY, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)smem));
     attr_set = true;
   }
@@ -358,12 +365,111 @@ int launch_fused_tma_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
   const int tiles_x = (s.g.nx + TX - 1) / TX;
   const dim3 grid(tiles_x * tiles_y, 1, (s.g.nz + zc - 1) / zc);
   const dim3 block(32, BY + 1);
-  k_fused_tma<BY, NBUF><<<grid, block, smem, s.stream>>>(s.g, A, s.maps[BY == 16 ? 1 : 0], S, zc,
-                                                         tiles_y, tiles_x, ctx->opts.reserved[3] == 0);
+  k_fused_tma<BY, NG><<<grid, block, smem, s.stream>>>(s.g, A, s.maps[map_index(BY)], S, zc,
+                                                       tiles_y, tiles_x, ctx->opts.reserved[3] == 0);
   CK(cudaGetLastError());
   s.cur ^= 1;
   ++*launches;
   return THIIM_OK;
+}
+
+// ---- TBLOCK (two steps per launch)
+int smid_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    n = std::max(256, 2 * sms);  // %smid < %nsmid <= this bound on sm_100
+  }
+  return n;
+}
+
+template <int BY>
+int ensure_scratch(Slab& s) {
+  const size_t tile = (size_t)BY * 32;
+  const int nsm = smid_count();
+  const size_t bytes = (size_t)nsm * 24 * tile * sizeof(double2);  // 2 planes x 12 fields
+  if (s.scratch && s.scratch_bytes >= bytes && s.smap_by == BY) return THIIM_OK;
+  if (s.scratch) cudaFree(s.scratch);
+  s.scratch = nullptr;
+  CK(cudaMalloc(&s.scratch, bytes));
+  CK(cudaMemset(s.scratch, 0, bytes));
+  s.scratch_bytes = bytes;
+  auto fn = get_encode_fn();
+  if (!fn) return fail(THIIM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[3] = {64, (cuuint64_t)BY, (cuuint64_t)nsm * 24};
+  const cuuint64_t strides[2] = {32 * 16, (cuuint64_t)BY * 32 * 16};
+  const cuuint32_t box[3] = {64, (cuuint32_t)BY, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(&s.smap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, s.scratch, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(THIIM_ERR_CUDA, "scratch tensor map failed");
+  s.smap_by = BY;
+  return THIIM_OK;
+}
+
+template <int BY, int NG>
+int launch_tblock2_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
+  if (s.g.halo_lo || s.z1 < ctx->dims.nz)
+    return fail(THIIM_ERR_CONFIG, "TBLOCK needs a whole-z context (no halo slabs yet)");
+  const Arrays A = s.arrays(s.cur, s.cur ^ 1);
+  const int cur = s.cur, nf = s.nfield_sets;
+  auto fslot = [&](int k) { return cur * 12 + k; };
+  auto cslot = [&](int a) { return nf * 12 + (a - 12); };
+  GroupSeq S1, S2;
+  seq_plane(S1, fslot, cslot);
+  seq_level2(S2, cslot);
+  int r = ensure_tmap(s, BY, ctx->opts.reserved[2]);
+  if (r) return r;
+  if ((r = ensure_scratch<BY>(s))) return r;
+  const size_t smem = sizeof(TbSmem<BY, NG>);
+  static bool attr_set = false;
+  if (!attr_set) {
+    CK(cudaFuncSetAttribute(k_tblock2<BY, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)smem));
+    attr_set = true;
+  }
+  constexpr int TX2 = 28, TY2 = BY - 4;
+  const int tiles_x = (s.g.nx + TX2 - 1) / TX2, tiles_y = (s.g.ny + TY2 - 1) / TY2;
+  // z-chunks: each CTA re-does ~2 planes of level-1/level-2 work at its start
+  const long long cols = (long long)tiles_x * tiles_y;
+  int zc = ctx->opts.z_chunk;
+  if (zc <= 0) {
+    const long long slots = sm_count(s.device);
+    double best = 1e300;
+    int best_c = 1;
+    for (int c = 1; c <= std::max(1, s.g.nz / 8); ++c) {
+      const int planes = (s.g.nz + c - 1) / c;
+      const long long waves = (cols * c + slots - 1) / slots;
+      const double t = (double)waves * (planes + 2.0);
+      if (t < best - 1e-9) {
+        best = t;
+        best_c = c;
+      }
+    }
+    zc = (s.g.nz + best_c - 1) / best_c;
+  }
+  TbParams P;
+  P.zc = zc;
+  P.tiles_x = tiles_x;
+  for (int k = 0; k < 12; ++k) P.field_in[k] = fslot(k);
+  P.scratch = s.scratch;
+  const dim3 grid(tiles_x * tiles_y, 1, (s.g.nz + zc - 1) / zc);
+  const dim3 block(32, BY + 1);
+  k_tblock2<BY, NG><<<grid, block, smem, s.stream>>>(s.g, A, s.maps[map_index(BY)], s.smap, S1,
+                                                     S2, P);
+  CK(cudaGetLastError());
+  s.cur ^= 1;
+  ++*launches;
+  return THIIM_OK;
+}
+
+int launch_tblock2(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
+  CK(cudaSetDevice(s.device));
+  return launch_tblock2_t<15, 6>(ctx, s, launches);
 }
 
 int launch_fused(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
@@ -379,8 +485,10 @@ int launch_fused(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
     if (minb == 1) return launch_fused_t<32, 8, 1>(ctx, s, launches);
     return launch_fused_t<32, 8, 2>(ctx, s, launches);
   }
-  if (ctx->opts.tile_y == 8) return launch_fused_tma_t<8, 40>(ctx, s, launches);
-  return launch_fused_tma_t<16, 20>(ctx, s, launches);
+  if (ctx->opts.tile_y == 8) return launch_fused_tma_t<8, 12>(ctx, s, launches);
+  if (ctx->opts.tile_y == 16) return launch_fused_tma_t<16, 5>(ctx, s, launches);
+  if (ctx->opts.tile_y == 116) return launch_fused_tma_t<16, 2>(ctx, s, launches);  // stress: tiny ring
+  return launch_fused_tma_t<15, 6>(ctx, s, launches);
 }
 
 bool valid_dims(const thiim_dims* d) {
@@ -408,7 +516,7 @@ void thiim_gpu_default_opts(thiim_gpu_opts* o) {
 double thiim_gpu_balance_model(int engine, int time_block) {
   switch (engine) {
     case THIIM_ENGINE_SPLIT: return 1024.0;
-    case THIIM_ENGINE_TBLOCK: return 832.0 / std::max(1, time_block);
+    case THIIM_ENGINE_TBLOCK: return 832.0 / (time_block > 0 ? time_block : 2);
     default: return 832.0;
   }
 }
@@ -430,8 +538,10 @@ static int create_impl(const thiim_dims* dims, const thiim_gpu_opts* opts,
   if (o.n_gpus < 1 || o.n_gpus > 8) return fail(THIIM_ERR_CONFIG, "n_gpus must be in 1..8");
   if (o.engine < THIIM_ENGINE_AUTO || o.engine > THIIM_ENGINE_TBLOCK)
     return fail(THIIM_ERR_CONFIG, "unknown engine");
-  if (o.engine == THIIM_ENGINE_TBLOCK)
-    return fail(THIIM_ERR_CONFIG, "engine TBLOCK is not built yet");
+  if (o.engine == THIIM_ENGINE_TBLOCK && o.time_block != 0 && o.time_block != 2)
+    return fail(THIIM_ERR_CONFIG, "engine TBLOCK supports time_block 2");
+  if (o.engine == THIIM_ENGINE_TBLOCK && ranges.size() != 1)
+    return fail(THIIM_ERR_CONFIG, "engine TBLOCK runs on one GPU (halo slabs need 2-plane halos)");
   for (const auto& r : ranges)
     if (r.first < 0 || r.second > dims->nz || r.second - r.first < 4)
       return fail(THIIM_ERR_CONFIG, "each z-slab needs at least 4 planes inside the grid");
@@ -563,6 +673,7 @@ void thiim_gpu_destroy(thiim_gpu_ctx* ctx) {
     cudaSetDevice(sl.device);
     if (sl.stream) cudaStreamSynchronize(sl.stream);
     if (sl.buf) cudaFree(sl.buf);
+    if (sl.scratch) cudaFree(sl.scratch);
     if (sl.ev0) cudaEventDestroy(sl.ev0);
     if (sl.ev1) cudaEventDestroy(sl.ev1);
     if (sl.stream) cudaStreamDestroy(sl.stream);
@@ -665,7 +776,13 @@ int thiim_gpu_step(thiim_gpu_ctx* ctx, int steps, thiim_gpu_stats* stats) {
     CK(cudaEventRecord(sl.ev0, sl.stream));
   }
   int r;
-  for (int n = 0; n < steps; ++n) {
+  int n = 0;
+  if (ctx->engine == THIIM_ENGINE_TBLOCK) {
+    for (; n + 2 <= steps; n += 2)
+      for (auto& sl : ctx->slabs)
+        if ((r = launch_tblock2(ctx, sl, &launches))) return r;
+  }
+  for (; n < steps; ++n) {
     if (ctx->engine == THIIM_ENGINE_SPLIT) {
       if (multi && (r = exchange(ctx, 0))) return r;
       for (auto& sl : ctx->slabs)

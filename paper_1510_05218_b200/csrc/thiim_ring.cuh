@@ -1,0 +1,118 @@
+// thiim_ring.cuh -- grouped TMA ring shared by the fused and temporally
+// blocked sweeps.
+//
+// The ring holds NG group slots of G boxes each (a box = one array-plane of the
+// 32 x BY thread tile, up to BY*32 double2).  One producer lane fills a group
+// with up to G TMA loads that all complete on the group's `full` mbarrier
+// (expect_tx = the group's total bytes); every consumer warp waits on it once,
+// reads its elements of all boxes, and releases the group once (one proxy
+// fence + one arrive on `empty`).  Grouping the array-planes a component needs
+// (F, t, c, src) cuts the per-box wait/fence/arrive latency chain that
+// otherwise bounds the sweep (measured: 80 sequential takes per plane pair).
+//
+// Cross-proxy WAR: consumers read slots with generic-proxy LDS and the
+// producer overwrites them with async-proxy TMA writes; mbarrier release /
+// acquire alone does not order the two proxies, so every consumer thread
+// issues fence.proxy.async.shared::cta before its warp releases the group
+// (without it, reads of a slot raced its refill whenever the ring ran full).
+#pragma once
+
+#include <cuda.h>
+
+#include "thiim_async.cuh"
+#include "thiim_common.cuh"
+
+namespace thiim_gpu {
+
+// Box shapes within the 32 x BY thread tile (own cells = [1,30] x [1,BY-2] for a
+// one-level sweep):
+//   BOX_A  32 x BY     everything (E_old: own, both rings, +x/+y neighbours)
+//   BOX_B  31 x (BY-1) own + ring_x + ring_y        (Hzx, Hzy operands)
+//   BOX_BX 31 x (BY-2) own + ring_x (x0-1 column)   (Hyx, Hyz operands)
+//   BOX_BY 30 x (BY-1) own + ring_y (y0-1 row)      (Hxy, Hxz operands)
+//   BOX_C  30 x (BY-2) own only                     (E-phase coefficients)
+// Fetching only what each group needs keeps the tile overlap (re-read by the
+// neighbouring CTA) at ~7% instead of ~22%.
+enum : int { BOX_A = 0, BOX_B = 1, BOX_BX = 2, BOX_BY = 3, BOX_C = 4, NBOX = 5 };
+
+template <int BY>
+struct BoxGeom {
+  __host__ __device__ static constexpr int x0(int b) { return b >= BOX_BY ? 1 : 0; }
+  __host__ __device__ static constexpr int y0(int b) { return (b == BOX_BX || b == BOX_C) ? 1 : 0; }
+  __host__ __device__ static constexpr int w(int b) { return b == BOX_A ? 32 : b <= BOX_BX ? 31 : 30; }
+  __host__ __device__ static constexpr int h(int b) {
+    return b == BOX_A ? BY : (b == BOX_B || b == BOX_BY) ? BY - 1 : BY - 2;
+  }
+  __host__ __device__ static constexpr int bytes(int b) { return w(b) * h(b) * 16; }
+};
+
+struct TmaMaps {
+  CUtensorMap m[NBOX];
+};
+
+// One element of a producer sequence.
+struct SeqElem {
+  short slot;   // array slot of the allocation (4th map coordinate), or scratch component
+  char box;     // BOX_* (main) -- scratch boxes are always the full tile
+  char src;     // 0 main at plane z, 1 main at plane z+1, 2 level-1 field of plane r
+  char coef;    // 1 if a coefficient array (L2 policy)
+  char pad[3];
+};
+
+// A producer sequence: groups of up to 4 elements.
+struct GroupSeq {
+  int ngroups;
+  int nelem;
+  unsigned char gsize[24];
+  SeqElem e[96];
+};
+
+template <int BY, int NG>
+struct Ring {
+  static constexpr int G = 4;
+  double2 buf[NG][G][BY * 32];
+  uint64_t full[NG];
+  uint64_t empty[NG];
+};
+
+// consumer-side cursor
+struct RingCursor {
+  int g = 0;
+  uint32_t ph = 0;
+};
+
+template <int BY, int NG>
+__device__ __forceinline__ void ring_init(Ring<BY, NG>& r, int consumer_warps) {
+  for (int k = 0; k < NG; ++k) {
+    mbar_init(&r.full[k], 1);
+    mbar_init(&r.empty[k], consumer_warps);
+  }
+}
+
+template <int BY, int NG>
+__device__ __forceinline__ void ring_wait(Ring<BY, NG>& r, const RingCursor& c) {
+  mbar_wait(&r.full[c.g], c.ph);
+}
+
+// element k (box kind b) of the current group, for thread (tx, ty)
+template <int BY, int NG>
+__device__ __forceinline__ double2 ring_read(Ring<BY, NG>& r, const RingCursor& c, int k, int b,
+                                             int tx, int ty) {
+  using Gm = BoxGeom<BY>;
+  const int cx = tx - Gm::x0(b), cy = ty - Gm::y0(b);
+  if (cx >= 0 && cx < Gm::w(b) && cy >= 0 && cy < Gm::h(b)) return r.buf[c.g][k][cy * Gm::w(b) + cx];
+  return make_double2(0.0, 0.0);
+}
+
+template <int BY, int NG>
+__device__ __forceinline__ void ring_release(Ring<BY, NG>& r, RingCursor& c, int tx) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncwarp();
+  if (tx == 0) mbar_arrive(&r.empty[c.g]);
+  if (++c.g == NG) {
+    c.g = 0;
+    c.ph ^= 1;
+  }
+}
+
+}  // namespace thiim_gpu

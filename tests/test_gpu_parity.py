@@ -16,7 +16,7 @@ from oracle import oracle as O
 
 pytestmark = pytest.mark.gpu
 
-ENGINES = [P.ENGINE_SPLIT, P.ENGINE_FUSED]
+ENGINES = [P.ENGINE_SPLIT, P.ENGINE_FUSED, P.ENGINE_TBLOCK]
 REL_L2_TOL = 1e-12  # BASELINE.json north_star
 
 
@@ -60,7 +60,7 @@ SHAPES = [
 def test_engine_matches_oracle(engine, shape):
     dims = P.GridDims(*shape)
     s = P.generate_problem(dims, P.GEN_RANDOM, seed=11)
-    for steps in (1, 3):
+    for steps in (1, 2, 5):
         assert_same(gpu_run(s, steps, engine), oracle_run(s, steps))
 
 
@@ -92,6 +92,22 @@ def test_config0_full_length_vs_reference():
         O.c_step((64, 64, 64), want.arrays, 50, threads=threads())
     for engine in ENGINES:
         assert_same(gpu_run(s, 50, engine), want)
+
+
+def test_tblock_full_config1_grid_vs_fused():
+    """TBLOCK (2 steps per HBM pass) == fused, bitwise, on the 256^3 grid."""
+    d = P.GridDims(256, 256, 256)
+    with P.GpuEngine(d, P.GpuOptions(engine=P.ENGINE_FUSED)) as a:
+        a.generate(P.GEN_RANDOM, 1)
+        a.step(6)
+        ref = P.allocate_state(d)
+        a.download_fields(ref)
+    with P.GpuEngine(d, P.GpuOptions(engine=P.ENGINE_TBLOCK)) as b:
+        b.generate(P.GEN_RANDOM, 1)
+        st = b.step(6)
+        assert st.kernel_launches == 3
+        diff = b.compare_fields(ref)
+    assert diff.bitwise_equal, diff
 
 
 # ---------------------------------------------------------------- generator
