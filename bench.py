@@ -35,11 +35,20 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-GRID = (256, 256, 256)
-ITERS = 100
 SEED = 1
-WORKLOAD = ("configs[1]: 256x256x256 grid, 100 THIIM iterations (H then E half-step) per "
-            "bench step, complex128, fields U[-1,1], coeffs |c|<=0.45, seed 1, zero halo")
+# BASELINE.json configs; the driver's default bench line is configs[1]
+CONFIGS = {
+    "c0": ((64, 64, 64), 50, 0, "configs[0]: 64^3 grid, 50 THIIM iterations"),
+    "c1": ((256, 256, 256), 100, 0, "configs[1]: 256x256x256 grid, 100 THIIM iterations"),
+    "c2": ((512, 512, 512), 200, 0, "configs[2]: 512^3 grid, 200 THIIM iterations"),
+    "c3": ((1024, 1024, 256), 200, 1, "configs[3]: layered thin-film 1024x1024x256, 200 THIIM "
+                                      "iterations, 6 z-layers, +-8-cell seeded interfaces"),
+    "c4": ((1024, 1024, 128), 100, 0, "configs[4]: weak-scaling slab 1024x1024x128 per GPU, 100 "
+                                      "THIIM iterations"),
+}
+GRID, ITERS, KIND, _DESC = CONFIGS["c1"]
+WORKLOAD = (_DESC + " (H then E half-step) per bench step, complex128, fields U[-1,1], "
+            "coeffs |c|<=0.45, seed 1, zero halo")
 METRIC = "MLUP/s (double-complex E+H update) at N B200; % of HBM roofline"
 
 
@@ -233,7 +242,8 @@ def _line(P, args, world, dims_rank, engine_ran, dev_secs, launches, e2e, clk, e
     lups_step = dims_rank.interior_cells() * args.iters
     value = world * lups_step * args.steps / dev_secs / 1e6
     padded = dims_rank.padded_cells() * 16
-    cfg = {"workload": WORKLOAD, "grid_per_rank": [dims_rank.nx, dims_rank.ny, dims_rank.nz],
+    cfg = {"workload": WORKLOAD, "config": args.config,
+           "grid_per_rank": [dims_rank.nx, dims_rank.ny, dims_rank.nz],
            "iterations_per_step": args.iters, "engine": P.ENGINE_NAMES.get(engine_ran),
            "parallelism": "z-slab x%d" % world if world > 1 else "single GPU",
            "l2": "inputs (%.1f GB state per GPU) larger than the 126 MB L2; no flush needed"
@@ -256,7 +266,7 @@ def _line(P, args, world, dims_rank, engine_ran, dev_secs, launches, e2e, clk, e
 def run_native_single(P, args, opts, iters):
     dims = P.GridDims(*GRID)
     eng = P.GpuEngine(dims, opts)
-    eng.generate(P.GEN_RANDOM, SEED)
+    eng.generate(KIND, SEED)
     for _ in range(args.warmup):
         eng.step(iters)
     dev_secs, launches = 0.0, 0
@@ -272,7 +282,7 @@ def run_native_single(P, args, opts, iters):
     # `iters` iterations, download of the 12 fields), every step
     e2e = None
     if not args.no_e2e:
-        host = P.generate_problem(dims, P.GEN_RANDOM, SEED)
+        host = P.generate_problem(dims, KIND, SEED)
         for a in host.arrays:
             P.lib().thiim_gpu_pin_host(a.ctypes.data, a.nbytes)
         secs = 0.0
@@ -360,7 +370,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--engine", default="auto", choices=["auto", "split", "fused", "tblock"])
-    ap.add_argument("--iters", type=int, default=ITERS)
+    ap.add_argument("--iters", type=int, default=None)
     ap.add_argument("--device", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -371,7 +381,14 @@ def main():
     ap.add_argument("--l2-promotion", type=int, default=0)
     ap.add_argument("--y-fastest", type=int, default=0)
     ap.add_argument("--full-boxes", type=int, default=0)
+    ap.add_argument("--config", default="c1", choices=sorted(CONFIGS))
     args = ap.parse_args()
+    global GRID, ITERS, KIND, WORKLOAD
+    GRID, ITERS, KIND, desc = CONFIGS[args.config]
+    if args.iters is None:
+        args.iters = ITERS
+    WORKLOAD = (desc + " (H then E half-step) per bench step, complex128, fields U[-1,1], "
+                + ("per-layer coeffs" if KIND else "coeffs") + " |c|<=0.45, seed 1, zero halo")
     world, rank, local = dist_env()
     if args.impl == "reference":
         run_reference_arm(args, world, rank)

@@ -59,8 +59,8 @@ struct Slab {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   // 4-D tensor maps over the allocation {x (doubles), y, plane, array slot},
   // one set of box shapes per tile height (8 / 16 rows), built lazily
-  TmaMaps maps[3];  // tile heights 8, 16, 15
-  bool maps_ok[3] = {false, false, false};
+  TmaMaps maps[4];  // tile heights 8, 16, 15, 12
+  bool maps_ok[4] = {false, false, false, false};
   // TBLOCK: per-SM scratch ring (3 planes x 12 fields x tile) and its tensor map
   double2* scratch = nullptr;
   size_t scratch_bytes = 0;
@@ -312,7 +312,7 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
   return fn;
 }
 
-int map_index(int by) { return by == 16 ? 1 : by == 15 ? 2 : 0; }
+int map_index(int by) { return by == 16 ? 1 : by == 15 ? 2 : by == 12 ? 3 : 0; }
 // (tile heights 8, 16 and 15 each get their own set of box shapes)
 
 int ensure_tmap(Slab& s, int by, int promo) {
@@ -469,6 +469,7 @@ int launch_tblock2_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
 
 int launch_tblock2(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
   CK(cudaSetDevice(s.device));
+  if (ctx->opts.tile_y == 12) return launch_tblock2_t<12, 7>(ctx, s, launches);
   return launch_tblock2_t<15, 6>(ctx, s, launches);
 }
 
@@ -554,10 +555,22 @@ static int create_impl(const thiim_dims* dims, const thiim_gpu_opts* opts,
   auto* ctx = new thiim_gpu_ctx;
   ctx->dims = *dims;
   ctx->opts = o;
-  ctx->engine = o.engine == THIIM_ENGINE_AUTO ? THIIM_ENGINE_FUSED : o.engine;
-  const int nf = ctx->engine == THIIM_ENGINE_SPLIT ? 1 : 2;
   const long long pxy = ctx->pxy();
   const int n = (int)ranges.size();
+  ctx->engine = o.engine;
+  if (o.engine == THIIM_ENGINE_AUTO) {
+    // fused (ping-pong fields, 52 arrays) when it fits, else split in place (40)
+    ctx->engine = THIIM_ENGINE_FUSED;
+    for (int s = 0; s < n; ++s) {
+      size_t freeb = 0, totalb = 0;
+      cudaSetDevice(o.device + s);
+      cudaMemGetInfo(&freeb, &totalb);
+      const size_t need = (size_t)(ranges[s].second - ranges[s].first + 2) * (size_t)pxy *
+                          sizeof(double2) * 52 + ((size_t)256 << 20);
+      if (need > freeb) ctx->engine = THIIM_ENGINE_SPLIT;
+    }
+  }
+  const int nf = ctx->engine == THIIM_ENGINE_SPLIT ? 1 : 2;
   for (int s = 0; s < n; ++s) {
     Slab sl;
     sl.device = o.device + s;
