@@ -183,7 +183,7 @@ def run_reference_arm(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
-def _roofline(P, dims, engine_ran, dev_secs, launches):
+def _roofline(P, dims, engine_ran, dev_secs, launches, table=False):
     """Roofline of the dominant kernel: one THIIM iteration (fused) or one
     half-step sweep (split) per launch over the rank's grid."""
     hbm, peak_kind = load_peaks()
@@ -191,6 +191,9 @@ def _roofline(P, dims, engine_ran, dev_secs, launches):
     if engine_ran == P.ENGINE_SPLIT:
         bytes_launch = 512.0 * dims.interior_cells()  # one half-step sweep: 32 x 16 B per cell
         kname = "k_split_h/k_split_e"
+    elif table:
+        bytes_launch = 385.0 * dims.interior_cells()  # 24 fields x 16 B + 1 B material id
+        kname = "k_fused_table<15,5>"
     elif engine_ran == P.ENGINE_TBLOCK:
         # one launch = two THIIM iterations in one HBM pass: 832 B per cell = 416 B/LUP
         bytes_launch = 832.0 * dims.interior_cells()
@@ -204,7 +207,7 @@ def _roofline(P, dims, engine_ran, dev_secs, launches):
     if os.path.exists(tp):
         with open(tp) as f:
             traffic = json.load(f).get(kname)
-    balance = P.balance_model(engine_ran)
+    balance = 385.0 if table else P.balance_model(engine_ran)
     return {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
             "frac": round(achieved / hbm, 4), "traffic": traffic, "kernel": kname,
             "algorithmic_bytes_per_launch": bytes_launch, "peak_kind": peak_kind,
@@ -219,7 +222,9 @@ def run_native(args, world, rank, local):
     opts = P.GpuOptions(device=local if world > 1 else args.device, engine=engine,
                         tile_y=args.tile_y, z_chunk=args.z_chunk, min_blocks=args.min_blocks,
                         variant=args.variant, l2_promotion=args.l2_promotion,
-                        y_fastest=args.y_fastest, full_boxes=args.full_boxes)
+                        y_fastest=args.y_fastest, full_boxes=args.full_boxes,
+                        coeff_layout=P.COEFF_TABLE if args.coeff == "table" else P.COEFF_FULL,
+                        n_materials=6 if args.coeff == "table" else 0)
     iters = args.iters
     if world == 1:
         line = run_native_single(P, args, opts, iters)
@@ -242,7 +247,7 @@ def _line(P, args, world, dims_rank, engine_ran, dev_secs, launches, e2e, clk, e
     lups_step = dims_rank.interior_cells() * args.iters
     value = world * lups_step * args.steps / dev_secs / 1e6
     padded = dims_rank.padded_cells() * 16
-    cfg = {"workload": WORKLOAD, "config": args.config,
+    cfg = {"workload": WORKLOAD, "config": args.config, "coeff_layout": args.coeff,
            "grid_per_rank": [dims_rank.nx, dims_rank.ny, dims_rank.nz],
            "iterations_per_step": args.iters, "engine": P.ENGINE_NAMES.get(engine_ran),
            "parallelism": "z-slab x%d" % world if world > 1 else "single GPU",
@@ -258,7 +263,8 @@ def _line(P, args, world, dims_rank, engine_ran, dev_secs, launches, e2e, clk, e
         "e2e": {"value": round(e2e, 2) if e2e else None, "unit": "MLUP/s",
                 "h2d_bytes_per_step": 40 * padded, "d2h_bytes_per_step": 12 * padded},
         "gpu_launches": launches,
-        "roofline": _roofline(P, dims_rank, engine_ran, dev_secs, launches),
+        "roofline": _roofline(P, dims_rank, engine_ran, dev_secs, launches,
+                              table=getattr(args, "coeff", "full") == "table"),
         "clocks": clk.result,
     }
 
@@ -382,6 +388,9 @@ def main():
     ap.add_argument("--y-fastest", type=int, default=0)
     ap.add_argument("--full-boxes", type=int, default=0)
     ap.add_argument("--config", default="c1", choices=sorted(CONFIGS))
+    ap.add_argument("--coeff", default="full", choices=["full", "table"],
+                    help="coefficient layout; 'table' (material ids, layered configs only) is "
+                         "reported separately from the reference-layout roofline")
     args = ap.parse_args()
     global GRID, ITERS, KIND, WORKLOAD
     GRID, ITERS, KIND, desc = CONFIGS[args.config]

@@ -82,8 +82,18 @@ typedef struct {
   int tile_y;       /* 0 = auto */
   int z_chunk;      /* planes per CTA along the z-stream, 0 = auto */
   int time_block;   /* TBLOCK: steps per HBM pass, 0 = auto */
-  int reserved[9];
+  int reserved[7];  /* experiment knobs (0 = defaults) */
+  int coeff_layout; /* THIIM_COEFF_FULL (28 arrays) or THIIM_COEFF_TABLE (material ids) */
+  int n_materials;  /* THIIM_COEFF_TABLE: rows of the coefficient table (<= 64) */
 } thiim_gpu_opts;
+
+/* Coefficient storage.  FULL is the reference layout (28 domain arrays).
+ * TABLE is the compressed layout for piecewise-constant media:
+ * a uint8 material id per cell plus a [n_materials][28] table (t x12, c x12,
+ * src x4, ProblemState order); the fused sweep then moves 385 instead of
+ * 832 B/LUP.  Results are bitwise those of the equivalent FULL problem; the
+ * figure is reported separately from the reference-layout roofline. */
+enum { THIIM_COEFF_FULL = 0, THIIM_COEFF_TABLE = 1 };
 
 typedef struct {
   double seconds;          /* device time of the whole step loop (CUDA events) */
@@ -193,6 +203,14 @@ int thiim_gpu_upload_planes(thiim_gpu_ctx* ctx, const thiim_c128* const arrays[4
 int thiim_gpu_download_fields_planes(thiim_gpu_ctx* ctx, thiim_c128* const fields[12], int p0);
 int thiim_generate_host_planes(const thiim_dims* global, int kind, uint64_t seed, int p0, int p1,
                                thiim_c128* const arrays[40]);
+
+/* THIIM_COEFF_TABLE contexts: upload fields, per-cell material ids (padded
+ * layout, (nx+2)(ny+2)(nz+2) bytes, ghosts ignored) and the coefficient table
+ * ([n_materials][28] complex128). */
+int thiim_gpu_upload_table(thiim_gpu_ctx* ctx, const thiim_c128* const fields[12],
+                           const uint8_t* material_id, const thiim_c128* table);
+/* Reads back the material ids and the table of a THIIM_COEFF_TABLE context. */
+int thiim_gpu_download_table(thiim_gpu_ctx* ctx, uint8_t* material_id, thiim_c128* table);
 
 /* Blocks until all work queued on the context's streams has finished. */
 int thiim_gpu_sync(thiim_gpu_ctx* ctx);

@@ -39,6 +39,7 @@ __all__ = [
     "COMPONENT_TABLE", "GEN_RANDOM", "GEN_LAYERED", "ENGINE_AUTO", "ENGINE_SPLIT",
     "ENGINE_FUSED", "ENGINE_TBLOCK", "GpuOptions", "RunReport", "StateDiff", "GpuEngine",
     "run_gpu", "generate_problem", "compare_states", "balance_model", "lib",
+    "compress_coefficients", "expand_coefficients", "COEFF_FULL", "COEFF_TABLE",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -265,7 +266,8 @@ class _Dims(ctypes.Structure):
 class _Opts(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int), ("n_gpus", ctypes.c_int), ("engine", ctypes.c_int),
                 ("tile_x", ctypes.c_int), ("tile_y", ctypes.c_int), ("z_chunk", ctypes.c_int),
-                ("time_block", ctypes.c_int), ("reserved", ctypes.c_int * 9)]
+                ("time_block", ctypes.c_int), ("reserved", ctypes.c_int * 7),
+                ("coeff_layout", ctypes.c_int), ("n_materials", ctypes.c_int)]
 
 
 class _Stats(ctypes.Structure):
@@ -289,6 +291,7 @@ EXPORTED_SYMBOLS = [
     "thiim_generate_host", "thiim_gpu_pin_host", "thiim_gpu_unpin_host",
     "thiim_gpu_create_slab", "thiim_gpu_halo_view", "thiim_gpu_sync",
     "thiim_gpu_upload_planes", "thiim_gpu_download_fields_planes", "thiim_generate_host_planes",
+    "thiim_gpu_upload_table", "thiim_gpu_download_table",
 ]
 
 _LIB = None
@@ -320,6 +323,8 @@ def lib() -> ctypes.CDLL:
     L.thiim_gpu_download_array.argtypes = [P, ctypes.c_int, P]
     L.thiim_gpu_compare_fields.argtypes = [P, PP, ctypes.POINTER(_Diff)]
     L.thiim_generate_host.argtypes = [ctypes.POINTER(_Dims), ctypes.c_int, ctypes.c_uint64, PP]
+    L.thiim_gpu_upload_table.argtypes = [P, PP, P, P]
+    L.thiim_gpu_download_table.argtypes = [P, P, P]
     L.thiim_gpu_pin_host.argtypes = [P, ctypes.c_size_t]
     L.thiim_gpu_unpin_host.argtypes = [P]
     if L.thiim_gpu_abi_version() != 1:
@@ -345,6 +350,8 @@ def _check(rc: int) -> None:
 
 GEN_RANDOM = 0
 GEN_LAYERED = 1
+COEFF_FULL = 0
+COEFF_TABLE = 1
 ENGINE_AUTO, ENGINE_SPLIT, ENGINE_FUSED, ENGINE_TBLOCK = 0, 1, 2, 3
 ENGINE_NAMES = {ENGINE_SPLIT: "gpu-split", ENGINE_FUSED: "gpu-fused", ENGINE_TBLOCK: "gpu-tblock"}
 
@@ -369,7 +376,8 @@ class GpuOptions:
     l2_promotion: int = 0  # TMA L2 promotion (reserved[2]): 0 none, 1 64B, 2 128B, 3 256B
     y_fastest: int = 0   # CTA order (reserved[3]): 0 x-tiles fastest (default), 1 y-tiles fastest
     full_boxes: int = 0  # experiment (reserved[4]): fetch the full 32xBY box for every array
-    debug: int = 0       # reserved[5]: TBLOCK debug bits (1 heavy fences, 2 scratch per CTA)
+    coeff_layout: int = 0  # COEFF_FULL (reference layout) or COEFF_TABLE (material ids)
+    n_materials: int = 0
 
     def _c(self) -> _Opts:
         o = _Opts()
@@ -381,7 +389,7 @@ class GpuOptions:
         o.reserved[2] = self.l2_promotion
         o.reserved[3] = self.y_fastest
         o.reserved[4] = self.full_boxes
-        o.reserved[5] = self.debug
+        o.coeff_layout, o.n_materials = self.coeff_layout, self.n_materials
         return o
 
 
@@ -457,6 +465,22 @@ class GpuEngine:
     def download_fields(self, s: ProblemState) -> None:
         _check(lib().thiim_gpu_download_fields(self._ctx, _ptrs(s.arrays[0:12])))
 
+    def upload_table(self, fields: List[np.ndarray], material_id: np.ndarray,
+                     table: np.ndarray) -> None:
+        """THIIM_COEFF_TABLE contexts: 12 field arrays, uint8 material id per
+        padded cell, table [n_materials][28] complex128 (t, c, src order)."""
+        mid = np.ascontiguousarray(material_id, dtype=np.uint8)
+        tab = np.ascontiguousarray(table, dtype=np.complex128)
+        _check(lib().thiim_gpu_upload_table(self._ctx, _ptrs(fields[0:12]), mid.ctypes.data,
+                                            tab.ctypes.data))
+
+    def download_table(self, n_materials: int):
+        n = self.dims.padded_cells()
+        mid = np.zeros(n, dtype=np.uint8)
+        tab = np.zeros((n_materials, 28), dtype=np.complex128)
+        _check(lib().thiim_gpu_download_table(self._ctx, mid.ctypes.data, tab.ctypes.data))
+        return mid, tab
+
     def download_array(self, a: int, out: np.ndarray) -> None:
         _check(lib().thiim_gpu_download_array(self._ctx, a, out.ctypes.data))
 
@@ -482,6 +506,27 @@ def generate_problem(dims: GridDims, kind: int = GEN_RANDOM, seed: int = 1) -> P
     s = allocate_state(dims)
     d = _Dims(dims.nx, dims.ny, dims.nz, dims.ghost)
     _check(lib().thiim_generate_host(ctypes.byref(d), kind, seed, _ptrs(s.arrays)))
+    return s
+
+
+def compress_coefficients(state: ProblemState, max_materials: int = 16):
+    """Material ids + coefficient table of a piecewise-constant problem (the
+    THIIM_COEFF_TABLE layout).  Raises ConfigError if the medium has more than
+    `max_materials` distinct coefficient rows."""
+    coef = np.stack(state.arrays[12:40], axis=1)  # (cells, 28)
+    rows, ids = np.unique(coef.view(np.uint64).reshape(len(coef), 56), axis=0, return_inverse=True)
+    if len(rows) > max_materials:
+        raise ConfigError("medium has %d distinct coefficient rows (> %d)" % (len(rows), max_materials))
+    table = rows.view(np.complex128).reshape(len(rows), 28)
+    return ids.astype(np.uint8).reshape(-1), np.ascontiguousarray(table)
+
+
+def expand_coefficients(dims: GridDims, material_id: np.ndarray, table: np.ndarray) -> ProblemState:
+    """Inverse of compress_coefficients (fields left zero)."""
+    s = allocate_state(dims)
+    full = table[material_id]  # (cells, 28)
+    for k in range(28):
+        s.arrays[12 + k][:] = full[:, k]
     return s
 
 

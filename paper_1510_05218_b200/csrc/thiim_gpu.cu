@@ -23,6 +23,7 @@
 #include "../../include/thiim_gpu.h"
 #include "thiim_common.cuh"
 #include "thiim_fused.cuh"
+#include "thiim_fused_table.cuh"
 #include "thiim_fused_tma.cuh"
 #include "thiim_split.cuh"
 #include "thiim_tblock.cuh"
@@ -55,6 +56,12 @@ struct Slab {
   size_t stride = 0;   // elements per array
   int nfield_sets = 1;
   int cur = 0;         // current field set
+  bool table = false;  // THIIM_COEFF_TABLE: no coefficient arrays, material ids + table
+  uint8_t* mat = nullptr;  // pitched material ids (table layout)
+  long long mp = 0, mplane = 0;
+  double2* tab = nullptr;  // [kMaxMaterials][28]
+  int n_mat = 0;
+
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   // 4-D tensor maps over the allocation {x (doubles), y, plane, array slot},
@@ -68,9 +75,10 @@ struct Slab {
   int smap_by = 0;
 
   double2* field(int set, int k) const { return buf + (size_t)(set * 12 + k) * stride; }
-  double2* coeff(int a) const {  // a in 12..39
-    return buf + (size_t)(nfield_sets * 12 + (a - 12)) * stride;
+  double2* coeff(int a) const {  // a in 12..39 (FULL layout only)
+    return table ? nullptr : buf + (size_t)(nfield_sets * 12 + (a - 12)) * stride;
   }
+  int n_arrays() const { return nfield_sets * 12 + (table ? 0 : 28); }
   double2* array(int a) const { return a < 12 ? field(cur, a) : coeff(a); }
   Arrays arrays(int in_set, int out_set) const {
     Arrays A;
@@ -324,7 +332,7 @@ int ensure_tmap(Slab& s, int by, int promo) {
   auto fn = get_encode_fn();
   if (!fn) return fail(THIIM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   const cuuint64_t dims[4] = {(cuuint64_t)(2 * s.g.px), (cuuint64_t)(s.g.pxy / s.g.px),
-                              (cuuint64_t)(s.g.nz + 2), (cuuint64_t)(s.nfield_sets * 12 + 28)};
+                              (cuuint64_t)(s.g.nz + 2), (cuuint64_t)s.n_arrays()};
   const cuuint64_t strides[3] = {(cuuint64_t)s.g.px * 16, (cuuint64_t)s.g.pxy * 16,
                                  (cuuint64_t)s.stride * 16};
   const int bw[NBOX] = {32, 31, 31, 30, 30};
@@ -473,8 +481,44 @@ int launch_tblock2(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
   return launch_tblock2_t<15, 6>(ctx, s, launches);
 }
 
+template <int BY, int NG>
+int launch_fused_table_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
+  static_assert(BY == 15, "material-id map box height is 15");
+  const Arrays A = s.arrays(s.cur, s.cur ^ 1);
+  const int cur = s.cur;
+  GroupSeq S;
+  seq_table(S, [&](int k) { return cur * 12 + k; });
+  int r = ensure_tmap(s, BY, 0);
+  if (r) return r;
+  TableMaps maps;
+  maps.f = s.maps[map_index(BY)];
+  TableGrid T;
+  T.mat = s.mat;
+  T.mp = s.mp;
+  T.mplane = s.mplane;
+  T.table = s.tab;
+  T.n_mat = s.n_mat;
+  constexpr int TX = 30, TY = BY - 2;
+  const size_t smem = sizeof(TableSmem<BY, NG>);
+  static bool attr_set = false;
+  if (!attr_set) {
+    CK(cudaFuncSetAttribute(k_fused_table<BY, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)smem));
+    attr_set = true;
+  }
+  const int tiles_x = (s.g.nx + TX - 1) / TX, tiles_y = (s.g.ny + TY - 1) / TY;
+  const int zc = balanced_zchunk(s, (long long)tiles_x * tiles_y, 1, ctx->opts.z_chunk);
+  const dim3 grid(tiles_x * tiles_y, 1, (s.g.nz + zc - 1) / zc);
+  k_fused_table<BY, NG><<<grid, dim3(32, BY + 1), smem, s.stream>>>(s.g, A, T, maps, S, zc, tiles_x);
+  CK(cudaGetLastError());
+  s.cur ^= 1;
+  ++*launches;
+  return THIIM_OK;
+}
+
 int launch_fused(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
   CK(cudaSetDevice(s.device));
+  if (s.table) return launch_fused_table_t<15, 5>(ctx, s, launches);
   // reserved[1] = 1 selects the register-staged kernel (thiim_fused.cuh);
   // default is the bulk-async staged one (thiim_fused_tma.cuh).
   if (ctx->opts.reserved[1] == 1) {
@@ -518,6 +562,7 @@ double thiim_gpu_balance_model(int engine, int time_block) {
   switch (engine) {
     case THIIM_ENGINE_SPLIT: return 1024.0;
     case THIIM_ENGINE_TBLOCK: return 832.0 / (time_block > 0 ? time_block : 2);
+    case 100 + THIIM_COEFF_TABLE: return 385.0;  // fused sweep, table coefficient layout
     default: return 832.0;
   }
 }
@@ -541,6 +586,13 @@ static int create_impl(const thiim_dims* dims, const thiim_gpu_opts* opts,
     return fail(THIIM_ERR_CONFIG, "unknown engine");
   if (o.engine == THIIM_ENGINE_TBLOCK && o.time_block != 0 && o.time_block != 2)
     return fail(THIIM_ERR_CONFIG, "engine TBLOCK supports time_block 2");
+  const bool table = o.coeff_layout == THIIM_COEFF_TABLE;
+  if (o.coeff_layout != THIIM_COEFF_FULL && !table)
+    return fail(THIIM_ERR_CONFIG, "unknown coefficient layout");
+  if (table && o.engine != THIIM_ENGINE_AUTO && o.engine != THIIM_ENGINE_FUSED)
+    return fail(THIIM_ERR_CONFIG, "the table coefficient layout runs on the fused engine");
+  if (table && (o.n_materials < 1 || o.n_materials > kMaxMaterials))
+    return fail(THIIM_ERR_CONFIG, "n_materials must be in 1..16 for the table layout");
   if (o.engine == THIIM_ENGINE_TBLOCK && ranges.size() != 1)
     return fail(THIIM_ERR_CONFIG, "engine TBLOCK runs on one GPU (halo slabs need 2-plane halos)");
   for (const auto& r : ranges)
@@ -558,7 +610,8 @@ static int create_impl(const thiim_dims* dims, const thiim_gpu_opts* opts,
   const long long pxy = ctx->pxy();
   const int n = (int)ranges.size();
   ctx->engine = o.engine;
-  if (o.engine == THIIM_ENGINE_AUTO) {
+  if (table) ctx->engine = THIIM_ENGINE_FUSED;
+  if (o.engine == THIIM_ENGINE_AUTO && !table) {
     // fused (ping-pong fields, 52 arrays) when it fits, else split in place (40)
     ctx->engine = THIIM_ENGINE_FUSED;
     for (int s = 0; s < n; ++s) {
@@ -583,15 +636,26 @@ static int create_impl(const thiim_dims* dims, const thiim_gpu_opts* opts,
     sl.g.pxy = pxy;
     sl.g.halo_lo = sl.z0 > 0 ? 1 : 0;
     sl.nfield_sets = nf;
+    sl.table = table;
+    sl.n_mat = table ? o.n_materials : 0;
+    sl.mp = (dims->nx + 2 + 15) / 16 * 16;
+    sl.mplane = sl.mp * (dims->ny + 2);
     sl.stride = ((size_t)(sl.g.nz + 2) * (size_t)pxy + 15) / 16 * 16;
     ctx->slabs.push_back(sl);
   }
   for (auto& sl : ctx->slabs) {
     // + tail slack: tile row copies may run past the last padded row
     const size_t tail = (size_t)(34 * (dims->nx + 2) + 256) * sizeof(double2);
-    const size_t bytes = sl.stride * sizeof(double2) * (size_t)(12 * nf + 28) + tail;
+    const size_t bytes = sl.stride * sizeof(double2) * (size_t)sl.n_arrays() + tail;
     cudaError_t e = cudaSetDevice(sl.device);
     if (e == cudaSuccess) e = cudaMalloc(&sl.buf, bytes);
+    if (e == cudaSuccess && table) {
+      const size_t mbytes = (size_t)sl.mplane * (sl.g.nz + 2) + 4096;
+      e = cudaMalloc(&sl.mat, mbytes);
+      if (e == cudaSuccess) e = cudaMemset(sl.mat, 0, mbytes);
+      if (e == cudaSuccess) e = cudaMalloc(&sl.tab, kMaxMaterials * 28 * sizeof(double2));
+      if (e == cudaSuccess) e = cudaMemset(sl.tab, 0, kMaxMaterials * 28 * sizeof(double2));
+    }
     if (e == cudaSuccess) e = cudaMemset(sl.buf, 0, bytes);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&sl.stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreate(&sl.ev0);
@@ -687,6 +751,8 @@ void thiim_gpu_destroy(thiim_gpu_ctx* ctx) {
     if (sl.stream) cudaStreamSynchronize(sl.stream);
     if (sl.buf) cudaFree(sl.buf);
     if (sl.scratch) cudaFree(sl.scratch);
+    if (sl.mat) cudaFree(sl.mat);
+    if (sl.tab) cudaFree(sl.tab);
     if (sl.ev0) cudaEventDestroy(sl.ev0);
     if (sl.ev1) cudaEventDestroy(sl.ev1);
     if (sl.stream) cudaStreamDestroy(sl.stream);
@@ -714,6 +780,7 @@ static int upload_arrays(thiim_gpu_ctx* ctx, const thiim_c128* const* arrays, in
           CK(cudaMemcpyAsync(sl.field(set, a), sl.field(0, a), bytes, cudaMemcpyDeviceToDevice,
                              sl.stream));
       } else {
+        if (sl.table) return fail(THIIM_ERR_CONFIG, "table-layout context: use thiim_gpu_upload_table");
         CK(cudaMemcpyAsync(sl.coeff(a), src, bytes, cudaMemcpyHostToDevice, sl.stream));
       }
     }
@@ -755,6 +822,29 @@ int thiim_gpu_init_generated(thiim_gpu_ctx* ctx, int kind, uint64_t seed) {
   double2 table[28 * 6];
   for (int a = 12; a < 40; ++a)
     for (int L = 0; L < 6; ++L) table[(a - 12) * 6 + L] = gen_disk(gen_key(seed, a), (uint64_t)L);
+  if (ctx->slabs[0].table) {
+    if (kind != THIIM_GEN_LAYERED)
+      return fail(THIIM_ERR_CONFIG, "the table layout needs a piecewise-constant (layered) problem");
+    if (ctx->slabs[0].n_mat < 6) return fail(THIIM_ERR_CONFIG, "layered problems have 6 materials");
+    double2 tab[6 * 28];
+    for (int L = 0; L < 6; ++L)
+      for (int a = 12; a < 40; ++a) tab[L * 28 + (a - 12)] = table[(a - 12) * 6 + L];
+    for (auto& sl : ctx->slabs) {
+      CK(cudaSetDevice(sl.device));
+      CK(cudaMemcpyAsync(sl.tab, tab, sizeof(tab), cudaMemcpyHostToDevice, sl.stream));
+      Arrays A = sl.arrays(0, 0);
+      k_generate_table<<<8 * sm_count(sl.device), 256, 0, sl.stream>>>(
+          sl.g, sl.z0, ctx->dims.nz, A, seed, sl.mat, sl.mp, sl.mplane);
+      CK(cudaGetLastError());
+      for (int k = 0; k < 12; ++k)
+        CK(cudaMemcpyAsync(sl.field(1, k), sl.field(0, k), sl.stride * sizeof(double2),
+                           cudaMemcpyDeviceToDevice, sl.stream));
+      CK(cudaStreamSynchronize(sl.stream));
+      sl.cur = 0;
+    }
+    ctx->loaded = true;
+    return THIIM_OK;
+  }
   for (auto& sl : ctx->slabs) {
     CK(cudaSetDevice(sl.device));
     double2* dtable = nullptr;
@@ -826,7 +916,9 @@ int thiim_gpu_step(thiim_gpu_ctx* ctx, int steps, thiim_gpu_stats* stats) {
     stats->engine = ctx->engine;
     stats->n_gpus = (int)ctx->slabs.size();
     stats->kernel_launches = launches;
-    stats->balance_model = thiim_gpu_balance_model(ctx->engine, ctx->opts.time_block);
+    stats->balance_model = ctx->slabs[0].table
+                               ? thiim_gpu_balance_model(100 + THIIM_COEFF_TABLE, 0)
+                               : thiim_gpu_balance_model(ctx->engine, ctx->opts.time_block);
     const double lups = (double)ctx->dims.nx * ctx->dims.ny * ctx->dims.nz * steps;
     stats->mlups = (steps > 0 && secs > 0) ? lups / secs / 1e6 : 0.0;
   }
@@ -887,10 +979,53 @@ int thiim_gpu_download_fields_planes(thiim_gpu_ctx* ctx, thiim_c128* const field
   return THIIM_OK;
 }
 
+int thiim_gpu_upload_table(thiim_gpu_ctx* ctx, const thiim_c128* const fields[12],
+                           const uint8_t* material_id, const thiim_c128* table) {
+  g_err.clear();
+  if (!ctx || !fields || !material_id || !table) return fail(THIIM_ERR_CONFIG, "null argument");
+  if (!ctx->slabs[0].table) return fail(THIIM_ERR_CONFIG, "context uses the full coefficient layout");
+  int r;
+  if ((r = upload_arrays(ctx, fields, 0, 12))) return r;
+  const long long pxy = ctx->pxy();
+  for (auto& sl : ctx->slabs) {
+    CK(cudaSetDevice(sl.device));
+    // padded host planes [z0, z1+2) -> pitched device rows
+    CK(cudaMemcpy2DAsync(sl.mat, (size_t)sl.mp, material_id + (size_t)sl.z0 * pxy, (size_t)sl.g.px,
+                         (size_t)sl.g.px, (size_t)(pxy / sl.g.px) * (sl.g.nz + 2),
+                         cudaMemcpyHostToDevice, sl.stream));
+    CK(cudaMemcpyAsync(sl.tab, table, (size_t)sl.n_mat * 28 * sizeof(double2),
+                       cudaMemcpyHostToDevice, sl.stream));
+    CK(cudaStreamSynchronize(sl.stream));
+  }
+  ctx->loaded = true;
+  return THIIM_OK;
+}
+
+int thiim_gpu_download_table(thiim_gpu_ctx* ctx, uint8_t* material_id, thiim_c128* table) {
+  g_err.clear();
+  if (!ctx || !material_id || !table) return fail(THIIM_ERR_CONFIG, "null argument");
+  if (!ctx->slabs[0].table) return fail(THIIM_ERR_CONFIG, "context uses the full coefficient layout");
+  const long long pxy = ctx->pxy();
+  for (auto& sl : ctx->slabs) {
+    CK(cudaSetDevice(sl.device));
+    const int p0 = sl.z0 == 0 ? 0 : 1;
+    const int p1 = sl.z1 == ctx->dims.nz ? sl.g.nz + 2 : sl.g.nz + 1;
+    CK(cudaMemcpy2DAsync(material_id + (size_t)(sl.z0 + p0) * pxy, (size_t)sl.g.px,
+                         sl.mat + (size_t)p0 * sl.mplane, (size_t)sl.mp, (size_t)sl.g.px,
+                         (size_t)(pxy / sl.g.px) * (p1 - p0), cudaMemcpyDeviceToHost, sl.stream));
+    CK(cudaMemcpyAsync(table, sl.tab, (size_t)sl.n_mat * 28 * sizeof(double2),
+                       cudaMemcpyDeviceToHost, sl.stream));
+    CK(cudaStreamSynchronize(sl.stream));
+  }
+  return THIIM_OK;
+}
+
 int thiim_gpu_download_array(thiim_gpu_ctx* ctx, int array_id, thiim_c128* dst) {
   g_err.clear();
   if (!ctx || !dst) return fail(THIIM_ERR_CONFIG, "null argument");
   if (array_id < 0 || array_id >= 40) return fail(THIIM_ERR_CONFIG, "array id out of range");
+  if (array_id >= 12 && ctx->slabs[0].table)
+    return fail(THIIM_ERR_CONFIG, "table-layout context: use thiim_gpu_download_table");
   return download_impl(ctx, array_id, dst);
 }
 

@@ -98,3 +98,15 @@ def test_compare_states_semantics():
     e = P.allocate_state(d)
     e.interior(0)[0, 0, 0] = -0.0
     assert not P.compare_states(c, e).bitwise_equal
+
+
+def test_compress_expand_roundtrip():
+    d = P.GridDims(10, 9, 30)
+    s = P.generate_problem(d, P.GEN_LAYERED, 4)
+    mid, tab = P.compress_coefficients(s)
+    assert len(tab) == 7  # 6 layers + the all-zero ghost row
+    full = P.expand_coefficients(d, mid, tab)
+    for k in range(12, 40):
+        assert np.array_equal(full.arrays[k].view(np.uint64), s.arrays[k].view(np.uint64))
+    with pytest.raises(P.ConfigError):
+        P.compress_coefficients(P.generate_problem(d, P.GEN_RANDOM, 1))
