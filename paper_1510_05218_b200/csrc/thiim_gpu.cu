@@ -477,7 +477,6 @@ int launch_tblock2_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
 
 int launch_tblock2(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
   CK(cudaSetDevice(s.device));
-  if (ctx->opts.tile_y == 12) return launch_tblock2_t<12, 7>(ctx, s, launches);
   return launch_tblock2_t<15, 6>(ctx, s, launches);
 }
 

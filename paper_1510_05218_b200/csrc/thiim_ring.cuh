@@ -68,7 +68,7 @@ struct GroupSeq {
 };
 
 template <int BY, int NG>
-struct Ring {
+struct alignas(128) Ring {
   static constexpr int G = 4;
   double2 buf[NG][G][BY * 32];
   uint64_t full[NG];
