@@ -82,7 +82,8 @@ typedef struct {
   int tile_y;       /* 0 = auto */
   int z_chunk;      /* planes per CTA along the z-stream, 0 = auto */
   int time_block;   /* TBLOCK: steps per HBM pass, 0 = auto */
-  int reserved[7];  /* experiment knobs (0 = defaults) */
+  int reserved[7];  /* experiment / test knobs (0 = defaults); reserved[6] = 1 places
+                       every slab on `device` (exercises multi-slab paths on one GPU) */
   int coeff_layout; /* THIIM_COEFF_FULL (28 arrays) or THIIM_COEFF_TABLE (material ids) */
   int n_materials;  /* THIIM_COEFF_TABLE: rows of the coefficient table (<= 64) */
 } thiim_gpu_opts;

@@ -376,6 +376,7 @@ class GpuOptions:
     l2_promotion: int = 0  # TMA L2 promotion (reserved[2]): 0 none, 1 64B, 2 128B, 3 256B
     y_fastest: int = 0   # CTA order (reserved[3]): 0 x-tiles fastest (default), 1 y-tiles fastest
     full_boxes: int = 0  # experiment (reserved[4]): fetch the full 32xBY box for every array
+    same_device: int = 0  # test knob (reserved[6]): all slabs of a multi-slab context on `device`
     coeff_layout: int = 0  # COEFF_FULL (reference layout) or COEFF_TABLE (material ids)
     n_materials: int = 0
 
@@ -389,6 +390,7 @@ class GpuOptions:
         o.reserved[2] = self.l2_promotion
         o.reserved[3] = self.y_fastest
         o.reserved[4] = self.full_boxes
+        o.reserved[6] = self.same_device
         o.coeff_layout, o.n_materials = self.coeff_layout, self.n_materials
         return o
 

@@ -82,3 +82,31 @@ def test_cpp_adapter_binary():
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failed" in r.stdout
+
+
+@pytest.mark.parametrize("engine", [P.ENGINE_SPLIT, P.ENGINE_FUSED])
+@pytest.mark.parametrize("n", [2, 3])
+def test_single_process_multi_slab_context(engine, n):
+    """One context driving n z-slabs with peer-copy halo exchange (the path
+    thiim::run_gpu takes with n_gpus > 1), all slabs placed on cuda:0."""
+    dims = P.GridDims(40, 30, 36)
+    s = P.generate_problem(dims, P.GEN_RANDOM, 12)
+    want = P.clone_state(s)
+    O.c_step((40, 30, 36), want.arrays, 5, threads=8)
+    got = P.clone_state(s)
+    P.run_gpu(got, 5, P.GpuOptions(engine=engine, n_gpus=n, same_device=1))
+    assert P.compare_states(got, want).bitwise_equal
+
+
+def test_single_process_multi_slab_table_layout():
+    dims = P.GridDims(30, 26, 48)
+    host = P.generate_problem(dims, P.GEN_LAYERED, 3)
+    want = P.clone_state(host)
+    O.c_step((30, 26, 48), want.arrays, 4, threads=8)
+    with P.GpuEngine(dims, P.GpuOptions(n_gpus=3, same_device=1, coeff_layout=P.COEFF_TABLE,
+                                        n_materials=6)) as eng:
+        eng.generate(P.GEN_LAYERED, 3)
+        eng.step(4)
+        got = P.allocate_state(dims)
+        eng.download_fields(got)
+    assert P.compare_states(got, want).bitwise_equal
