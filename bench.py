@@ -312,8 +312,14 @@ def run_native_multi(P, args, opts, iters, world, rank, local):
     import torch
     import torch.distributed as dist
     from paper_1510_05218_b200 import distributed as D
+    # THIIM_DIST_BACKEND=gloo + THIIM_SAME_DEVICE=1 run every rank on cuda:0 with
+    # host-staged halos (test mode for hosts with one GPU); default NCCL, GPU = local rank
+    backend = os.environ.get("THIIM_DIST_BACKEND", "nccl")
+    if os.environ.get("THIIM_SAME_DEVICE") == "1":
+        local = 0
+        opts.device = 0
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl")
+    dist.init_process_group(backend)
     gdims = P.GridDims(GRID[0], GRID[1], GRID[2] * world)
     z0, z1 = D.slab_bounds(gdims.nz, world, rank)
     eng = D.SlabGpuEngine(gdims, z0, z1, opts)
@@ -332,7 +338,8 @@ def run_native_multi(P, args, opts, iters, world, rank, local):
         torch.cuda.synchronize()
         e1.record()
         e1.synchronize()
-        t = torch.tensor([e0.elapsed_time(e1) * 1e-3], device="cuda")
+        dev = "cuda" if backend == "nccl" else "cpu"
+        t = torch.tensor([e0.elapsed_time(e1) * 1e-3], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item()), out
 
@@ -361,6 +368,27 @@ def run_native_multi(P, args, opts, iters, world, rank, local):
             P.lib().thiim_gpu_unpin_host(a.ctypes.data)
         eng.close()
         e2e = world * 256 ** 3 * iters * args.steps / e2e_run_secs / 1e6
+    if args.check:
+        # decomposed run vs one oracle run of the global grid, gathered on rank 0
+        eng = D.SlabGpuEngine(gdims, z0, z1, opts)
+        host = eng.local_host_problem(KIND, SEED)
+        eng.upload_local(host)
+        D.run_distributed(eng, args.check, ex)
+        eng.download_local(host)
+        eng.close()
+        pxy = (gdims.nx + 2) * (gdims.ny + 2)
+        mine = np.stack([a[pxy:(z1 - z0 + 1) * pxy] for a in host[:12]])
+        parts = [None] * world
+        dist.all_gather_object(parts, (z0, z1, mine))
+        if rank == 0:
+            from oracle import oracle as O  # parity check only
+            ref = P.generate_problem(gdims, KIND, SEED)
+            O.c_step((gdims.nx, gdims.ny, gdims.nz), ref.arrays, args.check, threads=cpu_threads())
+            ok = all(np.array_equal(m[k].view(np.uint64),
+                                    ref.arrays[k][(a + 1) * pxy:(b + 1) * pxy].view(np.uint64))
+                     for a, b, m in parts for k in range(12))
+            print(json.dumps({"check": "z-slab decomposition vs oracle", "ranks": world,
+                              "steps": args.check, "bitwise_equal": bool(ok)}), flush=True)
     line = _line(P, args, world, P.GridDims(*GRID), P.ENGINE_FUSED, dev_secs, launches, e2e, clk,
                  {"global_grid": [gdims.nx, gdims.ny, gdims.nz],
                   "halo_bytes_per_rank_per_step": halo // max(1, args.steps),
@@ -388,6 +416,8 @@ def main():
     ap.add_argument("--y-fastest", type=int, default=0)
     ap.add_argument("--full-boxes", type=int, default=0)
     ap.add_argument("--config", default="c1", choices=sorted(CONFIGS))
+    ap.add_argument("--check", type=int, default=0,
+                    help="multi-rank: also run CHECK steps and compare with the oracle (rank 0)")
     ap.add_argument("--coeff", default="full", choices=["full", "table"],
                     help="coefficient layout; 'table' (material ids, layered configs only) is "
                          "reported separately from the reference-layout roofline")

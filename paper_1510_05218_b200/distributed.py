@@ -143,10 +143,26 @@ class HaloExchanger:
             for t in engine.halo(RECV_DOWN):
                 ops.append(dist.P2POp(dist.irecv, t, down, self.group))
         if ops:
-            for req in dist.batch_isend_irecv(ops):
-                req.wait()
-            if torch.cuda.is_available() and ops[0].tensor.is_cuda:
+            staged = ops[0].tensor.is_cuda and dist.get_backend(self.group) == "gloo"
+            if staged:
+                # gloo moves host tensors only: stage device planes through host memory
+                host_ops, backs = [], []
+                for op in ops:
+                    h = op.tensor.detach().cpu() if op.op is dist.isend else torch.empty(
+                        op.tensor.shape, dtype=op.tensor.dtype)
+                    host_ops.append(dist.P2POp(op.op, h, op.peer, self.group))
+                    if op.op is dist.irecv:
+                        backs.append((op.tensor, h))
+                for req in dist.batch_isend_irecv(host_ops):
+                    req.wait()
+                for dev, h in backs:
+                    dev.copy_(h)
                 torch.cuda.synchronize()
+            else:
+                for req in dist.batch_isend_irecv(ops):
+                    req.wait()
+                if torch.cuda.is_available() and ops[0].tensor.is_cuda:
+                    torch.cuda.synchronize()
         return sent
 
 

@@ -1,0 +1,38 @@
+"""GPU: bench.py's multi-rank path (one process per GPU, z-slab weak scaling)
+end to end on one B200: two torchrun ranks share cuda:0, halos move through
+host-staged gloo (THIIM_DIST_BACKEND=gloo, THIIM_SAME_DEVICE=1) instead of
+NCCL, and a --check run gathers the decomposed result and compares it with
+the oracle bitwise."""
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_bench_two_ranks_one_gpu():
+    env = dict(os.environ, THIIM_DIST_BACKEND="gloo", THIIM_SAME_DEVICE="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()), "bench.py", "--gpus", "2",
+           "--config", "c0", "--steps", "1", "--warmup", "1", "--iters", "4", "--check", "3"]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    lines = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
+    check = [l for l in lines if "check" in l]
+    bench = [l for l in lines if "metric" in l]
+    assert check and check[0]["bitwise_equal"], lines
+    assert bench and bench[0]["n_gpus"] == 2 and bench[0]["value"] > 0
+    assert bench[0]["config"]["halo_bytes_per_rank_per_step"] > 0
