@@ -375,7 +375,7 @@ class GpuOptions:
     variant: int = 0     # fused kernel variant (reserved[1]): 0 bulk-async staged, 1 register-staged
     l2_promotion: int = 0  # TMA L2 promotion (reserved[2]): 0 none, 1 64B, 2 128B, 3 256B
     y_fastest: int = 0   # CTA order (reserved[3]): 0 x-tiles fastest (default), 1 y-tiles fastest
-    full_boxes: int = 0  # experiment (reserved[4]): fetch the full 32xBY box for every array
+    runtime_seq: int = 0  # experiment (reserved[4]): 1 = fused producer interprets its box sequence at run time
     same_device: int = 0  # test knob (reserved[6]): all slabs of a multi-slab context on `device`
     coeff_layout: int = 0  # COEFF_FULL (reference layout) or COEFF_TABLE (material ids)
     n_materials: int = 0
@@ -389,7 +389,7 @@ class GpuOptions:
         o.reserved[1] = self.variant
         o.reserved[2] = self.l2_promotion
         o.reserved[3] = self.y_fastest
-        o.reserved[4] = self.full_boxes
+        o.reserved[4] = self.runtime_seq
         o.reserved[6] = self.same_device
         o.coeff_layout, o.n_materials = self.coeff_layout, self.n_materials
         return o

@@ -23,6 +23,7 @@
 
 #include "thiim_async.cuh"
 #include "thiim_common.cuh"
+#include "thiim_producer.cuh"
 #include "thiim_ring.cuh"
 
 namespace thiim_gpu {
@@ -115,7 +116,7 @@ template <int BY, int NG>
 __global__ void __launch_bounds__(32 * (BY + 1), 1)
     k_fused_tma(Grid g, Arrays A, const __grid_constant__ TmaMaps maps,
                 const __grid_constant__ GroupSeq S, int zc, int tiles_y, int tiles_x,
-                int x_fastest) {
+                int x_fastest, int fb, int cb, int ct) {
   constexpr int BX = 32, TX = BX - 2, TY = BY - 2, NCOMP = 32 * BY;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   FusedSmem<BY, NG>& sm = *reinterpret_cast<FusedSmem<BY, NG>*>(smem_raw);
@@ -142,7 +143,12 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
       for (int b = 0; b < NBOX; ++b) tma_prefetch_desc(&maps.m[b]);
       int gi = 0;
       uint32_t ph = 0;
-      for (int z = z0; z < z1; ++z) produce_plane(sm.ring, gi, ph, S, maps, xb, yb, z);
+      if (ct) {  // compile-time sequence (thiim_producer.cuh)
+        RingProducer<BY, NG> P(sm.ring, maps, xb, yb);
+        for (int z = z0; z < z1; ++z) produce_plane_ct<false>(P, fb, cb, z);
+      } else {
+        for (int z = z0; z < z1; ++z) produce_plane(sm.ring, gi, ph, S, maps, xb, yb, z);
+      }
     }
     return;
   }

@@ -361,11 +361,11 @@ int launch_fused_tma_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
   if (r) return r;
   constexpr int TX = 30, TY = BY - 2;
   const size_t smem = sizeof(FusedSmem<BY, NG>);
-  static bool attr_set = false;  // per process; the attribute is per function
-  if (!attr_set) {
+  static unsigned attr_set = 0;  // bit per device: the attribute is per function and device
+  if (!(attr_set >> s.device & 1u)) {
     CK(cudaFuncSetAttribute(k_fused_tma<BY, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)smem));
-    attr_set = true;
+    attr_set |= 1u << s.device;
   }
   const long long cols = (long long)((s.g.nx + TX - 1) / TX) * ((s.g.ny + TY - 1) / TY);
   const int zc = balanced_zchunk(s, cols, 1, ctx->opts.z_chunk);
@@ -374,7 +374,8 @@ int launch_fused_tma_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
   const dim3 grid(tiles_x * tiles_y, 1, (s.g.nz + zc - 1) / zc);
   const dim3 block(32, BY + 1);
   k_fused_tma<BY, NG><<<grid, block, smem, s.stream>>>(s.g, A, s.maps[map_index(BY)], S, zc,
-                                                       tiles_y, tiles_x, ctx->opts.reserved[3] == 0);
+                                                       tiles_y, tiles_x, ctx->opts.reserved[3] == 0,
+                                                       cur * 12, nf * 12, ctx->opts.reserved[4] == 0);
   CK(cudaGetLastError());
   s.cur ^= 1;
   ++*launches;
@@ -427,18 +428,26 @@ int launch_tblock2_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
   const int cur = s.cur, nf = s.nfield_sets;
   auto fslot = [&](int k) { return cur * 12 + k; };
   auto cslot = [&](int a) { return nf * 12 + (a - 12); };
+  // reserved[1] = 2 selects the L2-scratch hand-off kernel (k_tblock2);
+  // default: the TMEM hand-off (k_tblock_tm)
+  const bool scratch = ctx->opts.reserved[1] == 2;
   GroupSeq S1, S2;
   seq_plane(S1, fslot, cslot);
-  seq_level2(S2, cslot);
+  if (scratch)
+    seq_level2(S2, cslot);
+  else
+    seq_level2_coef(S2, cslot);
   int r = ensure_tmap(s, BY, ctx->opts.reserved[2]);
   if (r) return r;
-  if ((r = ensure_scratch<BY>(s))) return r;
-  const size_t smem = sizeof(TbSmem<BY, NG>);
-  static bool attr_set = false;
-  if (!attr_set) {
+  if (scratch && (r = ensure_scratch<BY>(s))) return r;
+  const size_t smem = scratch ? sizeof(TbSmem<BY, NG>) : sizeof(TmSmem<BY, NG>);
+  static unsigned attr_set = 0;  // bit per device
+  if (!(attr_set >> s.device & 1u)) {
     CK(cudaFuncSetAttribute(k_tblock2<BY, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)smem));
-    attr_set = true;
+                            (int)sizeof(TbSmem<BY, NG>)));
+    CK(cudaFuncSetAttribute(k_tblock_tm<BY, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)sizeof(TmSmem<BY, NG>)));
+    attr_set |= 1u << s.device;
   }
   constexpr int TX2 = 28, TY2 = BY - 4;
   const int tiles_x = (s.g.nx + TX2 - 1) / TX2, tiles_y = (s.g.ny + TY2 - 1) / TY2;
@@ -460,15 +469,20 @@ int launch_tblock2_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
     }
     zc = (s.g.nz + best_c - 1) / best_c;
   }
-  TbParams P;
-  P.zc = zc;
-  P.tiles_x = tiles_x;
-  for (int k = 0; k < 12; ++k) P.field_in[k] = fslot(k);
-  P.scratch = s.scratch;
   const dim3 grid(tiles_x * tiles_y, 1, (s.g.nz + zc - 1) / zc);
   const dim3 block(32, BY + 1);
-  k_tblock2<BY, NG><<<grid, block, smem, s.stream>>>(s.g, A, s.maps[map_index(BY)], s.smap, S1,
-                                                     S2, P);
+  if (scratch) {
+    TbParams P;
+    P.zc = zc;
+    P.tiles_x = tiles_x;
+    for (int k = 0; k < 12; ++k) P.field_in[k] = fslot(k);
+    P.scratch = s.scratch;
+    k_tblock2<BY, NG><<<grid, block, smem, s.stream>>>(s.g, A, s.maps[map_index(BY)], s.smap, S1,
+                                                       S2, P);
+  } else {
+    k_tblock_tm<BY, NG><<<grid, block, smem, s.stream>>>(s.g, A, s.maps[map_index(BY)], cur * 12,
+                                                         nf * 12, zc, tiles_x);
+  }
   CK(cudaGetLastError());
   s.cur ^= 1;
   ++*launches;
@@ -499,11 +513,11 @@ int launch_fused_table_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
   T.n_mat = s.n_mat;
   constexpr int TX = 30, TY = BY - 2;
   const size_t smem = sizeof(TableSmem<BY, NG>);
-  static bool attr_set = false;
-  if (!attr_set) {
+  static unsigned attr_set = 0;  // bit per device
+  if (!(attr_set >> s.device & 1u)) {
     CK(cudaFuncSetAttribute(k_fused_table<BY, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)smem));
-    attr_set = true;
+    attr_set |= 1u << s.device;
   }
   const int tiles_x = (s.g.nx + TX - 1) / TX, tiles_y = (s.g.ny + TY - 1) / TY;
   const int zc = balanced_zchunk(s, (long long)tiles_x * tiles_y, 1, ctx->opts.z_chunk);

@@ -1,0 +1,207 @@
+// thiim_producer.cuh -- compile-time producer sequences for the TMA ring.
+//
+// The producer is a single lane issuing ~40 (fused) or ~68 (TBLOCK) TMA boxes
+// per plane.  Interpreting a runtime sequence (GroupSeq in param space: one
+// LDC per element, box geometry by branch, R2UR of every operand) costs ~100+
+// dependent cycles per box, which starved the TBLOCK consumers (ncu: 51% of
+// warp samples on full-barrier waits while the producer almost never waited
+// for an empty slot).  Here the sequence is straight-line code: box shapes,
+// byte counts and L2 policies are template constants, only the slot bases
+// (which field set is current) and the tile / plane coordinates are runtime.
+//
+// The group order and contents equal seq_plane / seq_level2_coef, which the
+// consumer code reads in the same order.
+#pragma once
+
+#include "thiim_async.cuh"
+#include "thiim_common.cuh"
+#include "thiim_ring.cuh"
+
+namespace thiim_gpu {
+
+template <int BY, int NG>
+struct RingProducer {
+  using Gm = BoxGeom<BY>;
+  Ring<BY, NG>& R;
+  const TmaMaps& maps;
+  int xb, yb;  // interior coordinates of thread (0,0)
+  int gi = 0;
+  uint32_t ph = 0;
+
+  __device__ RingProducer(Ring<BY, NG>& r, const TmaMaps& m, int xb_, int yb_)
+      : R(r), maps(m), xb(xb_), yb(yb_) {}
+
+  template <int BYTES>
+  __device__ __forceinline__ void begin() {
+    mbar_wait(&R.empty[gi], ph ^ 1);
+    mbar_arrive_expect_tx(&R.full[gi], (uint32_t)BYTES);
+  }
+  __device__ __forceinline__ void end() {
+    if (++gi == NG) {
+      gi = 0;
+      ph ^= 1;
+    }
+  }
+  // box k of the current group: array `slot` at padded plane `pz`
+  template <int B>
+  __device__ __forceinline__ void box(int k, int slot, int pz) {
+    tma_load_4d(&R.buf[gi][k][0], &maps.m[B], 2 * (xb + 1 + Gm::x0(B)), yb + 1 + Gm::y0(B), pz, slot,
+                &R.full[gi]);
+  }
+  template <int B>
+  __device__ __forceinline__ void box(int k, int slot, int pz, uint64_t pol) {
+    tma_load_4d_hint(&R.buf[gi][k][0], &maps.m[B], 2 * (xb + 1 + Gm::x0(B)), yb + 1 + Gm::y0(B), pz,
+                     slot, &R.full[gi], pol);
+  }
+};
+
+// Slot bases: field component c of the current set = fb + c; coefficient
+// array a (12..39 in the reference's 40-array order) = cb + (a - 12).
+//
+// One fused / level-1 plane z (seq_plane): E_old(z+1) x6, then per H component
+// F, t, c (, src), then the E coefficients.  HINT: per-class L2 policies
+// (fields, coefficients) or none.
+template <bool HINT, int BY, int NG>
+__device__ __forceinline__ void produce_plane_ct(RingProducer<BY, NG>& P, int fb, int cb, int z,
+                                                 uint64_t pf = 0, uint64_t pc = 0) {
+  using Gm = BoxGeom<BY>;
+  constexpr int SA = Gm::bytes(BOX_A), SB = Gm::bytes(BOX_B), SBX = Gm::bytes(BOX_BX),
+                SBY = Gm::bytes(BOX_BY), SC = Gm::bytes(BOX_C);
+  const int p0 = z + 1, p1 = z + 2;
+#define BOXF(B, k, slot, pz) \
+  do {                        \
+    if (HINT)                 \
+      P.template box<B>(k, slot, pz, pf); \
+    else                      \
+      P.template box<B>(k, slot, pz);     \
+  } while (0)
+#define BOXC(B, k, slot, pz) \
+  do {                        \
+    if (HINT)                 \
+      P.template box<B>(k, slot, pz, pc); \
+    else                      \
+      P.template box<B>(k, slot, pz);     \
+  } while (0)
+  P.template begin<4 * SA>();
+  BOXF(BOX_A, 0, fb + EXY, p1);
+  BOXF(BOX_A, 1, fb + EXZ, p1);
+  BOXF(BOX_A, 2, fb + EYX, p1);
+  BOXF(BOX_A, 3, fb + EYZ, p1);
+  P.end();
+  P.template begin<2 * SA>();
+  BOXF(BOX_A, 0, fb + EZX, p1);
+  BOXF(BOX_A, 1, fb + EZY, p1);
+  P.end();
+  P.template begin<3 * SBY>();  // Hxy
+  BOXF(BOX_BY, 0, fb + HXY, p0);
+  BOXC(BOX_BY, 1, cb + HXY, p0);
+  BOXC(BOX_BY, 2, cb + 12 + HXY, p0);
+  P.end();
+  P.template begin<4 * SBY>();  // Hxz
+  BOXF(BOX_BY, 0, fb + HXZ, p0);
+  BOXC(BOX_BY, 1, cb + HXZ, p0);
+  BOXC(BOX_BY, 2, cb + 12 + HXZ, p0);
+  BOXC(BOX_BY, 3, cb + 24 + SRC_HXZ, p0);
+  P.end();
+  P.template begin<3 * SBX>();  // Hyx
+  BOXF(BOX_BX, 0, fb + HYX, p0);
+  BOXC(BOX_BX, 1, cb + HYX, p0);
+  BOXC(BOX_BX, 2, cb + 12 + HYX, p0);
+  P.end();
+  P.template begin<4 * SBX>();  // Hyz
+  BOXF(BOX_BX, 0, fb + HYZ, p0);
+  BOXC(BOX_BX, 1, cb + HYZ, p0);
+  BOXC(BOX_BX, 2, cb + 12 + HYZ, p0);
+  BOXC(BOX_BX, 3, cb + 24 + SRC_HYZ, p0);
+  P.end();
+  P.template begin<3 * SB>();  // Hzx
+  BOXF(BOX_B, 0, fb + HZX, p0);
+  BOXC(BOX_B, 1, cb + HZX, p0);
+  BOXC(BOX_B, 2, cb + 12 + HZX, p0);
+  P.end();
+  P.template begin<3 * SB>();  // Hzy
+  BOXF(BOX_B, 0, fb + HZY, p0);
+  BOXC(BOX_B, 1, cb + HZY, p0);
+  BOXC(BOX_B, 2, cb + 12 + HZY, p0);
+  P.end();
+  P.template begin<4 * SC>();  // Exy, Eyx
+  BOXC(BOX_C, 0, cb + EXY, p0);
+  BOXC(BOX_C, 1, cb + 12 + EXY, p0);
+  BOXC(BOX_C, 2, cb + EYX, p0);
+  BOXC(BOX_C, 3, cb + 12 + EYX, p0);
+  P.end();
+  P.template begin<3 * SC>();  // Exz
+  BOXC(BOX_C, 0, cb + EXZ, p0);
+  BOXC(BOX_C, 1, cb + 12 + EXZ, p0);
+  BOXC(BOX_C, 2, cb + 24 + SRC_EXZ, p0);
+  P.end();
+  P.template begin<3 * SC>();  // Eyz
+  BOXC(BOX_C, 0, cb + EYZ, p0);
+  BOXC(BOX_C, 1, cb + 12 + EYZ, p0);
+  BOXC(BOX_C, 2, cb + 24 + SRC_EYZ, p0);
+  P.end();
+  P.template begin<4 * SC>();  // Ezx, Ezy
+  BOXC(BOX_C, 0, cb + EZX, p0);
+  BOXC(BOX_C, 1, cb + 12 + EZX, p0);
+  BOXC(BOX_C, 2, cb + EZY, p0);
+  BOXC(BOX_C, 3, cb + 12 + EZY, p0);
+  P.end();
+#undef BOXF
+#undef BOXC
+}
+
+// Level-2 coefficient groups of plane r (seq_level2_coef), policy `pol`.
+template <int BY, int NG>
+__device__ __forceinline__ void produce_level2_coef_ct(RingProducer<BY, NG>& P, int cb, int r,
+                                                       uint64_t pol) {
+  using Gm = BoxGeom<BY>;
+  constexpr int SB = Gm::bytes(BOX_B), SBX = Gm::bytes(BOX_BX), SBY = Gm::bytes(BOX_BY),
+                SC = Gm::bytes(BOX_C);
+  const int p0 = r + 1;
+  P.template begin<2 * SBY + 2 * SBX>();  // Hxy t c, Hyx t c
+  P.template box<BOX_BY>(0, cb + HXY, p0, pol);
+  P.template box<BOX_BY>(1, cb + 12 + HXY, p0, pol);
+  P.template box<BOX_BX>(2, cb + HYX, p0, pol);
+  P.template box<BOX_BX>(3, cb + 12 + HYX, p0, pol);
+  P.end();
+  P.template begin<3 * SBY>();  // Hxz t c src
+  P.template box<BOX_BY>(0, cb + HXZ, p0, pol);
+  P.template box<BOX_BY>(1, cb + 12 + HXZ, p0, pol);
+  P.template box<BOX_BY>(2, cb + 24 + SRC_HXZ, p0, pol);
+  P.end();
+  P.template begin<3 * SBX>();  // Hyz t c src
+  P.template box<BOX_BX>(0, cb + HYZ, p0, pol);
+  P.template box<BOX_BX>(1, cb + 12 + HYZ, p0, pol);
+  P.template box<BOX_BX>(2, cb + 24 + SRC_HYZ, p0, pol);
+  P.end();
+  P.template begin<4 * SB>();  // Hzx t c, Hzy t c
+  P.template box<BOX_B>(0, cb + HZX, p0, pol);
+  P.template box<BOX_B>(1, cb + 12 + HZX, p0, pol);
+  P.template box<BOX_B>(2, cb + HZY, p0, pol);
+  P.template box<BOX_B>(3, cb + 12 + HZY, p0, pol);
+  P.end();
+  P.template begin<4 * SC>();  // Exy t c, Eyx t c
+  P.template box<BOX_C>(0, cb + EXY, p0, pol);
+  P.template box<BOX_C>(1, cb + 12 + EXY, p0, pol);
+  P.template box<BOX_C>(2, cb + EYX, p0, pol);
+  P.template box<BOX_C>(3, cb + 12 + EYX, p0, pol);
+  P.end();
+  P.template begin<3 * SC>();  // Exz t c src
+  P.template box<BOX_C>(0, cb + EXZ, p0, pol);
+  P.template box<BOX_C>(1, cb + 12 + EXZ, p0, pol);
+  P.template box<BOX_C>(2, cb + 24 + SRC_EXZ, p0, pol);
+  P.end();
+  P.template begin<3 * SC>();  // Eyz t c src
+  P.template box<BOX_C>(0, cb + EYZ, p0, pol);
+  P.template box<BOX_C>(1, cb + 12 + EYZ, p0, pol);
+  P.template box<BOX_C>(2, cb + 24 + SRC_EYZ, p0, pol);
+  P.end();
+  P.template begin<4 * SC>();  // Ezx t c, Ezy t c
+  P.template box<BOX_C>(0, cb + EZX, p0, pol);
+  P.template box<BOX_C>(1, cb + 12 + EZX, p0, pol);
+  P.template box<BOX_C>(2, cb + EZY, p0, pol);
+  P.template box<BOX_C>(3, cb + 12 + EZY, p0, pol);
+  P.end();
+}
+
+}  // namespace thiim_gpu

@@ -38,6 +38,8 @@
 #include "thiim_common.cuh"
 #include "thiim_fused_tma.cuh"
 #include "thiim_ring.cuh"
+#include "thiim_producer.cuh"
+#include "thiim_tmem.cuh"
 
 namespace thiim_gpu {
 
@@ -522,6 +524,408 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
     }
   }
 #undef RD
+}
+
+// ---------------------------------------------------------------------------
+// k_tblock_tm: the same two-level wavefront with the level-1 -> level-2
+// hand-off kept on chip.  Every value level 2 reads at its own cell from level 1
+// (E^1 and H^1 of plane r, 12 double2) was computed by the SAME thread one
+// iteration earlier, so it never needs to leave the thread: it is parked in the
+// thread's TMEM lane (double-buffered by plane parity), together with the
+// E_old splits level 1 carries to the next plane.  That removes the L2 scratch
+// ring (12 array-planes written and re-fetched per iteration), its ready
+// barriers and the register spills of the register-carried variant; level 2's
+// producer sequence shrinks to the 8 coefficient groups.
+//
+// TMEM columns per warp (warp w: lanes 32*(w%4).., columns 128*(w/4)..):
+//   [0,48)   slot 0: E^1 (24 cols), H^1 (24 cols)   -- planes with r even
+//   [48,96)  slot 1: same                            -- r odd
+//   [96,120) E_old splits of the next level-1 plane
+template <class CS>
+inline void seq_level2_coef(GroupSeq& S, CS cslot) {
+  GroupSeq full;
+  seq_level2(full, cslot);
+  S.ngroups = 0;
+  S.nelem = 0;
+  int e = 0;
+  for (int gr = 0; gr < full.ngroups; ++gr) {
+    const int n = full.gsize[gr];
+    if (full.e[e].src != 2) {  // drop the three scratch groups
+      S.gsize[S.ngroups++] = (unsigned char)n;
+      for (int k = 0; k < n; ++k) S.e[S.nelem++] = full.e[e + k];
+    }
+    e += n;
+  }
+}
+
+template <int BY, int NG>
+struct TmSmem {
+  Ring<BY, NG> ring;
+  double2 sE[3][BY][32];
+  double2 sH[3][BY][32];
+  uint32_t tmem_base;
+};
+
+template <int BY, int NG>
+__global__ void __launch_bounds__(32 * (BY + 1), 1)
+    k_tblock_tm(Grid g, Arrays A, const __grid_constant__ TmaMaps maps, int fb, int cb, int zc,
+                int tiles_x) {
+  constexpr int NCOMP = 32 * BY;
+  constexpr int TX2 = 28, TY2 = BY - 4;
+  constexpr int LAG = 1;
+  static_assert(BY <= 16, "TMEM carry layout: at most 4 consumer warps per lane quadrant");
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  TmSmem<BY, NG>& sm = *reinterpret_cast<TmSmem<BY, NG>*>(smem_raw);
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int btx = blockIdx.x % tiles_x, bty = blockIdx.x / tiles_x;
+  const int xb = btx * TX2 - 2, yb = bty * TY2 - 2;
+  const int z0 = blockIdx.z * zc;
+  const int z1 = min(g.nz, z0 + zc);
+  const long long pxy = g.pxy;
+  const int qs = max(z0 - 1, 0);
+  const int q1 = min(z1, g.nz - 1);
+  const int qe = z1 + LAG - 1;
+
+  if (ty == 0) tm_alloc<512>(&sm.tmem_base);
+  if (tx == 0 && ty == 0) {
+    ring_init(sm.ring, BY);
+    fence_mbar_init();
+  }
+  tm_fence_before();
+  __syncthreads();
+  tm_fence_after();
+
+  if (ty == BY) {
+    // ------------------------------------------------------------ producer
+    if (tx == 0) {
+#pragma unroll
+      for (int b = 0; b < NBOX; ++b) tma_prefetch_desc(&maps.m[b]);
+      const uint64_t keep = policy_evict_last(), drop = policy_evict_first();
+      RingProducer<BY, NG> P(sm.ring, maps, xb, yb);
+      for (int q = qs; q <= qe; ++q) {
+        // level 1 keeps coefficients in L2 for level 2 (their last use)
+        if (q <= q1) produce_plane_ct<true>(P, fb, cb, q, drop, keep);
+        const int r = q - LAG;
+        if (r >= z0 - 1 && r < z1) produce_level2_coef_ct(P, cb, r, drop);
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------- consumers
+  const uint32_t tcar = tm_warp_addr(sm.tmem_base, ty, 128 * (ty >> 2));
+  const uint32_t tnext = tcar + 96;
+  const int x = xb + tx, y = yb + ty;
+  const bool inpad = (x >= -1) && (x <= g.nx) && (y >= -1) && (y <= g.ny);
+  const bool interior = (x >= 0) && (x < g.nx) && (y >= 0) && (y < g.ny);
+  const int xs = inpad ? x : 0, ys = inpad ? y : 0;
+  const bool own1 = tx >= 1 && tx <= 30 && ty >= 1 && ty <= BY - 2;
+  const bool rx1 = (tx == 0) && (ty >= 1) && (ty <= BY - 2);
+  const bool ry1 = (ty == 0) && (tx >= 1) && (tx <= 30);
+  const bool own2 = tx >= 2 && tx <= 29 && ty >= 2 && ty <= BY - 3;
+  const bool rx2 = (tx == 1) && (ty >= 2) && (ty <= BY - 3);
+  const bool ry2 = (ty == 1) && (tx >= 2) && (tx <= 29);
+  const bool upd1_x = (own1 || ry1) && interior;
+  const bool upd1_y = (own1 || rx1) && interior;
+  const bool upd1_z = (own1 || rx1 || ry1) && interior;
+  const bool upd2_x = (own2 || ry2) && interior;
+  const bool upd2_y = (own2 || rx2) && interior;
+  const bool upd2_z = (own2 || rx2 || ry2) && interior;
+
+  auto& R = sm.ring;
+  RingCursor rc;
+#define RD(k, b) ring_read(R, rc, k, b, tx, ty)
+
+  // ---- level-1 prologue: E_old splits at qs (to TMEM), H^1 sums at qs-1
+  double2 pH1x = make_double2(0.0, 0.0), pH1y = make_double2(0.0, 0.0);
+  {
+    double2 e[6];
+    const long long i1 = g.idx(xs, ys, qs);
+#pragma unroll
+    for (int k = 0; k < 6; ++k) e[k] = inpad ? __ldg(A.f[k] + i1) : make_double2(0.0, 0.0);
+    tm_st6(tnext, e);
+    const long long im = i1 - pxy;
+    if (qs == 0) {
+      if (own1 && inpad) {  // ghost plane below the grid: H never updated
+        pH1x = csum(__ldg(A.f[HXY] + im), __ldg(A.f[HXZ] + im));
+        pH1y = csum(__ldg(A.f[HYX] + im), __ldg(A.f[HYZ] + im));
+      }
+    } else {
+      if (inpad) {
+        double2 m[6];
+#pragma unroll
+        for (int k = 0; k < 6; ++k) m[k] = __ldg(A.f[k] + im);
+        sm.sE[0][ty][tx] = csum(m[EXY], m[EXZ]);
+        sm.sE[1][ty][tx] = csum(m[EYX], m[EYZ]);
+        sm.sE[2][ty][tx] = csum(m[EZX], m[EZY]);
+      }
+      named_sync(1, NCOMP);
+      if (own1 && inpad) {
+        if (interior) {
+          const double2 sEx = sm.sE[0][ty][tx], sEy = sm.sE[1][ty][tx], sEz = sm.sE[2][ty][tx];
+          const double2 nEx = csum(e[EXY], e[EXZ]), nEy = csum(e[EYX], e[EYZ]);
+          const double2 hxy = upd(__ldg(A.f[HXY] + im), __ldg(A.t[HXY] + im),
+                                  __ldg(A.c[HXY] + im), sm.sE[2][ty + 1][tx], sEz);
+          const double2 hxz = upd_src(__ldg(A.f[HXZ] + im), __ldg(A.t[HXZ] + im),
+                                      __ldg(A.c[HXZ] + im), nEy, sEy, __ldg(A.src[SRC_HXZ] + im));
+          const double2 hyx = upd(__ldg(A.f[HYX] + im), __ldg(A.t[HYX] + im),
+                                  __ldg(A.c[HYX] + im), sm.sE[2][ty][tx + 1], sEz);
+          const double2 hyz = upd_src(__ldg(A.f[HYZ] + im), __ldg(A.t[HYZ] + im),
+                                      __ldg(A.c[HYZ] + im), nEx, sEx, __ldg(A.src[SRC_HYZ] + im));
+          pH1x = csum(hxy, hxz);
+          pH1y = csum(hyx, hyz);
+        } else {
+          pH1x = csum(__ldg(A.f[HXY] + im), __ldg(A.f[HXZ] + im));
+          pH1y = csum(__ldg(A.f[HYX] + im), __ldg(A.f[HYZ] + im));
+        }
+      }
+      named_sync(1, NCOMP);
+    }
+  }
+  double2 pH2x = make_double2(0.0, 0.0), pH2y = make_double2(0.0, 0.0);
+  double2 nE2x = make_double2(0.0, 0.0), nE2y = make_double2(0.0, 0.0);
+  const uint64_t first = policy_evict_first();
+
+  for (int q = qs; q <= qe; ++q) {
+    // ================= level 1 at plane q (step n) -> TMEM slot q&1
+    if (q <= q1) {
+      const uint32_t tslot = tcar + 48 * (q & 1);
+      double2 e[6];
+      tm_ld6(tnext, e);  // E_old(q)
+      double2 nEx, nEy;
+      {
+        double2 en[6];
+        ring_wait(R, rc);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) en[k] = RD(k, BOX_A);
+        ring_release(R, rc, tx);
+        ring_wait(R, rc);
+        en[4] = RD(0, BOX_A);
+        en[5] = RD(1, BOX_A);
+        ring_release(R, rc, tx);
+        tm_st6(tnext, en);  // E_old(q+1) for the next plane
+        nEx = csum(en[EXY], en[EXZ]);
+        nEy = csum(en[EYX], en[EYZ]);
+      }
+      if (inpad) {
+        sm.sE[0][ty][tx] = csum(e[EXY], e[EXZ]);
+        sm.sE[1][ty][tx] = csum(e[EYX], e[EYZ]);
+        sm.sE[2][ty][tx] = csum(e[EZX], e[EZY]);
+      }
+      named_sync(1, NCOMP);
+      const double2 sEx = sm.sE[0][ty][tx], sEy = sm.sE[1][ty][tx], sEz = sm.sE[2][ty][tx];
+      double2 h[6];
+      {
+        ring_wait(R, rc);
+        h[0] = RD(0, BOX_BY);
+        const double2 t = RD(1, BOX_BY), c = RD(2, BOX_BY);
+        ring_release(R, rc, tx);
+        if (upd1_x) h[0] = upd(h[0], t, c, sm.sE[2][ty + 1][tx], sEz);
+      }
+      {
+        ring_wait(R, rc);
+        h[1] = RD(0, BOX_BY);
+        const double2 t = RD(1, BOX_BY), c = RD(2, BOX_BY), s = RD(3, BOX_BY);
+        ring_release(R, rc, tx);
+        if (upd1_x) h[1] = upd_src(h[1], t, c, nEy, sEy, s);
+      }
+      {
+        ring_wait(R, rc);
+        h[2] = RD(0, BOX_BX);
+        const double2 t = RD(1, BOX_BX), c = RD(2, BOX_BX);
+        ring_release(R, rc, tx);
+        if (upd1_y) h[2] = upd(h[2], t, c, sm.sE[2][ty][tx + 1], sEz);
+      }
+      {
+        ring_wait(R, rc);
+        h[3] = RD(0, BOX_BX);
+        const double2 t = RD(1, BOX_BX), c = RD(2, BOX_BX), s = RD(3, BOX_BX);
+        ring_release(R, rc, tx);
+        if (upd1_y) h[3] = upd_src(h[3], t, c, nEx, sEx, s);
+      }
+      {
+        ring_wait(R, rc);
+        h[4] = RD(0, BOX_B);
+        const double2 t = RD(1, BOX_B), c = RD(2, BOX_B);
+        ring_release(R, rc, tx);
+        if (upd1_z) h[4] = upd(h[4], t, c, sm.sE[1][ty][tx + 1], sEy);
+      }
+      {
+        ring_wait(R, rc);
+        h[5] = RD(0, BOX_B);
+        const double2 t = RD(1, BOX_B), c = RD(2, BOX_B);
+        ring_release(R, rc, tx);
+        if (upd1_z) h[5] = upd(h[5], t, c, sm.sE[0][ty + 1][tx], sEx);
+      }
+      if (own1 || rx1 || ry1) {
+        sm.sH[0][ty][tx] = csum(h[0], h[1]);
+        sm.sH[1][ty][tx] = csum(h[2], h[3]);
+        sm.sH[2][ty][tx] = csum(h[4], h[5]);
+      }
+      tm_st6(tslot + 24, h);  // H^1(q)
+      named_sync(1, NCOMP);
+      const double2 sHx = sm.sH[0][ty][tx], sHy = sm.sH[1][ty][tx], sHz = sm.sH[2][ty][tx];
+      const bool ue = own1 && interior;
+      {
+        ring_wait(R, rc);
+        const double2 t0 = RD(0, BOX_C), c0 = RD(1, BOX_C), t1 = RD(2, BOX_C), c1 = RD(3, BOX_C);
+        ring_release(R, rc, tx);
+        if (ue) {
+          e[EXY] = upd(e[EXY], t0, c0, sm.sH[2][ty - 1][tx], sHz);
+          e[EYX] = upd(e[EYX], t1, c1, sm.sH[2][ty][tx - 1], sHz);
+        }
+      }
+      {
+        ring_wait(R, rc);
+        const double2 t = RD(0, BOX_C), c = RD(1, BOX_C), s = RD(2, BOX_C);
+        ring_release(R, rc, tx);
+        if (ue) e[EXZ] = upd_src(e[EXZ], t, c, pH1y, sHy, s);
+      }
+      {
+        ring_wait(R, rc);
+        const double2 t = RD(0, BOX_C), c = RD(1, BOX_C), s = RD(2, BOX_C);
+        ring_release(R, rc, tx);
+        if (ue) e[EYZ] = upd_src(e[EYZ], t, c, pH1x, sHx, s);
+      }
+      {
+        ring_wait(R, rc);
+        const double2 t0 = RD(0, BOX_C), c0 = RD(1, BOX_C), t1 = RD(2, BOX_C), c1 = RD(3, BOX_C);
+        ring_release(R, rc, tx);
+        if (ue) {
+          e[EZX] = upd(e[EZX], t0, c0, sm.sH[1][ty][tx - 1], sHy);
+          e[EZY] = upd(e[EZY], t1, c1, sm.sH[0][ty - 1][tx], sHx);
+        }
+      }
+      tm_st6(tslot, e);  // E^1(q) (ghost cells pass through unchanged)
+      nE2x = csum(e[EXY], e[EXZ]);
+      nE2y = csum(e[EYX], e[EYZ]);
+      pH1x = sHx;
+      pH1y = sHy;
+    }
+
+    // ================= level 2 at plane r = q-1 (step n+1) -> output set
+    const int r = q - LAG;
+    if (r >= z0 - 1 && r < z1) {
+      const long long i = g.idx(xs, ys, r);
+      const bool plane_ok = r >= 0;
+      double2 nEx = nE2x, nEy = nE2y;
+      if (q > q1) {  // plane r+1 is the top ghost plane: level 1 did not run
+        double2 e[6];
+        tm_ld6(tnext, e);
+        nEx = csum(e[EXY], e[EXZ]);
+        nEy = csum(e[EYX], e[EYZ]);
+      }
+      double2 e1[6], h[6];
+      if (plane_ok) {
+        const uint32_t tslot = tcar + 48 * (r & 1);
+        tm_ld6(tslot, e1);
+        tm_ld6(tslot + 24, h);
+      } else {  // ghost plane -1: never updated, read the input set
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+          e1[k] = inpad ? __ldg(A.f[k] + i) : make_double2(0.0, 0.0);
+          h[k] = inpad ? __ldg(A.f[HXY + k] + i) : make_double2(0.0, 0.0);
+        }
+      }
+      if (inpad) {
+        sm.sE[0][ty][tx] = csum(e1[EXY], e1[EXZ]);
+        sm.sE[1][ty][tx] = csum(e1[EYX], e1[EYZ]);
+        sm.sE[2][ty][tx] = csum(e1[EZX], e1[EZY]);
+      }
+      named_sync(1, NCOMP);
+      const double2 sEx = sm.sE[0][ty][tx], sEy = sm.sE[1][ty][tx], sEz = sm.sE[2][ty][tx];
+      const bool u2x = upd2_x && plane_ok, u2y = upd2_y && plane_ok, u2z = upd2_z && plane_ok;
+      {  // Hxy, Hyx
+        ring_wait(R, rc);
+        const double2 t0 = RD(0, BOX_BY), c0 = RD(1, BOX_BY), t1 = RD(2, BOX_BX), c1 = RD(3, BOX_BX);
+        ring_release(R, rc, tx);
+        if (u2x) h[0] = upd(h[0], t0, c0, sm.sE[2][ty + 1][tx], sEz);
+        if (u2y) h[2] = upd(h[2], t1, c1, sm.sE[2][ty][tx + 1], sEz);
+      }
+      {  // Hxz
+        ring_wait(R, rc);
+        const double2 t = RD(0, BOX_BY), c = RD(1, BOX_BY), s = RD(2, BOX_BY);
+        ring_release(R, rc, tx);
+        if (u2x) h[1] = upd_src(h[1], t, c, nEy, sEy, s);
+      }
+      {  // Hyz
+        ring_wait(R, rc);
+        const double2 t = RD(0, BOX_BX), c = RD(1, BOX_BX), s = RD(2, BOX_BX);
+        ring_release(R, rc, tx);
+        if (u2y) h[3] = upd_src(h[3], t, c, nEx, sEx, s);
+      }
+      {  // Hzx, Hzy
+        ring_wait(R, rc);
+        const double2 t0 = RD(0, BOX_B), c0 = RD(1, BOX_B), t1 = RD(2, BOX_B), c1 = RD(3, BOX_B);
+        ring_release(R, rc, tx);
+        if (u2z) h[4] = upd(h[4], t0, c0, sm.sE[1][ty][tx + 1], sEy);
+        if (u2z) h[5] = upd(h[5], t1, c1, sm.sE[0][ty + 1][tx], sEx);
+      }
+      if (r == z0 - 1) {
+        // chunk prologue: only the H_new sums of the plane below the chunk
+        if (own2) {
+          pH2x = csum(h[0], h[1]);
+          pH2y = csum(h[2], h[3]);
+        }
+        for (int k = 0; k < 4; ++k) {  // E-coefficient groups, unused here
+          ring_wait(R, rc);
+          ring_release(R, rc, tx);
+        }
+        named_sync(1, NCOMP);  // sE reads done before the next level-1 writes
+        continue;
+      }
+      if (own2 && interior) {
+#pragma unroll
+        for (int k = 0; k < 6; ++k) st_hint(A.fo[HXY + k] + i, h[k], first);
+      }
+      if (own2 || rx2 || ry2) {
+        sm.sH[0][ty][tx] = csum(h[0], h[1]);
+        sm.sH[1][ty][tx] = csum(h[2], h[3]);
+        sm.sH[2][ty][tx] = csum(h[4], h[5]);
+      }
+      named_sync(1, NCOMP);
+      const double2 sHx = sm.sH[0][ty][tx], sHy = sm.sH[1][ty][tx], sHz = sm.sH[2][ty][tx];
+      const bool ue = own2 && interior;
+      {  // Exy, Eyx
+        ring_wait(R, rc);
+        const double2 t0 = RD(0, BOX_C), c0 = RD(1, BOX_C), t1 = RD(2, BOX_C), c1 = RD(3, BOX_C);
+        ring_release(R, rc, tx);
+        if (ue) {
+          st_hint(A.fo[EXY] + i, upd(e1[EXY], t0, c0, sm.sH[2][ty - 1][tx], sHz), first);
+          st_hint(A.fo[EYX] + i, upd(e1[EYX], t1, c1, sm.sH[2][ty][tx - 1], sHz), first);
+        }
+      }
+      {  // Exz
+        ring_wait(R, rc);
+        const double2 t = RD(0, BOX_C), c = RD(1, BOX_C), s = RD(2, BOX_C);
+        ring_release(R, rc, tx);
+        if (ue) st_hint(A.fo[EXZ] + i, upd_src(e1[EXZ], t, c, pH2y, sHy, s), first);
+      }
+      {  // Eyz
+        ring_wait(R, rc);
+        const double2 t = RD(0, BOX_C), c = RD(1, BOX_C), s = RD(2, BOX_C);
+        ring_release(R, rc, tx);
+        if (ue) st_hint(A.fo[EYZ] + i, upd_src(e1[EYZ], t, c, pH2x, sHx, s), first);
+      }
+      {  // Ezx, Ezy
+        ring_wait(R, rc);
+        const double2 t0 = RD(0, BOX_C), c0 = RD(1, BOX_C), t1 = RD(2, BOX_C), c1 = RD(3, BOX_C);
+        ring_release(R, rc, tx);
+        if (ue) {
+          st_hint(A.fo[EZX] + i, upd(e1[EZX], t0, c0, sm.sH[1][ty][tx - 1], sHy), first);
+          st_hint(A.fo[EZY] + i, upd(e1[EZY], t1, c1, sm.sH[0][ty - 1][tx], sHx), first);
+        }
+      }
+      pH2x = sHx;
+      pH2y = sHy;
+    }
+  }
+#undef RD
+  // release TMEM once every consumer warp is done with it
+  tm_fence_before();
+  named_sync(1, NCOMP);
+  tm_fence_after();
+  if (ty == 0) tm_dealloc<512>(sm.tmem_base);
 }
 
 }  // namespace thiim_gpu
