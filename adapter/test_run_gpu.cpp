@@ -60,7 +60,7 @@ ProblemState random_state(const GridDims& d, uint64_t seed, int kind = THIIM_GEN
 
 void test_matches_run_naive_random() {
   for (GridDims d : {GridDims(12, 16, 20), GridDims(33, 7, 9), GridDims(64, 64, 64)}) {
-    for (int engine : {THIIM_ENGINE_SPLIT, THIIM_ENGINE_FUSED}) {
+    for (int engine : {THIIM_ENGINE_SPLIT, THIIM_ENGINE_FUSED, THIIM_ENGINE_TBLOCK}) {
       ProblemState a = random_state(d, 42);
       ProblemState b = clone_state(a);
       run_naive(a, 6, 4);
@@ -70,7 +70,9 @@ void test_matches_run_naive_random() {
       const StateDiff diff = compare_states(a, b);
       CHECK(diff.bitwise_equal);
       CHECK(r.steps == 6 && r.threads == 1 && r.mlups.has_value());
-      CHECK(r.balance_model == (engine == THIIM_ENGINE_SPLIT ? 1024.0 : 832.0));
+      CHECK(r.balance_model == (engine == THIIM_ENGINE_SPLIT    ? 1024.0
+                                : engine == THIIM_ENGINE_FUSED ? 832.0
+                                                               : 416.0));
     }
   }
 }

@@ -197,7 +197,7 @@ def _roofline(P, dims, engine_ran, dev_secs, launches, table=False):
     elif engine_ran == P.ENGINE_TBLOCK:
         # one launch = two THIIM iterations in one HBM pass: 832 B per cell = 416 B/LUP
         bytes_launch = 832.0 * dims.interior_cells()
-        kname = "k_tblock2<15,6>"
+        kname = "k_tblock_tm<15,6>"
     else:
         bytes_launch = 832.0 * dims.interior_cells()
         kname = "k_fused_tma<15,6>"
@@ -222,7 +222,7 @@ def run_native(args, world, rank, local):
     opts = P.GpuOptions(device=local if world > 1 else args.device, engine=engine,
                         tile_y=args.tile_y, z_chunk=args.z_chunk, min_blocks=args.min_blocks,
                         variant=args.variant, l2_promotion=args.l2_promotion,
-                        y_fastest=args.y_fastest, runtime_seq=args.runtime_seq,
+                        y_fastest=args.y_fastest, runtime_seq=args.runtime_seq, pol_mode=args.pol_mode,
                         coeff_layout=P.COEFF_TABLE if args.coeff == "table" else P.COEFF_FULL,
                         n_materials=6 if args.coeff == "table" else 0)
     iters = args.iters
@@ -415,6 +415,7 @@ def main():
     ap.add_argument("--l2-promotion", type=int, default=0)
     ap.add_argument("--y-fastest", type=int, default=0)
     ap.add_argument("--runtime-seq", type=int, default=0)
+    ap.add_argument("--pol-mode", type=int, default=0)
     ap.add_argument("--config", default="c1", choices=sorted(CONFIGS))
     ap.add_argument("--check", type=int, default=0,
                     help="multi-rank: also run CHECK steps and compare with the oracle (rank 0)")

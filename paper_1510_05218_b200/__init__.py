@@ -356,7 +356,8 @@ ENGINE_AUTO, ENGINE_SPLIT, ENGINE_FUSED, ENGINE_TBLOCK = 0, 1, 2, 3
 ENGINE_NAMES = {ENGINE_SPLIT: "gpu-split", ENGINE_FUSED: "gpu-fused", ENGINE_TBLOCK: "gpu-tblock"}
 
 
-def balance_model(engine: int, time_block: int = 1) -> float:
+def balance_model(engine: int, time_block: int = 0) -> float:
+    """Modelled HBM bytes per LUP of an engine (TBLOCK: 832 / time_block, default 2)."""
     return float(lib().thiim_gpu_balance_model(engine, time_block))
 
 
@@ -376,6 +377,7 @@ class GpuOptions:
     l2_promotion: int = 0  # TMA L2 promotion (reserved[2]): 0 none, 1 64B, 2 128B, 3 256B
     y_fastest: int = 0   # CTA order (reserved[3]): 0 x-tiles fastest (default), 1 y-tiles fastest
     runtime_seq: int = 0  # experiment (reserved[4]): 1 = fused producer interprets its box sequence at run time
+    pol_mode: int = 0  # experiment (reserved[5]): TBLOCK L2 policy set
     same_device: int = 0  # test knob (reserved[6]): all slabs of a multi-slab context on `device`
     coeff_layout: int = 0  # COEFF_FULL (reference layout) or COEFF_TABLE (material ids)
     n_materials: int = 0
@@ -390,6 +392,7 @@ class GpuOptions:
         o.reserved[2] = self.l2_promotion
         o.reserved[3] = self.y_fastest
         o.reserved[4] = self.runtime_seq
+        o.reserved[5] = self.pol_mode
         o.reserved[6] = self.same_device
         o.coeff_layout, o.n_materials = self.coeff_layout, self.n_materials
         return o

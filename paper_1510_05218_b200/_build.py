@@ -42,7 +42,9 @@ def needs_build() -> bool:
 def build(verbose: bool = False, force: bool = False) -> str:
     if not force and not needs_build():
         return LIB
-    cmd = [NVCC, *NVCC_FLAGS, "-o", LIB + ".tmp", os.path.join(CSRC, "thiim_gpu.cu"), "-lgomp"]
+    # THIIM_NVCC_EXTRA: extra flags for experiments (e.g. -DTHIIM_RING_FENCE=1)
+    extra = os.environ.get("THIIM_NVCC_EXTRA", "").split()
+    cmd = [NVCC, *NVCC_FLAGS, *extra, "-o", LIB + ".tmp", os.path.join(CSRC, "thiim_gpu.cu"), "-lgomp"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(HERE, "build.log")
     with open(log, "w") as f:

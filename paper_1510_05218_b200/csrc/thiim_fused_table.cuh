@@ -181,8 +181,8 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
     }
   }
 
-  RingCursor rc;
   auto& R = sm.ring;
+  RingCursor rc = ring_cursor(R);
 #define RD(k, b) ring_read(R, rc, k, b, tx, ty)
   int mid_next = inpad ? mat_at(z0 + 1) : 0;  // material id, one plane ahead
   for (int z = z0; z < z1; ++z, i += pxy) {
@@ -192,11 +192,11 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
     ring_wait(R, rc);
 #pragma unroll
     for (int k = 0; k < 4; ++k) en[k] = RD(k, BOX_A);
-    ring_release(R, rc, tx);
+    ring_release(R, rc, tx, ring_dep(en[0], en[1], en[2], en[3]));
     ring_wait(R, rc);
     en[4] = RD(0, BOX_A);
     en[5] = RD(1, BOX_A);
-    ring_release(R, rc, tx);
+    ring_release(R, rc, tx, ring_dep(en[4], en[5]));
     const double2* C = sm.tab[mid];
     if (inpad) {
       sm.sE[0][ty][tx] = csum(e[EXY], e[EXZ]);
@@ -213,11 +213,11 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
     h[1] = RD(1, BOX_BY);
     h[2] = RD(2, BOX_BX);
     h[3] = RD(3, BOX_BX);
-    ring_release(R, rc, tx);
+    ring_release(R, rc, tx, ring_dep(h[0], h[1], h[2], h[3]));
     ring_wait(R, rc);
     h[4] = RD(0, BOX_B);
     h[5] = RD(1, BOX_B);
-    ring_release(R, rc, tx);
+    ring_release(R, rc, tx, ring_dep(h[4], h[5]));
     if (upd_x) {
       h[0] = upd(h[0], C[HXY], C[12 + HXY], sm.sE[2][ty + 1][tx], sEz);
       h[1] = upd_src(h[1], C[HXZ], C[12 + HXZ], nEy, sEy, C[24 + SRC_HXZ]);

@@ -207,8 +207,8 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
     }
   }
 
-  RingCursor rc;
   auto& R = sm.ring;
+  RingCursor rc = ring_cursor(R);
 #define RD(k, b) ring_read(R, rc, k, b, tx, ty)
   for (int z = z0; z < z1; ++z, i += pxy) {
     // (a) E_old(z+1) splits (carried to the next plane); E sums at z to smem
@@ -216,11 +216,11 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
     ring_wait(R, rc);
 #pragma unroll
     for (int k = 0; k < 4; ++k) en[k] = RD(k, BOX_A);
-    ring_release(R, rc, tx);
+    ring_release(R, rc, tx, ring_dep(en[0], en[1], en[2], en[3]));
     ring_wait(R, rc);
     en[4] = RD(0, BOX_A);
     en[5] = RD(1, BOX_A);
-    ring_release(R, rc, tx);
+    ring_release(R, rc, tx, ring_dep(en[4], en[5]));
     if (inpad) {
       sm.sE[0][ty][tx] = csum(e[EXY], e[EXZ]);
       sm.sE[1][ty][tx] = csum(e[EYX], e[EYZ]);
@@ -236,42 +236,42 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
       ring_wait(R, rc);
       h[0] = RD(0, BOX_BY);
       const double2 t = RD(1, BOX_BY), c = RD(2, BOX_BY);
-      ring_release(R, rc, tx);
+      ring_release(R, rc, tx, ring_dep(h[0], c, t));
       if (upd_x) h[0] = upd(h[0], t, c, sm.sE[2][ty + 1][tx], sEz);
     }
     {  // Hxz
       ring_wait(R, rc);
       h[1] = RD(0, BOX_BY);
       const double2 t = RD(1, BOX_BY), c = RD(2, BOX_BY), s = RD(3, BOX_BY);
-      ring_release(R, rc, tx);
+      ring_release(R, rc, tx, ring_dep(h[1], s, c, t));
       if (upd_x) h[1] = upd_src(h[1], t, c, nEy, sEy, s);
     }
     {  // Hyx
       ring_wait(R, rc);
       h[2] = RD(0, BOX_BX);
       const double2 t = RD(1, BOX_BX), c = RD(2, BOX_BX);
-      ring_release(R, rc, tx);
+      ring_release(R, rc, tx, ring_dep(h[2], c, t));
       if (upd_y) h[2] = upd(h[2], t, c, sm.sE[2][ty][tx + 1], sEz);
     }
     {  // Hyz
       ring_wait(R, rc);
       h[3] = RD(0, BOX_BX);
       const double2 t = RD(1, BOX_BX), c = RD(2, BOX_BX), s = RD(3, BOX_BX);
-      ring_release(R, rc, tx);
+      ring_release(R, rc, tx, ring_dep(h[3], s, c, t));
       if (upd_y) h[3] = upd_src(h[3], t, c, nEx, sEx, s);
     }
     {  // Hzx
       ring_wait(R, rc);
       h[4] = RD(0, BOX_B);
       const double2 t = RD(1, BOX_B), c = RD(2, BOX_B);
-      ring_release(R, rc, tx);
+      ring_release(R, rc, tx, ring_dep(h[4], c, t));
       if (upd_z) h[4] = upd(h[4], t, c, sm.sE[1][ty][tx + 1], sEy);
     }
     {  // Hzy
       ring_wait(R, rc);
       h[5] = RD(0, BOX_B);
       const double2 t = RD(1, BOX_B), c = RD(2, BOX_B);
-      ring_release(R, rc, tx);
+      ring_release(R, rc, tx, ring_dep(h[5], c, t));
       if (upd_z) h[5] = upd(h[5], t, c, sm.sE[0][ty + 1][tx], sEx);
     }
     if (own) {
@@ -290,7 +290,7 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
     {  // Exy, Eyx
       ring_wait(R, rc);
       const double2 t0 = RD(0, BOX_C), c0 = RD(1, BOX_C), t1 = RD(2, BOX_C), c1 = RD(3, BOX_C);
-      ring_release(R, rc, tx);
+      ring_release(R, rc, tx, ring_dep(c1, t1, c0, t0));
       if (own) {
         A.fo[EXY][i] = upd(e[EXY], t0, c0, sm.sH[2][ty - 1][tx], sHz);
         A.fo[EYX][i] = upd(e[EYX], t1, c1, sm.sH[2][ty][tx - 1], sHz);
@@ -299,19 +299,19 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
     {  // Exz
       ring_wait(R, rc);
       const double2 t = RD(0, BOX_C), c = RD(1, BOX_C), s = RD(2, BOX_C);
-      ring_release(R, rc, tx);
+      ring_release(R, rc, tx, ring_dep(s, c, t));
       if (own) A.fo[EXZ][i] = upd_src(e[EXZ], t, c, pHy, sHy, s);
     }
     {  // Eyz
       ring_wait(R, rc);
       const double2 t = RD(0, BOX_C), c = RD(1, BOX_C), s = RD(2, BOX_C);
-      ring_release(R, rc, tx);
+      ring_release(R, rc, tx, ring_dep(s, c, t));
       if (own) A.fo[EYZ][i] = upd_src(e[EYZ], t, c, pHx, sHx, s);
     }
     {  // Ezx, Ezy
       ring_wait(R, rc);
       const double2 t0 = RD(0, BOX_C), c0 = RD(1, BOX_C), t1 = RD(2, BOX_C), c1 = RD(3, BOX_C);
-      ring_release(R, rc, tx);
+      ring_release(R, rc, tx, ring_dep(c1, t1, c0, t0));
       if (own) {
         A.fo[EZX][i] = upd(e[EZX], t0, c0, sm.sH[1][ty][tx - 1], sHy);
         A.fo[EZY][i] = upd(e[EZY], t1, c1, sm.sH[0][ty - 1][tx], sHx);

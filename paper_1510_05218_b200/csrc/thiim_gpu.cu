@@ -481,7 +481,8 @@ int launch_tblock2_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
                                                        S2, P);
   } else {
     k_tblock_tm<BY, NG><<<grid, block, smem, s.stream>>>(s.g, A, s.maps[map_index(BY)], cur * 12,
-                                                         nf * 12, zc, tiles_x);
+                                                         nf * 12, zc, tiles_x,
+                                                         ctx->opts.reserved[5]);
   }
   CK(cudaGetLastError());
   s.cur ^= 1;
@@ -606,7 +607,8 @@ static int create_impl(const thiim_dims* dims, const thiim_gpu_opts* opts,
     return fail(THIIM_ERR_CONFIG, "the table coefficient layout runs on the fused engine");
   if (table && (o.n_materials < 1 || o.n_materials > kMaxMaterials))
     return fail(THIIM_ERR_CONFIG, "n_materials must be in 1..16 for the table layout");
-  if (o.engine == THIIM_ENGINE_TBLOCK && ranges.size() != 1)
+  if (o.engine == THIIM_ENGINE_TBLOCK &&
+      (ranges.size() != 1 || ranges[0].first != 0 || ranges[0].second != dims->nz))
     return fail(THIIM_ERR_CONFIG, "engine TBLOCK runs on one GPU (halo slabs need 2-plane halos)");
   for (const auto& r : ranges)
     if (r.first < 0 || r.second > dims->nz || r.second - r.first < 4)
@@ -628,8 +630,11 @@ static int create_impl(const thiim_dims* dims, const thiim_gpu_opts* opts,
   ctx->engine = o.engine;
   if (table) ctx->engine = THIIM_ENGINE_FUSED;
   if (o.engine == THIIM_ENGINE_AUTO && !table) {
-    // fused (ping-pong fields, 52 arrays) when it fits, else split in place (40)
-    ctx->engine = THIIM_ENGINE_FUSED;
+    // one whole-z slab: TBLOCK (two steps per HBM pass; odd remainders run
+    // fused); z-slabs: fused (halo exchange every step); either needs the
+    // ping-pong field set (52 arrays) -- else split in place (40)
+    const bool whole_z = n == 1 && ranges[0].first == 0 && ranges[0].second == dims->nz;
+    ctx->engine = whole_z ? THIIM_ENGINE_TBLOCK : THIIM_ENGINE_FUSED;
     for (int s = 0; s < n; ++s) {
       size_t freeb = 0, totalb = 0;
       cudaSetDevice(o.device + dev_step * s);

@@ -11,10 +11,19 @@
 // otherwise bounds the sweep (measured: 80 sequential takes per plane pair).
 //
 // Cross-proxy WAR: consumers read slots with generic-proxy LDS and the
-// producer overwrites them with async-proxy TMA writes; mbarrier release /
-// acquire alone does not order the two proxies, so every consumer thread
-// issues fence.proxy.async.shared::cta before its warp releases the group
-// (without it, reads of a slot raced its refill whenever the ring ran full).
+// producer overwrites them with async-proxy TMA writes, so a slot may only be
+// released once the warp's reads of it have LANDED -- an mbarrier arrive
+// issued right after the LDS overtakes them (measured: reads of a slot raced
+// its refill whenever the ring ran full).  Two ways to order them:
+//   * fence.proxy.async.shared::cta before the arrive (THIIM_RING_FENCE=1):
+//     lowers to MEMBAR.ALL.CTA + FENCE.VIEW.ASYNC, which also drains every
+//     other outstanding access of the thread (~15% of TBLOCK's warp samples);
+//   * (default) a data dependency: the arrive's address is offset by a token
+//     = AND of the loaded registers AND a zero the compiler cannot see (read
+//     from shared memory at run time -- a literal 0 is folded away by ptxas,
+//     which reintroduced the race), so the warp cannot issue the arrive before
+//     those LDS have written back: the read is complete before the producer
+//     can observe the phase and refill the slot.
 #pragma once
 
 #include <cuda.h>
@@ -73,12 +82,14 @@ struct alignas(128) Ring {
   double2 buf[NG][G][BY * 32];
   uint64_t full[NG];
   uint64_t empty[NG];
+  uint32_t zero;  // 0, written at init: the opaque operand of the release token
 };
 
 // consumer-side cursor
 struct RingCursor {
   int g = 0;
   uint32_t ph = 0;
+  uint32_t zero = 0;  // loaded from Ring::zero by ring_cursor()
 };
 
 template <int BY, int NG>
@@ -87,6 +98,15 @@ __device__ __forceinline__ void ring_init(Ring<BY, NG>& r, int consumer_warps) {
     mbar_init(&r.full[k], 1);
     mbar_init(&r.empty[k], consumer_warps);
   }
+  r.zero = 0;
+}
+
+// consumer cursor (after the barrier that publishes ring_init)
+template <int BY, int NG>
+__device__ __forceinline__ RingCursor ring_cursor(Ring<BY, NG>& r) {
+  RingCursor c;
+  asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(c.zero) : "r"(smem_u32(&r.zero)));
+  return c;
 }
 
 template <int BY, int NG>
@@ -104,11 +124,33 @@ __device__ __forceinline__ double2 ring_read(Ring<BY, NG>& r, const RingCursor& 
   return make_double2(0.0, 0.0);
 }
 
+#ifndef THIIM_RING_FENCE
+#define THIIM_RING_FENCE 0
+#endif
+
+// AND of the low words of both halves of every value read from a group
+// (ring_release masks it with the opaque zero)
+template <class... T>
+__device__ __forceinline__ uint32_t ring_dep(const T&... v) {
+  uint32_t acc = 0xffffffffu;
+  ((acc &= (uint32_t)__double2loint(v.x) & (uint32_t)__double2loint(v.y)), ...);
+  return acc;
+}
+
+// release the current group; `dep` = ring_dep(every value read from it)
 template <int BY, int NG>
-__device__ __forceinline__ void ring_release(Ring<BY, NG>& r, RingCursor& c, int tx) {
+__device__ __forceinline__ void ring_release(Ring<BY, NG>& r, RingCursor& c, int tx, uint32_t dep) {
+#if THIIM_RING_FENCE == 1
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  dep = 0;
+#elif THIIM_RING_FENCE == 2
+  dep = 0;  // NO ordering: test builds only (tools/stress_ring.py must then fail)
+#endif
   __syncwarp();
-  if (tx == 0) mbar_arrive(&r.empty[c.g]);
+  if (tx == 0)
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&r.empty[c.g]) +
+                                                                  (dep & c.zero))
+                 : "memory");
   if (++c.g == NG) {
     c.g = 0;
     c.ph ^= 1;

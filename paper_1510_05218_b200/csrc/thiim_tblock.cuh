@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
   const bool upd2_z = (own2 || rx2 || ry2) && interior;
 
   auto& R = sm.ring;
-  RingCursor rc;
+  RingCursor rc = ring_cursor(R);
 #define RD(k, b) ring_read(R, rc, k, b, tx, ty)
 
   // ---- level-1 prologue: E^0 splits at qs (carried), H^1 sums at qs-1
@@ -293,11 +293,11 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
       ring_wait(R, rc);
 #pragma unroll
       for (int k = 0; k < 4; ++k) en[k] = RD(k, BOX_A);
-      ring_release(R, rc, tx);
+      ring_release(R, rc, tx, ring_dep(en[0], en[1], en[2], en[3]));
       ring_wait(R, rc);
       en[4] = RD(0, BOX_A);
       en[5] = RD(1, BOX_A);
-      ring_release(R, rc, tx);
+      ring_release(R, rc, tx, ring_dep(en[4], en[5]));
       if (inpad) {
         sm.sE[0][ty][tx] = csum(e[EXY], e[EXZ]);
         sm.sE[1][ty][tx] = csum(e[EYX], e[EYZ]);
@@ -311,42 +311,42 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
         ring_wait(R, rc);
         h[0] = RD(0, BOX_BY);
         const double2 t = RD(1, BOX_BY), c = RD(2, BOX_BY);
-        ring_release(R, rc, tx);
+        ring_release(R, rc, tx, ring_dep(h[0], c, t));
         if (upd1_x) h[0] = upd(h[0], t, c, sm.sE[2][ty + 1][tx], sEz);
       }
       {
         ring_wait(R, rc);
         h[1] = RD(0, BOX_BY);
         const double2 t = RD(1, BOX_BY), c = RD(2, BOX_BY), s = RD(3, BOX_BY);
-        ring_release(R, rc, tx);
+        ring_release(R, rc, tx, ring_dep(h[1], s, c, t));
         if (upd1_x) h[1] = upd_src(h[1], t, c, nEy, sEy, s);
       }
       {
         ring_wait(R, rc);
         h[2] = RD(0, BOX_BX);
         const double2 t = RD(1, BOX_BX), c = RD(2, BOX_BX);
-        ring_release(R, rc, tx);
+        ring_release(R, rc, tx, ring_dep(h[2], c, t));
         if (upd1_y) h[2] = upd(h[2], t, c, sm.sE[2][ty][tx + 1], sEz);
       }
       {
         ring_wait(R, rc);
         h[3] = RD(0, BOX_BX);
         const double2 t = RD(1, BOX_BX), c = RD(2, BOX_BX), s = RD(3, BOX_BX);
-        ring_release(R, rc, tx);
+        ring_release(R, rc, tx, ring_dep(h[3], s, c, t));
         if (upd1_y) h[3] = upd_src(h[3], t, c, nEx, sEx, s);
       }
       {
         ring_wait(R, rc);
         h[4] = RD(0, BOX_B);
         const double2 t = RD(1, BOX_B), c = RD(2, BOX_B);
-        ring_release(R, rc, tx);
+        ring_release(R, rc, tx, ring_dep(h[4], c, t));
         if (upd1_z) h[4] = upd(h[4], t, c, sm.sE[1][ty][tx + 1], sEy);
       }
       {
         ring_wait(R, rc);
         h[5] = RD(0, BOX_B);
         const double2 t = RD(1, BOX_B), c = RD(2, BOX_B);
-        ring_release(R, rc, tx);
+        ring_release(R, rc, tx, ring_dep(h[5], c, t));
         if (upd1_z) h[5] = upd(h[5], t, c, sm.sE[0][ty + 1][tx], sEx);
       }
       if (own1 || rx1 || ry1) {
@@ -361,26 +361,26 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
       {
         ring_wait(R, rc);
         const double2 t0 = RD(0, BOX_C), c0 = RD(1, BOX_C), t1 = RD(2, BOX_C), c1 = RD(3, BOX_C);
-        ring_release(R, rc, tx);
+        ring_release(R, rc, tx, ring_dep(c1, t1, c0, t0));
         eo[EXY] = ue ? upd(e[EXY], t0, c0, sm.sH[2][ty - 1][tx], sHz) : e[EXY];
         eo[EYX] = ue ? upd(e[EYX], t1, c1, sm.sH[2][ty][tx - 1], sHz) : e[EYX];
       }
       {
         ring_wait(R, rc);
         const double2 t = RD(0, BOX_C), c = RD(1, BOX_C), s = RD(2, BOX_C);
-        ring_release(R, rc, tx);
+        ring_release(R, rc, tx, ring_dep(s, c, t));
         eo[EXZ] = ue ? upd_src(e[EXZ], t, c, pH1y, sHy, s) : e[EXZ];
       }
       {
         ring_wait(R, rc);
         const double2 t = RD(0, BOX_C), c = RD(1, BOX_C), s = RD(2, BOX_C);
-        ring_release(R, rc, tx);
+        ring_release(R, rc, tx, ring_dep(s, c, t));
         eo[EYZ] = ue ? upd_src(e[EYZ], t, c, pH1x, sHx, s) : e[EYZ];
       }
       {
         ring_wait(R, rc);
         const double2 t0 = RD(0, BOX_C), c0 = RD(1, BOX_C), t1 = RD(2, BOX_C), c1 = RD(3, BOX_C);
-        ring_release(R, rc, tx);
+        ring_release(R, rc, tx, ring_dep(c1, t1, c0, t0));
         eo[EZX] = ue ? upd(e[EZX], t0, c0, sm.sH[1][ty][tx - 1], sHy) : e[EZX];
         eo[EZY] = ue ? upd(e[EZY], t1, c1, sm.sH[0][ty - 1][tx], sHx) : e[EZY];
       }
@@ -419,17 +419,17 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
       e1[EXZ] = RD(1, BOX_A);
       e1[EYX] = RD(2, BOX_A);
       e1[EYZ] = RD(3, BOX_A);
-      ring_release(R, rc, tx);
+      ring_release(R, rc, tx, ring_dep(e1[EXY], e1[EXZ], e1[EYX], e1[EYZ]));
       ring_wait(R, rc);
       e1[EZX] = RD(0, BOX_A);
       e1[EZY] = RD(1, BOX_A);
       h[4] = RD(2, BOX_A);
       h[5] = RD(3, BOX_A);
-      ring_release(R, rc, tx);
+      ring_release(R, rc, tx, ring_dep(e1[EZX], e1[EZY], h[4], h[5]));
       ring_wait(R, rc);
 #pragma unroll
       for (int k = 0; k < 4; ++k) h[k] = RD(k, BOX_A);
-      ring_release(R, rc, tx);
+      ring_release(R, rc, tx, ring_dep(h[0], h[1], h[2], h[3]));
       if (inpad) {
         sm.sE[0][ty][tx] = csum(e1[EXY], e1[EXZ]);
         sm.sE[1][ty][tx] = csum(e1[EYX], e1[EYZ]);
@@ -441,26 +441,26 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
       {  // Hxy, Hyx
         ring_wait(R, rc);
         const double2 t0 = RD(0, BOX_BY), c0 = RD(1, BOX_BY), t1 = RD(2, BOX_BX), c1 = RD(3, BOX_BX);
-        ring_release(R, rc, tx);
+        ring_release(R, rc, tx, ring_dep(c1, t1, c0, t0));
         if (u2x) h[0] = upd(h[0], t0, c0, sm.sE[2][ty + 1][tx], sEz);
         if (u2y) h[2] = upd(h[2], t1, c1, sm.sE[2][ty][tx + 1], sEz);
       }
       {  // Hxz
         ring_wait(R, rc);
         const double2 t = RD(0, BOX_BY), c = RD(1, BOX_BY), s = RD(2, BOX_BY);
-        ring_release(R, rc, tx);
+        ring_release(R, rc, tx, ring_dep(s, c, t));
         if (u2x) h[1] = upd_src(h[1], t, c, nEy, sEy, s);
       }
       {  // Hyz
         ring_wait(R, rc);
         const double2 t = RD(0, BOX_BX), c = RD(1, BOX_BX), s = RD(2, BOX_BX);
-        ring_release(R, rc, tx);
+        ring_release(R, rc, tx, ring_dep(s, c, t));
         if (u2y) h[3] = upd_src(h[3], t, c, nEx, sEx, s);
       }
       {  // Hzx, Hzy
         ring_wait(R, rc);
         const double2 t0 = RD(0, BOX_B), c0 = RD(1, BOX_B), t1 = RD(2, BOX_B), c1 = RD(3, BOX_B);
-        ring_release(R, rc, tx);
+        ring_release(R, rc, tx, ring_dep(c1, t1, c0, t0));
         if (u2z) h[4] = upd(h[4], t0, c0, sm.sE[1][ty][tx + 1], sEy);
         if (u2z) h[5] = upd(h[5], t1, c1, sm.sE[0][ty + 1][tx], sEx);
       }
@@ -472,7 +472,7 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
         }
         for (int k = 0; k < 4; ++k) {  // E-coefficient groups, unused here
           ring_wait(R, rc);
-          ring_release(R, rc, tx);
+          ring_release(R, rc, tx, ring_dep());
         }
         named_sync(1, NCOMP);  // sE reads done before the next level-1 writes
         continue;
@@ -492,7 +492,7 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
       {  // Exy, Eyx
         ring_wait(R, rc);
         const double2 t0 = RD(0, BOX_C), c0 = RD(1, BOX_C), t1 = RD(2, BOX_C), c1 = RD(3, BOX_C);
-        ring_release(R, rc, tx);
+        ring_release(R, rc, tx, ring_dep(c1, t1, c0, t0));
         if (ue) {
           st_hint(A.fo[EXY] + i, upd(e1[EXY], t0, c0, sm.sH[2][ty - 1][tx], sHz), first);
           st_hint(A.fo[EYX] + i, upd(e1[EYX], t1, c1, sm.sH[2][ty][tx - 1], sHz), first);
@@ -501,19 +501,19 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
       {  // Exz
         ring_wait(R, rc);
         const double2 t = RD(0, BOX_C), c = RD(1, BOX_C), s = RD(2, BOX_C);
-        ring_release(R, rc, tx);
+        ring_release(R, rc, tx, ring_dep(s, c, t));
         if (ue) st_hint(A.fo[EXZ] + i, upd_src(e1[EXZ], t, c, pH2y, sHy, s), first);
       }
       {  // Eyz
         ring_wait(R, rc);
         const double2 t = RD(0, BOX_C), c = RD(1, BOX_C), s = RD(2, BOX_C);
-        ring_release(R, rc, tx);
+        ring_release(R, rc, tx, ring_dep(s, c, t));
         if (ue) st_hint(A.fo[EYZ] + i, upd_src(e1[EYZ], t, c, pH2x, sHx, s), first);
       }
       {  // Ezx, Ezy
         ring_wait(R, rc);
         const double2 t0 = RD(0, BOX_C), c0 = RD(1, BOX_C), t1 = RD(2, BOX_C), c1 = RD(3, BOX_C);
-        ring_release(R, rc, tx);
+        ring_release(R, rc, tx, ring_dep(c1, t1, c0, t0));
         if (ue) {
           st_hint(A.fo[EZX] + i, upd(e1[EZX], t0, c0, sm.sH[1][ty][tx - 1], sHy), first);
           st_hint(A.fo[EZY] + i, upd(e1[EZY], t1, c1, sm.sH[0][ty - 1][tx], sHx), first);
@@ -569,7 +569,7 @@ struct TmSmem {
 template <int BY, int NG>
 __global__ void __launch_bounds__(32 * (BY + 1), 1)
     k_tblock_tm(Grid g, Arrays A, const __grid_constant__ TmaMaps maps, int fb, int cb, int zc,
-                int tiles_x) {
+                int tiles_x, int pol_mode) {
   constexpr int NCOMP = 32 * BY;
   constexpr int TX2 = 28, TY2 = BY - 4;
   constexpr int LAG = 1;
@@ -600,13 +600,18 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
     if (tx == 0) {
 #pragma unroll
       for (int b = 0; b < NBOX; ++b) tma_prefetch_desc(&maps.m[b]);
-      const uint64_t keep = policy_evict_last(), drop = policy_evict_first();
+      const uint64_t keep = policy_evict_last(), drop = policy_evict_first(),
+                     norm = policy_evict_normal();
+      // experiment knob: L2 policies (level-1 fields, level-1 coefs, level-2 coefs)
+      const uint64_t pf1 = pol_mode == 3 ? norm : drop;
+      const uint64_t pc1 = pol_mode == 2 ? norm : keep;
+      const uint64_t pc2 = pol_mode == 1 || pol_mode == 2 ? norm : pol_mode == 4 ? keep : drop;
       RingProducer<BY, NG> P(sm.ring, maps, xb, yb);
       for (int q = qs; q <= qe; ++q) {
         // level 1 keeps coefficients in L2 for level 2 (their last use)
-        if (q <= q1) produce_plane_ct<true>(P, fb, cb, q, drop, keep);
+        if (q <= q1) produce_plane_ct<true>(P, fb, cb, q, pf1, pc1);
         const int r = q - LAG;
-        if (r >= z0 - 1 && r < z1) produce_level2_coef_ct(P, cb, r, drop);
+        if (r >= z0 - 1 && r < z1) produce_level2_coef_ct(P, cb, r, pc2);
       }
     }
     return;
@@ -633,7 +638,7 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
   const bool upd2_z = (own2 || rx2 || ry2) && interior;
 
   auto& R = sm.ring;
-  RingCursor rc;
+  RingCursor rc = ring_cursor(R);
 #define RD(k, b) ring_read(R, rc, k, b, tx, ty)
 
   // ---- level-1 prologue: E_old splits at qs (to TMEM), H^1 sums at qs-1
@@ -698,11 +703,11 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
         ring_wait(R, rc);
 #pragma unroll
         for (int k = 0; k < 4; ++k) en[k] = RD(k, BOX_A);
-        ring_release(R, rc, tx);
+        ring_release(R, rc, tx, ring_dep(en[0], en[1], en[2], en[3]));
         ring_wait(R, rc);
         en[4] = RD(0, BOX_A);
         en[5] = RD(1, BOX_A);
-        ring_release(R, rc, tx);
+        ring_release(R, rc, tx, ring_dep(en[4], en[5]));
         tm_st6(tnext, en);  // E_old(q+1) for the next plane
         nEx = csum(en[EXY], en[EXZ]);
         nEy = csum(en[EYX], en[EYZ]);
@@ -719,42 +724,42 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
         ring_wait(R, rc);
         h[0] = RD(0, BOX_BY);
         const double2 t = RD(1, BOX_BY), c = RD(2, BOX_BY);
-        ring_release(R, rc, tx);
+        ring_release(R, rc, tx, ring_dep(h[0], c, t));
         if (upd1_x) h[0] = upd(h[0], t, c, sm.sE[2][ty + 1][tx], sEz);
       }
       {
         ring_wait(R, rc);
         h[1] = RD(0, BOX_BY);
         const double2 t = RD(1, BOX_BY), c = RD(2, BOX_BY), s = RD(3, BOX_BY);
-        ring_release(R, rc, tx);
+        ring_release(R, rc, tx, ring_dep(h[1], s, c, t));
         if (upd1_x) h[1] = upd_src(h[1], t, c, nEy, sEy, s);
       }
       {
         ring_wait(R, rc);
         h[2] = RD(0, BOX_BX);
         const double2 t = RD(1, BOX_BX), c = RD(2, BOX_BX);
-        ring_release(R, rc, tx);
+        ring_release(R, rc, tx, ring_dep(h[2], c, t));
         if (upd1_y) h[2] = upd(h[2], t, c, sm.sE[2][ty][tx + 1], sEz);
       }
       {
         ring_wait(R, rc);
         h[3] = RD(0, BOX_BX);
         const double2 t = RD(1, BOX_BX), c = RD(2, BOX_BX), s = RD(3, BOX_BX);
-        ring_release(R, rc, tx);
+        ring_release(R, rc, tx, ring_dep(h[3], s, c, t));
         if (upd1_y) h[3] = upd_src(h[3], t, c, nEx, sEx, s);
       }
       {
         ring_wait(R, rc);
         h[4] = RD(0, BOX_B);
         const double2 t = RD(1, BOX_B), c = RD(2, BOX_B);
-        ring_release(R, rc, tx);
+        ring_release(R, rc, tx, ring_dep(h[4], c, t));
         if (upd1_z) h[4] = upd(h[4], t, c, sm.sE[1][ty][tx + 1], sEy);
       }
       {
         ring_wait(R, rc);
         h[5] = RD(0, BOX_B);
         const double2 t = RD(1, BOX_B), c = RD(2, BOX_B);
-        ring_release(R, rc, tx);
+        ring_release(R, rc, tx, ring_dep(h[5], c, t));
         if (upd1_z) h[5] = upd(h[5], t, c, sm.sE[0][ty + 1][tx], sEx);
       }
       if (own1 || rx1 || ry1) {
@@ -769,7 +774,7 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
       {
         ring_wait(R, rc);
         const double2 t0 = RD(0, BOX_C), c0 = RD(1, BOX_C), t1 = RD(2, BOX_C), c1 = RD(3, BOX_C);
-        ring_release(R, rc, tx);
+        ring_release(R, rc, tx, ring_dep(c1, t1, c0, t0));
         if (ue) {
           e[EXY] = upd(e[EXY], t0, c0, sm.sH[2][ty - 1][tx], sHz);
           e[EYX] = upd(e[EYX], t1, c1, sm.sH[2][ty][tx - 1], sHz);
@@ -778,19 +783,19 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
       {
         ring_wait(R, rc);
         const double2 t = RD(0, BOX_C), c = RD(1, BOX_C), s = RD(2, BOX_C);
-        ring_release(R, rc, tx);
+        ring_release(R, rc, tx, ring_dep(s, c, t));
         if (ue) e[EXZ] = upd_src(e[EXZ], t, c, pH1y, sHy, s);
       }
       {
         ring_wait(R, rc);
         const double2 t = RD(0, BOX_C), c = RD(1, BOX_C), s = RD(2, BOX_C);
-        ring_release(R, rc, tx);
+        ring_release(R, rc, tx, ring_dep(s, c, t));
         if (ue) e[EYZ] = upd_src(e[EYZ], t, c, pH1x, sHx, s);
       }
       {
         ring_wait(R, rc);
         const double2 t0 = RD(0, BOX_C), c0 = RD(1, BOX_C), t1 = RD(2, BOX_C), c1 = RD(3, BOX_C);
-        ring_release(R, rc, tx);
+        ring_release(R, rc, tx, ring_dep(c1, t1, c0, t0));
         if (ue) {
           e[EZX] = upd(e[EZX], t0, c0, sm.sH[1][ty][tx - 1], sHy);
           e[EZY] = upd(e[EZY], t1, c1, sm.sH[0][ty - 1][tx], sHx);
@@ -838,26 +843,26 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
       {  // Hxy, Hyx
         ring_wait(R, rc);
         const double2 t0 = RD(0, BOX_BY), c0 = RD(1, BOX_BY), t1 = RD(2, BOX_BX), c1 = RD(3, BOX_BX);
-        ring_release(R, rc, tx);
+        ring_release(R, rc, tx, ring_dep(c1, t1, c0, t0));
         if (u2x) h[0] = upd(h[0], t0, c0, sm.sE[2][ty + 1][tx], sEz);
         if (u2y) h[2] = upd(h[2], t1, c1, sm.sE[2][ty][tx + 1], sEz);
       }
       {  // Hxz
         ring_wait(R, rc);
         const double2 t = RD(0, BOX_BY), c = RD(1, BOX_BY), s = RD(2, BOX_BY);
-        ring_release(R, rc, tx);
+        ring_release(R, rc, tx, ring_dep(s, c, t));
         if (u2x) h[1] = upd_src(h[1], t, c, nEy, sEy, s);
       }
       {  // Hyz
         ring_wait(R, rc);
         const double2 t = RD(0, BOX_BX), c = RD(1, BOX_BX), s = RD(2, BOX_BX);
-        ring_release(R, rc, tx);
+        ring_release(R, rc, tx, ring_dep(s, c, t));
         if (u2y) h[3] = upd_src(h[3], t, c, nEx, sEx, s);
       }
       {  // Hzx, Hzy
         ring_wait(R, rc);
         const double2 t0 = RD(0, BOX_B), c0 = RD(1, BOX_B), t1 = RD(2, BOX_B), c1 = RD(3, BOX_B);
-        ring_release(R, rc, tx);
+        ring_release(R, rc, tx, ring_dep(c1, t1, c0, t0));
         if (u2z) h[4] = upd(h[4], t0, c0, sm.sE[1][ty][tx + 1], sEy);
         if (u2z) h[5] = upd(h[5], t1, c1, sm.sE[0][ty + 1][tx], sEx);
       }
@@ -869,7 +874,7 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
         }
         for (int k = 0; k < 4; ++k) {  // E-coefficient groups, unused here
           ring_wait(R, rc);
-          ring_release(R, rc, tx);
+          ring_release(R, rc, tx, ring_dep());
         }
         named_sync(1, NCOMP);  // sE reads done before the next level-1 writes
         continue;
@@ -889,7 +894,7 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
       {  // Exy, Eyx
         ring_wait(R, rc);
         const double2 t0 = RD(0, BOX_C), c0 = RD(1, BOX_C), t1 = RD(2, BOX_C), c1 = RD(3, BOX_C);
-        ring_release(R, rc, tx);
+        ring_release(R, rc, tx, ring_dep(c1, t1, c0, t0));
         if (ue) {
           st_hint(A.fo[EXY] + i, upd(e1[EXY], t0, c0, sm.sH[2][ty - 1][tx], sHz), first);
           st_hint(A.fo[EYX] + i, upd(e1[EYX], t1, c1, sm.sH[2][ty][tx - 1], sHz), first);
@@ -898,19 +903,19 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
       {  // Exz
         ring_wait(R, rc);
         const double2 t = RD(0, BOX_C), c = RD(1, BOX_C), s = RD(2, BOX_C);
-        ring_release(R, rc, tx);
+        ring_release(R, rc, tx, ring_dep(s, c, t));
         if (ue) st_hint(A.fo[EXZ] + i, upd_src(e1[EXZ], t, c, pH2y, sHy, s), first);
       }
       {  // Eyz
         ring_wait(R, rc);
         const double2 t = RD(0, BOX_C), c = RD(1, BOX_C), s = RD(2, BOX_C);
-        ring_release(R, rc, tx);
+        ring_release(R, rc, tx, ring_dep(s, c, t));
         if (ue) st_hint(A.fo[EYZ] + i, upd_src(e1[EYZ], t, c, pH2x, sHx, s), first);
       }
       {  // Ezx, Ezy
         ring_wait(R, rc);
         const double2 t0 = RD(0, BOX_C), c0 = RD(1, BOX_C), t1 = RD(2, BOX_C), c1 = RD(3, BOX_C);
-        ring_release(R, rc, tx);
+        ring_release(R, rc, tx, ring_dep(c1, t1, c0, t0));
         if (ue) {
           st_hint(A.fo[EZX] + i, upd(e1[EZX], t0, c0, sm.sH[1][ty][tx - 1], sHy), first);
           st_hint(A.fo[EZY] + i, upd(e1[EZY], t1, c1, sm.sH[0][ty - 1][tx], sHx), first);

@@ -1,0 +1,60 @@
+"""Race stress for the TMA ring's slot release (thiim_ring.cuh): many random
+shapes / seeds / step counts through the fused, TBLOCK and table engines,
+each compared bitwise with the C oracle.  Prints one JSON line with the
+number of cases and failures.  Test infrastructure: imports oracle/.
+
+    python tools/stress_ring.py --seconds 120
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_1510_05218_b200 as P  # noqa: E402
+from oracle import oracle as O  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--seconds", type=float, default=120)
+    ap.add_argument("--seed", type=int, default=7)
+    a = ap.parse_args()
+    rng = np.random.default_rng(a.seed)
+    t_end = time.time() + a.seconds
+    cases = fails = 0
+    bad = []
+    while time.time() < t_end:
+        d = P.GridDims(int(rng.integers(4, 120)), int(rng.integers(4, 90)), int(rng.integers(4, 70)))
+        steps = int(rng.integers(1, 6))
+        seed = int(rng.integers(1, 1 << 30))
+        layered = bool(rng.integers(0, 2))
+        kind = P.GEN_LAYERED if layered else P.GEN_RANDOM
+        ref = P.generate_problem(d, kind, seed)
+        O.c_step((d.nx, d.ny, d.nz), ref.arrays, steps, threads=8)
+        runs = [("fused", P.GpuOptions(engine=P.ENGINE_FUSED)),
+                ("tblock", P.GpuOptions(engine=P.ENGINE_TBLOCK))]
+        if layered:
+            runs.append(("table", P.GpuOptions(coeff_layout=P.COEFF_TABLE, n_materials=6)))
+        for name, o in runs:
+            out = P.generate_problem(d, kind, seed)
+            with P.GpuEngine(d, o) as e:
+                e.generate(kind, seed)
+                e.step(steps)
+                e.download_fields(out)
+            cases += 1
+            diff = P.compare_states(ref, out)
+            if not diff.bitwise_equal:
+                fails += 1
+                bad.append([name, d.nx, d.ny, d.nz, steps, seed, layered])
+    print(json.dumps({"stress": "ring release", "cases": cases, "failures": fails, "bad": bad[:20]}))
+    sys.exit(1 if fails else 0)
+
+
+if __name__ == "__main__":
+    main()
