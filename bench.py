@@ -292,18 +292,32 @@ def run_native_single(P, args, opts, iters):
         for a in host.arrays:
             P.lib().thiim_gpu_pin_host(a.ctypes.data, a.nbytes)
         secs = 0.0
+        phases = [0.0] * 5
         for k in range(1 + args.steps):  # 1 untimed warm-up
-            t0 = time.perf_counter()
-            with P.GpuEngine(dims, opts) as e:
-                e.upload(host)
-                e.step(iters)
-                e.download_fields(host)
+            t = [time.perf_counter()]
+            e = P.GpuEngine(dims, opts)
+            t.append(time.perf_counter())
+            e.upload(host)
+            t.append(time.perf_counter())
+            e.step(iters)
+            t.append(time.perf_counter())
+            e.download_fields(host)
+            t.append(time.perf_counter())
+            e.close()
+            t.append(time.perf_counter())
             if k >= 1:
-                secs += time.perf_counter() - t0
+                secs += t[-1] - t[0]
+                for j in range(5):
+                    phases[j] += t[j + 1] - t[j]
         for a in host.arrays:
             P.lib().thiim_gpu_unpin_host(a.ctypes.data)
         e2e = dims.interior_cells() * iters * args.steps / secs / 1e6
-    return _line(P, args, 1, dims, engine_ran, dev_secs, launches, e2e, clk, {})
+        e2e_phases = dict(zip(["create", "upload", "step", "download", "destroy"],
+                              [round(1e3 * v / args.steps, 2) for v in phases]))
+    line = _line(P, args, 1, dims, engine_ran, dev_secs, launches, e2e, clk, {})
+    if e2e:
+        line["e2e"]["phases_ms_per_step"] = e2e_phases
+    return line
 
 
 def run_native_multi(P, args, opts, iters, world, rank, local):

@@ -66,8 +66,8 @@ struct Slab {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   // 4-D tensor maps over the allocation {x (doubles), y, plane, array slot},
   // one set of box shapes per tile height (8 / 16 rows), built lazily
-  TmaMaps maps[4];  // tile heights 8, 16, 15, 12
-  bool maps_ok[4] = {false, false, false, false};
+  TmaMaps maps[6];  // tile heights 8, 16, 15, 12, 14, 13 (map_index)
+  bool maps_ok[6] = {false, false, false, false, false, false};
   // TBLOCK: per-SM scratch ring (3 planes x 12 fields x tile) and its tensor map
   double2* scratch = nullptr;
   size_t scratch_bytes = 0;
@@ -320,11 +320,14 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
   return fn;
 }
 
-int map_index(int by) { return by == 16 ? 1 : by == 15 ? 2 : by == 12 ? 3 : 0; }
-// (tile heights 8, 16 and 15 each get their own set of box shapes)
+int map_index(int by) {
+  return by == 8 ? 0 : by == 16 ? 1 : by == 15 ? 2 : by == 12 ? 3 : by == 14 ? 4 : by == 13 ? 5 : -1;
+}
+// (each tile height gets its own set of box shapes)
 
 int ensure_tmap(Slab& s, int by, int promo) {
   const int w = map_index(by);
+  if (w < 0) return fail(THIIM_ERR_CONFIG, "no tensor maps for tile height " + std::to_string(by));
   if (s.maps_ok[w]) return THIIM_OK;
   const CUtensorMapL2promotion pr[4] = {CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_64B,
                                         CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
@@ -443,8 +446,9 @@ int launch_tblock2_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
   const size_t smem = scratch ? sizeof(TbSmem<BY, NG>) : sizeof(TmSmem<BY, NG>);
   static unsigned attr_set = 0;  // bit per device
   if (!(attr_set >> s.device & 1u)) {
-    CK(cudaFuncSetAttribute(k_tblock2<BY, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)sizeof(TbSmem<BY, NG>)));
+    if constexpr (BY == 15)
+      CK(cudaFuncSetAttribute(k_tblock2<BY, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)sizeof(TbSmem<BY, NG>)));
     CK(cudaFuncSetAttribute(k_tblock_tm<BY, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)sizeof(TmSmem<BY, NG>)));
     attr_set |= 1u << s.device;
@@ -472,13 +476,17 @@ int launch_tblock2_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
   const dim3 grid(tiles_x * tiles_y, 1, (s.g.nz + zc - 1) / zc);
   const dim3 block(32, BY + 1);
   if (scratch) {
-    TbParams P;
-    P.zc = zc;
-    P.tiles_x = tiles_x;
-    for (int k = 0; k < 12; ++k) P.field_in[k] = fslot(k);
-    P.scratch = s.scratch;
-    k_tblock2<BY, NG><<<grid, block, smem, s.stream>>>(s.g, A, s.maps[map_index(BY)], s.smap, S1,
-                                                       S2, P);
+    if constexpr (BY == 15) {
+      TbParams P;
+      P.zc = zc;
+      P.tiles_x = tiles_x;
+      for (int k = 0; k < 12; ++k) P.field_in[k] = fslot(k);
+      P.scratch = s.scratch;
+      k_tblock2<BY, NG><<<grid, block, smem, s.stream>>>(s.g, A, s.maps[map_index(BY)], s.smap,
+                                                         S1, S2, P);
+    } else {
+      return fail(THIIM_ERR_CONFIG, "the scratch TBLOCK variant has tile height 15 only");
+    }
   } else {
     k_tblock_tm<BY, NG><<<grid, block, smem, s.stream>>>(s.g, A, s.maps[map_index(BY)], cur * 12,
                                                          nf * 12, zc, tiles_x,
@@ -492,7 +500,12 @@ int launch_tblock2_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
 
 int launch_tblock2(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
   CK(cudaSetDevice(s.device));
-  return launch_tblock2_t<15, 6>(ctx, s, launches);
+  switch (ctx->opts.tile_y) {  // CTA height incl. the 4 halo rows; ring depth fills the smem
+    case 16: return launch_tblock2_t<16, 5>(ctx, s, launches);
+    case 14: return launch_tblock2_t<14, 6>(ctx, s, launches);
+    case 12: return launch_tblock2_t<12, 7>(ctx, s, launches);
+    default: return launch_tblock2_t<15, 6>(ctx, s, launches);
+  }
 }
 
 template <int BY, int NG>
@@ -581,6 +594,48 @@ double thiim_gpu_balance_model(int engine, int time_block) {
   }
 }
 
+// ---- device memory: the slab state comes from the device's stream-ordered
+// pool with an unbounded release threshold, so destroying a context keeps the
+// pages mapped for the next one (a caching allocator, like torch's): context
+// create/destroy stay in the milliseconds, while cudaFree of a 14 GB state
+// costs ~0.1 s.  Reserved-but-unused pool memory counts as available.
+static cudaMemPool_t device_pool(int dev) {
+  static unsigned configured = 0;
+  cudaMemPool_t pool = nullptr;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return nullptr;
+  if (!(configured >> dev & 1u)) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    configured |= 1u << dev;
+  }
+  return pool;
+}
+
+static size_t device_available(int dev) {
+  size_t freeb = 0, totalb = 0;
+  cudaSetDevice(dev);
+  cudaMemGetInfo(&freeb, &totalb);
+  if (cudaMemPool_t pool = device_pool(dev)) {
+    uint64_t reserved = 0, used = 0;
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+    if (reserved > used) freeb += (size_t)(reserved - used);
+  }
+  return freeb;
+}
+
+static cudaError_t pool_alloc(void** p, size_t bytes, int dev, cudaStream_t st) {
+  cudaError_t e = cudaMallocAsync(p, bytes, st);
+  if (e == cudaErrorMemoryAllocation) {  // give cached pages back and retry once
+    cudaGetLastError();
+    cudaStreamSynchronize(st);
+    if (cudaMemPool_t pool = device_pool(dev)) cudaMemPoolTrimTo(pool, 0);
+    e = cudaMallocAsync(p, bytes, st);
+  }
+  return e;
+}
+
+
 // Shared by thiim_gpu_create (n_gpus slabs split like the reference's z_slab,
 // reference_engines.cpp:26-30) and thiim_gpu_create_slab (one explicit slab).
 static int create_impl(const thiim_dims* dims, const thiim_gpu_opts* opts,
@@ -636,9 +691,7 @@ static int create_impl(const thiim_dims* dims, const thiim_gpu_opts* opts,
     const bool whole_z = n == 1 && ranges[0].first == 0 && ranges[0].second == dims->nz;
     ctx->engine = whole_z ? THIIM_ENGINE_TBLOCK : THIIM_ENGINE_FUSED;
     for (int s = 0; s < n; ++s) {
-      size_t freeb = 0, totalb = 0;
-      cudaSetDevice(o.device + dev_step * s);
-      cudaMemGetInfo(&freeb, &totalb);
+      const size_t freeb = device_available(o.device + dev_step * s);
       const size_t need = (size_t)(ranges[s].second - ranges[s].first + 2) * (size_t)pxy *
                           sizeof(double2) * 52 + ((size_t)256 << 20);
       if (need > freeb) ctx->engine = THIIM_ENGINE_SPLIT;
@@ -669,7 +722,14 @@ static int create_impl(const thiim_dims* dims, const thiim_gpu_opts* opts,
     const size_t tail = (size_t)(34 * (dims->nx + 2) + 256) * sizeof(double2);
     const size_t bytes = sl.stride * sizeof(double2) * (size_t)sl.n_arrays() + tail;
     cudaError_t e = cudaSetDevice(sl.device);
-    if (e == cudaSuccess) e = cudaMalloc(&sl.buf, bytes);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&sl.stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) {
+      device_pool(sl.device);
+      e = pool_alloc(reinterpret_cast<void**>(&sl.buf), bytes, sl.device, sl.stream);
+      if (e == cudaSuccess) e = cudaMemsetAsync(sl.buf, 0, bytes, sl.stream);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(sl.stream);
+      if (e != cudaSuccess) sl.buf = nullptr;
+    }
     if (e == cudaSuccess && table) {
       const size_t mbytes = (size_t)sl.mplane * (sl.g.nz + 2) + 4096;
       e = cudaMalloc(&sl.mat, mbytes);
@@ -677,8 +737,6 @@ static int create_impl(const thiim_dims* dims, const thiim_gpu_opts* opts,
       if (e == cudaSuccess) e = cudaMalloc(&sl.tab, kMaxMaterials * 28 * sizeof(double2));
       if (e == cudaSuccess) e = cudaMemset(sl.tab, 0, kMaxMaterials * 28 * sizeof(double2));
     }
-    if (e == cudaSuccess) e = cudaMemset(sl.buf, 0, bytes);
-    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&sl.stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreate(&sl.ev0);
     if (e == cudaSuccess) e = cudaEventCreate(&sl.ev1);
     if (e != cudaSuccess) {
@@ -771,7 +829,10 @@ void thiim_gpu_destroy(thiim_gpu_ctx* ctx) {
   for (auto& sl : ctx->slabs) {
     cudaSetDevice(sl.device);
     if (sl.stream) cudaStreamSynchronize(sl.stream);
-    if (sl.buf) cudaFree(sl.buf);
+    if (sl.buf) {  // back to the pool; the sync lets the next context reuse it at once
+      cudaFreeAsync(sl.buf, sl.stream);
+      cudaStreamSynchronize(sl.stream);
+    }
     if (sl.scratch) cudaFree(sl.scratch);
     if (sl.mat) cudaFree(sl.mat);
     if (sl.tab) cudaFree(sl.tab);
