@@ -191,6 +191,10 @@ def _roofline(P, dims, engine_ran, dev_secs, launches, table=False):
     if engine_ran == P.ENGINE_SPLIT:
         bytes_launch = 512.0 * dims.interior_cells()  # one half-step sweep: 32 x 16 B per cell
         kname = "k_split_h/k_split_e"
+    elif table and engine_ran == P.ENGINE_TBLOCK:
+        # one launch = two iterations: 24 fields x 16 B + 1 B material id per cell
+        bytes_launch = 385.0 * dims.interior_cells()
+        kname = "k_tblock_table<15,5>"
     elif table:
         bytes_launch = 385.0 * dims.interior_cells()  # 24 fields x 16 B + 1 B material id
         kname = "k_fused_table<15,5>"
@@ -207,7 +211,8 @@ def _roofline(P, dims, engine_ran, dev_secs, launches, table=False):
     if os.path.exists(tp):
         with open(tp) as f:
             traffic = json.load(f).get(kname)
-    balance = 385.0 if table else P.balance_model(engine_ran)
+    balance = (385.0 / (2 if engine_ran == P.ENGINE_TBLOCK else 1)) if table \
+        else P.balance_model(engine_ran)
     return {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
             "frac": round(achieved / hbm, 4), "traffic": traffic, "kernel": kname,
             "algorithmic_bytes_per_launch": bytes_launch, "peak_kind": peak_kind,

@@ -219,7 +219,8 @@ int thiim_gpu_sync(thiim_gpu_ctx* ctx);
 /* Message of the last failing call on this thread ("" if none). */
 const char* thiim_gpu_last_error(void);
 
-/* Algorithmic bytes per LUP of an engine (832 / time_block for TBLOCK). */
+/* Algorithmic bytes per LUP of an engine (832 / time_block for TBLOCK);
+   engine 100 + THIIM_COEFF_TABLE: the table layout, 385 / time_block. */
 double thiim_gpu_balance_model(int engine, int time_block);
 
 int thiim_gpu_abi_version(void);

@@ -27,6 +27,7 @@
 #include "thiim_fused_tma.cuh"
 #include "thiim_split.cuh"
 #include "thiim_tblock.cuh"
+#include "thiim_tblock_table.cuh"
 
 using namespace thiim_gpu;
 
@@ -407,7 +408,8 @@ int ensure_scratch(Slab& s) {
   if (s.scratch) cudaFree(s.scratch);
   s.scratch = nullptr;
   CK(cudaMalloc(&s.scratch, bytes));
-  CK(cudaMemset(s.scratch, 0, bytes));
+  CK(cudaMemsetAsync(s.scratch, 0, bytes, s.stream));
+  CK(cudaStreamSynchronize(s.stream));
   s.scratch_bytes = bytes;
   auto fn = get_encode_fn();
   if (!fn) return fail(THIIM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
@@ -421,6 +423,24 @@ int ensure_scratch(Slab& s) {
   if (r != CUDA_SUCCESS) return fail(THIIM_ERR_CUDA, "scratch tensor map failed");
   s.smap_by = BY;
   return THIIM_OK;
+}
+
+// z-chunks of a TBLOCK launch: each CTA re-does ~2 planes of level-1/level-2
+// work at its start; minimise waves x (planes + 2) over one CTA per SM
+int tblock_zchunk(const Slab& s, long long cols) {
+  const long long slots = sm_count(s.device);
+  double best = 1e300;
+  int best_c = 1;
+  for (int c = 1; c <= std::max(1, s.g.nz / 8); ++c) {
+    const int planes = (s.g.nz + c - 1) / c;
+    const long long waves = (cols * c + slots - 1) / slots;
+    const double t = (double)waves * (planes + 2.0);
+    if (t < best - 1e-9) {
+      best = t;
+      best_c = c;
+    }
+  }
+  return (s.g.nz + best_c - 1) / best_c;
 }
 
 template <int BY, int NG>
@@ -455,24 +475,8 @@ int launch_tblock2_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
   }
   constexpr int TX2 = 28, TY2 = BY - 4;
   const int tiles_x = (s.g.nx + TX2 - 1) / TX2, tiles_y = (s.g.ny + TY2 - 1) / TY2;
-  // z-chunks: each CTA re-does ~2 planes of level-1/level-2 work at its start
-  const long long cols = (long long)tiles_x * tiles_y;
   int zc = ctx->opts.z_chunk;
-  if (zc <= 0) {
-    const long long slots = sm_count(s.device);
-    double best = 1e300;
-    int best_c = 1;
-    for (int c = 1; c <= std::max(1, s.g.nz / 8); ++c) {
-      const int planes = (s.g.nz + c - 1) / c;
-      const long long waves = (cols * c + slots - 1) / slots;
-      const double t = (double)waves * (planes + 2.0);
-      if (t < best - 1e-9) {
-        best = t;
-        best_c = c;
-      }
-    }
-    zc = (s.g.nz + best_c - 1) / best_c;
-  }
+  if (zc <= 0) zc = tblock_zchunk(s, (long long)tiles_x * tiles_y);
   const dim3 grid(tiles_x * tiles_y, 1, (s.g.nz + zc - 1) / zc);
   const dim3 block(32, BY + 1);
   if (scratch) {
@@ -498,8 +502,42 @@ int launch_tblock2_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
   return THIIM_OK;
 }
 
+template <int BY, int NG>
+int launch_tblock_table_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
+  if (s.g.halo_lo || s.z1 < ctx->dims.nz)
+    return fail(THIIM_ERR_CONFIG, "TBLOCK needs a whole-z context (no halo slabs yet)");
+  const Arrays A = s.arrays(s.cur, s.cur ^ 1);
+  int r = ensure_tmap(s, BY, 0);
+  if (r) return r;
+  TableGrid T;
+  T.mat = s.mat;
+  T.mp = s.mp;
+  T.mplane = s.mplane;
+  T.table = s.tab;
+  T.n_mat = s.n_mat;
+  const size_t smem = sizeof(TbTableSmem<BY, NG>);
+  static unsigned attr_set = 0;  // bit per device
+  if (!(attr_set >> s.device & 1u)) {
+    CK(cudaFuncSetAttribute(k_tblock_table<BY, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)smem));
+    attr_set |= 1u << s.device;
+  }
+  constexpr int TX2 = 28, TY2 = BY - 4;
+  const int tiles_x = (s.g.nx + TX2 - 1) / TX2, tiles_y = (s.g.ny + TY2 - 1) / TY2;
+  int zc = ctx->opts.z_chunk;
+  if (zc <= 0) zc = tblock_zchunk(s, (long long)tiles_x * tiles_y);
+  const dim3 grid(tiles_x * tiles_y, 1, (s.g.nz + zc - 1) / zc);
+  k_tblock_table<BY, NG><<<grid, dim3(32, BY + 1), smem, s.stream>>>(s.g, A, T, s.maps[map_index(BY)],
+                                                                     s.cur * 12, zc, tiles_x);
+  CK(cudaGetLastError());
+  s.cur ^= 1;
+  ++*launches;
+  return THIIM_OK;
+}
+
 int launch_tblock2(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
   CK(cudaSetDevice(s.device));
+  if (s.table) return launch_tblock_table_t<15, 5>(ctx, s, launches);
   switch (ctx->opts.tile_y) {  // CTA height incl. the 4 halo rows; ring depth fills the smem
     case 16: return launch_tblock2_t<16, 5>(ctx, s, launches);
     case 14: return launch_tblock2_t<14, 6>(ctx, s, launches);
@@ -589,7 +627,8 @@ double thiim_gpu_balance_model(int engine, int time_block) {
   switch (engine) {
     case THIIM_ENGINE_SPLIT: return 1024.0;
     case THIIM_ENGINE_TBLOCK: return 832.0 / (time_block > 0 ? time_block : 2);
-    case 100 + THIIM_COEFF_TABLE: return 385.0;  // fused sweep, table coefficient layout
+    // table coefficient layout: 24 fields x 16 B + 1 B id per HBM pass of time_block steps
+    case 100 + THIIM_COEFF_TABLE: return 385.0 / (time_block > 0 ? time_block : 1);
     default: return 832.0;
   }
 }
@@ -658,8 +697,8 @@ static int create_impl(const thiim_dims* dims, const thiim_gpu_opts* opts,
   const bool table = o.coeff_layout == THIIM_COEFF_TABLE;
   if (o.coeff_layout != THIIM_COEFF_FULL && !table)
     return fail(THIIM_ERR_CONFIG, "unknown coefficient layout");
-  if (table && o.engine != THIIM_ENGINE_AUTO && o.engine != THIIM_ENGINE_FUSED)
-    return fail(THIIM_ERR_CONFIG, "the table coefficient layout runs on the fused engine");
+  if (table && o.engine == THIIM_ENGINE_SPLIT)
+    return fail(THIIM_ERR_CONFIG, "the table coefficient layout runs on the fused or TBLOCK engine");
   if (table && (o.n_materials < 1 || o.n_materials > kMaxMaterials))
     return fail(THIIM_ERR_CONFIG, "n_materials must be in 1..16 for the table layout");
   if (o.engine == THIIM_ENGINE_TBLOCK &&
@@ -683,12 +722,14 @@ static int create_impl(const thiim_dims* dims, const thiim_gpu_opts* opts,
   const long long pxy = ctx->pxy();
   const int n = (int)ranges.size();
   ctx->engine = o.engine;
-  if (table) ctx->engine = THIIM_ENGINE_FUSED;
+  const bool whole_z = n == 1 && ranges[0].first == 0 && ranges[0].second == dims->nz;
+  // table layout: TBLOCK on a whole-z context, else fused (it has no split form)
+  if (table && o.engine == THIIM_ENGINE_AUTO)
+    ctx->engine = whole_z ? THIIM_ENGINE_TBLOCK : THIIM_ENGINE_FUSED;
   if (o.engine == THIIM_ENGINE_AUTO && !table) {
     // one whole-z slab: TBLOCK (two steps per HBM pass; odd remainders run
     // fused); z-slabs: fused (halo exchange every step); either needs the
     // ping-pong field set (52 arrays) -- else split in place (40)
-    const bool whole_z = n == 1 && ranges[0].first == 0 && ranges[0].second == dims->nz;
     ctx->engine = whole_z ? THIIM_ENGINE_TBLOCK : THIIM_ENGINE_FUSED;
     for (int s = 0; s < n; ++s) {
       const size_t freeb = device_available(o.device + dev_step * s);
@@ -732,10 +773,14 @@ static int create_impl(const thiim_dims* dims, const thiim_gpu_opts* opts,
     }
     if (e == cudaSuccess && table) {
       const size_t mbytes = (size_t)sl.mplane * (sl.g.nz + 2) + 4096;
+      // zero-fills on the slab stream: a legacy-stream cudaMemset does not order
+      // against this non-blocking stream and raced the generator's id writes
       e = cudaMalloc(&sl.mat, mbytes);
-      if (e == cudaSuccess) e = cudaMemset(sl.mat, 0, mbytes);
+      if (e == cudaSuccess) e = cudaMemsetAsync(sl.mat, 0, mbytes, sl.stream);
       if (e == cudaSuccess) e = cudaMalloc(&sl.tab, kMaxMaterials * 28 * sizeof(double2));
-      if (e == cudaSuccess) e = cudaMemset(sl.tab, 0, kMaxMaterials * 28 * sizeof(double2));
+      if (e == cudaSuccess)
+        e = cudaMemsetAsync(sl.tab, 0, kMaxMaterials * 28 * sizeof(double2), sl.stream);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(sl.stream);
     }
     if (e == cudaSuccess) e = cudaEventCreate(&sl.ev0);
     if (e == cudaSuccess) e = cudaEventCreate(&sl.ev1);
@@ -1000,7 +1045,8 @@ int thiim_gpu_step(thiim_gpu_ctx* ctx, int steps, thiim_gpu_stats* stats) {
     stats->n_gpus = (int)ctx->slabs.size();
     stats->kernel_launches = launches;
     stats->balance_model = ctx->slabs[0].table
-                               ? thiim_gpu_balance_model(100 + THIIM_COEFF_TABLE, 0)
+                               ? thiim_gpu_balance_model(100 + THIIM_COEFF_TABLE,
+                                                         ctx->engine == THIIM_ENGINE_TBLOCK ? 2 : 1)
                                : thiim_gpu_balance_model(ctx->engine, ctx->opts.time_block);
     const double lups = (double)ctx->dims.nx * ctx->dims.ny * ctx->dims.nz * steps;
     stats->mlups = (steps > 0 && secs > 0) ? lups / secs / 1e6 : 0.0;
@@ -1128,11 +1174,11 @@ int thiim_gpu_compare_fields(thiim_gpu_ctx* ctx, const thiim_c128* const ref[12]
     CK(cudaMalloc(&dref, elems * sizeof(double2)));
     CK(cudaMalloc(&acc, 24 * sizeof(double)));
     CK(cudaMalloc(&cnt, sizeof(unsigned long long)));
-    CK(cudaMemset(acc, 0, 24 * sizeof(double)));
-    CK(cudaMemset(cnt, 0, sizeof(unsigned long long)));
+    CK(cudaMemsetAsync(acc, 0, 24 * sizeof(double), sl.stream));
+    CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), sl.stream));
     for (int k = 0; k < 12; ++k) {
-      CK(cudaMemcpy(dref, ref[k] + (size_t)sl.z0 * pxy, elems * sizeof(double2),
-                    cudaMemcpyHostToDevice));
+      CK(cudaMemcpyAsync(dref, ref[k] + (size_t)sl.z0 * pxy, elems * sizeof(double2),
+                         cudaMemcpyHostToDevice, sl.stream));
       k_compare<<<4 * sm_count(sl.device), 256, 0, sl.stream>>>(sl.g, sl.field(sl.cur, k), dref,
                                                                 acc + 2 * k, cnt);
       CK(cudaGetLastError());
@@ -1140,8 +1186,9 @@ int thiim_gpu_compare_fields(thiim_gpu_ctx* ctx, const thiim_c128* const ref[12]
     }
     double h[24];
     unsigned long long c = 0;
-    CK(cudaMemcpy(h, acc, sizeof(h), cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(&c, cnt, sizeof(c), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpyAsync(h, acc, sizeof(h), cudaMemcpyDeviceToHost, sl.stream));
+    CK(cudaMemcpyAsync(&c, cnt, sizeof(c), cudaMemcpyDeviceToHost, sl.stream));
+    CK(cudaStreamSynchronize(sl.stream));
     for (int k = 0; k < 12; ++k) {
       num[k] += h[2 * k];
       den[k] += h[2 * k + 1];

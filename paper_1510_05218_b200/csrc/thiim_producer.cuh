@@ -204,4 +204,35 @@ __device__ __forceinline__ void produce_level2_coef_ct(RingProducer<BY, NG>& P, 
   P.end();
 }
 
+// Table-layout plane z (seq_table): E_old(z+1) x6, H_old(z) x6 -- the only
+// HBM-streamed arrays when coefficients come from the material table.
+template <int BY, int NG>
+__device__ __forceinline__ void produce_table_plane_ct(RingProducer<BY, NG>& P, int fb, int z,
+                                                       uint64_t pol) {
+  using Gm = BoxGeom<BY>;
+  constexpr int SA = Gm::bytes(BOX_A), SB = Gm::bytes(BOX_B), SBX = Gm::bytes(BOX_BX),
+                SBY = Gm::bytes(BOX_BY);
+  const int p0 = z + 1, p1 = z + 2;
+  P.template begin<4 * SA>();
+  P.template box<BOX_A>(0, fb + EXY, p1, pol);
+  P.template box<BOX_A>(1, fb + EXZ, p1, pol);
+  P.template box<BOX_A>(2, fb + EYX, p1, pol);
+  P.template box<BOX_A>(3, fb + EYZ, p1, pol);
+  P.end();
+  P.template begin<2 * SA>();
+  P.template box<BOX_A>(0, fb + EZX, p1, pol);
+  P.template box<BOX_A>(1, fb + EZY, p1, pol);
+  P.end();
+  P.template begin<2 * SBY + 2 * SBX>();
+  P.template box<BOX_BY>(0, fb + HXY, p0, pol);
+  P.template box<BOX_BY>(1, fb + HXZ, p0, pol);
+  P.template box<BOX_BX>(2, fb + HYX, p0, pol);
+  P.template box<BOX_BX>(3, fb + HYZ, p0, pol);
+  P.end();
+  P.template begin<2 * SB>();
+  P.template box<BOX_B>(0, fb + HZX, p0, pol);
+  P.template box<BOX_B>(1, fb + HZY, p0, pol);
+  P.end();
+}
+
 }  // namespace thiim_gpu

@@ -17,13 +17,15 @@ def oracle_run(s, steps):
     return out
 
 
+@pytest.mark.parametrize("engine", [P.ENGINE_FUSED, P.ENGINE_TBLOCK])
 @pytest.mark.parametrize("shape,steps,zc", [((40, 36, 48), 4, 0), ((31, 29, 60), 3, 7),
-                                           ((64, 64, 64), 5, 0), ((9, 7, 12), 2, 0)])
-def test_table_layout_generated_matches_oracle(shape, steps, zc):
+                                           ((64, 64, 64), 5, 0), ((9, 7, 12), 2, 0),
+                                           ((57, 30, 19), 6, 5)])
+def test_table_layout_generated_matches_oracle(shape, steps, zc, engine):
     d = P.GridDims(*shape)
     host = P.generate_problem(d, P.GEN_LAYERED, seed=5)
     want = oracle_run(host, steps)
-    opts = P.GpuOptions(coeff_layout=P.COEFF_TABLE, n_materials=6, z_chunk=zc)
+    opts = P.GpuOptions(coeff_layout=P.COEFF_TABLE, n_materials=6, z_chunk=zc, engine=engine)
     with P.GpuEngine(d, opts) as eng:
         eng.generate(P.GEN_LAYERED, seed=5)
         mid, tab = eng.download_table(6)
@@ -32,14 +34,16 @@ def test_table_layout_generated_matches_oracle(shape, steps, zc):
         for k in range(12, 40):
             assert np.array_equal(full.interior(k).view(np.uint64), host.interior(k).view(np.uint64))
         st = eng.step(steps)
-        assert st.balance_model == 385.0
+        assert st.engine == engine
+        assert st.balance_model == (192.5 if engine == P.ENGINE_TBLOCK else 385.0)
         got = P.allocate_state(d)
         eng.download_fields(got)
     diff = P.compare_states(got, want)
     assert diff.bitwise_equal, diff
 
 
-def test_table_layout_upload_benchmark_problem():
+@pytest.mark.parametrize("engine", [P.ENGINE_FUSED, P.ENGINE_TBLOCK])
+def test_table_layout_upload_benchmark_problem(engine):
     """build_benchmark_problem (coefficients.cpp:94-111): vacuum + source plane,
     compressed to 3 coefficient rows (interior, source plane, ghosts)."""
     d = P.GridDims(24, 20, 28)
@@ -55,7 +59,8 @@ def test_table_layout_upload_benchmark_problem():
     mid, tab = P.compress_coefficients(s)
     assert len(tab) <= 4
     want = oracle_run(s, 6)
-    with P.GpuEngine(d, P.GpuOptions(coeff_layout=P.COEFF_TABLE, n_materials=len(tab))) as eng:
+    with P.GpuEngine(d, P.GpuOptions(coeff_layout=P.COEFF_TABLE, n_materials=len(tab),
+                                     engine=engine)) as eng:
         eng.upload_table(s.fields, mid, tab)
         eng.step(6)
         got = P.allocate_state(d)

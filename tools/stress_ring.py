@@ -24,6 +24,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--seconds", type=float, default=120)
     ap.add_argument("--seed", type=int, default=7)
+    ap.add_argument("--only", default="", help="comma list of fused,tblock,table,table-fused")
     a = ap.parse_args()
     rng = np.random.default_rng(a.seed)
     t_end = time.time() + a.seconds
@@ -33,14 +34,19 @@ def main():
         d = P.GridDims(int(rng.integers(4, 120)), int(rng.integers(4, 90)), int(rng.integers(4, 70)))
         steps = int(rng.integers(1, 6))
         seed = int(rng.integers(1, 1 << 30))
-        layered = bool(rng.integers(0, 2))
+        layered = bool(rng.integers(0, 2)) or a.only in ("table", "table-fused")
         kind = P.GEN_LAYERED if layered else P.GEN_RANDOM
         ref = P.generate_problem(d, kind, seed)
         O.c_step((d.nx, d.ny, d.nz), ref.arrays, steps, threads=8)
         runs = [("fused", P.GpuOptions(engine=P.ENGINE_FUSED)),
                 ("tblock", P.GpuOptions(engine=P.ENGINE_TBLOCK))]
         if layered:
-            runs.append(("table", P.GpuOptions(coeff_layout=P.COEFF_TABLE, n_materials=6)))
+            runs.append(("table", P.GpuOptions(coeff_layout=P.COEFF_TABLE, n_materials=6,
+                                               engine=P.ENGINE_TBLOCK)))
+            runs.append(("table-fused", P.GpuOptions(coeff_layout=P.COEFF_TABLE, n_materials=6,
+                                                     engine=P.ENGINE_FUSED)))
+        if a.only:
+            runs = [r for r in runs if r[0] in a.only.split(",")]
         for name, o in runs:
             out = P.generate_problem(d, kind, seed)
             with P.GpuEngine(d, o) as e:
