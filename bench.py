@@ -368,6 +368,7 @@ def run_native_multi(P, args, opts, iters, world, rank, local):
                                          for _ in range(args.steps)])
     launches = sum(s["kernel_launches"] for s in stats)
     halo = sum(s["halo_bytes_sent"] for s in stats)
+    engine_ran, period = eng.engine, eng.exchange_period
     eng.close()
 
     e2e = None
@@ -394,9 +395,9 @@ def run_native_multi(P, args, opts, iters, world, rank, local):
         eng.upload_local(host)
         D.run_distributed(eng, args.check, ex)
         eng.download_local(host)
+        mine = np.stack([eng.owned_planes(host, k) for k in range(12)])
         eng.close()
         pxy = (gdims.nx + 2) * (gdims.ny + 2)
-        mine = np.stack([a[pxy:(z1 - z0 + 1) * pxy] for a in host[:12]])
         parts = [None] * world
         dist.all_gather_object(parts, (z0, z1, mine))
         if rank == 0:
@@ -408,10 +409,11 @@ def run_native_multi(P, args, opts, iters, world, rank, local):
                      for a, b, m in parts for k in range(12))
             print(json.dumps({"check": "z-slab decomposition vs oracle", "ranks": world,
                               "steps": args.check, "bitwise_equal": bool(ok)}), flush=True)
-    line = _line(P, args, world, P.GridDims(*GRID), P.ENGINE_FUSED, dev_secs, launches, e2e, clk,
+    line = _line(P, args, world, P.GridDims(*GRID), engine_ran, dev_secs, launches, e2e, clk,
                  {"global_grid": [gdims.nx, gdims.ny, gdims.nz],
                   "halo_bytes_per_rank_per_step": halo // max(1, args.steps),
-                  "exchange": "torch.distributed NCCL batch_isend_irecv, before every iteration"})
+                  "exchange": "torch.distributed %s batch_isend_irecv after every %d-step pass"
+                              % (backend, period)})
     dist.destroy_process_group()
     return line if rank == 0 else None
 

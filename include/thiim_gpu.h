@@ -175,7 +175,20 @@ void thiim_gpu_destroy(thiim_gpu_ctx* ctx);
  *   upper rank SEND_DOWN (E x6 of its first plane)
  *        -> lower rank RECV_UP (its plane above z1-1)
  * The upper rank recomputes H_new on the received plane, so a step needs no
- * mid-step exchange.  Fused engines only. */
+ * mid-step exchange (engine FUSED).
+ *
+ * Engine TBLOCK (default for AUTO) makes a DEEP-halo slab: two steps per HBM
+ * pass need two-plane halos, so the slab also holds one extended interior
+ * plane per internal interface (recomputed redundantly, refreshed by the
+ * exchange) and every view is two contiguous planes of all 12 fields:
+ *   SEND_DOWN: owned planes z0, z0+1      -> lower rank's RECV_UP
+ *   RECV_DOWN: ghost z0-2, extended z0-1  <- lower rank's SEND_UP
+ *   SEND_UP:   owned planes z1-2, z1-1    -> upper rank's RECV_DOWN
+ *   RECV_UP:   extended z1, ghost z1+1    <- upper rank's SEND_DOWN
+ * Driver loop for both kinds (thiim_gpu_slab_info gives the period):
+ *   k = min(period, remaining); thiim_gpu_step(ctx, k); exchange;
+ * (the uploaded halos are valid for the first pass).  Downloads and compares
+ * touch the owned planes only. */
 int thiim_gpu_create_slab(const thiim_dims* global, int z0, int z1, const thiim_gpu_opts* opts,
                           thiim_gpu_ctx** out);
 
@@ -198,8 +211,19 @@ typedef struct {
 } thiim_halo_view;
 int thiim_gpu_halo_view(thiim_gpu_ctx* ctx, int which, thiim_halo_view* view);
 
+/* Plane ranges and exchange period of a slab context. */
+typedef struct {
+  int own_z0, own_z1;      /* owned global interior planes [own_z0, own_z1) */
+  int local_z0, local_z1;  /* planes held as local interior (incl. extended planes) */
+  int exchange_period;     /* steps per exchange: 1 (FUSED), 2 (TBLOCK deep halo) */
+  int engine;              /* THIIM_ENGINE_* the context runs */
+} thiim_slab_info;
+int thiim_gpu_slab_info(thiim_gpu_ctx* ctx, thiim_slab_info* info);
+
 /* Plane-range variants for rank-local host buffers: the host arrays hold the
- * global padded planes [p0, ...) only (plane p = global interior z p-1). */
+ * global padded planes [p0, ...) only (plane p = global interior z p-1); a
+ * slab reads padded planes [local_z0, local_z1 + 2) and writes back its owned
+ * planes (plus the global ghost planes it borders). */
 int thiim_gpu_upload_planes(thiim_gpu_ctx* ctx, const thiim_c128* const arrays[40], int p0);
 int thiim_gpu_download_fields_planes(thiim_gpu_ctx* ctx, thiim_c128* const fields[12], int p0);
 int thiim_generate_host_planes(const thiim_dims* global, int kind, uint64_t seed, int p0, int p1,

@@ -289,7 +289,7 @@ EXPORTED_SYMBOLS = [
     "thiim_gpu_upload_fields", "thiim_gpu_init_generated", "thiim_gpu_step",
     "thiim_gpu_download_fields", "thiim_gpu_download_array", "thiim_gpu_compare_fields",
     "thiim_generate_host", "thiim_gpu_pin_host", "thiim_gpu_unpin_host",
-    "thiim_gpu_create_slab", "thiim_gpu_halo_view", "thiim_gpu_sync",
+    "thiim_gpu_create_slab", "thiim_gpu_halo_view", "thiim_gpu_slab_info", "thiim_gpu_sync",
     "thiim_gpu_upload_planes", "thiim_gpu_download_fields_planes", "thiim_generate_host_planes",
     "thiim_gpu_upload_table", "thiim_gpu_download_table",
 ]

@@ -51,8 +51,12 @@ constexpr int kSplitBY = 4;
 
 struct Slab {
   int device = 0;
-  int z0 = 0, z1 = 0;  // global interior planes [z0, z1)
+  int z0 = 0, z1 = 0;  // global interior planes [z0, z1) held as local interior
   Grid g{};            // local grid: nz = z1 - z0
+  // owned planes [own0, own1); a TBLOCK ("deep") slab also holds one extended
+  // plane per internal interface (ext_lo / ext_hi) that the exchange refreshes
+  int own0 = 0, own1 = 0, ext_lo = 0, ext_hi = 0;
+  bool deep = false;
   double2* buf = nullptr;
   size_t stride = 0;   // elements per array
   int nfield_sets = 1;
@@ -255,6 +259,45 @@ int exchange_fused(thiim_gpu_ctx* ctx) {
   return THIIM_OK;
 }
 
+// Deep-halo exchange (TBLOCK slabs), after a pass: per interface the lower
+// slab's two last owned planes -> the upper slab's ghost + extended planes, and
+// the upper slab's two first owned planes -> the lower slab's extended + ghost
+// planes; all 12 fields of the current set.
+int deep_first_plane(const Slab& sl, int which) {  // local padded plane of a 2-plane view
+  switch (which) {
+    case THIIM_HALO_SEND_DOWN: return 1 + sl.ext_lo;         // owned own0, own0+1
+    case THIIM_HALO_RECV_DOWN: return 0;                     // ghost own0-2, extended own0-1
+    case THIIM_HALO_SEND_UP: return sl.g.nz - 1 - sl.ext_hi;  // owned own1-2, own1-1
+    default: return sl.g.nz;                                 // extended own1, ghost own1+1
+  }
+}
+
+int exchange_deep(thiim_gpu_ctx* ctx) {
+  const int n = (int)ctx->slabs.size();
+  const size_t bytes2 = 2 * (size_t)ctx->pxy() * sizeof(double2);
+  for (auto& sl : ctx->slabs) {  // the pass finished everywhere
+    CK(cudaSetDevice(sl.device));
+    CK(cudaStreamSynchronize(sl.stream));
+  }
+  for (int s = 0; s + 1 < n; ++s) {
+    Slab& lo = ctx->slabs[s];
+    Slab& hi = ctx->slabs[s + 1];
+    const size_t lo_send = (size_t)deep_first_plane(lo, THIIM_HALO_SEND_UP) * lo.g.pxy;
+    const size_t lo_recv = (size_t)deep_first_plane(lo, THIIM_HALO_RECV_UP) * lo.g.pxy;
+    const size_t hi_send = (size_t)deep_first_plane(hi, THIIM_HALO_SEND_DOWN) * hi.g.pxy;
+    const size_t hi_recv = (size_t)deep_first_plane(hi, THIIM_HALO_RECV_DOWN) * hi.g.pxy;
+    CK(cudaSetDevice(hi.device));
+    for (int k = 0; k < 12; ++k)
+      CK(cudaMemcpyPeerAsync(hi.field(hi.cur, k) + hi_recv, hi.device, lo.field(lo.cur, k) + lo_send,
+                             lo.device, bytes2, hi.stream));
+    CK(cudaSetDevice(lo.device));
+    for (int k = 0; k < 12; ++k)
+      CK(cudaMemcpyPeerAsync(lo.field(lo.cur, k) + lo_recv, lo.device, hi.field(hi.cur, k) + hi_send,
+                             hi.device, bytes2, lo.stream));
+  }
+  return THIIM_OK;
+}
+
 int launch_split(thiim_gpu_ctx* ctx, Slab& s, int fam, long long* launches) {
   CK(cudaSetDevice(s.device));
   const Arrays A = s.arrays(s.cur, s.cur);
@@ -445,8 +488,8 @@ int tblock_zchunk(const Slab& s, long long cols) {
 
 template <int BY, int NG>
 int launch_tblock2_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
-  if (s.g.halo_lo || s.z1 < ctx->dims.nz)
-    return fail(THIIM_ERR_CONFIG, "TBLOCK needs a whole-z context (no halo slabs yet)");
+  if (!s.deep && (s.g.halo_lo || s.z1 < ctx->dims.nz))
+    return fail(THIIM_ERR_CONFIG, "TBLOCK on a slab needs a deep-halo slab context");
   const Arrays A = s.arrays(s.cur, s.cur ^ 1);
   const int cur = s.cur, nf = s.nfield_sets;
   auto fslot = [&](int k) { return cur * 12 + k; };
@@ -479,6 +522,7 @@ int launch_tblock2_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
   if (zc <= 0) zc = tblock_zchunk(s, (long long)tiles_x * tiles_y);
   const dim3 grid(tiles_x * tiles_y, 1, (s.g.nz + zc - 1) / zc);
   const dim3 block(32, BY + 1);
+  if (scratch && s.deep) return fail(THIIM_ERR_CONFIG, "the scratch TBLOCK variant is whole-z only");
   if (scratch) {
     if constexpr (BY == 15) {
       TbParams P;
@@ -504,8 +548,8 @@ int launch_tblock2_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
 
 template <int BY, int NG>
 int launch_tblock_table_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
-  if (s.g.halo_lo || s.z1 < ctx->dims.nz)
-    return fail(THIIM_ERR_CONFIG, "TBLOCK needs a whole-z context (no halo slabs yet)");
+  if (!s.deep && (s.g.halo_lo || s.z1 < ctx->dims.nz))
+    return fail(THIIM_ERR_CONFIG, "TBLOCK on a slab needs a deep-halo slab context");
   const Arrays A = s.arrays(s.cur, s.cur ^ 1);
   int r = ensure_tmap(s, BY, 0);
   if (r) return r;
@@ -701,9 +745,6 @@ static int create_impl(const thiim_dims* dims, const thiim_gpu_opts* opts,
     return fail(THIIM_ERR_CONFIG, "the table coefficient layout runs on the fused or TBLOCK engine");
   if (table && (o.n_materials < 1 || o.n_materials > kMaxMaterials))
     return fail(THIIM_ERR_CONFIG, "n_materials must be in 1..16 for the table layout");
-  if (o.engine == THIIM_ENGINE_TBLOCK &&
-      (ranges.size() != 1 || ranges[0].first != 0 || ranges[0].second != dims->nz))
-    return fail(THIIM_ERR_CONFIG, "engine TBLOCK runs on one GPU (halo slabs need 2-plane halos)");
   for (const auto& r : ranges)
     if (r.first < 0 || r.second > dims->nz || r.second - r.first < 4)
       return fail(THIIM_ERR_CONFIG, "each z-slab needs at least 4 planes inside the grid");
@@ -723,14 +764,12 @@ static int create_impl(const thiim_dims* dims, const thiim_gpu_opts* opts,
   const int n = (int)ranges.size();
   ctx->engine = o.engine;
   const bool whole_z = n == 1 && ranges[0].first == 0 && ranges[0].second == dims->nz;
-  // table layout: TBLOCK on a whole-z context, else fused (it has no split form)
-  if (table && o.engine == THIIM_ENGINE_AUTO)
-    ctx->engine = whole_z ? THIIM_ENGINE_TBLOCK : THIIM_ENGINE_FUSED;
+  // AUTO: TBLOCK (two steps per HBM pass, odd remainders fused; z-slabs keep
+  // deep two-plane halos exchanged per pass); the table layout has no split form
+  if (table && o.engine == THIIM_ENGINE_AUTO) ctx->engine = THIIM_ENGINE_TBLOCK;
   if (o.engine == THIIM_ENGINE_AUTO && !table) {
-    // one whole-z slab: TBLOCK (two steps per HBM pass; odd remainders run
-    // fused); z-slabs: fused (halo exchange every step); either needs the
-    // ping-pong field set (52 arrays) -- else split in place (40)
-    ctx->engine = whole_z ? THIIM_ENGINE_TBLOCK : THIIM_ENGINE_FUSED;
+    // TBLOCK needs the ping-pong field set (52 arrays); else split in place (40)
+    ctx->engine = THIIM_ENGINE_TBLOCK;
     for (int s = 0; s < n; ++s) {
       const size_t freeb = device_available(o.device + dev_step * s);
       const size_t need = (size_t)(ranges[s].second - ranges[s].first + 2) * (size_t)pxy *
@@ -742,8 +781,14 @@ static int create_impl(const thiim_dims* dims, const thiim_gpu_opts* opts,
   for (int s = 0; s < n; ++s) {
     Slab sl;
     sl.device = o.device + dev_step * s;
-    sl.z0 = ranges[s].first;
-    sl.z1 = ranges[s].second;
+    sl.own0 = ranges[s].first;
+    sl.own1 = ranges[s].second;
+    // TBLOCK slabs keep two-plane halos: one extended interior plane + the ghost
+    sl.deep = ctx->engine == THIIM_ENGINE_TBLOCK && !whole_z;
+    sl.ext_lo = sl.deep && sl.own0 > 0 ? 1 : 0;
+    sl.ext_hi = sl.deep && sl.own1 < dims->nz ? 1 : 0;
+    sl.z0 = sl.own0 - sl.ext_lo;
+    sl.z1 = sl.own1 + sl.ext_hi;
     sl.g.nx = dims->nx;
     sl.g.ny = dims->ny;
     sl.g.nz = sl.z1 - sl.z0;
@@ -843,6 +888,16 @@ int thiim_gpu_halo_view(thiim_gpu_ctx* ctx, int which, thiim_halo_view* v) {
   if (!ctx || !v) return fail(THIIM_ERR_CONFIG, "null argument");
   if (ctx->slabs.size() != 1) return fail(THIIM_ERR_CONFIG, "halo views need a slab context");
   const Slab& sl = ctx->slabs[0];
+  if (which < THIIM_HALO_SEND_DOWN || which > THIIM_HALO_RECV_UP)
+    return fail(THIIM_ERR_CONFIG, "unknown halo view");
+  if (sl.deep) {  // two contiguous planes of all 12 fields
+    v->base = sl.field(sl.cur, 0) + (size_t)deep_first_plane(sl, which) * (size_t)sl.g.pxy;
+    v->array_stride_bytes = (long long)(sl.stride * sizeof(double2));
+    v->plane_bytes = 2 * (long long)(sl.g.pxy * sizeof(double2));
+    v->n_arrays = 12;
+    v->device = sl.device;
+    return THIIM_OK;
+  }
   int plane, n;
   switch (which) {
     case THIIM_HALO_SEND_DOWN: plane = 1; n = 6; break;             // E of my first plane
@@ -856,6 +911,20 @@ int thiim_gpu_halo_view(thiim_gpu_ctx* ctx, int which, thiim_halo_view* v) {
   v->plane_bytes = (long long)(sl.g.pxy * sizeof(double2));
   v->n_arrays = n;
   v->device = sl.device;
+  return THIIM_OK;
+}
+
+int thiim_gpu_slab_info(thiim_gpu_ctx* ctx, thiim_slab_info* info) {
+  g_err.clear();
+  if (!ctx || !info) return fail(THIIM_ERR_CONFIG, "null argument");
+  if (ctx->slabs.size() != 1) return fail(THIIM_ERR_CONFIG, "slab info needs a slab context");
+  const Slab& sl = ctx->slabs[0];
+  info->own_z0 = sl.own0;
+  info->own_z1 = sl.own1;
+  info->local_z0 = sl.z0;
+  info->local_z1 = sl.z1;
+  info->exchange_period = sl.deep ? 2 : 1;
+  info->engine = ctx->engine;
   return THIIM_OK;
 }
 
@@ -1009,9 +1078,19 @@ int thiim_gpu_step(thiim_gpu_ctx* ctx, int steps, thiim_gpu_stats* stats) {
   int r;
   int n = 0;
   if (ctx->engine == THIIM_ENGINE_TBLOCK) {
-    for (; n + 2 <= steps; n += 2)
+    // deep slabs: a pass (2 steps, or 1 fused remainder step) leaves the owned
+    // planes current and the extended + ghost planes stale; the exchange after
+    // it refreshes them from the neighbours' owned planes
+    for (; n + 2 <= steps; n += 2) {
       for (auto& sl : ctx->slabs)
         if ((r = launch_tblock2(ctx, sl, &launches))) return r;
+      if (multi && (r = exchange_deep(ctx))) return r;
+    }
+    for (; n < steps; ++n) {
+      for (auto& sl : ctx->slabs)
+        if ((r = launch_fused(ctx, sl, &launches))) return r;
+      if (multi && (r = exchange_deep(ctx))) return r;
+    }
   }
   for (; n < steps; ++n) {
     if (ctx->engine == THIIM_ENGINE_SPLIT) {
@@ -1058,9 +1137,9 @@ static int download_impl(thiim_gpu_ctx* ctx, int a, thiim_c128* dst, int hp0 = 0
   const long long pxy = ctx->pxy();
   for (auto& sl : ctx->slabs) {
     CK(cudaSetDevice(sl.device));
-    // interior planes, plus the global ghost plane(s) this slab borders
-    const int p0 = sl.z0 == 0 ? 0 : 1;
-    const int p1 = sl.z1 == ctx->dims.nz ? sl.g.nz + 2 : sl.g.nz + 1;
+    // owned interior planes, plus the global ghost plane(s) this slab borders
+    const int p0 = sl.z0 == 0 ? 0 : 1 + sl.ext_lo;
+    const int p1 = sl.z1 == ctx->dims.nz ? sl.g.nz + 2 : sl.g.nz + 1 - sl.ext_hi;
     if (sl.z0 + p0 < hp0) return fail(THIIM_ERR_CONFIG, "host planes start above the slab");
     const size_t off_host = (size_t)(sl.z0 + p0 - hp0) * (size_t)pxy;
     CK(cudaMemcpyAsync(dst + off_host, sl.array(a) + (size_t)p0 * pxy,
@@ -1137,8 +1216,8 @@ int thiim_gpu_download_table(thiim_gpu_ctx* ctx, uint8_t* material_id, thiim_c12
   const long long pxy = ctx->pxy();
   for (auto& sl : ctx->slabs) {
     CK(cudaSetDevice(sl.device));
-    const int p0 = sl.z0 == 0 ? 0 : 1;
-    const int p1 = sl.z1 == ctx->dims.nz ? sl.g.nz + 2 : sl.g.nz + 1;
+    const int p0 = sl.z0 == 0 ? 0 : 1 + sl.ext_lo;
+    const int p1 = sl.z1 == ctx->dims.nz ? sl.g.nz + 2 : sl.g.nz + 1 - sl.ext_hi;
     CK(cudaMemcpy2DAsync(material_id + (size_t)(sl.z0 + p0) * pxy, (size_t)sl.g.px,
                          sl.mat + (size_t)p0 * sl.mplane, (size_t)sl.mp, (size_t)sl.g.px,
                          (size_t)(pxy / sl.g.px) * (p1 - p0), cudaMemcpyDeviceToHost, sl.stream));
@@ -1167,7 +1246,11 @@ int thiim_gpu_compare_fields(thiim_gpu_ctx* ctx, const thiim_c128* const ref[12]
   double num[12] = {0}, den[12] = {0};
   for (auto& sl : ctx->slabs) {
     CK(cudaSetDevice(sl.device));
-    const size_t elems = (size_t)(sl.g.nz + 2) * (size_t)pxy;
+    // owned planes only (a deep slab's extended planes duplicate its neighbours')
+    Grid go = sl.g;
+    go.nz = sl.own1 - sl.own0;
+    const size_t lofs = (size_t)sl.ext_lo * (size_t)pxy;
+    const size_t elems = (size_t)(go.nz + 2) * (size_t)pxy;
     double2* dref = nullptr;
     double* acc = nullptr;
     unsigned long long* cnt = nullptr;
@@ -1177,9 +1260,9 @@ int thiim_gpu_compare_fields(thiim_gpu_ctx* ctx, const thiim_c128* const ref[12]
     CK(cudaMemsetAsync(acc, 0, 24 * sizeof(double), sl.stream));
     CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), sl.stream));
     for (int k = 0; k < 12; ++k) {
-      CK(cudaMemcpyAsync(dref, ref[k] + (size_t)sl.z0 * pxy, elems * sizeof(double2),
+      CK(cudaMemcpyAsync(dref, ref[k] + (size_t)sl.own0 * pxy, elems * sizeof(double2),
                          cudaMemcpyHostToDevice, sl.stream));
-      k_compare<<<4 * sm_count(sl.device), 256, 0, sl.stream>>>(sl.g, sl.field(sl.cur, k), dref,
+      k_compare<<<4 * sm_count(sl.device), 256, 0, sl.stream>>>(go, sl.field(sl.cur, k) + lofs, dref,
                                                                 acc + 2 * k, cnt);
       CK(cudaGetLastError());
       CK(cudaStreamSynchronize(sl.stream));

@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
   double2 pH1x = make_double2(0.0, 0.0), pH1y = make_double2(0.0, 0.0);
   {
     const long long im = g.idx(xs, ys, qs) - pxy;
-    if (qs == 0) {
+    if (qs == 0 && !g.halo_lo) {
       if (own1 && inpad) {  // ghost plane below the grid: H never updated
         pH1x = csum(__ldg(A.f[HXY] + im), __ldg(A.f[HXZ] + im));
         pH1y = csum(__ldg(A.f[HYX] + im), __ldg(A.f[HYZ] + im));
@@ -650,7 +650,7 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
     for (int k = 0; k < 6; ++k) e[k] = inpad ? __ldg(A.f[k] + i1) : make_double2(0.0, 0.0);
     tm_st6(tnext, e);
     const long long im = i1 - pxy;
-    if (qs == 0) {
+    if (qs == 0 && !g.halo_lo) {
       if (own1 && inpad) {  // ghost plane below the grid: H never updated
         pH1x = csum(__ldg(A.f[HXY] + im), __ldg(A.f[HXZ] + im));
         pH1y = csum(__ldg(A.f[HYX] + im), __ldg(A.f[HYZ] + im));

@@ -11,7 +11,11 @@ ranks exchange, per interface:
     upper rank  SEND_DOWN : E x6 of its first plane                   -> lower RECV_UP
 
 The upper rank recomputes H_new on the received plane inside its sweep, so a
-step needs no mid-step exchange.  The exchange is torch.distributed
+step needs no mid-step exchange.  With the TBLOCK engine (two steps per HBM
+pass) slabs are "deep": two-plane halos of all 12 fields, exchanged after
+every 2-step pass (include/thiim_gpu.h).  Either way the driver loop is
+step(k <= exchange_period), then exchange -- the uploaded halos are valid for
+the first pass.  The exchange is torch.distributed
 point-to-point (batch_isend_irecv: NCCL over NVLink on GPUs, gloo on CPU for
 the tests); the engine object supplies the plane buffers, so the same logic
 drives the CUDA engine and the CPU test double.
@@ -50,8 +54,14 @@ class _CudaPlane:
                                          "data": (ptr, False), "version": 3, "strides": None}
 
 
+class _SlabInfo(ctypes.Structure):
+    _fields_ = [("own_z0", ctypes.c_int), ("own_z1", ctypes.c_int), ("local_z0", ctypes.c_int),
+                ("local_z1", ctypes.c_int), ("exchange_period", ctypes.c_int),
+                ("engine", ctypes.c_int)]
+
+
 class SlabGpuEngine:
-    """One rank's slab of the global grid on its GPU (fused engine)."""
+    """One rank's slab of the global grid on its GPU (AUTO: TBLOCK deep-halo slab)."""
 
     def __init__(self, global_dims: GridDims, z0: int, z1: int, opts: Optional[GpuOptions] = None):
         self.dims, self.z0, self.z1 = global_dims, z0, z1
@@ -66,6 +76,13 @@ class SlabGpuEngine:
         o = self.opts._c()
         _check(L.thiim_gpu_create_slab(ctypes.byref(d), z0, z1, ctypes.byref(o),
                                        ctypes.byref(self._ctx)))
+        L.thiim_gpu_slab_info.argtypes = [ctypes.c_void_p, ctypes.POINTER(_SlabInfo)]
+        info = _SlabInfo()
+        _check(L.thiim_gpu_slab_info(self._ctx, ctypes.byref(info)))
+        # padded planes this rank's host buffers hold: [local_z0, local_z1 + 2)
+        self.local_z0, self.local_z1 = info.local_z0, info.local_z1
+        self.exchange_period = info.exchange_period
+        self.engine = info.engine
 
     def close(self):
         if self._ctx:
@@ -83,20 +100,28 @@ class SlabGpuEngine:
     def download_fields(self, s: ProblemState):
         _check(lib().thiim_gpu_download_fields(self._ctx, _ptrs(s.arrays[0:12])))
 
-    # rank-local host buffers: global padded planes [z0, z1+2)
+    # rank-local host buffers: global padded planes [local_z0, local_z1 + 2)
     def local_host_problem(self, kind: int = GEN_RANDOM, seed: int = 1) -> List[np.ndarray]:
         pxy = (self.dims.nx + 2) * (self.dims.ny + 2)
-        arrays = [np.zeros((self.z1 - self.z0 + 2) * pxy, dtype=np.complex128) for _ in range(40)]
+        n = self.local_z1 - self.local_z0 + 2
+        arrays = [np.zeros(n * pxy, dtype=np.complex128) for _ in range(40)]
         d = _Dims(self.dims.nx, self.dims.ny, self.dims.nz, self.dims.ghost)
-        _check(lib().thiim_generate_host_planes(ctypes.byref(d), kind, seed, self.z0, self.z1 + 2,
-                                                _ptrs(arrays)))
+        _check(lib().thiim_generate_host_planes(ctypes.byref(d), kind, seed, self.local_z0,
+                                                self.local_z1 + 2, _ptrs(arrays)))
         return arrays
 
+    def owned_planes(self, arrays: List[np.ndarray], k: int) -> np.ndarray:
+        """Interior planes [z0, z1) of host array k of local_host_problem()."""
+        pxy = (self.dims.nx + 2) * (self.dims.ny + 2)
+        a = self.z0 - self.local_z0 + 1
+        return arrays[k][a * pxy:(a + self.z1 - self.z0) * pxy]
+
     def upload_local(self, arrays: List[np.ndarray]):
-        _check(lib().thiim_gpu_upload_planes(self._ctx, _ptrs(arrays), self.z0))
+        _check(lib().thiim_gpu_upload_planes(self._ctx, _ptrs(arrays), self.local_z0))
 
     def download_local(self, arrays: List[np.ndarray]):
-        _check(lib().thiim_gpu_download_fields_planes(self._ctx, _ptrs(arrays[0:12]), self.z0))
+        _check(lib().thiim_gpu_download_fields_planes(self._ctx, _ptrs(arrays[0:12]),
+                                                      self.local_z0))
 
     def step(self, steps: int = 1):
         st = _Stats()
@@ -167,11 +192,16 @@ class HaloExchanger:
 
 
 def run_distributed(engine, steps: int, exchanger: HaloExchanger) -> dict:
-    """`steps` THIIM iterations of the decomposed grid: exchange, then step."""
+    """`steps` THIIM iterations of the decomposed grid: passes of up to
+    engine.exchange_period steps, each followed by the halo exchange."""
+    period = max(1, int(getattr(engine, "exchange_period", 1)))
     sent = 0
     launches = 0
-    for _ in range(steps):
-        sent += exchanger.exchange(engine)
-        st = engine.step(1)
+    done = 0
+    while done < steps:
+        k = min(period, steps - done)
+        st = engine.step(k)
         launches += getattr(st, "kernel_launches", 0)
+        sent += exchanger.exchange(engine)
+        done += k
     return {"halo_bytes_sent": sent, "kernel_launches": launches}

@@ -43,6 +43,42 @@ class SlabCpuEngine:
             O.c_step_slab(self.ldims, self.local, self.z0 > 0)
 
 
+class SlabCpuDeepEngine:
+    """Test double of a TBLOCK (deep-halo) slab: local interior planes
+    [z0-e_lo, z1+e_hi) -- one extended plane per internal interface -- plus a
+    ghost each side; a pass of k <= 2 steps is k oracle slab steps on that
+    extended domain, and every view is two planes of all 12 fields
+    (include/thiim_gpu.h, deep-halo protocol)."""
+
+    exchange_period = 2
+
+    def __init__(self, global_arrays, dims, z0, z1):
+        self.dims, self.z0, self.z1 = dims, z0, z1
+        self.elo, self.ehi = int(z0 > 0), int(z1 < dims.nz)
+        self.lz0, self.lz1 = z0 - self.elo, z1 + self.ehi
+        self.pxy = pxy = (dims.nx + 2) * (dims.ny + 2)
+        self.local = [np.ascontiguousarray(a[self.lz0 * pxy:(self.lz1 + 2) * pxy])
+                      for a in global_arrays]
+        self.ldims = (dims.nx, dims.ny, self.lz1 - self.lz0)
+
+    def halo(self, which):
+        nzl = self.lz1 - self.lz0
+        first = {D.SEND_DOWN: 1 + self.elo, D.RECV_DOWN: 0, D.SEND_UP: nzl - 1 - self.ehi,
+                 D.RECV_UP: nzl}[which]
+        p = self.pxy
+        return [torch.from_numpy(self.local[k][first * p:(first + 2) * p].view(np.float64))
+                for k in range(12)]
+
+    def step(self, n=1):
+        assert n <= 2, "deep slabs exchange after at most two steps"
+        for _ in range(n):
+            O.c_step_slab(self.ldims, self.local, self.lz0 > 0)
+
+    def owned(self, k):
+        a = self.z0 - self.lz0 + 1
+        return self.local[k][a * self.pxy:(a + self.z1 - self.z0) * self.pxy]
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -51,18 +87,19 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, shape, steps, seed, out_dir):
+def _worker(rank, world, port, shape, steps, seed, out_dir, deep=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     dims = P.GridDims(*shape)
     arrays = O.c_generate(shape, seed)
     z0, z1 = D.slab_bounds(dims.nz, world, rank)
-    eng = SlabCpuEngine(arrays, dims, z0, z1)
+    eng = (SlabCpuDeepEngine if deep else SlabCpuEngine)(arrays, dims, z0, z1)
     stats = D.run_distributed(eng, steps, D.HaloExchanger(rank, world))
     pxy = eng.pxy
-    np.save(os.path.join(out_dir, "r%d.npy" % rank),
-            np.stack([a[pxy:(z1 - z0 + 1) * pxy] for a in eng.local[:12]]))
+    owned = [eng.owned(k) for k in range(12)] if deep else \
+        [a[pxy:(z1 - z0 + 1) * pxy] for a in eng.local[:12]]
+    np.save(os.path.join(out_dir, "r%d.npy" % rank), np.stack(owned))
     np.save(os.path.join(out_dir, "s%d.npy" % rank), np.array([stats["halo_bytes_sent"]]))
     dist.destroy_process_group()
 
@@ -86,6 +123,30 @@ def test_slab_decomposition_matches_single_domain(tmp_path, world, shape, steps)
         sent += int(np.load(tmp_path / ("s%d.npy" % r))[0])
     # 16 array-planes cross each interface per step (10 up, 6 down)
     assert sent == steps * (world - 1) * 16 * pxy * 16
+
+
+@pytest.mark.parametrize("world,shape,steps", [(2, (9, 7, 12), 5), (3, (6, 5, 14), 4),
+                                               (2, (8, 8, 8), 2), (3, (7, 6, 15), 7)])
+def test_deep_halo_decomposition_matches_single_domain(tmp_path, world, shape, steps):
+    """The TBLOCK slab protocol: two-plane halos of all 12 fields exchanged
+    after every pass of <= 2 steps; bitwise equal to the undecomposed run."""
+    mp.spawn(_worker, args=(world, _free_port(), shape, steps, 23, str(tmp_path), True),
+             nprocs=world, join=True)
+    ref = O.c_generate(shape, 23)
+    O.c_step(shape, ref, steps)
+    dims = P.GridDims(*shape)
+    pxy = (dims.nx + 2) * (dims.ny + 2)
+    sent = 0
+    for r in range(world):
+        z0, z1 = D.slab_bounds(dims.nz, world, r)
+        got = np.load(tmp_path / ("r%d.npy" % r))
+        for k in range(12):
+            want = ref[k][(z0 + 1) * pxy:(z1 + 1) * pxy]
+            assert np.array_equal(got[k].view(np.uint64), want.view(np.uint64)), (r, k)
+        sent += int(np.load(tmp_path / ("s%d.npy" % r))[0])
+    # per pass and interface: 2 planes x 12 fields each way
+    passes = (steps + 1) // 2
+    assert sent == passes * (world - 1) * 48 * pxy * 16
 
 
 def test_slab_bounds_match_reference_z_slab():

@@ -27,24 +27,31 @@ def local_exchange(engines):
     torch.cuda.synchronize()
 
 
+@pytest.mark.parametrize("engine", [P.ENGINE_FUSED, P.ENGINE_TBLOCK])
 @pytest.mark.parametrize("nslabs,shape,steps", [(2, (40, 33, 24), 4), (3, (64, 40, 30), 3),
-                                                (4, (31, 29, 17), 2)])
-def test_gpu_slabs_match_single_domain(nslabs, shape, steps):
+                                                (4, (31, 29, 17), 2), (2, (70, 45, 40), 7)])
+def test_gpu_slabs_match_single_domain(nslabs, shape, steps, engine):
+    """Driver protocol of include/thiim_gpu.h: passes of <= exchange_period
+    steps, each followed by the halo exchange (TBLOCK: deep two-plane halos)."""
     dims = P.GridDims(*shape)
     host = P.generate_problem(dims, P.GEN_RANDOM, 8)
     engines = []
     for r in range(nslabs):
         z0, z1 = D.slab_bounds(dims.nz, nslabs, r)
-        e = D.SlabGpuEngine(dims, z0, z1, P.GpuOptions(device=0))
+        e = D.SlabGpuEngine(dims, z0, z1, P.GpuOptions(device=0, engine=engine))
+        assert e.exchange_period == (2 if engine == P.ENGINE_TBLOCK else 1)
         if r % 2:
             e.generate(P.GEN_RANDOM, 8)  # device generator == host generator
         else:
             e.upload(host)
         engines.append(e)
-    for _ in range(steps):
-        local_exchange(engines)
+    done = 0
+    while done < steps:
+        k = min(engines[0].exchange_period, steps - done)
         for e in engines:
-            e.step(1)
+            e.step(k)
+        local_exchange(engines)
+        done += k
     got = P.allocate_state(dims)
     for e in engines:
         e.download_fields(got)
@@ -84,7 +91,7 @@ def test_cpp_adapter_binary():
     assert "0 failed" in r.stdout
 
 
-@pytest.mark.parametrize("engine", [P.ENGINE_SPLIT, P.ENGINE_FUSED])
+@pytest.mark.parametrize("engine", [P.ENGINE_SPLIT, P.ENGINE_FUSED, P.ENGINE_TBLOCK])
 @pytest.mark.parametrize("n", [2, 3])
 def test_single_process_multi_slab_context(engine, n):
     """One context driving n z-slabs with peer-copy halo exchange (the path
@@ -98,15 +105,17 @@ def test_single_process_multi_slab_context(engine, n):
     assert P.compare_states(got, want).bitwise_equal
 
 
-def test_single_process_multi_slab_table_layout():
+@pytest.mark.parametrize("engine,steps", [(P.ENGINE_FUSED, 4), (P.ENGINE_TBLOCK, 4),
+                                          (P.ENGINE_TBLOCK, 5)])
+def test_single_process_multi_slab_table_layout(engine, steps):
     dims = P.GridDims(30, 26, 48)
     host = P.generate_problem(dims, P.GEN_LAYERED, 3)
     want = P.clone_state(host)
-    O.c_step((30, 26, 48), want.arrays, 4, threads=8)
+    O.c_step((30, 26, 48), want.arrays, steps, threads=8)
     with P.GpuEngine(dims, P.GpuOptions(n_gpus=3, same_device=1, coeff_layout=P.COEFF_TABLE,
-                                        n_materials=6)) as eng:
+                                        n_materials=6, engine=engine)) as eng:
         eng.generate(P.GEN_LAYERED, 3)
-        eng.step(4)
+        eng.step(steps)
         got = P.allocate_state(dims)
         eng.download_fields(got)
     assert P.compare_states(got, want).bitwise_equal
