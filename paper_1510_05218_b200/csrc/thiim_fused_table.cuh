@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
 
   auto& R = sm.ring;
   RingCursor rc = ring_cursor(R);
-#define RD(k, b) ring_read(R, rc, k, b, tx, ty)
+#define RD(k, b) ring_read<true>(R, rc, k, b, tx, ty)
   int mid_next = inpad ? mat_at(z0 + 1) : 0;  // material id, one plane ahead
   for (int z = z0; z < z1; ++z, i += pxy) {
     int mid = mid_next;

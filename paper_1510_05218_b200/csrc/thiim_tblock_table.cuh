@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
 
   auto& R = sm.ring;
   RingCursor rc = ring_cursor(R);
-#define RD(k, b) ring_read(R, rc, k, b, tx, ty)
+#define RD(k, b) ring_read<true>(R, rc, k, b, tx, ty)
 
   // ---- level-1 prologue: E_old splits at qs (to TMEM), H^1 sums at qs-1
   double2 pH1x = make_double2(0.0, 0.0), pH1y = make_double2(0.0, 0.0);
