@@ -221,15 +221,16 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
     en[4] = RD(0, BOX_A);
     en[5] = RD(1, BOX_A);
     ring_release(R, rc, tx, ring_dep(en[4], en[5]));
+    // own sums from registers; neighbours read them from shared memory
+    const double2 sEx = csum(e[EXY], e[EXZ]), sEy = csum(e[EYX], e[EYZ]), sEz = csum(e[EZX], e[EZY]);
     if (inpad) {
-      sm.sE[0][ty][tx] = csum(e[EXY], e[EXZ]);
-      sm.sE[1][ty][tx] = csum(e[EYX], e[EYZ]);
-      sm.sE[2][ty][tx] = csum(e[EZX], e[EZY]);
+      sm.sE[0][ty][tx] = sEx;
+      sm.sE[1][ty][tx] = sEy;
+      sm.sE[2][ty][tx] = sEz;
     }
     named_sync(1, NCOMP);
 
     // (b) H half-step at plane z (own cells: all six; ring: the four needed)
-    const double2 sEx = sm.sE[0][ty][tx], sEy = sm.sE[1][ty][tx], sEz = sm.sE[2][ty][tx];
     const double2 nEx = csum(en[EXY], en[EXZ]), nEy = csum(en[EYX], en[EYZ]);
     double2 h[6];
     {  // Hxy
@@ -278,15 +279,15 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
 #pragma unroll
       for (int k = 0; k < 6; ++k) A.fo[HXY + k][i] = h[k];
     }
+    const double2 sHx = csum(h[0], h[1]), sHy = csum(h[2], h[3]), sHz = csum(h[4], h[5]);
     if (own || ring_x || ring_y) {
-      sm.sH[0][ty][tx] = csum(h[0], h[1]);
-      sm.sH[1][ty][tx] = csum(h[2], h[3]);
-      sm.sH[2][ty][tx] = csum(h[4], h[5]);
+      sm.sH[0][ty][tx] = sHx;
+      sm.sH[1][ty][tx] = sHy;
+      sm.sH[2][ty][tx] = sHz;
     }
     named_sync(1, NCOMP);
 
     // (c) E half-step at plane z for own cells
-    const double2 sHx = sm.sH[0][ty][tx], sHy = sm.sH[1][ty][tx], sHz = sm.sH[2][ty][tx];
     {  // Exy, Eyx
       ring_wait(R, rc);
       const double2 t0 = RD(0, BOX_C), c0 = RD(1, BOX_C), t1 = RD(2, BOX_C), c1 = RD(3, BOX_C);

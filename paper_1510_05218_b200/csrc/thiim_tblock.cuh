@@ -298,13 +298,15 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
       en[4] = RD(0, BOX_A);
       en[5] = RD(1, BOX_A);
       ring_release(R, rc, tx, ring_dep(en[4], en[5]));
+      // own sums from registers; neighbours read them from shared memory
+      const double2 sEx = csum(e[EXY], e[EXZ]), sEy = csum(e[EYX], e[EYZ]),
+                    sEz = csum(e[EZX], e[EZY]);
       if (inpad) {
-        sm.sE[0][ty][tx] = csum(e[EXY], e[EXZ]);
-        sm.sE[1][ty][tx] = csum(e[EYX], e[EYZ]);
-        sm.sE[2][ty][tx] = csum(e[EZX], e[EZY]);
+        sm.sE[0][ty][tx] = sEx;
+        sm.sE[1][ty][tx] = sEy;
+        sm.sE[2][ty][tx] = sEz;
       }
       named_sync(1, NCOMP);
-      const double2 sEx = sm.sE[0][ty][tx], sEy = sm.sE[1][ty][tx], sEz = sm.sE[2][ty][tx];
       const double2 nEx = csum(en[EXY], en[EXZ]), nEy = csum(en[EYX], en[EYZ]);
       double2 h[6];
       {
@@ -349,13 +351,13 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
         ring_release(R, rc, tx, ring_dep(h[5], c, t));
         if (upd1_z) h[5] = upd(h[5], t, c, sm.sE[0][ty + 1][tx], sEx);
       }
+      const double2 sHx = csum(h[0], h[1]), sHy = csum(h[2], h[3]), sHz = csum(h[4], h[5]);
       if (own1 || rx1 || ry1) {
-        sm.sH[0][ty][tx] = csum(h[0], h[1]);
-        sm.sH[1][ty][tx] = csum(h[2], h[3]);
-        sm.sH[2][ty][tx] = csum(h[4], h[5]);
+        sm.sH[0][ty][tx] = sHx;
+        sm.sH[1][ty][tx] = sHy;
+        sm.sH[2][ty][tx] = sHz;
       }
       named_sync(1, NCOMP);
-      const double2 sHx = sm.sH[0][ty][tx], sHy = sm.sH[1][ty][tx], sHz = sm.sH[2][ty][tx];
       double2 eo[6];
       const bool ue = own1 && interior;
       {
@@ -430,13 +432,15 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
 #pragma unroll
       for (int k = 0; k < 4; ++k) h[k] = RD(k, BOX_A);
       ring_release(R, rc, tx, ring_dep(h[0], h[1], h[2], h[3]));
+      // own sums from registers; neighbours read them from shared memory
+      const double2 sEx = csum(e1[EXY], e1[EXZ]), sEy = csum(e1[EYX], e1[EYZ]),
+                    sEz = csum(e1[EZX], e1[EZY]);
       if (inpad) {
-        sm.sE[0][ty][tx] = csum(e1[EXY], e1[EXZ]);
-        sm.sE[1][ty][tx] = csum(e1[EYX], e1[EYZ]);
-        sm.sE[2][ty][tx] = csum(e1[EZX], e1[EZY]);
+        sm.sE[0][ty][tx] = sEx;
+        sm.sE[1][ty][tx] = sEy;
+        sm.sE[2][ty][tx] = sEz;
       }
       named_sync(1, NCOMP);
-      const double2 sEx = sm.sE[0][ty][tx], sEy = sm.sE[1][ty][tx], sEz = sm.sE[2][ty][tx];
       const bool u2x = upd2_x && plane_ok, u2y = upd2_y && plane_ok, u2z = upd2_z && plane_ok;
       {  // Hxy, Hyx
         ring_wait(R, rc);
@@ -481,13 +485,13 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
 #pragma unroll
         for (int k = 0; k < 6; ++k) st_hint(A.fo[HXY + k] + i, h[k], first);
       }
+      const double2 sHx = csum(h[0], h[1]), sHy = csum(h[2], h[3]), sHz = csum(h[4], h[5]);
       if (own2 || rx2 || ry2) {
-        sm.sH[0][ty][tx] = csum(h[0], h[1]);
-        sm.sH[1][ty][tx] = csum(h[2], h[3]);
-        sm.sH[2][ty][tx] = csum(h[4], h[5]);
+        sm.sH[0][ty][tx] = sHx;
+        sm.sH[1][ty][tx] = sHy;
+        sm.sH[2][ty][tx] = sHz;
       }
       named_sync(1, NCOMP);
-      const double2 sHx = sm.sH[0][ty][tx], sHy = sm.sH[1][ty][tx], sHz = sm.sH[2][ty][tx];
       const bool ue = own2 && interior;
       {  // Exy, Eyx
         ring_wait(R, rc);
@@ -712,13 +716,15 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
         nEx = csum(en[EXY], en[EXZ]);
         nEy = csum(en[EYX], en[EYZ]);
       }
+      // own sums from registers; neighbours read them from shared memory
+      const double2 sEx = csum(e[EXY], e[EXZ]), sEy = csum(e[EYX], e[EYZ]),
+                    sEz = csum(e[EZX], e[EZY]);
       if (inpad) {
-        sm.sE[0][ty][tx] = csum(e[EXY], e[EXZ]);
-        sm.sE[1][ty][tx] = csum(e[EYX], e[EYZ]);
-        sm.sE[2][ty][tx] = csum(e[EZX], e[EZY]);
+        sm.sE[0][ty][tx] = sEx;
+        sm.sE[1][ty][tx] = sEy;
+        sm.sE[2][ty][tx] = sEz;
       }
       named_sync(1, NCOMP);
-      const double2 sEx = sm.sE[0][ty][tx], sEy = sm.sE[1][ty][tx], sEz = sm.sE[2][ty][tx];
       double2 h[6];
       {
         ring_wait(R, rc);
@@ -762,14 +768,14 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
         ring_release(R, rc, tx, ring_dep(h[5], c, t));
         if (upd1_z) h[5] = upd(h[5], t, c, sm.sE[0][ty + 1][tx], sEx);
       }
+      const double2 sHx = csum(h[0], h[1]), sHy = csum(h[2], h[3]), sHz = csum(h[4], h[5]);
       if (own1 || rx1 || ry1) {
-        sm.sH[0][ty][tx] = csum(h[0], h[1]);
-        sm.sH[1][ty][tx] = csum(h[2], h[3]);
-        sm.sH[2][ty][tx] = csum(h[4], h[5]);
+        sm.sH[0][ty][tx] = sHx;
+        sm.sH[1][ty][tx] = sHy;
+        sm.sH[2][ty][tx] = sHz;
       }
       tm_st6(tslot + 24, h);  // H^1(q)
       named_sync(1, NCOMP);
-      const double2 sHx = sm.sH[0][ty][tx], sHy = sm.sH[1][ty][tx], sHz = sm.sH[2][ty][tx];
       const bool ue = own1 && interior;
       {
         ring_wait(R, rc);
@@ -832,13 +838,15 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
           h[k] = inpad ? __ldg(A.f[HXY + k] + i) : make_double2(0.0, 0.0);
         }
       }
+      // own sums from registers; neighbours read them from shared memory
+      const double2 sEx = csum(e1[EXY], e1[EXZ]), sEy = csum(e1[EYX], e1[EYZ]),
+                    sEz = csum(e1[EZX], e1[EZY]);
       if (inpad) {
-        sm.sE[0][ty][tx] = csum(e1[EXY], e1[EXZ]);
-        sm.sE[1][ty][tx] = csum(e1[EYX], e1[EYZ]);
-        sm.sE[2][ty][tx] = csum(e1[EZX], e1[EZY]);
+        sm.sE[0][ty][tx] = sEx;
+        sm.sE[1][ty][tx] = sEy;
+        sm.sE[2][ty][tx] = sEz;
       }
       named_sync(1, NCOMP);
-      const double2 sEx = sm.sE[0][ty][tx], sEy = sm.sE[1][ty][tx], sEz = sm.sE[2][ty][tx];
       const bool u2x = upd2_x && plane_ok, u2y = upd2_y && plane_ok, u2z = upd2_z && plane_ok;
       {  // Hxy, Hyx
         ring_wait(R, rc);
@@ -883,13 +891,13 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
 #pragma unroll
         for (int k = 0; k < 6; ++k) st_hint(A.fo[HXY + k] + i, h[k], first);
       }
+      const double2 sHx = csum(h[0], h[1]), sHy = csum(h[2], h[3]), sHz = csum(h[4], h[5]);
       if (own2 || rx2 || ry2) {
-        sm.sH[0][ty][tx] = csum(h[0], h[1]);
-        sm.sH[1][ty][tx] = csum(h[2], h[3]);
-        sm.sH[2][ty][tx] = csum(h[4], h[5]);
+        sm.sH[0][ty][tx] = sHx;
+        sm.sH[1][ty][tx] = sHy;
+        sm.sH[2][ty][tx] = sHz;
       }
       named_sync(1, NCOMP);
-      const double2 sHx = sm.sH[0][ty][tx], sHy = sm.sH[1][ty][tx], sHz = sm.sH[2][ty][tx];
       const bool ue = own2 && interior;
       {  // Exy, Eyx
         ring_wait(R, rc);

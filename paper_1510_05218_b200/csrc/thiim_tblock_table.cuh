@@ -184,13 +184,15 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
         nEx = csum(en[EXY], en[EXZ]);
         nEy = csum(en[EYX], en[EYZ]);
       }
+      // own sums from registers; neighbours read them from shared memory
+      const double2 sEx = csum(e[EXY], e[EXZ]), sEy = csum(e[EYX], e[EYZ]),
+                    sEz = csum(e[EZX], e[EZY]);
       if (inpad) {
-        sm.sE[0][ty][tx] = csum(e[EXY], e[EXZ]);
-        sm.sE[1][ty][tx] = csum(e[EYX], e[EYZ]);
-        sm.sE[2][ty][tx] = csum(e[EZX], e[EZY]);
+        sm.sE[0][ty][tx] = sEx;
+        sm.sE[1][ty][tx] = sEy;
+        sm.sE[2][ty][tx] = sEz;
       }
       named_sync(1, NCOMP);
-      const double2 sEx = sm.sE[0][ty][tx], sEy = sm.sE[1][ty][tx], sEz = sm.sE[2][ty][tx];
       double2 h[6];
       ring_wait(R, rc);
       h[0] = RD(0, BOX_BY);
@@ -214,14 +216,14 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
         h[4] = upd(h[4], C[HZX], C[12 + HZX], sm.sE[1][ty][tx + 1], sEy);
         h[5] = upd(h[5], C[HZY], C[12 + HZY], sm.sE[0][ty + 1][tx], sEx);
       }
+      const double2 sHx = csum(h[0], h[1]), sHy = csum(h[2], h[3]), sHz = csum(h[4], h[5]);
       if (own1 || rx1 || ry1) {
-        sm.sH[0][ty][tx] = csum(h[0], h[1]);
-        sm.sH[1][ty][tx] = csum(h[2], h[3]);
-        sm.sH[2][ty][tx] = csum(h[4], h[5]);
+        sm.sH[0][ty][tx] = sHx;
+        sm.sH[1][ty][tx] = sHy;
+        sm.sH[2][ty][tx] = sHz;
       }
       tm_st6(tslot + 24, h);  // H^1(q)
       named_sync(1, NCOMP);
-      const double2 sHx = sm.sH[0][ty][tx], sHy = sm.sH[1][ty][tx], sHz = sm.sH[2][ty][tx];
       if (own1 && interior) {
         e[EXY] = upd(e[EXY], C[EXY], C[12 + EXY], sm.sH[2][ty - 1][tx], sHz);
         e[EXZ] = upd_src(e[EXZ], C[EXZ], C[12 + EXZ], pH1y, sHy, C[24 + SRC_EXZ]);
@@ -262,13 +264,15 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
           h[k] = inpad ? __ldg(A.f[HXY + k] + i) : make_double2(0.0, 0.0);
         }
       }
+      // own sums from registers; neighbours read them from shared memory
+      const double2 sEx = csum(e1[EXY], e1[EXZ]), sEy = csum(e1[EYX], e1[EYZ]),
+                    sEz = csum(e1[EZX], e1[EZY]);
       if (inpad) {
-        sm.sE[0][ty][tx] = csum(e1[EXY], e1[EXZ]);
-        sm.sE[1][ty][tx] = csum(e1[EYX], e1[EYZ]);
-        sm.sE[2][ty][tx] = csum(e1[EZX], e1[EZY]);
+        sm.sE[0][ty][tx] = sEx;
+        sm.sE[1][ty][tx] = sEy;
+        sm.sE[2][ty][tx] = sEz;
       }
       named_sync(1, NCOMP);
-      const double2 sEx = sm.sE[0][ty][tx], sEy = sm.sE[1][ty][tx], sEz = sm.sE[2][ty][tx];
       if (upd2_x && plane_ok) {
         h[0] = upd(h[0], C[HXY], C[12 + HXY], sm.sE[2][ty + 1][tx], sEz);
         h[1] = upd_src(h[1], C[HXZ], C[12 + HXZ], nEy, sEy, C[24 + SRC_HXZ]);
@@ -294,13 +298,13 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
 #pragma unroll
         for (int k = 0; k < 6; ++k) st_hint(A.fo[HXY + k] + i, h[k], first);
       }
+      const double2 sHx = csum(h[0], h[1]), sHy = csum(h[2], h[3]), sHz = csum(h[4], h[5]);
       if (own2 || rx2 || ry2) {
-        sm.sH[0][ty][tx] = csum(h[0], h[1]);
-        sm.sH[1][ty][tx] = csum(h[2], h[3]);
-        sm.sH[2][ty][tx] = csum(h[4], h[5]);
+        sm.sH[0][ty][tx] = sHx;
+        sm.sH[1][ty][tx] = sHy;
+        sm.sH[2][ty][tx] = sHz;
       }
       named_sync(1, NCOMP);
-      const double2 sHx = sm.sH[0][ty][tx], sHy = sm.sH[1][ty][tx], sHz = sm.sH[2][ty][tx];
       if (own2 && interior) {
         st_hint(A.fo[EXY] + i, upd(e1[EXY], C[EXY], C[12 + EXY], sm.sH[2][ty - 1][tx], sHz), first);
         st_hint(A.fo[EXZ] + i, upd_src(e1[EXZ], C[EXZ], C[12 + EXZ], pH2y, sHy, C[24 + SRC_EXZ]),
