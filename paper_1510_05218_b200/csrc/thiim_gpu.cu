@@ -382,8 +382,8 @@ int ensure_tmap(Slab& s, int by, int promo) {
                               (cuuint64_t)(s.g.nz + 2), (cuuint64_t)s.n_arrays()};
   const cuuint64_t strides[3] = {(cuuint64_t)s.g.px * 16, (cuuint64_t)s.g.pxy * 16,
                                  (cuuint64_t)s.stride * 16};
-  const int bw[NBOX] = {32, 31, 31, 30, 30};
-  const int bh[NBOX] = {by, by - 1, by - 2, by - 1, by - 2};
+  const int bw[NBOX] = {32, 31, 31, 30, 30, 29, 28};  // BoxGeom
+  const int bh[NBOX] = {by, by - 1, by - 2, by - 1, by - 2, by - 3, by - 4};
   for (int b = 0; b < NBOX; ++b) {
     const cuuint32_t box[4] = {(cuuint32_t)(2 * bw[b]), (cuuint32_t)bh[b], 1, 1};
     const cuuint32_t estr[4] = {1, 1, 1, 1};

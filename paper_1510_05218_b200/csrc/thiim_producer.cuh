@@ -150,57 +150,57 @@ __device__ __forceinline__ void produce_plane_ct(RingProducer<BY, NG>& P, int fb
 #undef BOXC
 }
 
-// Level-2 coefficient groups of plane r (seq_level2_coef), policy `pol`.
+// Level-2 coefficient groups of plane r, policy `pol`: seq_level2_coef's
+// grouping, boxed to the level-2 regions (BOX_H2 / BOX_E2).
 template <int BY, int NG>
 __device__ __forceinline__ void produce_level2_coef_ct(RingProducer<BY, NG>& P, int cb, int r,
                                                        uint64_t pol) {
   using Gm = BoxGeom<BY>;
-  constexpr int SB = Gm::bytes(BOX_B), SBX = Gm::bytes(BOX_BX), SBY = Gm::bytes(BOX_BY),
-                SC = Gm::bytes(BOX_C);
+  constexpr int SH = Gm::bytes(BOX_H2), SE = Gm::bytes(BOX_E2);
   const int p0 = r + 1;
-  P.template begin<2 * SBY + 2 * SBX>();  // Hxy t c, Hyx t c
-  P.template box<BOX_BY>(0, cb + HXY, p0, pol);
-  P.template box<BOX_BY>(1, cb + 12 + HXY, p0, pol);
-  P.template box<BOX_BX>(2, cb + HYX, p0, pol);
-  P.template box<BOX_BX>(3, cb + 12 + HYX, p0, pol);
+  P.template begin<4 * SH>();  // Hxy t c, Hyx t c
+  P.template box<BOX_H2>(0, cb + HXY, p0, pol);
+  P.template box<BOX_H2>(1, cb + 12 + HXY, p0, pol);
+  P.template box<BOX_H2>(2, cb + HYX, p0, pol);
+  P.template box<BOX_H2>(3, cb + 12 + HYX, p0, pol);
   P.end();
-  P.template begin<3 * SBY>();  // Hxz t c src
-  P.template box<BOX_BY>(0, cb + HXZ, p0, pol);
-  P.template box<BOX_BY>(1, cb + 12 + HXZ, p0, pol);
-  P.template box<BOX_BY>(2, cb + 24 + SRC_HXZ, p0, pol);
+  P.template begin<3 * SH>();  // Hxz t c src
+  P.template box<BOX_H2>(0, cb + HXZ, p0, pol);
+  P.template box<BOX_H2>(1, cb + 12 + HXZ, p0, pol);
+  P.template box<BOX_H2>(2, cb + 24 + SRC_HXZ, p0, pol);
   P.end();
-  P.template begin<3 * SBX>();  // Hyz t c src
-  P.template box<BOX_BX>(0, cb + HYZ, p0, pol);
-  P.template box<BOX_BX>(1, cb + 12 + HYZ, p0, pol);
-  P.template box<BOX_BX>(2, cb + 24 + SRC_HYZ, p0, pol);
+  P.template begin<3 * SH>();  // Hyz t c src
+  P.template box<BOX_H2>(0, cb + HYZ, p0, pol);
+  P.template box<BOX_H2>(1, cb + 12 + HYZ, p0, pol);
+  P.template box<BOX_H2>(2, cb + 24 + SRC_HYZ, p0, pol);
   P.end();
-  P.template begin<4 * SB>();  // Hzx t c, Hzy t c
-  P.template box<BOX_B>(0, cb + HZX, p0, pol);
-  P.template box<BOX_B>(1, cb + 12 + HZX, p0, pol);
-  P.template box<BOX_B>(2, cb + HZY, p0, pol);
-  P.template box<BOX_B>(3, cb + 12 + HZY, p0, pol);
+  P.template begin<4 * SH>();  // Hzx t c, Hzy t c
+  P.template box<BOX_H2>(0, cb + HZX, p0, pol);
+  P.template box<BOX_H2>(1, cb + 12 + HZX, p0, pol);
+  P.template box<BOX_H2>(2, cb + HZY, p0, pol);
+  P.template box<BOX_H2>(3, cb + 12 + HZY, p0, pol);
   P.end();
-  P.template begin<4 * SC>();  // Exy t c, Eyx t c
-  P.template box<BOX_C>(0, cb + EXY, p0, pol);
-  P.template box<BOX_C>(1, cb + 12 + EXY, p0, pol);
-  P.template box<BOX_C>(2, cb + EYX, p0, pol);
-  P.template box<BOX_C>(3, cb + 12 + EYX, p0, pol);
+  P.template begin<4 * SE>();  // Exy t c, Eyx t c
+  P.template box<BOX_E2>(0, cb + EXY, p0, pol);
+  P.template box<BOX_E2>(1, cb + 12 + EXY, p0, pol);
+  P.template box<BOX_E2>(2, cb + EYX, p0, pol);
+  P.template box<BOX_E2>(3, cb + 12 + EYX, p0, pol);
   P.end();
-  P.template begin<3 * SC>();  // Exz t c src
-  P.template box<BOX_C>(0, cb + EXZ, p0, pol);
-  P.template box<BOX_C>(1, cb + 12 + EXZ, p0, pol);
-  P.template box<BOX_C>(2, cb + 24 + SRC_EXZ, p0, pol);
+  P.template begin<3 * SE>();  // Exz t c src
+  P.template box<BOX_E2>(0, cb + EXZ, p0, pol);
+  P.template box<BOX_E2>(1, cb + 12 + EXZ, p0, pol);
+  P.template box<BOX_E2>(2, cb + 24 + SRC_EXZ, p0, pol);
   P.end();
-  P.template begin<3 * SC>();  // Eyz t c src
-  P.template box<BOX_C>(0, cb + EYZ, p0, pol);
-  P.template box<BOX_C>(1, cb + 12 + EYZ, p0, pol);
-  P.template box<BOX_C>(2, cb + 24 + SRC_EYZ, p0, pol);
+  P.template begin<3 * SE>();  // Eyz t c src
+  P.template box<BOX_E2>(0, cb + EYZ, p0, pol);
+  P.template box<BOX_E2>(1, cb + 12 + EYZ, p0, pol);
+  P.template box<BOX_E2>(2, cb + 24 + SRC_EYZ, p0, pol);
   P.end();
-  P.template begin<4 * SC>();  // Ezx t c, Ezy t c
-  P.template box<BOX_C>(0, cb + EZX, p0, pol);
-  P.template box<BOX_C>(1, cb + 12 + EZX, p0, pol);
-  P.template box<BOX_C>(2, cb + EZY, p0, pol);
-  P.template box<BOX_C>(3, cb + 12 + EZY, p0, pol);
+  P.template begin<4 * SE>();  // Ezx t c, Ezy t c
+  P.template box<BOX_E2>(0, cb + EZX, p0, pol);
+  P.template box<BOX_E2>(1, cb + 12 + EZX, p0, pol);
+  P.template box<BOX_E2>(2, cb + EZY, p0, pol);
+  P.template box<BOX_E2>(3, cb + 12 + EZY, p0, pol);
   P.end();
 }
 

@@ -40,17 +40,33 @@ namespace thiim_gpu {
 //   BOX_BX 31 x (BY-2) own + ring_x (x0-1 column)   (Hyx, Hyz operands)
 //   BOX_BY 30 x (BY-1) own + ring_y (y0-1 row)      (Hxy, Hxz operands)
 //   BOX_C  30 x (BY-2) own only                     (E-phase coefficients)
+// and for the second level of the temporally blocked sweep, whose output tile
+// is one ring smaller (28 x (BY-4) at thread (2,2)):
+//   BOX_H2 29 x (BY-3) level-2 own + its -x/-y ring  (level-2 H coefficients)
+//   BOX_E2 28 x (BY-4) level-2 own                   (level-2 E coefficients)
 // Fetching only what each group needs keeps the tile overlap (re-read by the
 // neighbouring CTA) at ~7% instead of ~22%.
-enum : int { BOX_A = 0, BOX_B = 1, BOX_BX = 2, BOX_BY = 3, BOX_C = 4, NBOX = 5 };
+enum : int {
+  BOX_A = 0, BOX_B = 1, BOX_BX = 2, BOX_BY = 3, BOX_C = 4, BOX_H2 = 5, BOX_E2 = 6, NBOX = 7
+};
 
 template <int BY>
 struct BoxGeom {
-  __host__ __device__ static constexpr int x0(int b) { return b >= BOX_BY ? 1 : 0; }
-  __host__ __device__ static constexpr int y0(int b) { return (b == BOX_BX || b == BOX_C) ? 1 : 0; }
-  __host__ __device__ static constexpr int w(int b) { return b == BOX_A ? 32 : b <= BOX_BX ? 31 : 30; }
+  __host__ __device__ static constexpr int x0(int b) {
+    return b == BOX_E2 ? 2 : (b == BOX_BY || b == BOX_C || b == BOX_H2) ? 1 : 0;
+  }
+  __host__ __device__ static constexpr int y0(int b) {
+    return b == BOX_E2 ? 2 : (b == BOX_BX || b == BOX_C || b == BOX_H2) ? 1 : 0;
+  }
+  __host__ __device__ static constexpr int w(int b) {
+    return b == BOX_A ? 32 : b <= BOX_BX ? 31 : b <= BOX_C ? 30 : b == BOX_H2 ? 29 : 28;
+  }
   __host__ __device__ static constexpr int h(int b) {
-    return b == BOX_A ? BY : (b == BOX_B || b == BOX_BY) ? BY - 1 : BY - 2;
+    return b == BOX_A                      ? BY
+           : (b == BOX_B || b == BOX_BY)   ? BY - 1
+           : (b == BOX_BX || b == BOX_C)   ? BY - 2
+           : b == BOX_H2                   ? BY - 3
+                                           : BY - 4;
   }
   __host__ __device__ static constexpr int bytes(int b) { return w(b) * h(b) * 16; }
 };

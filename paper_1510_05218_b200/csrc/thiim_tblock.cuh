@@ -850,26 +850,26 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
       const bool u2x = upd2_x && plane_ok, u2y = upd2_y && plane_ok, u2z = upd2_z && plane_ok;
       {  // Hxy, Hyx
         ring_wait(R, rc);
-        const double2 t0 = RD(0, BOX_BY), c0 = RD(1, BOX_BY), t1 = RD(2, BOX_BX), c1 = RD(3, BOX_BX);
+        const double2 t0 = RD(0, BOX_H2), c0 = RD(1, BOX_H2), t1 = RD(2, BOX_H2), c1 = RD(3, BOX_H2);
         ring_release(R, rc, tx, ring_dep(c1, t1, c0, t0));
         if (u2x) h[0] = upd(h[0], t0, c0, sm.sE[2][ty + 1][tx], sEz);
         if (u2y) h[2] = upd(h[2], t1, c1, sm.sE[2][ty][tx + 1], sEz);
       }
       {  // Hxz
         ring_wait(R, rc);
-        const double2 t = RD(0, BOX_BY), c = RD(1, BOX_BY), s = RD(2, BOX_BY);
+        const double2 t = RD(0, BOX_H2), c = RD(1, BOX_H2), s = RD(2, BOX_H2);
         ring_release(R, rc, tx, ring_dep(s, c, t));
         if (u2x) h[1] = upd_src(h[1], t, c, nEy, sEy, s);
       }
       {  // Hyz
         ring_wait(R, rc);
-        const double2 t = RD(0, BOX_BX), c = RD(1, BOX_BX), s = RD(2, BOX_BX);
+        const double2 t = RD(0, BOX_H2), c = RD(1, BOX_H2), s = RD(2, BOX_H2);
         ring_release(R, rc, tx, ring_dep(s, c, t));
         if (u2y) h[3] = upd_src(h[3], t, c, nEx, sEx, s);
       }
       {  // Hzx, Hzy
         ring_wait(R, rc);
-        const double2 t0 = RD(0, BOX_B), c0 = RD(1, BOX_B), t1 = RD(2, BOX_B), c1 = RD(3, BOX_B);
+        const double2 t0 = RD(0, BOX_H2), c0 = RD(1, BOX_H2), t1 = RD(2, BOX_H2), c1 = RD(3, BOX_H2);
         ring_release(R, rc, tx, ring_dep(c1, t1, c0, t0));
         if (u2z) h[4] = upd(h[4], t0, c0, sm.sE[1][ty][tx + 1], sEy);
         if (u2z) h[5] = upd(h[5], t1, c1, sm.sE[0][ty + 1][tx], sEx);
@@ -901,7 +901,7 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
       const bool ue = own2 && interior;
       {  // Exy, Eyx
         ring_wait(R, rc);
-        const double2 t0 = RD(0, BOX_C), c0 = RD(1, BOX_C), t1 = RD(2, BOX_C), c1 = RD(3, BOX_C);
+        const double2 t0 = RD(0, BOX_E2), c0 = RD(1, BOX_E2), t1 = RD(2, BOX_E2), c1 = RD(3, BOX_E2);
         ring_release(R, rc, tx, ring_dep(c1, t1, c0, t0));
         if (ue) {
           st_hint(A.fo[EXY] + i, upd(e1[EXY], t0, c0, sm.sH[2][ty - 1][tx], sHz), first);
@@ -910,19 +910,19 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
       }
       {  // Exz
         ring_wait(R, rc);
-        const double2 t = RD(0, BOX_C), c = RD(1, BOX_C), s = RD(2, BOX_C);
+        const double2 t = RD(0, BOX_E2), c = RD(1, BOX_E2), s = RD(2, BOX_E2);
         ring_release(R, rc, tx, ring_dep(s, c, t));
         if (ue) st_hint(A.fo[EXZ] + i, upd_src(e1[EXZ], t, c, pH2y, sHy, s), first);
       }
       {  // Eyz
         ring_wait(R, rc);
-        const double2 t = RD(0, BOX_C), c = RD(1, BOX_C), s = RD(2, BOX_C);
+        const double2 t = RD(0, BOX_E2), c = RD(1, BOX_E2), s = RD(2, BOX_E2);
         ring_release(R, rc, tx, ring_dep(s, c, t));
         if (ue) st_hint(A.fo[EYZ] + i, upd_src(e1[EYZ], t, c, pH2x, sHx, s), first);
       }
       {  // Ezx, Ezy
         ring_wait(R, rc);
-        const double2 t0 = RD(0, BOX_C), c0 = RD(1, BOX_C), t1 = RD(2, BOX_C), c1 = RD(3, BOX_C);
+        const double2 t0 = RD(0, BOX_E2), c0 = RD(1, BOX_E2), t1 = RD(2, BOX_E2), c1 = RD(3, BOX_E2);
         ring_release(R, rc, tx, ring_dep(c1, t1, c0, t0));
         if (ue) {
           st_hint(A.fo[EZX] + i, upd(e1[EZX], t0, c0, sm.sH[1][ty][tx - 1], sHy), first);
