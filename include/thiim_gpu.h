@@ -237,6 +237,18 @@ int thiim_gpu_upload_table(thiim_gpu_ctx* ctx, const thiim_c128* const fields[12
 /* Reads back the material ids and the table of a THIIM_COEFF_TABLE context. */
 int thiim_gpu_download_table(thiim_gpu_ctx* ctx, uint8_t* material_id, thiim_c128* table);
 
+/* Sanitizer (the reference's exactly-once coverage check, tools/main.cpp:20-41,
+ * for the GPU schedules): while on, the default kernels count every output
+ * store per (component, cell) and after every pass (one launch of the fused /
+ * TBLOCK engines, an H+E launch pair of the split engine) a check kernel
+ * demands exactly one store per interior cell of every slab -- extended
+ * planes of deep slabs included -- and none on ghosts.  Costs ~48 B/cell of
+ * device memory and atomics on every store: a debug mode. */
+int thiim_gpu_set_sanitize(thiim_gpu_ctx* ctx, int on);
+/* Passes checked and (component, cell) violations since thiim_gpu_set_sanitize. */
+int thiim_gpu_coverage(thiim_gpu_ctx* ctx, unsigned long long* passes,
+                       unsigned long long* violations);
+
 /* Blocks until all work queued on the context's streams has finished. */
 int thiim_gpu_sync(thiim_gpu_ctx* ctx);
 

@@ -29,7 +29,7 @@ import ctypes
 import enum
 import os
 from dataclasses import dataclass, field
-from typing import List, Optional
+from typing import Tuple, List, Optional
 
 import numpy as np
 
@@ -291,7 +291,8 @@ EXPORTED_SYMBOLS = [
     "thiim_generate_host", "thiim_gpu_pin_host", "thiim_gpu_unpin_host",
     "thiim_gpu_create_slab", "thiim_gpu_halo_view", "thiim_gpu_slab_info", "thiim_gpu_sync",
     "thiim_gpu_upload_planes", "thiim_gpu_download_fields_planes", "thiim_generate_host_planes",
-    "thiim_gpu_upload_table", "thiim_gpu_download_table",
+    "thiim_gpu_upload_table", "thiim_gpu_download_table", "thiim_gpu_set_sanitize",
+    "thiim_gpu_coverage",
 ]
 
 _LIB = None
@@ -327,6 +328,9 @@ def lib() -> ctypes.CDLL:
     L.thiim_gpu_download_table.argtypes = [P, P, P]
     L.thiim_gpu_pin_host.argtypes = [P, ctypes.c_size_t]
     L.thiim_gpu_unpin_host.argtypes = [P]
+    L.thiim_gpu_set_sanitize.argtypes = [P, ctypes.c_int]
+    L.thiim_gpu_coverage.argtypes = [P, ctypes.POINTER(ctypes.c_ulonglong),
+                                     ctypes.POINTER(ctypes.c_ulonglong)]
     if L.thiim_gpu_abi_version() != 1:
         raise GpuError("libthiim_gpu.so ABI mismatch")
     _LIB = L
@@ -469,6 +473,16 @@ class GpuEngine:
 
     def download_fields(self, s: ProblemState) -> None:
         _check(lib().thiim_gpu_download_fields(self._ctx, _ptrs(s.arrays[0:12])))
+
+    def set_sanitize(self, on: bool = True) -> None:
+        """Exactly-once store coverage check after every pass (debug mode)."""
+        _check(lib().thiim_gpu_set_sanitize(self._ctx, int(bool(on))))
+
+    def coverage(self) -> Tuple[int, int]:
+        """(passes checked, (component, cell) violations) since set_sanitize."""
+        p, v = ctypes.c_ulonglong(), ctypes.c_ulonglong()
+        _check(lib().thiim_gpu_coverage(self._ctx, ctypes.byref(p), ctypes.byref(v)))
+        return p.value, v.value
 
     def upload_table(self, fields: List[np.ndarray], material_id: np.ndarray,
                      table: np.ndarray) -> None:

@@ -93,7 +93,17 @@ struct Arrays {
   const double2* t[12];
   const double2* c[12];
   const double2* src[4];
+  unsigned* cnt = nullptr;  // sanitizer: per (component, padded cell) store counts
+  long long cstride = 0;
 };
+
+// Sanitizer hook at every output store of the default kernels (their COUNT
+// instances only): counts how often (component, cell) is written in a pass;
+// k_coverage then demands exactly once per interior cell, never on a ghost.
+template <bool COUNT>
+__device__ __forceinline__ void mark(const Arrays& A, int comp, long long i) {
+  if constexpr (COUNT) atomicAdd(A.cnt + (long long)comp * A.cstride + i, 1u);
+}
 
 // ---- synthetic problem generator
 THIIM_HD uint64_t splitmix64(uint64_t x) {

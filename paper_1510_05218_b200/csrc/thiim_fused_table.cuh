@@ -73,7 +73,7 @@ struct TableSmem {
   double2 tab[kMaxMaterials][28];  // t x12, c x12, src x4 per material
 };
 
-template <int BY, int NG>
+template <int BY, int NG, bool COUNT = false>
 __global__ void __launch_bounds__(32 * (BY + 1), 1)
     k_fused_table(Grid g, Arrays A, TableGrid T, const __grid_constant__ TableMaps maps,
                   const __grid_constant__ GroupSeq S, int zc, int tiles_x) {
@@ -233,7 +233,10 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
     }
     if (own) {
 #pragma unroll
-      for (int k = 0; k < 6; ++k) A.fo[HXY + k][i] = h[k];
+      for (int k = 0; k < 6; ++k) {
+        A.fo[HXY + k][i] = h[k];
+        mark<COUNT>(A, HXY + k, i);
+      }
     }
     const double2 sHx = csum(h[0], h[1]), sHy = csum(h[2], h[3]), sHz = csum(h[4], h[5]);
     if (own || ring_x || ring_y) {
@@ -250,6 +253,8 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
       A.fo[EYZ][i] = upd_src(e[EYZ], C[EYZ], C[12 + EYZ], pHx, sHx, C[24 + SRC_EYZ]);
       A.fo[EZX][i] = upd(e[EZX], C[EZX], C[12 + EZX], sm.sH[1][ty][tx - 1], sHy);
       A.fo[EZY][i] = upd(e[EZY], C[EZY], C[12 + EZY], sm.sH[0][ty - 1][tx], sHx);
+#pragma unroll
+      for (int k = EXY; k <= EZY; ++k) mark<COUNT>(A, k, i);
     }
     pHx = sHx;
     pHy = sHy;

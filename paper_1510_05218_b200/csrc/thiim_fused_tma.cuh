@@ -112,7 +112,7 @@ __device__ __forceinline__ void produce_plane(Ring<BY, NG>& r, int& g, uint32_t&
   }
 }
 
-template <int BY, int NG>
+template <int BY, int NG, bool COUNT = false>
 __global__ void __launch_bounds__(32 * (BY + 1), 1)
     k_fused_tma(Grid g, Arrays A, const __grid_constant__ TmaMaps maps,
                 const __grid_constant__ GroupSeq S, int zc, int tiles_y, int tiles_x,
@@ -277,7 +277,10 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
     }
     if (own) {
 #pragma unroll
-      for (int k = 0; k < 6; ++k) A.fo[HXY + k][i] = h[k];
+      for (int k = 0; k < 6; ++k) {
+        A.fo[HXY + k][i] = h[k];
+        mark<COUNT>(A, HXY + k, i);
+      }
     }
     const double2 sHx = csum(h[0], h[1]), sHy = csum(h[2], h[3]), sHz = csum(h[4], h[5]);
     if (own || ring_x || ring_y) {
@@ -295,19 +298,27 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
       if (own) {
         A.fo[EXY][i] = upd(e[EXY], t0, c0, sm.sH[2][ty - 1][tx], sHz);
         A.fo[EYX][i] = upd(e[EYX], t1, c1, sm.sH[2][ty][tx - 1], sHz);
+        mark<COUNT>(A, EXY, i);
+        mark<COUNT>(A, EYX, i);
       }
     }
     {  // Exz
       ring_wait(R, rc);
       const double2 t = RD(0, BOX_C), c = RD(1, BOX_C), s = RD(2, BOX_C);
       ring_release(R, rc, tx, ring_dep(s, c, t));
-      if (own) A.fo[EXZ][i] = upd_src(e[EXZ], t, c, pHy, sHy, s);
+      if (own) {
+        A.fo[EXZ][i] = upd_src(e[EXZ], t, c, pHy, sHy, s);
+        mark<COUNT>(A, EXZ, i);
+      }
     }
     {  // Eyz
       ring_wait(R, rc);
       const double2 t = RD(0, BOX_C), c = RD(1, BOX_C), s = RD(2, BOX_C);
       ring_release(R, rc, tx, ring_dep(s, c, t));
-      if (own) A.fo[EYZ][i] = upd_src(e[EYZ], t, c, pHx, sHx, s);
+      if (own) {
+        A.fo[EYZ][i] = upd_src(e[EYZ], t, c, pHx, sHx, s);
+        mark<COUNT>(A, EYZ, i);
+      }
     }
     {  // Ezx, Ezy
       ring_wait(R, rc);
@@ -316,6 +327,8 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
       if (own) {
         A.fo[EZX][i] = upd(e[EZX], t0, c0, sm.sH[1][ty][tx - 1], sHy);
         A.fo[EZY][i] = upd(e[EZY], t1, c1, sm.sH[0][ty - 1][tx], sHx);
+        mark<COUNT>(A, EZX, i);
+        mark<COUNT>(A, EZY, i);
       }
     }
     pHx = sHx;

@@ -57,6 +57,8 @@ struct Slab {
   // plane per internal interface (ext_lo / ext_hi) that the exchange refreshes
   int own0 = 0, own1 = 0, ext_lo = 0, ext_hi = 0;
   bool deep = false;
+  unsigned* cnt = nullptr;                 // sanitizer store counts [12][stride] (or null)
+  unsigned long long* cov_bad = nullptr;   // sanitizer violations (device)
   double2* buf = nullptr;
   size_t stride = 0;   // elements per array
   int nfield_sets = 1;
@@ -94,6 +96,8 @@ struct Slab {
       A.c[k] = coeff(24 + k);
     }
     for (int k = 0; k < 4; ++k) A.src[k] = coeff(36 + k);
+    A.cnt = cnt;
+    A.cstride = (long long)stride;
     return A;
   }
 };
@@ -106,6 +110,8 @@ struct thiim_gpu_ctx {
   int engine = THIIM_ENGINE_FUSED;
   std::vector<Slab> slabs;
   bool loaded = false;
+  bool sanitize = false;               // exactly-once store coverage per pass
+  unsigned long long cov_passes = 0;
   long long pxy() const { return (long long)(dims.nx + 2) * (dims.ny + 2); }
 };
 
@@ -145,6 +151,31 @@ __global__ void k_generate(Grid g, int z_global0, int nz_global, Arrays A, int k
       dst[p] = v;
     }
   }
+}
+
+// Sanitizer check of one pass (the reference's exactly-once
+// UpdateLog coverage, tools/main.cpp:20-41): every (component, interior cell) of
+// the slab's local grid was stored exactly once, no ghost ever; the counts are
+// reset for the next pass.
+__global__ void k_coverage(Grid g, unsigned* cnt, long long cstride, unsigned long long* bad) {
+  const long long n = (long long)(g.nz + 2) * g.pxy;
+  unsigned long long b = 0;
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
+       p += (long long)gridDim.x * blockDim.x) {
+    const int zp = (int)(p / g.pxy);
+    const long long r = p - (long long)zp * g.pxy;
+    const int yp = (int)(r / g.px);
+    const int xp = (int)(r - (long long)yp * g.px);
+    const bool interior = xp >= 1 && xp <= g.nx && yp >= 1 && yp <= g.ny && zp >= 1 && zp <= g.nz;
+    const unsigned want = interior ? 1u : 0u;
+    for (int k = 0; k < 12; ++k) {
+      unsigned* c = cnt + (long long)k * cstride + p;
+      b += *c != want;
+      *c = 0u;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) b += __shfl_xor_sync(0xffffffffu, b, o);
+  if ((threadIdx.x & 31) == 0 && b) atomicAdd(bad, b);
 }
 
 // Interior comparison of one field array against a reference copy.
@@ -308,9 +339,11 @@ int launch_split(thiim_gpu_ctx* ctx, Slab& s, int fam, long long* launches) {
   const dim3 grid((s.g.nx + kSplitBX - 1) / kSplitBX, (s.g.ny + kSplitBY - 1) / kSplitBY,
                   (s.g.nz + zc - 1) / zc);
   if (fam == 0)
-    k_split_h<kSplitBY><<<grid, block, 0, s.stream>>>(s.g, A, zc);
+    (s.cnt ? k_split_h<kSplitBY, true> : k_split_h<kSplitBY, false>)<<<grid, block, 0, s.stream>>>(
+        s.g, A, zc);
   else
-    k_split_e<kSplitBY><<<grid, block, 0, s.stream>>>(s.g, A, zc);
+    (s.cnt ? k_split_e<kSplitBY, true> : k_split_e<kSplitBY, false>)<<<grid, block, 0, s.stream>>>(
+        s.g, A, zc);
   CK(cudaGetLastError());
   ++*launches;
   return THIIM_OK;
@@ -412,6 +445,8 @@ int launch_fused_tma_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
   if (!(attr_set >> s.device & 1u)) {
     CK(cudaFuncSetAttribute(k_fused_tma<BY, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)smem));
+    CK(cudaFuncSetAttribute(k_fused_tma<BY, NG, true>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr_set |= 1u << s.device;
   }
   const long long cols = (long long)((s.g.nx + TX - 1) / TX) * ((s.g.ny + TY - 1) / TY);
@@ -420,7 +455,8 @@ int launch_fused_tma_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
   const int tiles_x = (s.g.nx + TX - 1) / TX;
   const dim3 grid(tiles_x * tiles_y, 1, (s.g.nz + zc - 1) / zc);
   const dim3 block(32, BY + 1);
-  k_fused_tma<BY, NG><<<grid, block, smem, s.stream>>>(s.g, A, s.maps[map_index(BY)], S, zc,
+  (s.cnt ? k_fused_tma<BY, NG, true> : k_fused_tma<BY, NG, false>)<<<grid, block, smem, s.stream>>>(
+      s.g, A, s.maps[map_index(BY)], S, zc,
                                                        tiles_y, tiles_x, ctx->opts.reserved[3] == 0,
                                                        cur * 12, nf * 12, ctx->opts.reserved[4] == 0);
   CK(cudaGetLastError());
@@ -514,6 +550,8 @@ int launch_tblock2_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
                               (int)sizeof(TbSmem<BY, NG>)));
     CK(cudaFuncSetAttribute(k_tblock_tm<BY, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)sizeof(TmSmem<BY, NG>)));
+    CK(cudaFuncSetAttribute(k_tblock_tm<BY, NG, true>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(TmSmem<BY, NG>)));
     attr_set |= 1u << s.device;
   }
   constexpr int TX2 = 28, TY2 = BY - 4;
@@ -536,7 +574,8 @@ int launch_tblock2_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
       return fail(THIIM_ERR_CONFIG, "the scratch TBLOCK variant has tile height 15 only");
     }
   } else {
-    k_tblock_tm<BY, NG><<<grid, block, smem, s.stream>>>(s.g, A, s.maps[map_index(BY)], cur * 12,
+    (s.cnt ? k_tblock_tm<BY, NG, true> : k_tblock_tm<BY, NG, false>)<<<grid, block, smem, s.stream>>>(
+        s.g, A, s.maps[map_index(BY)], cur * 12,
                                                          nf * 12, zc, tiles_x,
                                                          ctx->opts.reserved[5]);
   }
@@ -564,6 +603,8 @@ int launch_tblock_table_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
   if (!(attr_set >> s.device & 1u)) {
     CK(cudaFuncSetAttribute(k_tblock_table<BY, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)smem));
+    CK(cudaFuncSetAttribute(k_tblock_table<BY, NG, true>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr_set |= 1u << s.device;
   }
   constexpr int TX2 = 28, TY2 = BY - 4;
@@ -571,7 +612,9 @@ int launch_tblock_table_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
   int zc = ctx->opts.z_chunk;
   if (zc <= 0) zc = tblock_zchunk(s, (long long)tiles_x * tiles_y);
   const dim3 grid(tiles_x * tiles_y, 1, (s.g.nz + zc - 1) / zc);
-  k_tblock_table<BY, NG><<<grid, dim3(32, BY + 1), smem, s.stream>>>(s.g, A, T, s.maps[map_index(BY)],
+  (s.cnt ? k_tblock_table<BY, NG, true> : k_tblock_table<BY, NG, false>)<<<grid, dim3(32, BY + 1), smem,
+                                                                          s.stream>>>(
+      s.g, A, T, s.maps[map_index(BY)],
                                                                      s.cur * 12, zc, tiles_x);
   CK(cudaGetLastError());
   s.cur ^= 1;
@@ -613,12 +656,16 @@ int launch_fused_table_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
   if (!(attr_set >> s.device & 1u)) {
     CK(cudaFuncSetAttribute(k_fused_table<BY, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)smem));
+    CK(cudaFuncSetAttribute(k_fused_table<BY, NG, true>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr_set |= 1u << s.device;
   }
   const int tiles_x = (s.g.nx + TX - 1) / TX, tiles_y = (s.g.ny + TY - 1) / TY;
   const int zc = balanced_zchunk(s, (long long)tiles_x * tiles_y, 1, ctx->opts.z_chunk);
   const dim3 grid(tiles_x * tiles_y, 1, (s.g.nz + zc - 1) / zc);
-  k_fused_table<BY, NG><<<grid, dim3(32, BY + 1), smem, s.stream>>>(s.g, A, T, maps, S, zc, tiles_x);
+  (s.cnt ? k_fused_table<BY, NG, true> : k_fused_table<BY, NG, false>)<<<grid, dim3(32, BY + 1), smem,
+                                                                        s.stream>>>(s.g, A, T, maps,
+                                                                                    S, zc, tiles_x);
   CK(cudaGetLastError());
   s.cur ^= 1;
   ++*launches;
@@ -948,6 +995,8 @@ void thiim_gpu_destroy(thiim_gpu_ctx* ctx) {
       cudaStreamSynchronize(sl.stream);
     }
     if (sl.scratch) cudaFree(sl.scratch);
+    if (sl.cnt) cudaFree(sl.cnt);
+    if (sl.cov_bad) cudaFree(sl.cov_bad);
     if (sl.mat) cudaFree(sl.mat);
     if (sl.tab) cudaFree(sl.tab);
     if (sl.ev0) cudaEventDestroy(sl.ev0);
@@ -1064,6 +1113,62 @@ int thiim_gpu_init_generated(thiim_gpu_ctx* ctx, int kind, uint64_t seed) {
   return THIIM_OK;
 }
 
+static int coverage_pass(thiim_gpu_ctx* ctx) {
+  for (auto& sl : ctx->slabs) {
+    CK(cudaSetDevice(sl.device));
+    k_coverage<<<4 * sm_count(sl.device), 256, 0, sl.stream>>>(sl.g, sl.cnt, (long long)sl.stride,
+                                                               sl.cov_bad);
+    CK(cudaGetLastError());
+  }
+  ++ctx->cov_passes;
+  return THIIM_OK;
+}
+
+int thiim_gpu_set_sanitize(thiim_gpu_ctx* ctx, int on) {
+  g_err.clear();
+  if (!ctx) return fail(THIIM_ERR_CONFIG, "null context");
+  for (auto& sl : ctx->slabs) {
+    CK(cudaSetDevice(sl.device));
+    CK(cudaStreamSynchronize(sl.stream));
+    if (sl.cnt) CK(cudaFree(sl.cnt));
+    if (sl.cov_bad) CK(cudaFree(sl.cov_bad));
+    sl.cnt = nullptr;
+    sl.cov_bad = nullptr;
+    if (on) {
+      const size_t bytes = (size_t)12 * sl.stride * sizeof(unsigned);
+      if (cudaMalloc(&sl.cnt, bytes) != cudaSuccess ||
+          cudaMalloc(&sl.cov_bad, sizeof(unsigned long long)) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(THIIM_ERR_SETUP, "sanitizer counters: device allocation failed");
+      }
+      CK(cudaMemsetAsync(sl.cnt, 0, bytes, sl.stream));
+      CK(cudaMemsetAsync(sl.cov_bad, 0, sizeof(unsigned long long), sl.stream));
+      CK(cudaStreamSynchronize(sl.stream));
+    }
+  }
+  ctx->sanitize = on != 0;
+  ctx->cov_passes = 0;
+  return THIIM_OK;
+}
+
+int thiim_gpu_coverage(thiim_gpu_ctx* ctx, unsigned long long* passes,
+                       unsigned long long* violations) {
+  g_err.clear();
+  if (!ctx || !passes || !violations) return fail(THIIM_ERR_CONFIG, "null argument");
+  if (!ctx->sanitize) return fail(THIIM_ERR_STATE, "sanitizer not enabled");
+  unsigned long long v = 0;
+  for (auto& sl : ctx->slabs) {
+    CK(cudaSetDevice(sl.device));
+    unsigned long long b = 0;
+    CK(cudaMemcpyAsync(&b, sl.cov_bad, sizeof(b), cudaMemcpyDeviceToHost, sl.stream));
+    CK(cudaStreamSynchronize(sl.stream));
+    v += b;
+  }
+  *passes = ctx->cov_passes;
+  *violations = v;
+  return THIIM_OK;
+}
+
 int thiim_gpu_step(thiim_gpu_ctx* ctx, int steps, thiim_gpu_stats* stats) {
   g_err.clear();
   if (!ctx) return fail(THIIM_ERR_CONFIG, "null context");
@@ -1084,11 +1189,13 @@ int thiim_gpu_step(thiim_gpu_ctx* ctx, int steps, thiim_gpu_stats* stats) {
     for (; n + 2 <= steps; n += 2) {
       for (auto& sl : ctx->slabs)
         if ((r = launch_tblock2(ctx, sl, &launches))) return r;
+      if (ctx->sanitize && (r = coverage_pass(ctx))) return r;
       if (multi && (r = exchange_deep(ctx))) return r;
     }
     for (; n < steps; ++n) {
       for (auto& sl : ctx->slabs)
         if ((r = launch_fused(ctx, sl, &launches))) return r;
+      if (ctx->sanitize && (r = coverage_pass(ctx))) return r;
       if (multi && (r = exchange_deep(ctx))) return r;
     }
   }
@@ -1105,6 +1212,7 @@ int thiim_gpu_step(thiim_gpu_ctx* ctx, int steps, thiim_gpu_stats* stats) {
       for (auto& sl : ctx->slabs)
         if ((r = launch_fused(ctx, sl, &launches))) return r;
     }
+    if (ctx->sanitize && (r = coverage_pass(ctx))) return r;
   }
   double secs = 0.0;
   for (auto& sl : ctx->slabs) {

@@ -22,7 +22,7 @@ __device__ __forceinline__ double2 ldg2(const double2* p) { return __ldg(p); }
 
 // H half-step on planes [z0, z1) of the chunk (reference kHOrder,
 // components.hpp:80-86; shift +1, E operands).
-template <int BY>
+template <int BY, bool COUNT = false>
 __global__ void __launch_bounds__(kSplitBX* BY)
     k_split_h(Grid g, Arrays A, int zc) {
   const int lane = threadIdx.x;
@@ -70,6 +70,8 @@ __global__ void __launch_bounds__(kSplitBX* BY)
       F = A.f[HYZ] + i; *F = upd_src(*F, ldg2(A.t[HYZ] + i), ldg2(A.c[HYZ] + i), nEx, sEx, ldg2(A.src[SRC_HYZ] + i));
       F = A.f[HZX] + i; *F = upd(*F, ldg2(A.t[HZX] + i), ldg2(A.c[HZX] + i), xEy, sEy);
       F = A.f[HZY] + i; *F = upd(*F, ldg2(A.t[HZY] + i), ldg2(A.c[HZY] + i), yEx, sEx);
+#pragma unroll
+      for (int k = HXY; k <= HZY; ++k) mark<COUNT>(A, k, i);
     }
     sEx = nEx;
     sEy = nEy;
@@ -78,7 +80,7 @@ __global__ void __launch_bounds__(kSplitBX* BY)
 }
 
 // E half-step (reference kEOrder, components.hpp:73-79; shift -1, H operands).
-template <int BY>
+template <int BY, bool COUNT = false>
 __global__ void __launch_bounds__(kSplitBX* BY)
     k_split_e(Grid g, Arrays A, int zc) {
   const int lane = threadIdx.x;
@@ -122,6 +124,8 @@ __global__ void __launch_bounds__(kSplitBX* BY)
       F = A.f[EYZ] + i; *F = upd_src(*F, ldg2(A.t[EYZ] + i), ldg2(A.c[EYZ] + i), pHx, sHx, ldg2(A.src[SRC_EYZ] + i));
       F = A.f[EZX] + i; *F = upd(*F, ldg2(A.t[EZX] + i), ldg2(A.c[EZX] + i), xHy, sHy);
       F = A.f[EZY] + i; *F = upd(*F, ldg2(A.t[EZY] + i), ldg2(A.c[EZY] + i), yHx, sHx);
+#pragma unroll
+      for (int k = EXY; k <= EZY; ++k) mark<COUNT>(A, k, i);
     }
     pHx = sHx;
     pHy = sHy;

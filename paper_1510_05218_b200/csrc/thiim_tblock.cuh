@@ -570,7 +570,7 @@ struct TmSmem {
   uint32_t tmem_base;
 };
 
-template <int BY, int NG>
+template <int BY, int NG, bool COUNT = false>
 __global__ void __launch_bounds__(32 * (BY + 1), 1)
     k_tblock_tm(Grid g, Arrays A, const __grid_constant__ TmaMaps maps, int fb, int cb, int zc,
                 int tiles_x, int pol_mode) {
@@ -889,7 +889,10 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
       }
       if (own2 && interior) {
 #pragma unroll
-        for (int k = 0; k < 6; ++k) st_hint(A.fo[HXY + k] + i, h[k], first);
+        for (int k = 0; k < 6; ++k) {
+          st_hint(A.fo[HXY + k] + i, h[k], first);
+          mark<COUNT>(A, HXY + k, i);
+        }
       }
       const double2 sHx = csum(h[0], h[1]), sHy = csum(h[2], h[3]), sHz = csum(h[4], h[5]);
       if (own2 || rx2 || ry2) {
@@ -905,20 +908,28 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
         ring_release(R, rc, tx, ring_dep(c1, t1, c0, t0));
         if (ue) {
           st_hint(A.fo[EXY] + i, upd(e1[EXY], t0, c0, sm.sH[2][ty - 1][tx], sHz), first);
+          mark<COUNT>(A, EXY, i);
           st_hint(A.fo[EYX] + i, upd(e1[EYX], t1, c1, sm.sH[2][ty][tx - 1], sHz), first);
+          mark<COUNT>(A, EYX, i);
         }
       }
       {  // Exz
         ring_wait(R, rc);
         const double2 t = RD(0, BOX_E2), c = RD(1, BOX_E2), s = RD(2, BOX_E2);
         ring_release(R, rc, tx, ring_dep(s, c, t));
-        if (ue) st_hint(A.fo[EXZ] + i, upd_src(e1[EXZ], t, c, pH2y, sHy, s), first);
+        if (ue) {
+          st_hint(A.fo[EXZ] + i, upd_src(e1[EXZ], t, c, pH2y, sHy, s), first);
+          mark<COUNT>(A, EXZ, i);
+        }
       }
       {  // Eyz
         ring_wait(R, rc);
         const double2 t = RD(0, BOX_E2), c = RD(1, BOX_E2), s = RD(2, BOX_E2);
         ring_release(R, rc, tx, ring_dep(s, c, t));
-        if (ue) st_hint(A.fo[EYZ] + i, upd_src(e1[EYZ], t, c, pH2x, sHx, s), first);
+        if (ue) {
+          st_hint(A.fo[EYZ] + i, upd_src(e1[EYZ], t, c, pH2x, sHx, s), first);
+          mark<COUNT>(A, EYZ, i);
+        }
       }
       {  // Ezx, Ezy
         ring_wait(R, rc);
@@ -926,7 +937,9 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
         ring_release(R, rc, tx, ring_dep(c1, t1, c0, t0));
         if (ue) {
           st_hint(A.fo[EZX] + i, upd(e1[EZX], t0, c0, sm.sH[1][ty][tx - 1], sHy), first);
+          mark<COUNT>(A, EZX, i);
           st_hint(A.fo[EZY] + i, upd(e1[EZY], t1, c1, sm.sH[0][ty - 1][tx], sHx), first);
+          mark<COUNT>(A, EZY, i);
         }
       }
       pH2x = sHx;

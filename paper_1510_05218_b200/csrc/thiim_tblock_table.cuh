@@ -34,7 +34,7 @@ struct TbTableSmem {
   uint32_t tmem_base;
 };
 
-template <int BY, int NG>
+template <int BY, int NG, bool COUNT = false>
 __global__ void __launch_bounds__(32 * (BY + 1), 1)
     k_tblock_table(Grid g, Arrays A, TableGrid T, const __grid_constant__ TmaMaps maps, int fb,
                    int zc, int tiles_x) {
@@ -296,7 +296,10 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
       }
       if (own2 && interior) {
 #pragma unroll
-        for (int k = 0; k < 6; ++k) st_hint(A.fo[HXY + k] + i, h[k], first);
+        for (int k = 0; k < 6; ++k) {
+          st_hint(A.fo[HXY + k] + i, h[k], first);
+          mark<COUNT>(A, HXY + k, i);
+        }
       }
       const double2 sHx = csum(h[0], h[1]), sHy = csum(h[2], h[3]), sHz = csum(h[4], h[5]);
       if (own2 || rx2 || ry2) {
@@ -314,6 +317,8 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
                 first);
         st_hint(A.fo[EZX] + i, upd(e1[EZX], C[EZX], C[12 + EZX], sm.sH[1][ty][tx - 1], sHy), first);
         st_hint(A.fo[EZY] + i, upd(e1[EZY], C[EZY], C[12 + EZY], sm.sH[0][ty - 1][tx], sHx), first);
+#pragma unroll
+        for (int k = EXY; k <= EZY; ++k) mark<COUNT>(A, k, i);
       }
       pH2x = sHx;
       pH2y = sHy;
