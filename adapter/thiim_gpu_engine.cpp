@@ -44,6 +44,10 @@ struct CtxGuard {
 }  // namespace
 
 RunReport run_gpu(ProblemState& state, int steps, const GpuOptions& opts) {
+  return run_gpu(state, steps, opts, nullptr);
+}
+
+RunReport run_gpu(ProblemState& state, int steps, const GpuOptions& opts, GpuRunExtras* extras) {
   if (steps < 0) throw ConfigError("steps must be >= 0");  // reference_engines.cpp:35
   RunReport report;
   report.dims = state.dims;
@@ -58,9 +62,11 @@ RunReport run_gpu(ProblemState& state, int steps, const GpuOptions& opts) {
   o.engine = opts.engine;
   o.time_block = opts.time_block;
   o.z_chunk = opts.z_chunk;
+  o.tile_y = opts.tile_y;
 
   CtxGuard g;
   check(thiim_gpu_create(&d, &o, &g.ctx), "thiim_gpu_create");
+  if (opts.sanitize) check(thiim_gpu_set_sanitize(g.ctx, 1), "thiim_gpu_set_sanitize");
 
   const std::size_t bytes = state.dims.padded_cells() * sizeof(ComplexScalar);
   const thiim_c128* f[12];
@@ -86,6 +92,12 @@ RunReport run_gpu(ProblemState& state, int steps, const GpuOptions& opts) {
 
   thiim_gpu_stats st{};
   check(thiim_gpu_step(g.ctx, steps, &st), "thiim_gpu_step");
+  if (extras) {
+    extras->kernel_launches = st.kernel_launches;
+    if (opts.sanitize)
+      check(thiim_gpu_coverage(g.ctx, &extras->coverage_passes, &extras->coverage_violations),
+            "thiim_gpu_coverage");
+  }
 
   thiim_c128* out[12];
   for (int i = 0; i < kNumComponents; ++i)

@@ -28,6 +28,8 @@ struct GpuOptions {
   int engine = THIIM_ENGINE_AUTO;  // THIIM_ENGINE_SPLIT / FUSED / TBLOCK
   int time_block = 0;              // TBLOCK: steps per HBM pass (0 = auto)
   int z_chunk = 0;                 // planes per CTA along z (0 = auto)
+  int tile_y = 0;                  // CTA height in rows (0 = the engine default)
+  bool sanitize = false;           // exactly-once store coverage check per pass
   bool pin_host = true;            // page-lock the 40 arrays during the copies
   double hbm_gbs = 0.0;            // if > 0: predicted_mlups = hbm_gbs / balance
 };
@@ -37,5 +39,13 @@ struct GpuOptions {
 // threads = #GPUs, seconds = device time of the step loop (CUDA events),
 // mlups = interior*steps/seconds/1e6, balance_model = algorithmic bytes/LUP.
 RunReport run_gpu(ProblemState& state, int steps, const GpuOptions& opts = {});
+
+// What a run measured beyond RunReport.
+struct GpuRunExtras {
+  unsigned long long coverage_passes = 0;      // sanitize: passes checked
+  unsigned long long coverage_violations = 0;  // sanitize: (component, cell) violations
+  long long kernel_launches = 0;
+};
+RunReport run_gpu(ProblemState& state, int steps, const GpuOptions& opts, GpuRunExtras* extras);
 
 }  // namespace thiim
