@@ -130,6 +130,24 @@ int thiim_gpu_upload_fields(thiim_gpu_ctx* ctx, const thiim_c128* const fields[1
  * identical to thiim_generate_host with the same (kind, seed). */
 int thiim_gpu_init_generated(thiim_gpu_ctx* ctx, int kind, uint64_t seed);
 
+/* The reference's benchmark problem built on the device:
+ * build_benchmark_problem (coefficients.cpp:94-111) -- homogeneous vacuum
+ * medium, Dirichlet ghosts, plane-wave source layer at z = nz/4, fields zero --
+ * for scheme parameters `sp` (SchemeParams, coefficients.hpp:21-34).  The 28
+ * per-component coefficient values are the closed forms of derive_coefficients
+ * (coefficients.cpp:25-55) evaluated once on the host with the reference's
+ * complex arithmetic; the device broadcasts them, so the 40 arrays never cross
+ * PCIe and the result is bitwise the reference's.  Table-layout contexts get
+ * material ids (interior 1, source plane 2) and the 3-row table.  Errors:
+ * CONFIG for invalid parameters (SchemeParams::validate), SETUP for a vanishing
+ * update denominator. */
+typedef struct {
+  double omega, tau, delta;
+  thiim_c128 source_e, source_h;
+} thiim_scheme;
+void thiim_scheme_default(thiim_scheme* sp); /* omega 0.4, tau 1, delta 1, sources 1+0i */
+int thiim_gpu_init_benchmark(thiim_gpu_ctx* ctx, const thiim_scheme* sp);
+
 /* Advances `steps` THIIM iterations (== steps x step_reference).  Blocking.
  * steps < 0 -> THIIM_ERR_CONFIG (run_naive, reference_engines.cpp:35). */
 int thiim_gpu_step(thiim_gpu_ctx* ctx, int steps, thiim_gpu_stats* stats);

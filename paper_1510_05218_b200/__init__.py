@@ -258,6 +258,13 @@ def compare_states(a: ProblemState, b: ProblemState) -> StateDiff:
 
 
 # ---------------------------------------------------------------- C-ABI binding
+class _Scheme(ctypes.Structure):
+    """thiim_scheme (include/thiim_gpu.h) == SchemeParams (coefficients.hpp:21-34)."""
+    _fields_ = [("omega", ctypes.c_double), ("tau", ctypes.c_double), ("delta", ctypes.c_double),
+                ("se_re", ctypes.c_double), ("se_im", ctypes.c_double),
+                ("sh_re", ctypes.c_double), ("sh_im", ctypes.c_double)]
+
+
 class _Dims(ctypes.Structure):
     _fields_ = [("nx", ctypes.c_int), ("ny", ctypes.c_int), ("nz", ctypes.c_int),
                 ("ghost", ctypes.c_int)]
@@ -292,7 +299,7 @@ EXPORTED_SYMBOLS = [
     "thiim_gpu_create_slab", "thiim_gpu_halo_view", "thiim_gpu_slab_info", "thiim_gpu_sync",
     "thiim_gpu_upload_planes", "thiim_gpu_download_fields_planes", "thiim_generate_host_planes",
     "thiim_gpu_upload_table", "thiim_gpu_download_table", "thiim_gpu_set_sanitize",
-    "thiim_gpu_coverage",
+    "thiim_gpu_coverage", "thiim_scheme_default", "thiim_gpu_init_benchmark",
 ]
 
 _LIB = None
@@ -329,6 +336,8 @@ def lib() -> ctypes.CDLL:
     L.thiim_gpu_pin_host.argtypes = [P, ctypes.c_size_t]
     L.thiim_gpu_unpin_host.argtypes = [P]
     L.thiim_gpu_set_sanitize.argtypes = [P, ctypes.c_int]
+    L.thiim_scheme_default.argtypes = [ctypes.POINTER(_Scheme)]
+    L.thiim_gpu_init_benchmark.argtypes = [P, ctypes.POINTER(_Scheme)]
     L.thiim_gpu_coverage.argtypes = [P, ctypes.POINTER(ctypes.c_ulonglong),
                                      ctypes.POINTER(ctypes.c_ulonglong)]
     if L.thiim_gpu_abi_version() != 1:
@@ -465,6 +474,13 @@ class GpuEngine:
 
     def generate(self, kind: int = GEN_RANDOM, seed: int = 1) -> None:
         _check(lib().thiim_gpu_init_generated(self._ctx, kind, seed))
+
+    def init_benchmark(self, omega: float = 0.4, tau: float = 1.0, delta: float = 1.0,
+                       source_e: complex = 1.0 + 0j, source_h: complex = 1.0 + 0j) -> None:
+        """build_benchmark_problem (coefficients.cpp:94-111) on the device."""
+        sp = _Scheme(omega, tau, delta, source_e.real, source_e.imag, source_h.real,
+                     source_h.imag)
+        _check(lib().thiim_gpu_init_benchmark(self._ctx, ctypes.byref(sp)))
 
     def step(self, steps: int) -> _Stats:
         st = _Stats()

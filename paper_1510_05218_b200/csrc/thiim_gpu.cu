@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <complex>
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
@@ -150,6 +151,53 @@ __global__ void k_generate(Grid g, int z_global0, int nz_global, Arrays A, int k
                                                 : const_cast<double2*>(A.src[a - 36]);
       dst[p] = v;
     }
+  }
+}
+
+// Benchmark problem (build_benchmark_problem, coefficients.cpp:94-111): fields
+// and ghosts zero, every interior cell the same 24 t / c values, the 4 source
+// arrays non-zero on the injection plane only.  One thread per padded cell.
+struct BenchValues {
+  double2 v[28];  // t x12, c x12, src x4 (reference array order 12..39)
+};
+__global__ void k_init_benchmark(Grid g, int z_global0, int nz_global, Arrays A, BenchValues bv,
+                                 int zsrc) {
+  const long long n = (long long)(g.nz + 2) * g.pxy;
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
+       p += (long long)gridDim.x * blockDim.x) {
+    const int zp = (int)(p / g.pxy);
+    const long long r = p - (long long)zp * g.pxy;
+    const int yp = (int)(r / g.px);
+    const int xp = (int)(r - (long long)yp * g.px);
+    const int z = z_global0 + zp - 1;
+    const bool interior = xp >= 1 && xp <= g.nx && yp >= 1 && yp <= g.ny && z >= 0 && z < nz_global;
+    const double2 zero = make_double2(0.0, 0.0);
+    for (int a = 0; a < 12; ++a) A.f[a][p] = zero;
+    for (int k = 0; k < 12; ++k) {
+      const_cast<double2*>(A.t[k])[p] = interior ? bv.v[k] : zero;
+      const_cast<double2*>(A.c[k])[p] = interior ? bv.v[12 + k] : zero;
+    }
+    for (int k = 0; k < 4; ++k)
+      const_cast<double2*>(A.src[k])[p] = (interior && z == zsrc) ? bv.v[24 + k] : zero;
+  }
+}
+
+// Same problem in the table layout: material id 0 (ghost), 1 (interior), 2
+// (interior, injection plane); fields zero.
+__global__ void k_init_benchmark_table(Grid g, int z_global0, int nz_global, Arrays A,
+                                       uint8_t* mat, long long mp, long long mplane, int zsrc) {
+  const long long n = (long long)(g.nz + 2) * g.pxy;
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
+       p += (long long)gridDim.x * blockDim.x) {
+    const int zp = (int)(p / g.pxy);
+    const long long r = p - (long long)zp * g.pxy;
+    const int yp = (int)(r / g.px);
+    const int xp = (int)(r - (long long)yp * g.px);
+    const int z = z_global0 + zp - 1;
+    const bool interior = xp >= 1 && xp <= g.nx && yp >= 1 && yp <= g.ny && z >= 0 && z < nz_global;
+    for (int a = 0; a < 12; ++a) A.f[a][p] = make_double2(0.0, 0.0);
+    mat[(long long)zp * mplane + (long long)yp * mp + xp] =
+        interior ? (uint8_t)(z == zsrc ? 2 : 1) : (uint8_t)0;
   }
 }
 
@@ -1057,6 +1105,105 @@ int thiim_gpu_upload_fields(thiim_gpu_ctx* ctx, const thiim_c128* const fields[1
   g_err.clear();
   if (!ctx || !fields) return fail(THIIM_ERR_CONFIG, "null argument");
   return upload_arrays(ctx, fields, 0, 12);
+}
+
+void thiim_scheme_default(thiim_scheme* sp) {
+  if (!sp) return;
+  sp->omega = 0.4;  // SchemeParams defaults, coefficients.hpp:21-26
+  sp->tau = 1.0;
+  sp->delta = 1.0;
+  sp->source_e = {1.0, 0.0};
+  sp->source_h = {1.0, 0.0};
+}
+
+namespace {
+
+// Update coefficients of a homogeneous vacuum cell (MaterialCell{}: eps = 1,
+// mu = 1, sigma = sigma* = 0 -- coefficients.hpp:14-19), restating
+// derive_coefficients (coefficients.cpp:25-55) for family H and for family E
+// in Forward mode (select_mode picks Back only for Re(eps) < 0,
+// coefficients.hpp:50-53), then fill_coefficients' folding of the finite-
+// difference orientation (-1 for E) and the curl sign into c
+// (coefficients.cpp:63-66; curl signs components.hpp:54-67).  The complex
+// expressions keep the reference's structure and types, so libgcc's complex
+// division and libm's cos / sin round exactly as in the reference build.
+using cplx = std::complex<double>;
+
+int vacuum_coefficients(const thiim_scheme& sp, BenchValues& out) {
+  if (!(sp.tau > 0.0)) return fail(THIIM_ERR_CONFIG, "tau must be > 0");
+  if (!(sp.delta > 0.0)) return fail(THIIM_ERR_CONFIG, "delta must be > 0");
+  if (!(sp.omega * sp.tau <= 3.14159265358979323846 + 1e-12))
+    return fail(THIIM_ERR_CONFIG, "omega*tau must be <= pi");
+  const cplx eps(1.0, 0.0);
+  const double mu = 1.0, sigma = 0.0, sigma_star = 0.0;
+  const cplx src_e(sp.source_e.re, sp.source_e.im), src_h(sp.source_h.re, sp.source_h.im);
+  auto expi = [](double ph) { return cplx(std::cos(ph), std::sin(ph)); };
+  const double wt = sp.omega * sp.tau;
+  // H: [e^{-i wt/2} H + (tau/mu) D + tau S_H] / (e^{i wt/2} + tau sigma*/mu)
+  const cplx den_h = expi(wt / 2.0) + cplx(sp.tau * sigma_star / mu, 0.0);
+  // E forward: [e^{-i wt} E + (tau/eps) e^{-i wt/2} D + tau e^{-i wt} S_E] / (1 + tau sigma/eps)
+  const cplx den_e = cplx(1.0, 0.0) + sp.tau * sigma / eps;
+  if (std::abs(den_h) == 0.0 || std::abs(den_e) == 0.0)
+    return fail(THIIM_ERR_SETUP, "vanishing update denominator: resonant sigma/tau combination");
+  const cplx t_h = expi(-wt / 2.0) / den_h;
+  const cplx c_h = cplx(sp.tau / (mu * sp.delta), 0.0) / den_h;
+  const cplx s_h = sp.tau * src_h / den_h;
+  const cplx t_e = expi(-wt) / den_e;
+  const cplx c_e = (sp.tau / (eps * sp.delta)) * expi(-wt / 2.0) / den_e;
+  const cplx s_e = sp.tau * expi(-wt) * src_e / den_e;
+  // per component: curl sign (components.hpp:54-67), orientation -1 for E
+  static const double curl[12] = {+1, -1, -1, +1, +1, -1, -1, +1, +1, -1, -1, +1};
+  auto put = [](double2& d, const cplx& v) { d = make_double2(v.real(), v.imag()); };
+  for (int k = 0; k < 12; ++k) {
+    const bool e = k < HXY;
+    const double sign = (e ? -1.0 : 1.0) * curl[k];
+    put(out.v[k], e ? t_e : t_h);
+    put(out.v[12 + k], sign * (e ? c_e : c_h));
+  }
+  put(out.v[24 + SRC_EXZ], s_e);
+  put(out.v[24 + SRC_EYZ], s_e);
+  put(out.v[24 + SRC_HXZ], s_h);
+  put(out.v[24 + SRC_HYZ], s_h);
+  return THIIM_OK;
+}
+
+}  // namespace
+
+int thiim_gpu_init_benchmark(thiim_gpu_ctx* ctx, const thiim_scheme* spp) {
+  g_err.clear();
+  if (!ctx) return fail(THIIM_ERR_CONFIG, "null context");
+  thiim_scheme sp;
+  thiim_scheme_default(&sp);
+  if (spp) sp = *spp;
+  BenchValues bv;
+  int r = vacuum_coefficients(sp, bv);
+  if (r) return r;
+  const int zsrc = ctx->dims.nz / 4;  // source_plane_z, coefficients.hpp:70
+  for (auto& sl : ctx->slabs) {
+    CK(cudaSetDevice(sl.device));
+    Arrays A = sl.arrays(0, 0);
+    if (sl.table) {
+      if (sl.n_mat < 3) return fail(THIIM_ERR_CONFIG, "the benchmark problem has 3 materials");
+      double2 tab[3 * 28];
+      for (int m = 0; m < 3; ++m)
+        for (int a = 0; a < 28; ++a)
+          tab[m * 28 + a] = (m == 0 || (m == 1 && a >= 24)) ? make_double2(0.0, 0.0) : bv.v[a];
+      CK(cudaMemcpyAsync(sl.tab, tab, sizeof(tab), cudaMemcpyHostToDevice, sl.stream));
+      k_init_benchmark_table<<<8 * sm_count(sl.device), 256, 0, sl.stream>>>(
+          sl.g, sl.z0, ctx->dims.nz, A, sl.mat, sl.mp, sl.mplane, zsrc);
+    } else {
+      k_init_benchmark<<<8 * sm_count(sl.device), 256, 0, sl.stream>>>(sl.g, sl.z0, ctx->dims.nz,
+                                                                      A, bv, zsrc);
+    }
+    CK(cudaGetLastError());
+    for (int set = 1; set < sl.nfield_sets; ++set)
+      for (int k = 0; k < 12; ++k)
+        CK(cudaMemsetAsync(sl.field(set, k), 0, sl.stride * sizeof(double2), sl.stream));
+    CK(cudaStreamSynchronize(sl.stream));
+    sl.cur = 0;
+  }
+  ctx->loaded = true;
+  return THIIM_OK;
 }
 
 int thiim_gpu_init_generated(thiim_gpu_ctx* ctx, int kind, uint64_t seed) {
