@@ -64,6 +64,25 @@ def test_engine_matches_oracle(engine, shape):
         assert_same(gpu_run(s, steps, engine), oracle_run(s, steps))
 
 
+@pytest.mark.parametrize("engine,tile_y", [(P.ENGINE_TBLOCK, 12), (P.ENGINE_TBLOCK, 14),
+                                           (P.ENGINE_TBLOCK, 16), (P.ENGINE_FUSED, 8),
+                                           (P.ENGINE_FUSED, 16)])
+def test_tile_height_instances_match_oracle(engine, tile_y):
+    """The alternative CTA heights `tune` times (thiim-gpu-bench tune)."""
+    dims = P.GridDims(70, 45, 33)
+    s = P.generate_problem(dims, P.GEN_RANDOM, seed=13)
+    for steps in (2, 3):
+        assert_same(gpu_run(s, steps, engine, tile_y=tile_y), oracle_run(s, steps))
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("shape", [(300, 5, 4), (5, 300, 9), (4, 4, 130)])
+def test_extreme_aspect_ratios(engine, shape):
+    dims = P.GridDims(*shape)
+    s = P.generate_problem(dims, P.GEN_RANDOM, seed=17)
+    assert_same(gpu_run(s, 3, engine), oracle_run(s, 3))
+
+
 @pytest.mark.parametrize("engine", ENGINES)
 def test_layered_problem_matches_oracle(engine):
     dims = P.GridDims(40, 36, 48)
