@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <complex>
 #include <cstdlib>
@@ -35,6 +36,17 @@ using namespace thiim_gpu;
 namespace {
 
 thread_local std::string g_err;
+
+// One-time per-device setup flags (function attributes, pool configuration):
+// an atomic bit per device, set only after the setup succeeded.  The setups
+// are idempotent, so two host threads racing on one device merely both do it;
+// devices >= 32 redo it every time.
+bool setup_needed(const std::atomic<unsigned>& mask, int dev) {
+  return dev < 0 || dev >= 32 || !(mask.load() >> dev & 1u);
+}
+void setup_done(std::atomic<unsigned>& mask, int dev) {
+  if (dev >= 0 && dev < 32) mask.fetch_or(1u << dev);
+}
 
 int fail(int code, const std::string& msg) {
   g_err = msg;
@@ -489,13 +501,13 @@ int launch_fused_tma_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
   if (r) return r;
   constexpr int TX = 30, TY = BY - 2;
   const size_t smem = sizeof(FusedSmem<BY, NG>);
-  static unsigned attr_set = 0;  // bit per device: the attribute is per function and device
-  if (!(attr_set >> s.device & 1u)) {
+  static std::atomic<unsigned> attr_set{0};  // the attribute is per function and device
+  if (setup_needed(attr_set, s.device)) {
     CK(cudaFuncSetAttribute(k_fused_tma<BY, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)smem));
     CK(cudaFuncSetAttribute(k_fused_tma<BY, NG, true>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr_set |= 1u << s.device;
+    setup_done(attr_set, s.device);
   }
   const long long cols = (long long)((s.g.nx + TX - 1) / TX) * ((s.g.ny + TY - 1) / TY);
   const int zc = balanced_zchunk(s, cols, 1, ctx->opts.z_chunk);
@@ -591,8 +603,8 @@ int launch_tblock2_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
   if (r) return r;
   if (scratch && (r = ensure_scratch<BY>(s))) return r;
   const size_t smem = scratch ? sizeof(TbSmem<BY, NG>) : sizeof(TmSmem<BY, NG>);
-  static unsigned attr_set = 0;  // bit per device
-  if (!(attr_set >> s.device & 1u)) {
+  static std::atomic<unsigned> attr_set{0};
+  if (setup_needed(attr_set, s.device)) {
     if constexpr (BY == 15)
       CK(cudaFuncSetAttribute(k_tblock2<BY, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)sizeof(TbSmem<BY, NG>)));
@@ -600,7 +612,7 @@ int launch_tblock2_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
                             (int)sizeof(TmSmem<BY, NG>)));
     CK(cudaFuncSetAttribute(k_tblock_tm<BY, NG, true>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(TmSmem<BY, NG>)));
-    attr_set |= 1u << s.device;
+    setup_done(attr_set, s.device);
   }
   constexpr int TX2 = 28, TY2 = BY - 4;
   const int tiles_x = (s.g.nx + TX2 - 1) / TX2, tiles_y = (s.g.ny + TY2 - 1) / TY2;
@@ -647,13 +659,13 @@ int launch_tblock_table_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
   T.table = s.tab;
   T.n_mat = s.n_mat;
   const size_t smem = sizeof(TbTableSmem<BY, NG>);
-  static unsigned attr_set = 0;  // bit per device
-  if (!(attr_set >> s.device & 1u)) {
+  static std::atomic<unsigned> attr_set{0};
+  if (setup_needed(attr_set, s.device)) {
     CK(cudaFuncSetAttribute(k_tblock_table<BY, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)smem));
     CK(cudaFuncSetAttribute(k_tblock_table<BY, NG, true>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr_set |= 1u << s.device;
+    setup_done(attr_set, s.device);
   }
   constexpr int TX2 = 28, TY2 = BY - 4;
   const int tiles_x = (s.g.nx + TX2 - 1) / TX2, tiles_y = (s.g.ny + TY2 - 1) / TY2;
@@ -700,13 +712,13 @@ int launch_fused_table_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
   T.n_mat = s.n_mat;
   constexpr int TX = 30, TY = BY - 2;
   const size_t smem = sizeof(TableSmem<BY, NG>);
-  static unsigned attr_set = 0;  // bit per device
-  if (!(attr_set >> s.device & 1u)) {
+  static std::atomic<unsigned> attr_set{0};
+  if (setup_needed(attr_set, s.device)) {
     CK(cudaFuncSetAttribute(k_fused_table<BY, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)smem));
     CK(cudaFuncSetAttribute(k_fused_table<BY, NG, true>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr_set |= 1u << s.device;
+    setup_done(attr_set, s.device);
   }
   const int tiles_x = (s.g.nx + TX - 1) / TX, tiles_y = (s.g.ny + TY - 1) / TY;
   const int zc = balanced_zchunk(s, (long long)tiles_x * tiles_y, 1, ctx->opts.z_chunk);
@@ -778,13 +790,13 @@ double thiim_gpu_balance_model(int engine, int time_block) {
 // create/destroy stay in the milliseconds, while cudaFree of a 14 GB state
 // costs ~0.1 s.  Reserved-but-unused pool memory counts as available.
 static cudaMemPool_t device_pool(int dev) {
-  static unsigned configured = 0;
+  static std::atomic<unsigned> configured{0};
   cudaMemPool_t pool = nullptr;
   if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return nullptr;
-  if (!(configured >> dev & 1u)) {
+  if (setup_needed(configured, dev)) {
     uint64_t thr = UINT64_MAX;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    configured |= 1u << dev;
+    if (cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr) == cudaSuccess)
+      setup_done(configured, dev);
   }
   return pool;
 }
