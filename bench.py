@@ -125,6 +125,31 @@ def cpu_threads():
         return os.cpu_count() or 1
 
 
+def reference_engines_sample(grid, threads):
+    """The reference's other CPU engines on the same sample: its
+    spatially blocked sweep (block_y 8) and its multicore wavefront-diamond
+    engine (the paper's temporal blocking; dw 8, bz 1, one thread per group),
+    4 iterations each -- context for the naive baseline `value`."""
+    from oracle import oracle as O  # cpu baseline leg only
+    import paper_1510_05218_b200 as P
+    if not O.ref_available():
+        return {}
+    dims = P.GridDims(*grid)
+    cells = dims.interior_cells()
+    out = {}
+    try:
+        s = P.generate_problem(dims, P.GEN_RANDOM, SEED)
+        secs = O.ref_run_spatial(grid, s.arrays, 4, 8, 0, threads)
+        out["spatial_blocked_mlups"] = round(cells * 4 / secs / 1e6, 3)
+        s = P.generate_problem(dims, P.GEN_RANDOM, SEED)
+        secs, executed = O.ref_run_mwd(grid, s.arrays, 4, 8, 1, 1, 1, 1, threads)
+        out["mwd_mlups"] = round(cells * executed / secs / 1e6, 3)
+        out["mwd_params"] = "dw 8, bz 1, shape 1x1x1, %d threads" % threads
+    except Exception as e:  # report, never fail the bench line
+        out["reference_engines_error"] = str(e)[:200]
+    return out
+
+
 def reference_sample(grid, iters, threads):
     """Time the reference's run_naive (oracle/_ref) on a host problem."""
     from oracle import oracle as O  # cpu baseline leg only
@@ -245,6 +270,7 @@ def run_native(args, world, rank, local):
                                 "kind": kind,
                                 "sample": "reference run_naive (oracle/_ref, compiled unmodified), "
                                           "256x256x64 x 2 iterations, %d threads" % threads}
+        line["cpu_baseline"].update(reference_engines_sample(grid, threads))
     print(json.dumps(line), flush=True)
 
 
