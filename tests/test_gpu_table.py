@@ -78,3 +78,18 @@ def test_table_layout_rejections():
     with P.GpuEngine(d, P.GpuOptions(coeff_layout=P.COEFF_TABLE, n_materials=6)) as eng:
         with pytest.raises(P.ConfigError):
             eng.generate(P.GEN_RANDOM, 1)  # random media are not piecewise constant
+
+
+def test_config3_generator_at_256_cubed_vs_oracle():
+    """SURVEY s8d parity procedure: a 256^3 instance of the config-3 layered
+    generator against the CPU oracle -- reference layout (TBLOCK) and table
+    layout (TBLOCK-table), 4 iterations."""
+    d = P.GridDims(256, 256, 256)
+    host = P.generate_problem(d, P.GEN_LAYERED, seed=1)
+    want = oracle_run(host, 4)
+    for opts in (P.GpuOptions(), P.GpuOptions(coeff_layout=P.COEFF_TABLE, n_materials=6)):
+        with P.GpuEngine(d, opts) as eng:
+            eng.generate(P.GEN_LAYERED, seed=1)
+            eng.step(4)
+            diff = eng.compare_fields(want)
+        assert diff.bitwise_equal, (opts.coeff_layout, diff)
