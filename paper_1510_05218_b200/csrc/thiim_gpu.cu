@@ -88,6 +88,8 @@ struct Slab {
   // one set of box shapes per tile height (8 / 16 rows), built lazily
   TmaMaps maps[6];  // tile heights 8, 16, 15, 12, 14, 13 (map_index)
   bool maps_ok[6] = {false, false, false, false, false, false};
+  TmaMaps maps_seg[6][2];  // the same for 16- / 8-lane segments (folded TBLOCK tiles)
+  bool maps_seg_ok[6][2] = {};
   // TBLOCK: per-SM scratch ring (3 planes x 12 fields x tile) and its tensor map
   double2* scratch = nullptr;
   size_t scratch_bytes = 0;
@@ -462,10 +464,20 @@ int map_index(int by) {
 }
 // (each tile height gets its own set of box shapes)
 
-int ensure_tmap(Slab& s, int by, int promo) {
+// tensor maps for tile height `by` and thread-tile width `width` (32, or a
+// 16 / 8 lane segment of a folded CTA: every box 32 - width columns narrower)
+TmaMaps& tmaps(Slab& s, int by, int width = 32) {
+  const int w = map_index(by);
+  return width == 32 ? s.maps[w] : s.maps_seg[w][width == 16 ? 0 : 1];
+}
+
+int ensure_tmap(Slab& s, int by, int promo, int width = 32) {
   const int w = map_index(by);
   if (w < 0) return fail(THIIM_ERR_CONFIG, "no tensor maps for tile height " + std::to_string(by));
-  if (s.maps_ok[w]) return THIIM_OK;
+  if (width != 32 && width != 16 && width != 8)
+    return fail(THIIM_ERR_CONFIG, "no tensor maps for tile width " + std::to_string(width));
+  bool& ok = width == 32 ? s.maps_ok[w] : s.maps_seg_ok[w][width == 16 ? 0 : 1];
+  if (ok) return THIIM_OK;
   const CUtensorMapL2promotion pr[4] = {CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_64B,
                                         CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B};
@@ -475,18 +487,21 @@ int ensure_tmap(Slab& s, int by, int promo) {
                               (cuuint64_t)(s.g.nz + 2), (cuuint64_t)s.n_arrays()};
   const cuuint64_t strides[3] = {(cuuint64_t)s.g.px * 16, (cuuint64_t)s.g.pxy * 16,
                                  (cuuint64_t)s.stride * 16};
-  const int bw[NBOX] = {32, 31, 31, 30, 30, 29, 28};  // BoxGeom
-  const int bh[NBOX] = {by, by - 1, by - 2, by - 1, by - 2, by - 3, by - 4};
+  int bw[NBOX] = {32, 31, 31, 30, 30, 29, 28};  // BoxGeom
+  for (int b = 0; b < NBOX; ++b) bw[b] -= 32 - width;
+  int bh[NBOX] = {by, by - 1, by - 2, by - 1, by - 2, by - 3, by - 4};
+  for (int b = 0; b < NBOX; ++b) bh[b] += (32 / width - 1) * (by - 4);  // folded: all segments
   for (int b = 0; b < NBOX; ++b) {
     const cuuint32_t box[4] = {(cuuint32_t)(2 * bw[b]), (cuuint32_t)bh[b], 1, 1};
     const cuuint32_t estr[4] = {1, 1, 1, 1};
-    CUresult r = fn(&s.maps[w].m[b], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, s.buf, dims, strides, box,
+    CUresult r = fn(&tmaps(s, by, width).m[b], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, s.buf, dims,
+                    strides, box,
                     estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                     pr[promo & 3], CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS)
       return fail(THIIM_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
   }
-  s.maps_ok[w] = true;
+  ok = true;
   return THIIM_OK;
 }
 
@@ -516,7 +531,7 @@ int launch_fused_tma_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
   const dim3 grid(tiles_x * tiles_y, 1, (s.g.nz + zc - 1) / zc);
   const dim3 block(32, BY + 1);
   (s.cnt ? k_fused_tma<BY, NG, true> : k_fused_tma<BY, NG, false>)<<<grid, block, smem, s.stream>>>(
-      s.g, A, s.maps[map_index(BY)], S, zc,
+      s.g, A, tmaps(s, BY), S, zc,
                                                        tiles_y, tiles_x, ctx->opts.reserved[3] == 0,
                                                        cur * 12, nf * 12, ctx->opts.reserved[4] == 0);
   CK(cudaGetLastError());
@@ -608,17 +623,43 @@ int launch_tblock2_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
     if constexpr (BY == 15)
       CK(cudaFuncSetAttribute(k_tblock2<BY, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)sizeof(TbSmem<BY, NG>)));
+    const int tm_smem = (int)sizeof(TmSmem<BY, NG>);
     CK(cudaFuncSetAttribute(k_tblock_tm<BY, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)sizeof(TmSmem<BY, NG>)));
+                            tm_smem));
     CK(cudaFuncSetAttribute(k_tblock_tm<BY, NG, true>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(TmSmem<BY, NG>)));
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, tm_smem));
+    if constexpr (BY == 15) {
+      CK(cudaFuncSetAttribute(k_tblock_tm<BY, NG, false, 8>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, tm_smem));
+      CK(cudaFuncSetAttribute(k_tblock_tm<BY, NG, true, 8>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, tm_smem));
+      CK(cudaFuncSetAttribute(k_tblock_tm<BY, NG, false, 16>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, tm_smem));
+      CK(cudaFuncSetAttribute(k_tblock_tm<BY, NG, true, 16>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, tm_smem));
+    }
     setup_done(attr_set, s.device);
   }
   constexpr int TX2 = 28, TY2 = BY - 4;
-  const int tiles_x = (s.g.nx + TX2 - 1) / TX2, tiles_y = (s.g.ny + TY2 - 1) / TY2;
+  int tiles_x = (s.g.nx + TX2 - 1) / TX2;
+  const int tiles_y = (s.g.ny + TY2 - 1) / TY2;
+  // remainder column of <= 12 grid columns: folded CTAs of 16- or 8-lane
+  // segments (2 or 4 y-tiles per CTA) instead of a column of full tiles
+  int wf = 0, n_fold = 0;
+  const int rem = s.g.nx - (s.g.nx / TX2) * TX2;
+  static const bool no_fold = std::getenv("THIIM_NO_FOLD") != nullptr;  // A/B knob
+  if constexpr (BY == 15) {
+    if (!scratch && !no_fold && s.g.nx >= TX2 && rem > 0 && rem <= 12) {
+      wf = rem <= 4 ? 8 : 16;
+      tiles_x = s.g.nx / TX2;
+      n_fold = (tiles_y + 32 / wf - 1) / (32 / wf);
+      if ((r = ensure_tmap(s, BY, ctx->opts.reserved[2], wf))) return r;
+    }
+  }
+  const int n_main = tiles_x * tiles_y;
   int zc = ctx->opts.z_chunk;
-  if (zc <= 0) zc = tblock_zchunk(s, (long long)tiles_x * tiles_y);
-  const dim3 grid(tiles_x * tiles_y, 1, (s.g.nz + zc - 1) / zc);
+  if (zc <= 0) zc = tblock_zchunk(s, (long long)n_main + n_fold);
+  const dim3 grid(n_main + n_fold, 1, (s.g.nz + zc - 1) / zc);
   const dim3 block(32, BY + 1);
   if (scratch && s.deep) return fail(THIIM_ERR_CONFIG, "the scratch TBLOCK variant is whole-z only");
   if (scratch) {
@@ -628,16 +669,20 @@ int launch_tblock2_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
       P.tiles_x = tiles_x;
       for (int k = 0; k < 12; ++k) P.field_in[k] = fslot(k);
       P.scratch = s.scratch;
-      k_tblock2<BY, NG><<<grid, block, smem, s.stream>>>(s.g, A, s.maps[map_index(BY)], s.smap,
+      k_tblock2<BY, NG><<<grid, block, smem, s.stream>>>(s.g, A, tmaps(s, BY), s.smap,
                                                          S1, S2, P);
     } else {
       return fail(THIIM_ERR_CONFIG, "the scratch TBLOCK variant has tile height 15 only");
     }
   } else {
-    (s.cnt ? k_tblock_tm<BY, NG, true> : k_tblock_tm<BY, NG, false>)<<<grid, block, smem, s.stream>>>(
-        s.g, A, s.maps[map_index(BY)], cur * 12,
-                                                         nf * 12, zc, tiles_x,
-                                                         ctx->opts.reserved[5]);
+    auto kern = s.cnt ? k_tblock_tm<BY, NG, true> : k_tblock_tm<BY, NG, false>;
+    if constexpr (BY == 15) {
+      if (wf == 8) kern = s.cnt ? k_tblock_tm<BY, NG, true, 8> : k_tblock_tm<BY, NG, false, 8>;
+      if (wf == 16) kern = s.cnt ? k_tblock_tm<BY, NG, true, 16> : k_tblock_tm<BY, NG, false, 16>;
+    }
+    kern<<<grid, block, smem, s.stream>>>(s.g, A, tmaps(s, BY), tmaps(s, BY, wf ? wf : 32),
+                                          cur * 12, nf * 12, zc, tiles_x, n_main,
+                                          ctx->opts.reserved[5]);
   }
   CK(cudaGetLastError());
   s.cur ^= 1;
@@ -674,7 +719,7 @@ int launch_tblock_table_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
   const dim3 grid(tiles_x * tiles_y, 1, (s.g.nz + zc - 1) / zc);
   (s.cnt ? k_tblock_table<BY, NG, true> : k_tblock_table<BY, NG, false>)<<<grid, dim3(32, BY + 1), smem,
                                                                           s.stream>>>(
-      s.g, A, T, s.maps[map_index(BY)],
+      s.g, A, T, tmaps(s, BY),
                                                                      s.cur * 12, zc, tiles_x);
   CK(cudaGetLastError());
   s.cur ^= 1;
@@ -703,7 +748,7 @@ int launch_fused_table_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
   int r = ensure_tmap(s, BY, 0);
   if (r) return r;
   TableMaps maps;
-  maps.f = s.maps[map_index(BY)];
+  maps.f = tmaps(s, BY);
   TableGrid T;
   T.mat = s.mat;
   T.mp = s.mp;

@@ -19,12 +19,15 @@
 
 namespace thiim_gpu {
 
-template <int BY, int NG>
+// W < 32: a folded CTA -- its boxes (BoxGeom<BY, W>, `maps` built for W) span
+// all 32/W segments' rows, one TMA per array as for a full tile.
+template <int BY, int NG, int W = 32>
 struct RingProducer {
-  using Gm = BoxGeom<BY>;
+  using Gm = BoxGeom<BY, W>;
+  static_assert(32 % W == 0, "segment width must divide 32");
   Ring<BY, NG>& R;
   const TmaMaps& maps;
-  int xb, yb;  // interior coordinates of thread (0,0)
+  int xb, yb;  // interior coordinates of thread (0,0) (of segment 0)
   int gi = 0;
   uint32_t ph = 0;
 
@@ -35,6 +38,12 @@ struct RingProducer {
   __device__ __forceinline__ void begin() {
     mbar_wait(&R.empty[gi], ph ^ 1);
     mbar_arrive_expect_tx(&R.full[gi], (uint32_t)BYTES);
+  }
+  // a group of N boxes of kind B
+  template <int B, int N>
+  __device__ __forceinline__ void begin_group() {
+    static_assert(Gm::w(B) * Gm::h(B) <= 32 * BY, "box exceeds a ring box slot");
+    begin<N * Gm::bytes(B)>();
   }
   __device__ __forceinline__ void end() {
     if (++gi == NG) {
@@ -61,12 +70,9 @@ struct RingProducer {
 // One fused / level-1 plane z (seq_plane): E_old(z+1) x6, then per H component
 // F, t, c (, src), then the E coefficients.  HINT: per-class L2 policies
 // (fields, coefficients) or none.
-template <bool HINT, int BY, int NG>
-__device__ __forceinline__ void produce_plane_ct(RingProducer<BY, NG>& P, int fb, int cb, int z,
-                                                 uint64_t pf = 0, uint64_t pc = 0) {
-  using Gm = BoxGeom<BY>;
-  constexpr int SA = Gm::bytes(BOX_A), SB = Gm::bytes(BOX_B), SBX = Gm::bytes(BOX_BX),
-                SBY = Gm::bytes(BOX_BY), SC = Gm::bytes(BOX_C);
+template <bool HINT, class PR>
+__device__ __forceinline__ void produce_plane_ct(PR& P, int fb, int cb, int z, uint64_t pf = 0,
+                                                 uint64_t pc = 0) {
   const int p0 = z + 1, p1 = z + 2;
 #define BOXF(B, k, slot, pz) \
   do {                        \
@@ -82,65 +88,65 @@ __device__ __forceinline__ void produce_plane_ct(RingProducer<BY, NG>& P, int fb
     else                      \
       P.template box<B>(k, slot, pz);     \
   } while (0)
-  P.template begin<4 * SA>();
+  P.template begin_group<BOX_A, 4>();
   BOXF(BOX_A, 0, fb + EXY, p1);
   BOXF(BOX_A, 1, fb + EXZ, p1);
   BOXF(BOX_A, 2, fb + EYX, p1);
   BOXF(BOX_A, 3, fb + EYZ, p1);
   P.end();
-  P.template begin<2 * SA>();
+  P.template begin_group<BOX_A, 2>();
   BOXF(BOX_A, 0, fb + EZX, p1);
   BOXF(BOX_A, 1, fb + EZY, p1);
   P.end();
-  P.template begin<3 * SBY>();  // Hxy
+  P.template begin_group<BOX_BY, 3>();  // Hxy
   BOXF(BOX_BY, 0, fb + HXY, p0);
   BOXC(BOX_BY, 1, cb + HXY, p0);
   BOXC(BOX_BY, 2, cb + 12 + HXY, p0);
   P.end();
-  P.template begin<4 * SBY>();  // Hxz
+  P.template begin_group<BOX_BY, 4>();  // Hxz
   BOXF(BOX_BY, 0, fb + HXZ, p0);
   BOXC(BOX_BY, 1, cb + HXZ, p0);
   BOXC(BOX_BY, 2, cb + 12 + HXZ, p0);
   BOXC(BOX_BY, 3, cb + 24 + SRC_HXZ, p0);
   P.end();
-  P.template begin<3 * SBX>();  // Hyx
+  P.template begin_group<BOX_BX, 3>();  // Hyx
   BOXF(BOX_BX, 0, fb + HYX, p0);
   BOXC(BOX_BX, 1, cb + HYX, p0);
   BOXC(BOX_BX, 2, cb + 12 + HYX, p0);
   P.end();
-  P.template begin<4 * SBX>();  // Hyz
+  P.template begin_group<BOX_BX, 4>();  // Hyz
   BOXF(BOX_BX, 0, fb + HYZ, p0);
   BOXC(BOX_BX, 1, cb + HYZ, p0);
   BOXC(BOX_BX, 2, cb + 12 + HYZ, p0);
   BOXC(BOX_BX, 3, cb + 24 + SRC_HYZ, p0);
   P.end();
-  P.template begin<3 * SB>();  // Hzx
+  P.template begin_group<BOX_B, 3>();  // Hzx
   BOXF(BOX_B, 0, fb + HZX, p0);
   BOXC(BOX_B, 1, cb + HZX, p0);
   BOXC(BOX_B, 2, cb + 12 + HZX, p0);
   P.end();
-  P.template begin<3 * SB>();  // Hzy
+  P.template begin_group<BOX_B, 3>();  // Hzy
   BOXF(BOX_B, 0, fb + HZY, p0);
   BOXC(BOX_B, 1, cb + HZY, p0);
   BOXC(BOX_B, 2, cb + 12 + HZY, p0);
   P.end();
-  P.template begin<4 * SC>();  // Exy, Eyx
+  P.template begin_group<BOX_C, 4>();  // Exy, Eyx
   BOXC(BOX_C, 0, cb + EXY, p0);
   BOXC(BOX_C, 1, cb + 12 + EXY, p0);
   BOXC(BOX_C, 2, cb + EYX, p0);
   BOXC(BOX_C, 3, cb + 12 + EYX, p0);
   P.end();
-  P.template begin<3 * SC>();  // Exz
+  P.template begin_group<BOX_C, 3>();  // Exz
   BOXC(BOX_C, 0, cb + EXZ, p0);
   BOXC(BOX_C, 1, cb + 12 + EXZ, p0);
   BOXC(BOX_C, 2, cb + 24 + SRC_EXZ, p0);
   P.end();
-  P.template begin<3 * SC>();  // Eyz
+  P.template begin_group<BOX_C, 3>();  // Eyz
   BOXC(BOX_C, 0, cb + EYZ, p0);
   BOXC(BOX_C, 1, cb + 12 + EYZ, p0);
   BOXC(BOX_C, 2, cb + 24 + SRC_EYZ, p0);
   P.end();
-  P.template begin<4 * SC>();  // Ezx, Ezy
+  P.template begin_group<BOX_C, 4>();  // Ezx, Ezy
   BOXC(BOX_C, 0, cb + EZX, p0);
   BOXC(BOX_C, 1, cb + 12 + EZX, p0);
   BOXC(BOX_C, 2, cb + EZY, p0);
@@ -152,51 +158,48 @@ __device__ __forceinline__ void produce_plane_ct(RingProducer<BY, NG>& P, int fb
 
 // Level-2 coefficient groups of plane r, policy `pol`: seq_level2_coef's
 // grouping, boxed to the level-2 regions (BOX_H2 / BOX_E2).
-template <int BY, int NG>
-__device__ __forceinline__ void produce_level2_coef_ct(RingProducer<BY, NG>& P, int cb, int r,
-                                                       uint64_t pol) {
-  using Gm = BoxGeom<BY>;
-  constexpr int SH = Gm::bytes(BOX_H2), SE = Gm::bytes(BOX_E2);
+template <class PR>
+__device__ __forceinline__ void produce_level2_coef_ct(PR& P, int cb, int r, uint64_t pol) {
   const int p0 = r + 1;
-  P.template begin<4 * SH>();  // Hxy t c, Hyx t c
+  P.template begin_group<BOX_H2, 4>();  // Hxy t c, Hyx t c
   P.template box<BOX_H2>(0, cb + HXY, p0, pol);
   P.template box<BOX_H2>(1, cb + 12 + HXY, p0, pol);
   P.template box<BOX_H2>(2, cb + HYX, p0, pol);
   P.template box<BOX_H2>(3, cb + 12 + HYX, p0, pol);
   P.end();
-  P.template begin<3 * SH>();  // Hxz t c src
+  P.template begin_group<BOX_H2, 3>();  // Hxz t c src
   P.template box<BOX_H2>(0, cb + HXZ, p0, pol);
   P.template box<BOX_H2>(1, cb + 12 + HXZ, p0, pol);
   P.template box<BOX_H2>(2, cb + 24 + SRC_HXZ, p0, pol);
   P.end();
-  P.template begin<3 * SH>();  // Hyz t c src
+  P.template begin_group<BOX_H2, 3>();  // Hyz t c src
   P.template box<BOX_H2>(0, cb + HYZ, p0, pol);
   P.template box<BOX_H2>(1, cb + 12 + HYZ, p0, pol);
   P.template box<BOX_H2>(2, cb + 24 + SRC_HYZ, p0, pol);
   P.end();
-  P.template begin<4 * SH>();  // Hzx t c, Hzy t c
+  P.template begin_group<BOX_H2, 4>();  // Hzx t c, Hzy t c
   P.template box<BOX_H2>(0, cb + HZX, p0, pol);
   P.template box<BOX_H2>(1, cb + 12 + HZX, p0, pol);
   P.template box<BOX_H2>(2, cb + HZY, p0, pol);
   P.template box<BOX_H2>(3, cb + 12 + HZY, p0, pol);
   P.end();
-  P.template begin<4 * SE>();  // Exy t c, Eyx t c
+  P.template begin_group<BOX_E2, 4>();  // Exy t c, Eyx t c
   P.template box<BOX_E2>(0, cb + EXY, p0, pol);
   P.template box<BOX_E2>(1, cb + 12 + EXY, p0, pol);
   P.template box<BOX_E2>(2, cb + EYX, p0, pol);
   P.template box<BOX_E2>(3, cb + 12 + EYX, p0, pol);
   P.end();
-  P.template begin<3 * SE>();  // Exz t c src
+  P.template begin_group<BOX_E2, 3>();  // Exz t c src
   P.template box<BOX_E2>(0, cb + EXZ, p0, pol);
   P.template box<BOX_E2>(1, cb + 12 + EXZ, p0, pol);
   P.template box<BOX_E2>(2, cb + 24 + SRC_EXZ, p0, pol);
   P.end();
-  P.template begin<3 * SE>();  // Eyz t c src
+  P.template begin_group<BOX_E2, 3>();  // Eyz t c src
   P.template box<BOX_E2>(0, cb + EYZ, p0, pol);
   P.template box<BOX_E2>(1, cb + 12 + EYZ, p0, pol);
   P.template box<BOX_E2>(2, cb + 24 + SRC_EYZ, p0, pol);
   P.end();
-  P.template begin<4 * SE>();  // Ezx t c, Ezy t c
+  P.template begin_group<BOX_E2, 4>();  // Ezx t c, Ezy t c
   P.template box<BOX_E2>(0, cb + EZX, p0, pol);
   P.template box<BOX_E2>(1, cb + 12 + EZX, p0, pol);
   P.template box<BOX_E2>(2, cb + EZY, p0, pol);

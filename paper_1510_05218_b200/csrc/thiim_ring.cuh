@@ -50,7 +50,12 @@ enum : int {
   BOX_A = 0, BOX_B = 1, BOX_BX = 2, BOX_BY = 3, BOX_C = 4, BOX_H2 = 5, BOX_E2 = 6, NBOX = 7
 };
 
-template <int BY>
+// W: width of the thread tile the boxes belong to -- 32 (one warp row), or a
+// narrower segment of a folded CTA (k_tblock_tm's remainder tiles).  A folded
+// CTA's 32/W segments are consecutive y-tiles (BY - 4 rows apart), so one box
+// serves all of them: 32 - W columns narrower and (32/W - 1)(BY - 4) rows taller;
+// segment s reads rows s(BY - 4) + [0, h_seg).
+template <int BY, int W = 32>
 struct BoxGeom {
   __host__ __device__ static constexpr int x0(int b) {
     return b == BOX_E2 ? 2 : (b == BOX_BY || b == BOX_C || b == BOX_H2) ? 1 : 0;
@@ -59,14 +64,17 @@ struct BoxGeom {
     return b == BOX_E2 ? 2 : (b == BOX_BX || b == BOX_C || b == BOX_H2) ? 1 : 0;
   }
   __host__ __device__ static constexpr int w(int b) {
-    return b == BOX_A ? 32 : b <= BOX_BX ? 31 : b <= BOX_C ? 30 : b == BOX_H2 ? 29 : 28;
+    return (b == BOX_A ? 32 : b <= BOX_BX ? 31 : b <= BOX_C ? 30 : b == BOX_H2 ? 29 : 28) - (32 - W);
   }
-  __host__ __device__ static constexpr int h(int b) {
+  __host__ __device__ static constexpr int h_seg(int b) {  // rows one segment reads
     return b == BOX_A                      ? BY
            : (b == BOX_B || b == BOX_BY)   ? BY - 1
            : (b == BOX_BX || b == BOX_C)   ? BY - 2
            : b == BOX_H2                   ? BY - 3
                                            : BY - 4;
+  }
+  __host__ __device__ static constexpr int h(int b) {  // box rows
+    return h_seg(b) + (32 / W - 1) * (BY - 4);
   }
   __host__ __device__ static constexpr int bytes(int b) { return w(b) * h(b) * 16; }
 };
@@ -174,6 +182,22 @@ __device__ __forceinline__ uint32_t ring_dep(const T&... v) {
 }
 
 // release the current group; `dep` = ring_dep(every value read from it)
+// bounded read for thread (lx, ty) of segment `seg` of a folded CTA (W < 32):
+// the segment's window starts seg * (BY - 4) rows into the shared box
+template <int BY, int W, int NG>
+__device__ __forceinline__ double2 ring_read_seg(Ring<BY, NG>& r, const RingCursor& c, int k, int b,
+                                                 int lx, int ty, int seg) {
+  if constexpr (W == 32) {
+    return ring_read(r, c, k, b, lx, ty);
+  } else {
+    using Gm = BoxGeom<BY, W>;
+    const int cx = lx - Gm::x0(b), cy = ty - Gm::y0(b);
+    if (cx >= 0 && cx < Gm::w(b) && cy >= 0 && cy < Gm::h_seg(b))
+      return r.buf[c.g][k][(seg * (BY - 4) + cy) * Gm::w(b) + cx];
+    return make_double2(0.0, 0.0);
+  }
+}
+
 template <int BY, int NG>
 __device__ __forceinline__ void ring_release(Ring<BY, NG>& r, RingCursor& c, int tx, uint32_t dep) {
 #if THIIM_RING_FENCE == 1

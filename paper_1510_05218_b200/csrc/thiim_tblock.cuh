@@ -570,19 +570,23 @@ struct TmSmem {
   uint32_t tmem_base;
 };
 
-template <int BY, int NG, bool COUNT = false>
-__global__ void __launch_bounds__(32 * (BY + 1), 1)
-    k_tblock_tm(Grid g, Arrays A, const __grid_constant__ TmaMaps maps, int fb, int cb, int zc,
-                int tiles_x, int pol_mode) {
+// One CTA's sweep.  W = 32: the 32 x BY thread tile of one 28 x (BY-4) output
+// tile at (xb, yb0).  W < 32 (a folded remainder CTA): the warp rows split into
+// 32/W segments of W lanes, each the thread tile of a (W-4) x (BY-4) output
+// tile, stacked in y from yb0 -- the same sweep on narrow tiles, so a remainder
+// column of <= W-4 grid columns costs 32/W times fewer CTAs than full tiles
+// (256 = 9 x 28 + 4: the tenth tile column ran 24 nearly empty CTAs per chunk).
+template <int BY, int NG, bool COUNT, int W>
+__device__ __forceinline__ void tblock_tm_body(TmSmem<BY, NG>& sm, const Grid& g, const Arrays& A,
+                                               const TmaMaps& maps, int fb, int cb, int zc, int xb,
+                                               int yb0, int pol_mode) {
   constexpr int NCOMP = 32 * BY;
-  constexpr int TX2 = 28, TY2 = BY - 4;
+  constexpr int TY2 = BY - 4;
   constexpr int LAG = 1;
   static_assert(BY <= 16, "TMEM carry layout: at most 4 consumer warps per lane quadrant");
-  extern __shared__ __align__(1024) unsigned char smem_raw[];
-  TmSmem<BY, NG>& sm = *reinterpret_cast<TmSmem<BY, NG>*>(smem_raw);
   const int tx = threadIdx.x, ty = threadIdx.y;
-  const int btx = blockIdx.x % tiles_x, bty = blockIdx.x / tiles_x;
-  const int xb = btx * TX2 - 2, yb = bty * TY2 - 2;
+  const int lx = W == 32 ? tx : tx % W, seg = W == 32 ? 0 : tx / W;
+  const int yb = yb0 + seg * TY2;
   const int z0 = blockIdx.z * zc;
   const int z1 = min(g.nz, z0 + zc);
   const long long pxy = g.pxy;
@@ -610,7 +614,7 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
       const uint64_t pf1 = pol_mode == 3 ? norm : drop;
       const uint64_t pc1 = pol_mode == 2 ? norm : keep;
       const uint64_t pc2 = pol_mode == 1 || pol_mode == 2 ? norm : pol_mode == 4 ? keep : drop;
-      RingProducer<BY, NG> P(sm.ring, maps, xb, yb);
+      RingProducer<BY, NG, W> P(sm.ring, maps, xb, yb0);
       for (int q = qs; q <= qe; ++q) {
         // level 1 keeps coefficients in L2 for level 2 (their last use)
         if (q <= q1) produce_plane_ct<true>(P, fb, cb, q, pf1, pc1);
@@ -624,16 +628,18 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
   // -------------------------------------------------------------- consumers
   const uint32_t tcar = tm_warp_addr(sm.tmem_base, ty, 128 * (ty >> 2));
   const uint32_t tnext = tcar + 96;
-  const int x = xb + tx, y = yb + ty;
+  const int x = xb + lx, y = yb + ty;
   const bool inpad = (x >= -1) && (x <= g.nx) && (y >= -1) && (y <= g.ny);
   const bool interior = (x >= 0) && (x < g.nx) && (y >= 0) && (y < g.ny);
   const int xs = inpad ? x : 0, ys = inpad ? y : 0;
-  const bool own1 = tx >= 1 && tx <= 30 && ty >= 1 && ty <= BY - 2;
-  const bool rx1 = (tx == 0) && (ty >= 1) && (ty <= BY - 2);
-  const bool ry1 = (ty == 0) && (tx >= 1) && (tx <= 30);
-  const bool own2 = tx >= 2 && tx <= 29 && ty >= 2 && ty <= BY - 3;
-  const bool rx2 = (tx == 1) && (ty >= 2) && (ty <= BY - 3);
-  const bool ry2 = (ty == 1) && (tx >= 2) && (tx <= 29);
+  // segment-relative roles (x +-1 neighbours of every thread that reads one lie
+  // in its own segment)
+  const bool own1 = lx >= 1 && lx <= W - 2 && ty >= 1 && ty <= BY - 2;
+  const bool rx1 = (lx == 0) && (ty >= 1) && (ty <= BY - 2);
+  const bool ry1 = (ty == 0) && (lx >= 1) && (lx <= W - 2);
+  const bool own2 = lx >= 2 && lx <= W - 3 && ty >= 2 && ty <= BY - 3;
+  const bool rx2 = (lx == 1) && (ty >= 2) && (ty <= BY - 3);
+  const bool ry2 = (ty == 1) && (lx >= 2) && (lx <= W - 3);
   const bool upd1_x = (own1 || ry1) && interior;
   const bool upd1_y = (own1 || rx1) && interior;
   const bool upd1_z = (own1 || rx1 || ry1) && interior;
@@ -643,7 +649,7 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
 
   auto& R = sm.ring;
   RingCursor rc = ring_cursor(R);
-#define RD(k, b) ring_read(R, rc, k, b, tx, ty)
+#define RD(k, b) ring_read_seg<BY, W>(R, rc, k, b, lx, ty, seg)
 
   // ---- level-1 prologue: E_old splits at qs (to TMEM), H^1 sums at qs-1
   double2 pH1x = make_double2(0.0, 0.0), pH1y = make_double2(0.0, 0.0);
@@ -952,6 +958,25 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
   named_sync(1, NCOMP);
   tm_fence_after();
   if (ty == 0) tm_dealloc<512>(sm.tmem_base);
+}
+
+
+template <int BY, int NG, bool COUNT = false, int WF = 0>
+__global__ void __launch_bounds__(32 * (BY + 1), 1)
+    k_tblock_tm(Grid g, Arrays A, const __grid_constant__ TmaMaps maps,
+                const __grid_constant__ TmaMaps maps_f, int fb, int cb, int zc, int tiles_x,
+                int n_main, int pol_mode) {
+  constexpr int TX2 = 28, TY2 = BY - 4;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  TmSmem<BY, NG>& sm = *reinterpret_cast<TmSmem<BY, NG>*>(smem_raw);
+  const int b = blockIdx.x;
+  if (b < n_main) {  // full tiles, x-fastest
+    tblock_tm_body<BY, NG, COUNT, 32>(sm, g, A, maps, fb, cb, zc, (b % tiles_x) * TX2 - 2,
+                                      (b / tiles_x) * TY2 - 2, pol_mode);
+  } else if constexpr (WF > 0) {  // folded remainder column: 32/WF y-tiles per CTA
+    tblock_tm_body<BY, NG, COUNT, WF>(sm, g, A, maps_f, fb, cb, zc, tiles_x * TX2 - 2,
+                                      (b - n_main) * (32 / WF) * TY2 - 2, pol_mode);
+  }
 }
 
 }  // namespace thiim_gpu
