@@ -18,8 +18,11 @@ def _passes(engine, steps):
 
 
 @pytest.mark.parametrize("engine", [P.ENGINE_SPLIT, P.ENGINE_FUSED, P.ENGINE_TBLOCK])
+# nx mod 28 = 9, 8, 6 (TBLOCK folds the remainder into 16-lane segments),
+# 4, 3 (8-lane segments)
 @pytest.mark.parametrize("shape,steps,zc", [((37, 29, 23), 5, 0), ((64, 40, 48), 4, 7),
-                                           ((90, 61, 18), 3, 5)])
+                                           ((90, 61, 18), 3, 5), ((60, 47, 20), 4, 0),
+                                           ((31, 70, 16), 2, 3)])
 def test_exactly_once_single_slab(engine, shape, steps, zc):
     d = P.GridDims(*shape)
     with P.GpuEngine(d, P.GpuOptions(engine=engine, z_chunk=zc)) as e:
