@@ -97,6 +97,19 @@ struct Arrays {
   long long cstride = 0;
 };
 
+// Where a TBLOCK pass stores its level-2 outputs (the interior local plane r of
+// a slab): locally for r in [st0, st1) -- a deep slab's owned planes -- and, in a
+// multi-GPU context, also straight into the neighbour slabs' halo planes over
+// NVLink / NVSwitch peer memory (lo / hi: the neighbour's output field set,
+// element shift my index -> its index), which replaces the halo exchange step.
+struct PeerOut {
+  double2* lo[12];  // lower neighbour (null: none)
+  double2* hi[12];  // upper neighbour
+  long long lo_shift, hi_shift;
+  int lo_r0, lo_r1, hi_r0, hi_r1;  // my interior planes sent down / up
+  int st0, st1;                    // my interior planes stored locally
+};
+
 // Sanitizer hook at every output store of the default kernels (their COUNT
 // instances only): counts how often (component, cell) is written in a pass;
 // k_coverage then demands exactly once per interior cell, never on a ghost.

@@ -84,6 +84,7 @@ struct Slab {
 
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t ev_pass = nullptr;  // last TBLOCK pass (peer-store ordering between slabs)
   // 4-D tensor maps over the allocation {x (doubles), y, plane, array slot},
   // one set of box shapes per tile height (8 / 16 rows), built lazily
   TmaMaps maps[6];  // tile heights 8, 16, 15, 12, 14, 13 (map_index)
@@ -126,6 +127,7 @@ struct thiim_gpu_ctx {
   std::vector<Slab> slabs;
   bool loaded = false;
   bool sanitize = false;               // exactly-once store coverage per pass
+  bool peer_stores = false;  // deep slabs write each other's halos from the kernel
   unsigned long long cov_passes = 0;
   long long pxy() const { return (long long)(dims.nx + 2) * (dims.ny + 2); }
 };
@@ -219,7 +221,8 @@ __global__ void k_init_benchmark_table(Grid g, int z_global0, int nz_global, Arr
 // UpdateLog coverage, tools/main.cpp:20-41): every (component, interior cell) of
 // the slab's local grid was stored exactly once, no ghost ever; the counts are
 // reset for the next pass.
-__global__ void k_coverage(Grid g, unsigned* cnt, long long cstride, unsigned long long* bad) {
+__global__ void k_coverage(Grid g, unsigned* cnt, long long cstride, int r0, int r1,
+                           unsigned long long* bad) {
   const long long n = (long long)(g.nz + 2) * g.pxy;
   unsigned long long b = 0;
   for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
@@ -228,7 +231,8 @@ __global__ void k_coverage(Grid g, unsigned* cnt, long long cstride, unsigned lo
     const long long r = p - (long long)zp * g.pxy;
     const int yp = (int)(r / g.px);
     const int xp = (int)(r - (long long)yp * g.px);
-    const bool interior = xp >= 1 && xp <= g.nx && yp >= 1 && yp <= g.ny && zp >= 1 && zp <= g.nz;
+    const bool interior =
+        xp >= 1 && xp <= g.nx && yp >= 1 && yp <= g.ny && zp >= 1 + r0 && zp <= r1;  // r: zp - 1
     const unsigned want = interior ? 1u : 0u;
     for (int k = 0; k < 12; ++k) {
       unsigned* c = cnt + (long long)k * cstride + p;
@@ -363,6 +367,47 @@ int deep_first_plane(const Slab& sl, int which) {  // local padded plane of a 2-
     case THIIM_HALO_SEND_UP: return sl.g.nz - 1 - sl.ext_hi;  // owned own1-2, own1-1
     default: return sl.g.nz;                                 // extended own1, ghost own1+1
   }
+}
+
+// Store plan of slab `k` for its next TBLOCK pass (before any slab of the pass
+// is launched: launches flip the current field set).  Deep slabs store their
+// owned planes; with peer stores they also write their two boundary planes at
+// each internal interface straight into the neighbour's halo (SEND_* -> RECV_*
+// of the deep-halo protocol, the neighbour's output set).
+PeerOut peer_out(const thiim_gpu_ctx* ctx, int k) {
+  const Slab& sl = ctx->slabs[k];
+  PeerOut po{};
+  po.st0 = sl.deep ? sl.ext_lo : 0;
+  po.st1 = sl.deep ? sl.g.nz - sl.ext_hi : sl.g.nz;
+  if (!ctx->peer_stores) return po;
+  const long long pxy = sl.g.pxy;
+  if (k > 0) {
+    const Slab& lo = ctx->slabs[k - 1];
+    for (int c = 0; c < 12; ++c) po.lo[c] = lo.field(lo.cur ^ 1, c);
+    po.lo_r0 = sl.ext_lo;
+    po.lo_r1 = sl.ext_lo + 2;
+    po.lo_shift = (long long)(deep_first_plane(lo, THIIM_HALO_RECV_UP) -
+                              deep_first_plane(sl, THIIM_HALO_SEND_DOWN)) * pxy;
+  }
+  if (k + 1 < (int)ctx->slabs.size()) {
+    const Slab& hi = ctx->slabs[k + 1];
+    for (int c = 0; c < 12; ++c) po.hi[c] = hi.field(hi.cur ^ 1, c);
+    po.hi_r0 = sl.g.nz - 2 - sl.ext_hi;
+    po.hi_r1 = sl.g.nz - sl.ext_hi;
+    po.hi_shift = (long long)(deep_first_plane(hi, THIIM_HALO_RECV_DOWN) -
+                              deep_first_plane(sl, THIIM_HALO_SEND_UP)) * pxy;
+  }
+  return po;
+}
+
+// make slab k's stream wait for its neighbours' last pass (their peer stores
+// into k's halos, and their reads of the halos k's next pass overwrites)
+int wait_neighbours(thiim_gpu_ctx* ctx, int k) {
+  Slab& sl = ctx->slabs[k];
+  CK(cudaSetDevice(sl.device));
+  if (k > 0) CK(cudaStreamWaitEvent(sl.stream, ctx->slabs[k - 1].ev_pass, 0));
+  if (k + 1 < (int)ctx->slabs.size()) CK(cudaStreamWaitEvent(sl.stream, ctx->slabs[k + 1].ev_pass, 0));
+  return THIIM_OK;
 }
 
 int exchange_deep(thiim_gpu_ctx* ctx) {
@@ -598,7 +643,7 @@ int tblock_zchunk(const Slab& s, long long cols) {
 }
 
 template <int BY, int NG>
-int launch_tblock2_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
+int launch_tblock2_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches, const PeerOut& po) {
   if (!s.deep && (s.g.halo_lo || s.z1 < ctx->dims.nz))
     return fail(THIIM_ERR_CONFIG, "TBLOCK on a slab needs a deep-halo slab context");
   const Arrays A = s.arrays(s.cur, s.cur ^ 1);
@@ -637,6 +682,10 @@ int launch_tblock2_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
                               cudaFuncAttributeMaxDynamicSharedMemorySize, tm_smem));
       CK(cudaFuncSetAttribute(k_tblock_tm<BY, NG, true, 16>,
                               cudaFuncAttributeMaxDynamicSharedMemorySize, tm_smem));
+      for (auto f : {k_tblock_tm<BY, NG, false, 0, true>, k_tblock_tm<BY, NG, true, 0, true>,
+                     k_tblock_tm<BY, NG, false, 8, true>, k_tblock_tm<BY, NG, true, 8, true>,
+                     k_tblock_tm<BY, NG, false, 16, true>, k_tblock_tm<BY, NG, true, 16, true>})
+        CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, tm_smem));
     }
     setup_done(attr_set, s.device);
   }
@@ -677,10 +726,20 @@ int launch_tblock2_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
   } else {
     auto kern = s.cnt ? k_tblock_tm<BY, NG, true> : k_tblock_tm<BY, NG, false>;
     if constexpr (BY == 15) {
-      if (wf == 8) kern = s.cnt ? k_tblock_tm<BY, NG, true, 8> : k_tblock_tm<BY, NG, false, 8>;
-      if (wf == 16) kern = s.cnt ? k_tblock_tm<BY, NG, true, 16> : k_tblock_tm<BY, NG, false, 16>;
+      const bool c = s.cnt != nullptr;
+      if (s.deep) {  // owned-plane stores + peer stores (multi-GPU slabs)
+        kern = wf == 8    ? (c ? k_tblock_tm<BY, NG, true, 8, true> : k_tblock_tm<BY, NG, false, 8, true>)
+               : wf == 16 ? (c ? k_tblock_tm<BY, NG, true, 16, true>
+                               : k_tblock_tm<BY, NG, false, 16, true>)
+                          : (c ? k_tblock_tm<BY, NG, true, 0, true> : k_tblock_tm<BY, NG, false, 0, true>);
+      } else {
+        if (wf == 8) kern = c ? k_tblock_tm<BY, NG, true, 8> : k_tblock_tm<BY, NG, false, 8>;
+        if (wf == 16) kern = c ? k_tblock_tm<BY, NG, true, 16> : k_tblock_tm<BY, NG, false, 16>;
+      }
+    } else if (s.deep) {
+      return fail(THIIM_ERR_CONFIG, "deep-halo slabs run TBLOCK at tile height 15");
     }
-    kern<<<grid, block, smem, s.stream>>>(s.g, A, tmaps(s, BY), tmaps(s, BY, wf ? wf : 32),
+    kern<<<grid, block, smem, s.stream>>>(s.g, A, tmaps(s, BY), tmaps(s, BY, wf ? wf : 32), po,
                                           cur * 12, nf * 12, zc, tiles_x, n_main,
                                           ctx->opts.reserved[5]);
   }
@@ -691,7 +750,7 @@ int launch_tblock2_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
 }
 
 template <int BY, int NG>
-int launch_tblock_table_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
+int launch_tblock_table_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches, const PeerOut& po) {
   if (!s.deep && (s.g.halo_lo || s.z1 < ctx->dims.nz))
     return fail(THIIM_ERR_CONFIG, "TBLOCK on a slab needs a deep-halo slab context");
   const Arrays A = s.arrays(s.cur, s.cur ^ 1);
@@ -710,6 +769,10 @@ int launch_tblock_table_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
                             (int)smem));
     CK(cudaFuncSetAttribute(k_tblock_table<BY, NG, true>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaFuncSetAttribute(k_tblock_table<BY, NG, false, true>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaFuncSetAttribute(k_tblock_table<BY, NG, true, true>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     setup_done(attr_set, s.device);
   }
   constexpr int TX2 = 28, TY2 = BY - 4;
@@ -717,24 +780,25 @@ int launch_tblock_table_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
   int zc = ctx->opts.z_chunk;
   if (zc <= 0) zc = tblock_zchunk(s, (long long)tiles_x * tiles_y);
   const dim3 grid(tiles_x * tiles_y, 1, (s.g.nz + zc - 1) / zc);
-  (s.cnt ? k_tblock_table<BY, NG, true> : k_tblock_table<BY, NG, false>)<<<grid, dim3(32, BY + 1), smem,
-                                                                          s.stream>>>(
-      s.g, A, T, tmaps(s, BY),
-                                                                     s.cur * 12, zc, tiles_x);
+  auto kern = s.deep ? (s.cnt ? k_tblock_table<BY, NG, true, true> : k_tblock_table<BY, NG, false, true>)
+                     : (s.cnt ? k_tblock_table<BY, NG, true> : k_tblock_table<BY, NG, false>);
+  kern<<<grid, dim3(32, BY + 1), smem, s.stream>>>(
+      s.g, A, T, tmaps(s, BY), po, s.cur * 12, zc, tiles_x);
   CK(cudaGetLastError());
   s.cur ^= 1;
   ++*launches;
   return THIIM_OK;
 }
 
-int launch_tblock2(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
+int launch_tblock2(thiim_gpu_ctx* ctx, Slab& s, long long* launches, const PeerOut& po) {
   CK(cudaSetDevice(s.device));
-  if (s.table) return launch_tblock_table_t<15, 5>(ctx, s, launches);
+  if (s.table) return launch_tblock_table_t<15, 5>(ctx, s, launches, po);
+  if (s.deep) return launch_tblock2_t<15, 6>(ctx, s, launches, po);
   switch (ctx->opts.tile_y) {  // CTA height incl. the 4 halo rows; ring depth fills the smem
-    case 16: return launch_tblock2_t<16, 5>(ctx, s, launches);
-    case 14: return launch_tblock2_t<14, 6>(ctx, s, launches);
-    case 12: return launch_tblock2_t<12, 7>(ctx, s, launches);
-    default: return launch_tblock2_t<15, 6>(ctx, s, launches);
+    case 16: return launch_tblock2_t<16, 5>(ctx, s, launches, po);
+    case 14: return launch_tblock2_t<14, 6>(ctx, s, launches, po);
+    case 12: return launch_tblock2_t<12, 7>(ctx, s, launches, po);
+    default: return launch_tblock2_t<15, 6>(ctx, s, launches, po);
   }
 }
 
@@ -981,6 +1045,7 @@ static int create_impl(const thiim_dims* dims, const thiim_gpu_opts* opts,
     }
     if (e == cudaSuccess) e = cudaEventCreate(&sl.ev0);
     if (e == cudaSuccess) e = cudaEventCreate(&sl.ev1);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&sl.ev_pass, cudaEventDisableTiming);
     if (e != cudaSuccess) {
       const std::string msg = std::string("device allocation of ") + std::to_string(bytes) +
                               " bytes failed: " + cudaGetErrorString(e);
@@ -1002,6 +1067,21 @@ static int create_impl(const thiim_dims* dims, const thiim_gpu_opts* opts,
           if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
         }
       }
+  }
+  // deep slabs write each other's halos from the kernel when every adjacent
+  // pair shares a device or has peer access (else copy exchange per pass)
+  if (n > 1 && ctx->slabs[0].deep) {
+    bool ok = true;
+    for (int k = 0; k + 1 < n; ++k) {
+      const int a = ctx->slabs[k].device, b = ctx->slabs[k + 1].device;
+      int ab = 0, ba = 0;
+      if (a != b) {
+        cudaDeviceCanAccessPeer(&ab, a, b);
+        cudaDeviceCanAccessPeer(&ba, b, a);
+        ok = ok && ab && ba;
+      }
+    }
+    ctx->peer_stores = ok && std::getenv("THIIM_NO_PEER_STORES") == nullptr;
   }
   *out = ctx;
   return THIIM_OK;
@@ -1106,6 +1186,7 @@ void thiim_gpu_destroy(thiim_gpu_ctx* ctx) {
     if (sl.tab) cudaFree(sl.tab);
     if (sl.ev0) cudaEventDestroy(sl.ev0);
     if (sl.ev1) cudaEventDestroy(sl.ev1);
+    if (sl.ev_pass) cudaEventDestroy(sl.ev_pass);
     if (sl.stream) cudaStreamDestroy(sl.stream);
   }
   delete ctx;
@@ -1317,11 +1398,15 @@ int thiim_gpu_init_generated(thiim_gpu_ctx* ctx, int kind, uint64_t seed) {
   return THIIM_OK;
 }
 
-static int coverage_pass(thiim_gpu_ctx* ctx) {
+// tblock_pass: deep slabs store their owned planes only (the extended planes
+// come from the neighbours), other passes every local interior plane
+static int coverage_pass(thiim_gpu_ctx* ctx, bool tblock_pass = false) {
   for (auto& sl : ctx->slabs) {
     CK(cudaSetDevice(sl.device));
+    const bool owned = tblock_pass && sl.deep;
+    const int r0 = owned ? sl.ext_lo : 0, r1 = owned ? sl.g.nz - sl.ext_hi : sl.g.nz;
     k_coverage<<<4 * sm_count(sl.device), 256, 0, sl.stream>>>(sl.g, sl.cnt, (long long)sl.stride,
-                                                               sl.cov_bad);
+                                                               r0, r1, sl.cov_bad);
     CK(cudaGetLastError());
   }
   ++ctx->cov_passes;
@@ -1390,16 +1475,26 @@ int thiim_gpu_step(thiim_gpu_ctx* ctx, int steps, thiim_gpu_stats* stats) {
     // deep slabs: a pass (2 steps, or 1 fused remainder step) leaves the owned
     // planes current and the extended + ghost planes stale; the exchange after
     // it refreshes them from the neighbours' owned planes
+    // with peer stores a pass writes the neighbours' halos itself: no
+    // exchange step, only stream-event ordering between adjacent slabs
+    const int ns = (int)ctx->slabs.size();
+    std::vector<PeerOut> po(ns);
     for (; n + 2 <= steps; n += 2) {
-      for (auto& sl : ctx->slabs)
-        if ((r = launch_tblock2(ctx, sl, &launches))) return r;
-      if (ctx->sanitize && (r = coverage_pass(ctx))) return r;
-      if (multi && (r = exchange_deep(ctx))) return r;
+      for (int k = 0; k < ns; ++k) po[k] = peer_out(ctx, k);
+      for (int k = 0; k < ns; ++k) {
+        if (ctx->peer_stores && (r = wait_neighbours(ctx, k))) return r;
+        if ((r = launch_tblock2(ctx, ctx->slabs[k], &launches, po[k]))) return r;
+        if (multi) CK(cudaEventRecord(ctx->slabs[k].ev_pass, ctx->slabs[k].stream));
+      }
+      if (ctx->sanitize && (r = coverage_pass(ctx, true))) return r;
+      if (multi && !ctx->peer_stores && (r = exchange_deep(ctx))) return r;
     }
     for (; n < steps; ++n) {
-      for (auto& sl : ctx->slabs)
-        if ((r = launch_fused(ctx, sl, &launches))) return r;
-      if (ctx->sanitize && (r = coverage_pass(ctx))) return r;
+      for (int k = 0; k < ns; ++k) {
+        if (ctx->peer_stores && (r = wait_neighbours(ctx, k))) return r;
+        if ((r = launch_fused(ctx, ctx->slabs[k], &launches))) return r;
+      }
+      if (ctx->sanitize && (r = coverage_pass(ctx, false))) return r;
       if (multi && (r = exchange_deep(ctx))) return r;
     }
   }

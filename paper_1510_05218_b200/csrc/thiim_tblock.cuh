@@ -576,10 +576,10 @@ struct TmSmem {
 // tile, stacked in y from yb0 -- the same sweep on narrow tiles, so a remainder
 // column of <= W-4 grid columns costs 32/W times fewer CTAs than full tiles
 // (256 = 9 x 28 + 4: the tenth tile column ran 24 nearly empty CTAs per chunk).
-template <int BY, int NG, bool COUNT, int W>
+template <int BY, int NG, bool COUNT, int W, bool DEEP>
 __device__ __forceinline__ void tblock_tm_body(TmSmem<BY, NG>& sm, const Grid& g, const Arrays& A,
-                                               const TmaMaps& maps, int fb, int cb, int zc, int xb,
-                                               int yb0, int pol_mode) {
+                                               const TmaMaps& maps, const PeerOut& po, int fb, int cb,
+                                               int zc, int xb, int yb0, int pol_mode) {
   constexpr int NCOMP = 32 * BY;
   constexpr int TY2 = BY - 4;
   constexpr int LAG = 1;
@@ -824,6 +824,24 @@ __device__ __forceinline__ void tblock_tm_body(TmSmem<BY, NG>& sm, const Grid& g
     const int r = q - LAG;
     if (r >= z0 - 1 && r < z1) {
       const long long i = g.idx(xs, ys, r);
+      // level-2 outputs: owned planes locally, boundary planes also into the
+      // neighbours' halos (multi-GPU contexts, peer memory)
+      const bool st_ok = r >= po.st0 && r < po.st1;
+      const bool lo_ok = po.lo[0] != nullptr && r >= po.lo_r0 && r < po.lo_r1;
+      const bool hi_ok = po.hi[0] != nullptr && r >= po.hi_r0 && r < po.hi_r1;
+      auto put = [&](int comp, const double2 v) {
+        if constexpr (!DEEP) {  // whole-z context: every plane, locally
+          st_hint(A.fo[comp] + i, v, first);
+          mark<COUNT>(A, comp, i);
+        } else {
+          if (st_ok) {
+            st_hint(A.fo[comp] + i, v, first);
+            mark<COUNT>(A, comp, i);
+          }
+          if (lo_ok) st_hint(po.lo[comp] + i + po.lo_shift, v, first);
+          if (hi_ok) st_hint(po.hi[comp] + i + po.hi_shift, v, first);
+        }
+      };
       const bool plane_ok = r >= 0;
       double2 nEx = nE2x, nEy = nE2y;
       if (q > q1) {  // plane r+1 is the top ghost plane: level 1 did not run
@@ -895,10 +913,7 @@ __device__ __forceinline__ void tblock_tm_body(TmSmem<BY, NG>& sm, const Grid& g
       }
       if (own2 && interior) {
 #pragma unroll
-        for (int k = 0; k < 6; ++k) {
-          st_hint(A.fo[HXY + k] + i, h[k], first);
-          mark<COUNT>(A, HXY + k, i);
-        }
+        for (int k = 0; k < 6; ++k) put(HXY + k, h[k]);
       }
       const double2 sHx = csum(h[0], h[1]), sHy = csum(h[2], h[3]), sHz = csum(h[4], h[5]);
       if (own2 || rx2 || ry2) {
@@ -913,10 +928,8 @@ __device__ __forceinline__ void tblock_tm_body(TmSmem<BY, NG>& sm, const Grid& g
         const double2 t0 = RD(0, BOX_E2), c0 = RD(1, BOX_E2), t1 = RD(2, BOX_E2), c1 = RD(3, BOX_E2);
         ring_release(R, rc, tx, ring_dep(c1, t1, c0, t0));
         if (ue) {
-          st_hint(A.fo[EXY] + i, upd(e1[EXY], t0, c0, sm.sH[2][ty - 1][tx], sHz), first);
-          mark<COUNT>(A, EXY, i);
-          st_hint(A.fo[EYX] + i, upd(e1[EYX], t1, c1, sm.sH[2][ty][tx - 1], sHz), first);
-          mark<COUNT>(A, EYX, i);
+          put(EXY, upd(e1[EXY], t0, c0, sm.sH[2][ty - 1][tx], sHz));
+          put(EYX, upd(e1[EYX], t1, c1, sm.sH[2][ty][tx - 1], sHz));
         }
       }
       {  // Exz
@@ -924,8 +937,7 @@ __device__ __forceinline__ void tblock_tm_body(TmSmem<BY, NG>& sm, const Grid& g
         const double2 t = RD(0, BOX_E2), c = RD(1, BOX_E2), s = RD(2, BOX_E2);
         ring_release(R, rc, tx, ring_dep(s, c, t));
         if (ue) {
-          st_hint(A.fo[EXZ] + i, upd_src(e1[EXZ], t, c, pH2y, sHy, s), first);
-          mark<COUNT>(A, EXZ, i);
+          put(EXZ, upd_src(e1[EXZ], t, c, pH2y, sHy, s));
         }
       }
       {  // Eyz
@@ -933,8 +945,7 @@ __device__ __forceinline__ void tblock_tm_body(TmSmem<BY, NG>& sm, const Grid& g
         const double2 t = RD(0, BOX_E2), c = RD(1, BOX_E2), s = RD(2, BOX_E2);
         ring_release(R, rc, tx, ring_dep(s, c, t));
         if (ue) {
-          st_hint(A.fo[EYZ] + i, upd_src(e1[EYZ], t, c, pH2x, sHx, s), first);
-          mark<COUNT>(A, EYZ, i);
+          put(EYZ, upd_src(e1[EYZ], t, c, pH2x, sHx, s));
         }
       }
       {  // Ezx, Ezy
@@ -942,10 +953,8 @@ __device__ __forceinline__ void tblock_tm_body(TmSmem<BY, NG>& sm, const Grid& g
         const double2 t0 = RD(0, BOX_E2), c0 = RD(1, BOX_E2), t1 = RD(2, BOX_E2), c1 = RD(3, BOX_E2);
         ring_release(R, rc, tx, ring_dep(c1, t1, c0, t0));
         if (ue) {
-          st_hint(A.fo[EZX] + i, upd(e1[EZX], t0, c0, sm.sH[1][ty][tx - 1], sHy), first);
-          mark<COUNT>(A, EZX, i);
-          st_hint(A.fo[EZY] + i, upd(e1[EZY], t1, c1, sm.sH[0][ty - 1][tx], sHx), first);
-          mark<COUNT>(A, EZY, i);
+          put(EZX, upd(e1[EZX], t0, c0, sm.sH[1][ty][tx - 1], sHy));
+          put(EZY, upd(e1[EZY], t1, c1, sm.sH[0][ty - 1][tx], sHx));
         }
       }
       pH2x = sHx;
@@ -961,20 +970,20 @@ __device__ __forceinline__ void tblock_tm_body(TmSmem<BY, NG>& sm, const Grid& g
 }
 
 
-template <int BY, int NG, bool COUNT = false, int WF = 0>
+template <int BY, int NG, bool COUNT = false, int WF = 0, bool DEEP = false>
 __global__ void __launch_bounds__(32 * (BY + 1), 1)
     k_tblock_tm(Grid g, Arrays A, const __grid_constant__ TmaMaps maps,
-                const __grid_constant__ TmaMaps maps_f, int fb, int cb, int zc, int tiles_x,
-                int n_main, int pol_mode) {
+                const __grid_constant__ TmaMaps maps_f, const __grid_constant__ PeerOut po, int fb,
+                int cb, int zc, int tiles_x, int n_main, int pol_mode) {
   constexpr int TX2 = 28, TY2 = BY - 4;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   TmSmem<BY, NG>& sm = *reinterpret_cast<TmSmem<BY, NG>*>(smem_raw);
   const int b = blockIdx.x;
   if (b < n_main) {  // full tiles, x-fastest
-    tblock_tm_body<BY, NG, COUNT, 32>(sm, g, A, maps, fb, cb, zc, (b % tiles_x) * TX2 - 2,
+    tblock_tm_body<BY, NG, COUNT, 32, DEEP>(sm, g, A, maps, po, fb, cb, zc, (b % tiles_x) * TX2 - 2,
                                       (b / tiles_x) * TY2 - 2, pol_mode);
   } else if constexpr (WF > 0) {  // folded remainder column: 32/WF y-tiles per CTA
-    tblock_tm_body<BY, NG, COUNT, WF>(sm, g, A, maps_f, fb, cb, zc, tiles_x * TX2 - 2,
+    tblock_tm_body<BY, NG, COUNT, WF, DEEP>(sm, g, A, maps_f, po, fb, cb, zc, tiles_x * TX2 - 2,
                                       (b - n_main) * (32 / WF) * TY2 - 2, pol_mode);
   }
 }

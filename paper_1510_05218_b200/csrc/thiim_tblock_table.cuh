@@ -34,10 +34,10 @@ struct TbTableSmem {
   uint32_t tmem_base;
 };
 
-template <int BY, int NG, bool COUNT = false>
+template <int BY, int NG, bool COUNT = false, bool DEEP = false>
 __global__ void __launch_bounds__(32 * (BY + 1), 1)
-    k_tblock_table(Grid g, Arrays A, TableGrid T, const __grid_constant__ TmaMaps maps, int fb,
-                   int zc, int tiles_x) {
+    k_tblock_table(Grid g, Arrays A, TableGrid T, const __grid_constant__ TmaMaps maps,
+                   const __grid_constant__ PeerOut po, int fb, int zc, int tiles_x) {
   constexpr int NCOMP = 32 * BY;
   constexpr int TX2 = 28, TY2 = BY - 4;
   constexpr int LAG = 1;
@@ -243,6 +243,24 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
     const int r = q - LAG;
     if (r >= z0 - 1 && r < z1) {
       const long long i = g.idx(xs, ys, r);
+      // level-2 outputs: owned planes locally, boundary planes also into the
+      // neighbours' halos (multi-GPU contexts, peer memory)
+      const bool st_ok = r >= po.st0 && r < po.st1;
+      const bool lo_ok = po.lo[0] != nullptr && r >= po.lo_r0 && r < po.lo_r1;
+      const bool hi_ok = po.hi[0] != nullptr && r >= po.hi_r0 && r < po.hi_r1;
+      auto put = [&](int comp, const double2 v) {
+        if constexpr (!DEEP) {  // whole-z context: every plane, locally
+          st_hint(A.fo[comp] + i, v, first);
+          mark<COUNT>(A, comp, i);
+        } else {
+          if (st_ok) {
+            st_hint(A.fo[comp] + i, v, first);
+            mark<COUNT>(A, comp, i);
+          }
+          if (lo_ok) st_hint(po.lo[comp] + i + po.lo_shift, v, first);
+          if (hi_ok) st_hint(po.hi[comp] + i + po.hi_shift, v, first);
+        }
+      };
       const bool plane_ok = r >= 0;
       const double2* C = sm.tab[mid2];
       double2 nEx = nE2x, nEy = nE2y;
@@ -296,10 +314,7 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
       }
       if (own2 && interior) {
 #pragma unroll
-        for (int k = 0; k < 6; ++k) {
-          st_hint(A.fo[HXY + k] + i, h[k], first);
-          mark<COUNT>(A, HXY + k, i);
-        }
+        for (int k = 0; k < 6; ++k) put(HXY + k, h[k]);
       }
       const double2 sHx = csum(h[0], h[1]), sHy = csum(h[2], h[3]), sHz = csum(h[4], h[5]);
       if (own2 || rx2 || ry2) {
@@ -309,16 +324,12 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
       }
       named_sync(1, NCOMP);
       if (own2 && interior) {
-        st_hint(A.fo[EXY] + i, upd(e1[EXY], C[EXY], C[12 + EXY], sm.sH[2][ty - 1][tx], sHz), first);
-        st_hint(A.fo[EXZ] + i, upd_src(e1[EXZ], C[EXZ], C[12 + EXZ], pH2y, sHy, C[24 + SRC_EXZ]),
-                first);
-        st_hint(A.fo[EYX] + i, upd(e1[EYX], C[EYX], C[12 + EYX], sm.sH[2][ty][tx - 1], sHz), first);
-        st_hint(A.fo[EYZ] + i, upd_src(e1[EYZ], C[EYZ], C[12 + EYZ], pH2x, sHx, C[24 + SRC_EYZ]),
-                first);
-        st_hint(A.fo[EZX] + i, upd(e1[EZX], C[EZX], C[12 + EZX], sm.sH[1][ty][tx - 1], sHy), first);
-        st_hint(A.fo[EZY] + i, upd(e1[EZY], C[EZY], C[12 + EZY], sm.sH[0][ty - 1][tx], sHx), first);
-#pragma unroll
-        for (int k = EXY; k <= EZY; ++k) mark<COUNT>(A, k, i);
+        put(EXY, upd(e1[EXY], C[EXY], C[12 + EXY], sm.sH[2][ty - 1][tx], sHz));
+        put(EXZ, upd_src(e1[EXZ], C[EXZ], C[12 + EXZ], pH2y, sHy, C[24 + SRC_EXZ]));
+        put(EYX, upd(e1[EYX], C[EYX], C[12 + EYX], sm.sH[2][ty][tx - 1], sHz));
+        put(EYZ, upd_src(e1[EYZ], C[EYZ], C[12 + EYZ], pH2x, sHx, C[24 + SRC_EYZ]));
+        put(EZX, upd(e1[EZX], C[EZX], C[12 + EZX], sm.sH[1][ty][tx - 1], sHy));
+        put(EZY, upd(e1[EZY], C[EZY], C[12 + EZY], sm.sH[0][ty - 1][tx], sHx));
       }
       pH2x = sHx;
       pH2y = sHy;
