@@ -101,6 +101,15 @@ class Clocks:
             out = ""
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        post = False
+        if not out.strip():  # timed region shorter than the sampler's first tick
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.Q,
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=30).stdout
+                post = True
+            except Exception:
+                out = ""
         for line in out.strip().splitlines():
             f = [x.strip() for x in line.split(",")]
             if len(f) < 9:
@@ -115,7 +124,9 @@ class Clocks:
                     reasons.add(n)
         if sm:
             self.result = {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx,
-                           "reasons": sorted(reasons), "samples": len(sm)}
+                           "reasons": sorted(reasons), "samples": 0 if post else len(sm)}
+            if post:
+                self.result["note"] = "timed region shorter than one sampling tick: post-run sample"
 
 
 def cpu_threads():
