@@ -1,35 +1,27 @@
 // thiim_tblock.cuh -- engine TBLOCK: two THIIM steps per HBM pass.
 //
 // The paper's idea (wavefront temporal blocking, arXiv 1510.05218 s II)
-// re-derived for B200.  Its "shared cache" (the L3 holding a diamond tile's
-// working set) becomes the L2: 640 B of state per cell is far too much for
-// registers + shared memory to hold a second time level of a useful tile, but
-// a couple of planes of it fit in L2.
-//
-// One CTA owns an x-y tile and streams z.  Per iteration q it runs
+// re-derived for B200.  One CTA owns an x-y tile and streams z.  Per iteration
+// q it runs
 //   level 1 at plane q   (step n):   the fused plane sweep over the tile grown by
-//                                    one cell per side; E^1/H^1 go to a per-SM
-//                                    SCRATCH ring of 2 planes in global memory
-//                                    (~28 MB for 148 SMs, L2-resident, stored
-//                                    with an evict_last policy);
-//   level 2 at plane q-1 (step n+1): the same sweep; its F / E / H operands come
-//                                    back from scratch by TMA, the coefficients
-//                                    by TMA again (fetched by level 1 one plane
-//                                    earlier and kept in L2 with evict_last),
-//                                    outputs go to the ping-pong field set.
-// Level 2 needs E^1 one plane above its own only at its own cell, which the
-// same thread computed in this iteration's level 1, so that comes from
-// registers; everything else it reads was written in the previous iteration
-// and the producer only waits on a per-slot `ready` mbarrier that level-1
-// writers arrive on after fence.proxy.async.global.
+//                                    one cell per side (28 x (BY-4) output tile
+//                                    + two rings in the 32 x BY thread tile);
+//   level 2 at plane q-1 (step n+1): the same sweep on the output tile, which
+//                                    writes the ping-pong field set.
+// Halo cells are recomputed redundantly by neighbouring CTAs (bitwise
+// identical); chunk starts recompute one level-1 plane and one level-2 H plane
+// below.  DRAM traffic: 832 / 2 = 416 B/LUP plus tile-overlap re-fetch.
 //
-// Halo: level 2 owns the 28 x (BY-4) centre of the 32 x BY thread tile; level 1
-// computes the 30 x (BY-2) ring around it (redundant with the neighbours,
-// bitwise identical); the outermost ring recomputes H for the E sums.  Chunk
-// starts recompute one level-1 plane and one level-2 H plane below.
-//
-// DRAM traffic per LUP: 832/2 = 416 B + tile-overlap re-fetch + whatever the
-// L2 fails to keep; L2->SM traffic rises (coefficients twice, scratch).
+// Two kernels:
+//   k_tblock_tm (default): the level-1 -> level-2 hand-off (E^1 / H^1 of plane
+//     q-1, computed by the same thread) lives in the thread's TMEM lane; a
+//     remainder tile column of <= 12 grid columns runs as folded CTAs of 8- or
+//     16-lane segments; deep-halo slabs of multi-GPU contexts write their
+//     neighbours' halo planes directly (peer stores).  See the comments at
+//     k_tblock_tm and DESIGN.md "Temporal blocking".
+//   k_tblock2 (A/B only, `variant = 2`): the predecessor -- the hand-off through
+//     a per-SM scratch ring in global memory (L2-resident, evict_last stores,
+//     re-fetched by TMA behind a `ready` barrier); 5.4 vs 11.0 GLUP/s at 256^3.
 #pragma once
 
 #include <cuda.h>
