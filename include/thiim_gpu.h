@@ -148,6 +148,21 @@ typedef struct {
 void thiim_scheme_default(thiim_scheme* sp); /* omega 0.4, tau 1, delta 1, sources 1+0i */
 int thiim_gpu_init_benchmark(thiim_gpu_ctx* ctx, const thiim_scheme* sp);
 
+/* build_problem_from_voxels (coefficients.cpp:112-141) on the device: `materials`
+ * holds nx*ny*nz records of 5 doubles (eps_re, eps_im, mu, sigma, sigma_star),
+ * x fastest -- the reference's voxel-map layout; 40 B/cell cross PCIe instead of
+ * the 448 B/cell of coefficients.  The per-cell closed forms run on the GPU
+ * with the host build's complex arithmetic (libgcc's division restated), so the
+ * coefficients are bitwise the reference's.  Fields zero, source on plane nz/4.
+ * Errors: CONFIG (parameters, table layout), SETUP with the reference's message
+ * ("mu must be nonzero", "eps must be nonzero", "vanishing update denominator
+ * ... at cell (x,y,z) component C") for the first failing (component, cell). */
+int thiim_gpu_init_materials(thiim_gpu_ctx* ctx, const thiim_scheme* sp, const double* materials);
+
+/* Verification entry: n complex divisions (a+ib)/(c+id), in = {a,b,c,d}[n],
+ * out = {re,im}[n], with the device restatement of libgcc's __divdc3. */
+int thiim_gpu_selftest_cdiv(int n, const double* in, double* out);
+
 /* Advances `steps` THIIM iterations (== steps x step_reference).  Blocking.
  * steps < 0 -> THIIM_ERR_CONFIG (run_naive, reference_engines.cpp:35). */
 int thiim_gpu_step(thiim_gpu_ctx* ctx, int steps, thiim_gpu_stats* stats);

@@ -221,6 +221,25 @@ def ref_benchmark_problem(dims, omega=0.4, tau=1.0, delta=1.0):
     return arrays
 
 
+def ref_problem_from_voxels(dims, path, omega=0.4, tau=1.0, delta=1.0):
+    """reference build_problem_from_voxels (coefficients.cpp:112-141) of a voxel file."""
+    arrays = new_arrays(dims)
+    nx, ny, nz = dims
+    _ref_check(ref_lib().ref_build_problem_from_voxels(
+        nx, ny, nz, ctypes.c_double(omega), ctypes.c_double(tau), ctypes.c_double(delta),
+        str(path).encode(), _ptrs(arrays)))
+    return arrays
+
+
+def c_cdiv(operands):
+    """host C99 complex division (libgcc __divdc3) of (n, 4) operands -> (n, 2)."""
+    import numpy as np
+    a = np.ascontiguousarray(operands, dtype=np.float64).reshape(-1, 4)
+    out = np.zeros((a.shape[0], 2), dtype=np.float64)
+    c_lib().orc_cdiv_batch(a.shape[0], ctypes.c_void_p(a.ctypes.data), ctypes.c_void_p(out.ctypes.data))
+    return out
+
+
 def ref_derive(material, omega, tau, delta, family, back):
     out = (ctypes.c_double * 6)()
     d = [ctypes.c_double(v) for v in material]

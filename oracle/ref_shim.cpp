@@ -91,6 +91,19 @@ int ref_build_benchmark_problem(int nx, int ny, int nz, double omega, double tau
   });
 }
 
+// build_problem_from_voxels (coefficients.cpp:112-141) on a voxel-map file.
+int ref_build_problem_from_voxels(int nx, int ny, int nz, double omega, double tau, double delta,
+                                  const char* path, double* const* arrays) {
+  return guarded([&] {
+    SchemeParams sp;
+    sp.omega = omega;
+    sp.tau = tau;
+    sp.delta = delta;
+    ProblemState s = build_problem_from_voxels(GridDims(nx, ny, nz), sp, path);
+    export_all(s, arrays);
+  });
+}
+
 // derive_coefficients (coefficients.cpp:25-55); out = {t.re,t.im,c.re,c.im,src.re,src.im}.
 int ref_derive_coefficients(double eps_re, double eps_im, double mu, double sigma,
                             double sigma_star, double omega, double tau, double delta,

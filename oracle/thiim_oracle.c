@@ -230,6 +230,16 @@ int orc_derive_coefficients(const orc_material* m, const orc_scheme* sp, int fam
   return 0;
 }
 
+/* n complex divisions with the host compiler's C99 complex division (libgcc
+ * __divdc3, as std::complex<double> in the reference): in = {a,b,c,d}[n]. */
+void orc_cdiv_batch(int n, const double* in, double* out) {
+  for (int i = 0; i < n; ++i) {
+    const double complex q = mkc(in[4 * i], in[4 * i + 1]) / mkc(in[4 * i + 2], in[4 * i + 3]);
+    out[2 * i] = creal(q);
+    out[2 * i + 1] = cimag(q);
+  }
+}
+
 /* fill_coefficients, coefficients.cpp:57-92, homogeneous material. */
 int orc_fill_coefficients_uniform(orc_state* s, const orc_scheme* sp, const orc_material* m) {
   for (int ci = 0; ci < 12; ++ci) {

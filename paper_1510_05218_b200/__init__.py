@@ -300,6 +300,7 @@ EXPORTED_SYMBOLS = [
     "thiim_gpu_upload_planes", "thiim_gpu_download_fields_planes", "thiim_generate_host_planes",
     "thiim_gpu_upload_table", "thiim_gpu_download_table", "thiim_gpu_set_sanitize",
     "thiim_gpu_coverage", "thiim_scheme_default", "thiim_gpu_init_benchmark",
+    "thiim_gpu_init_materials", "thiim_gpu_selftest_cdiv",
 ]
 
 _LIB = None
@@ -338,6 +339,8 @@ def lib() -> ctypes.CDLL:
     L.thiim_gpu_set_sanitize.argtypes = [P, ctypes.c_int]
     L.thiim_scheme_default.argtypes = [ctypes.POINTER(_Scheme)]
     L.thiim_gpu_init_benchmark.argtypes = [P, ctypes.POINTER(_Scheme)]
+    L.thiim_gpu_init_materials.argtypes = [P, ctypes.POINTER(_Scheme), P]
+    L.thiim_gpu_selftest_cdiv.argtypes = [ctypes.c_int, P, P]
     L.thiim_gpu_coverage.argtypes = [P, ctypes.POINTER(ctypes.c_ulonglong),
                                      ctypes.POINTER(ctypes.c_ulonglong)]
     if L.thiim_gpu_abi_version() != 1:
@@ -367,6 +370,15 @@ COEFF_FULL = 0
 COEFF_TABLE = 1
 ENGINE_AUTO, ENGINE_SPLIT, ENGINE_FUSED, ENGINE_TBLOCK = 0, 1, 2, 3
 ENGINE_NAMES = {ENGINE_SPLIT: "gpu-split", ENGINE_FUSED: "gpu-fused", ENGINE_TBLOCK: "gpu-tblock"}
+
+
+def selftest_cdiv(operands: np.ndarray) -> np.ndarray:
+    """Device complex division (libgcc __divdc3 restated) of operands (n, 4) =
+    a, b, c, d -> (n, 2) = (a+ib)/(c+id); verification entry."""
+    a = np.ascontiguousarray(operands, dtype=np.float64).reshape(-1, 4)
+    out = np.zeros((a.shape[0], 2), dtype=np.float64)
+    _check(lib().thiim_gpu_selftest_cdiv(a.shape[0], a.ctypes.data, out.ctypes.data))
+    return out
 
 
 def balance_model(engine: int, time_block: int = 0) -> float:
@@ -481,6 +493,18 @@ class GpuEngine:
         sp = _Scheme(omega, tau, delta, source_e.real, source_e.imag, source_h.real,
                      source_h.imag)
         _check(lib().thiim_gpu_init_benchmark(self._ctx, ctypes.byref(sp)))
+
+    def init_materials(self, materials: np.ndarray, omega: float = 0.4, tau: float = 1.0,
+                       delta: float = 1.0, source_e: complex = 1.0 + 0j,
+                       source_h: complex = 1.0 + 0j) -> None:
+        """build_problem_from_voxels (coefficients.cpp:112-141) on the device;
+        `materials`: (nz, ny, nx, 5) float64 = eps re/im, mu, sigma, sigma*."""
+        m = np.ascontiguousarray(materials, dtype=np.float64)
+        if m.size != self.dims.interior_cells() * 5:
+            raise ConfigError("material map must hold nx*ny*nz records of 5 doubles")
+        sp = _Scheme(omega, tau, delta, source_e.real, source_e.imag, source_h.real,
+                     source_h.imag)
+        _check(lib().thiim_gpu_init_materials(self._ctx, ctypes.byref(sp), m.ctypes.data))
 
     def step(self, steps: int) -> _Stats:
         st = _Stats()

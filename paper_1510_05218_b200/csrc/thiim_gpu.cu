@@ -24,6 +24,7 @@
 
 #include "../../include/thiim_gpu.h"
 #include "thiim_common.cuh"
+#include "thiim_complex.cuh"
 #include "thiim_fused.cuh"
 #include "thiim_fused_table.cuh"
 #include "thiim_fused_tma.cuh"
@@ -214,6 +215,103 @@ __global__ void k_init_benchmark_table(Grid g, int z_global0, int nz_global, Arr
     for (int a = 0; a < 12; ++a) A.f[a][p] = make_double2(0.0, 0.0);
     mat[(long long)zp * mplane + (long long)yp * mp + xp] =
         interior ? (uint8_t)(z == zsrc ? 2 : 1) : (uint8_t)0;
+  }
+}
+
+// build_problem_from_voxels (coefficients.cpp:112-141) on the device: the 28
+// coefficients of every interior cell from its material record (eps re/im, mu,
+// sigma, sigma*; x fastest), derive_coefficients (coefficients.cpp:25-55) per
+// family and iteration mode with the host build's complex arithmetic
+// (thiim_complex.cuh), fill_coefficients' sign folding (:63-66); fields zero,
+// ghosts zero, sources on the injection plane only.  The first failing
+// (component, z, y, x) in the reference's loop order is kept as
+// key = ((comp * ncells + cell) << 3) | code (atomicMin; code 1 mu, 2 eps,
+// 3 / 4 vanishing denominator in forward / back mode).
+struct SchemeDev {
+  double tau, delta;
+  dcx ep_h, em_h, em_1, ep_1;  // expi(+wt/2), expi(-wt/2), expi(-wt), expi(+wt)
+  dcx src_e, src_h;
+  int zsrc;
+};
+__global__ void k_init_materials(Grid g, int z_global0, int nz_global, Arrays A,
+                                 const double* __restrict__ mats, int z_mat0, SchemeDev sp,
+                                 unsigned long long* err) {
+  static constexpr double kCurl[12] = {+1, -1, -1, +1, +1, -1, -1, +1, +1, -1, -1, +1};
+  const long long n = (long long)(g.nz + 2) * g.pxy;
+  const unsigned long long ncells = (unsigned long long)g.nx * g.ny * nz_global;
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n;
+       p += (long long)gridDim.x * blockDim.x) {
+    const int zp = (int)(p / g.pxy);
+    const long long rr = p - (long long)zp * g.pxy;
+    const int yp = (int)(rr / g.px);
+    const int xp = (int)(rr - (long long)yp * g.px);
+    const int x = xp - 1, y = yp - 1, z = z_global0 + zp - 1;
+    const bool interior = x >= 0 && x < g.nx && y >= 0 && y < g.ny && z >= 0 && z < nz_global;
+    const double2 zero = make_double2(0.0, 0.0);
+    for (int a = 0; a < 12; ++a) A.f[a][p] = zero;
+    if (!interior) {
+      for (int k = 0; k < 12; ++k) {
+        const_cast<double2*>(A.t[k])[p] = zero;
+        const_cast<double2*>(A.c[k])[p] = zero;
+      }
+      for (int k = 0; k < 4; ++k) const_cast<double2*>(A.src[k])[p] = zero;
+      continue;
+    }
+    const double* m = mats + (((long long)(z - z_mat0) * g.ny + y) * g.nx + x) * 5;
+    const dcx eps = cx(m[0], m[1]);
+    const double mu = m[2], sigma = m[3], sigma_star = m[4];
+    const unsigned long long cell = ((unsigned long long)z * g.ny + y) * g.nx + x;
+    auto fail_at = [&](int comp, unsigned code) {
+      atomicMin(err, (((unsigned long long)comp * ncells + cell) << 3) | code);
+    };
+    // per-cell checks of fill_coefficients (:70-72), first component first
+    if (mu == 0.0) { fail_at(0, 1); continue; }
+    if (eps.re == 0.0 && eps.im == 0.0) { fail_at(0, 2); continue; }
+    // H family (:29-36)
+    const dcx den_h = cadd(sp.ep_h, cx(sp.tau * sigma_star / mu, 0.0));
+    const bool bad_h = den_h.re == 0.0 && den_h.im == 0.0;
+    const dcx t_h = cdiv(sp.em_h, den_h);
+    const dcx c_h = cdiv(cx(sp.tau / (mu * sp.delta), 0.0), den_h);
+    const dcx s_h = cdiv(cscale(sp.tau, sp.src_h), den_h);
+    // E family: forward (:37-45) or back (:46-53) by select_mode (coefficients.hpp:50-53)
+    dcx t_e, c_e, s_e;
+    bool bad_e;
+    const dcx ed = cscale(sp.delta, eps);  // eps * delta
+    if (!(eps.re < 0.0)) {
+      const dcx den = cadd(cx(1.0, 0.0), cdiv(cx(sp.tau * sigma, 0.0), eps));
+      bad_e = den.re == 0.0 && den.im == 0.0;
+      t_e = cdiv(sp.em_1, den);
+      c_e = cdiv(cmul(cdiv(cx(sp.tau, 0.0), ed), sp.em_h), den);
+      s_e = cdiv(cmul(cscale(sp.tau, sp.em_1), sp.src_e), den);
+    } else {
+      const dcx den = csub(cx(1.0 / sp.tau, 0.0), cdiv(cx(sigma, 0.0), eps));
+      bad_e = den.re == 0.0 && den.im == 0.0;
+      t_e = cdiv(sp.ep_1, cscale(sp.tau, den));
+      c_e = cdiv(cmul(cneg(cdiv(cx(1.0, 0.0), ed)), sp.ep_h), den);
+      s_e = cdiv(cneg(sp.src_e), den);
+    }
+    if (bad_e) fail_at(EXY, eps.re < 0.0 ? 4 : 3);  // E components come first in the table
+    if (bad_h) fail_at(HXY, 3);                     // H: always forward
+    for (int k = 0; k < 12; ++k) {
+      const bool e = k < HXY;
+      const double sign = (e ? -1.0 : 1.0) * kCurl[k];
+      const dcx t = e ? t_e : t_h, c = cscale(sign, e ? c_e : c_h);
+      const_cast<double2*>(A.t[k])[p] = make_double2(t.re, t.im);
+      const_cast<double2*>(A.c[k])[p] = make_double2(c.re, c.im);
+    }
+    const bool on = z == sp.zsrc;
+    const_cast<double2*>(A.src[SRC_EXZ])[p] = on ? make_double2(s_e.re, s_e.im) : zero;
+    const_cast<double2*>(A.src[SRC_EYZ])[p] = on ? make_double2(s_e.re, s_e.im) : zero;
+    const_cast<double2*>(A.src[SRC_HXZ])[p] = on ? make_double2(s_h.re, s_h.im) : zero;
+    const_cast<double2*>(A.src[SRC_HYZ])[p] = on ? make_double2(s_h.re, s_h.im) : zero;
+  }
+}
+
+__global__ void k_selftest_cdiv(int n, const double* in, double* out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const dcx q = cdiv(cx(in[4 * i], in[4 * i + 1]), cx(in[4 * i + 2], in[4 * i + 3]));
+    out[2 * i] = q.re;
+    out[2 * i + 1] = q.im;
   }
 }
 
@@ -1341,6 +1439,96 @@ int thiim_gpu_init_benchmark(thiim_gpu_ctx* ctx, const thiim_scheme* spp) {
     sl.cur = 0;
   }
   ctx->loaded = true;
+  return THIIM_OK;
+}
+
+int thiim_gpu_init_materials(thiim_gpu_ctx* ctx, const thiim_scheme* spp, const double* materials) {
+  g_err.clear();
+  if (!ctx || !materials) return fail(THIIM_ERR_CONFIG, "null argument");
+  thiim_scheme sp;
+  thiim_scheme_default(&sp);
+  if (spp) sp = *spp;
+  if (!(sp.tau > 0.0)) return fail(THIIM_ERR_CONFIG, "tau must be > 0");
+  if (!(sp.delta > 0.0)) return fail(THIIM_ERR_CONFIG, "delta must be > 0");
+  if (!(sp.omega * sp.tau <= 3.14159265358979323846 + 1e-12))
+    return fail(THIIM_ERR_CONFIG, "omega*tau must be <= pi");
+  if (ctx->slabs[0].table)
+    return fail(THIIM_ERR_CONFIG, "material maps fill the full coefficient layout");
+  const double wt = sp.omega * sp.tau;  // expi with the host's libm, as the reference
+  SchemeDev sd;
+  sd.tau = sp.tau;
+  sd.delta = sp.delta;
+  sd.ep_h = dcx{std::cos(wt / 2.0), std::sin(wt / 2.0)};
+  sd.em_h = dcx{std::cos(-wt / 2.0), std::sin(-wt / 2.0)};
+  sd.em_1 = dcx{std::cos(-wt), std::sin(-wt)};
+  sd.ep_1 = dcx{std::cos(wt), std::sin(wt)};
+  sd.src_e = dcx{sp.source_e.re, sp.source_e.im};
+  sd.src_h = dcx{sp.source_h.re, sp.source_h.im};
+  sd.zsrc = ctx->dims.nz / 4;  // source_plane_z, coefficients.hpp:70
+  const size_t plane = (size_t)ctx->dims.nx * ctx->dims.ny * 5;
+  unsigned long long worst = ~0ull;
+  for (auto& sl : ctx->slabs) {
+    CK(cudaSetDevice(sl.device));
+    // the map planes the slab holds: its interior plus halo planes inside the grid
+    const int m0 = std::max(sl.z0 - 1, 0), m1 = std::min(sl.z1 + 1, ctx->dims.nz);
+    double* dm = nullptr;
+    unsigned long long* derr = nullptr;
+    CK(cudaMallocAsync(&dm, std::max<size_t>(1, (size_t)(m1 - m0) * plane) * sizeof(double), sl.stream));
+    CK(cudaMallocAsync(&derr, sizeof(unsigned long long), sl.stream));
+    CK(cudaMemcpyAsync(dm, materials + (size_t)m0 * plane, (size_t)(m1 - m0) * plane * sizeof(double),
+                       cudaMemcpyHostToDevice, sl.stream));
+    CK(cudaMemsetAsync(derr, 0xff, sizeof(unsigned long long), sl.stream));
+    Arrays A = sl.arrays(0, 0);
+    k_init_materials<<<8 * sm_count(sl.device), 256, 0, sl.stream>>>(sl.g, sl.z0, ctx->dims.nz, A, dm,
+                                                                    m0, sd, derr);
+    CK(cudaGetLastError());
+    for (int set = 1; set < sl.nfield_sets; ++set)
+      for (int k = 0; k < 12; ++k)
+        CK(cudaMemsetAsync(sl.field(set, k), 0, sl.stride * sizeof(double2), sl.stream));
+    unsigned long long e = ~0ull;
+    CK(cudaMemcpyAsync(&e, derr, sizeof(e), cudaMemcpyDeviceToHost, sl.stream));
+    CK(cudaFreeAsync(dm, sl.stream));
+    CK(cudaFreeAsync(derr, sl.stream));
+    CK(cudaStreamSynchronize(sl.stream));
+    worst = std::min(worst, e);
+    sl.cur = 0;
+  }
+  if (worst != ~0ull) {  // the reference's SetupError text (coefficients.cpp:14-21, 70-84)
+    static const char* names[12] = {"Exy", "Exz", "Eyx", "Eyz", "Ezx", "Ezy",
+                                    "Hxy", "Hxz", "Hyx", "Hyz", "Hzx", "Hzy"};
+    const unsigned code = (unsigned)(worst & 7);
+    const unsigned long long ncells = (unsigned long long)ctx->dims.nx * ctx->dims.ny * ctx->dims.nz;
+    const unsigned long long key = worst >> 3;
+    const int comp = (int)(key / ncells);
+    const unsigned long long cell = key % ncells;
+    const int x = (int)(cell % ctx->dims.nx), y = (int)(cell / ctx->dims.nx % ctx->dims.ny),
+              z = (int)(cell / ((unsigned long long)ctx->dims.nx * ctx->dims.ny));
+    ctx->loaded = false;
+    if (code == 1) return fail(THIIM_ERR_SETUP, "mu must be nonzero");
+    if (code == 2) return fail(THIIM_ERR_SETUP, "eps must be nonzero");
+    char where[96];
+    std::snprintf(where, sizeof where, " at cell (%d,%d,%d) component %s", x, y, z, names[comp]);
+    return fail(THIIM_ERR_SETUP, std::string("vanishing update denominator (") +
+                                     (comp < HXY ? "E" : "H") + (code == 4 ? ", back" : ", forward") +
+                                     "): resonant sigma/tau combination" + where);
+  }
+  ctx->loaded = true;
+  return THIIM_OK;
+}
+
+int thiim_gpu_selftest_cdiv(int n, const double* in, double* out) {
+  g_err.clear();
+  if (n < 0 || (n && (!in || !out))) return fail(THIIM_ERR_CONFIG, "bad arguments");
+  if (n == 0) return THIIM_OK;
+  double *din = nullptr, *dout = nullptr;
+  CK(cudaMalloc(&din, (size_t)n * 4 * sizeof(double)));
+  CK(cudaMalloc(&dout, (size_t)n * 2 * sizeof(double)));
+  CK(cudaMemcpy(din, in, (size_t)n * 4 * sizeof(double), cudaMemcpyHostToDevice));
+  k_selftest_cdiv<<<256, 256>>>(n, din, dout);
+  CK(cudaGetLastError());
+  CK(cudaMemcpy(out, dout, (size_t)n * 2 * sizeof(double), cudaMemcpyDeviceToHost));
+  cudaFree(din);
+  cudaFree(dout);
   return THIIM_OK;
 }
 

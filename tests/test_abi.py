@@ -45,7 +45,17 @@ def test_library_is_sm100a_cubin():
     assert "sm_100a" in out
     sass = subprocess.run(["cuobjdump", "-sass", P.LIB_PATH], capture_output=True, text=True).stdout
     assert "UTMALDG" in sass, "TMA tensor loads expected in the fused sweep"
-    assert "DFMA" not in sass, "-fmad=false: no contracted FP64 multiply-add may appear"
+    # -fmad=false: no contracted FP64 multiply-add in any stencil / setup kernel.  Only
+    # the kernels that divide (IEEE division is an FMA-refined sequence, still correctly
+    # rounded -- test_gpu_materials.py pins them bitwise against libgcc) contain DFMA.
+    fn, with_fma = None, set()
+    for line in sass.splitlines():
+        if "Function :" in line:
+            fn = line.split("Function :")[1].strip()
+        elif "DFMA" in line:
+            with_fma.add(fn)
+    divides = ("k_init_materials", "k_selftest_cdiv")
+    assert with_fma and all(any(d in f for d in divides) for f in with_fma), sorted(with_fma)
 
 
 def test_abi_version_and_models():
