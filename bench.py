@@ -378,9 +378,18 @@ def run_native_multi(P, args, opts, iters, world, rank, local):
     dist.init_process_group(backend)
     gdims = P.GridDims(GRID[0], GRID[1], GRID[2] * world)
     z0, z1 = D.slab_bounds(gdims.nz, world, rank)
-    eng = D.SlabGpuEngine(gdims, z0, z1, opts)
-    eng.generate(P.GEN_RANDOM, SEED)
     ex = D.HaloExchanger(rank, world)
+    # THIIM_PEER_STORES=0: exchange halos with torch.distributed after every pass
+    want_peer = os.environ.get("THIIM_PEER_STORES", "1") != "0"
+
+    def make_engine():
+        e = D.SlabGpuEngine(gdims, z0, z1, opts)
+        if want_peer:
+            e.enable_peer_stores(rank, world)
+        return e
+
+    eng = make_engine()
+    eng.generate(P.GEN_RANDOM, SEED)
     for _ in range(args.warmup):
         D.run_distributed(eng, iters, ex)
 
@@ -405,12 +414,12 @@ def run_native_multi(P, args, opts, iters, world, rank, local):
                                          for _ in range(args.steps)])
     launches = sum(s["kernel_launches"] for s in stats)
     halo = sum(s["halo_bytes_sent"] for s in stats)
-    engine_ran, period = eng.engine, eng.exchange_period
+    engine_ran, period, peer = eng.engine, eng.exchange_period, eng.peer_stores
     eng.close()
 
     e2e = None
     if not args.no_e2e:
-        eng = D.SlabGpuEngine(gdims, z0, z1, opts)
+        eng = make_engine()
         host = eng.local_host_problem(P.GEN_RANDOM, SEED)
         for a in host:
             P.lib().thiim_gpu_pin_host(a.ctypes.data, a.nbytes)
@@ -427,7 +436,7 @@ def run_native_multi(P, args, opts, iters, world, rank, local):
         e2e = world * 256 ** 3 * iters * args.steps / e2e_run_secs / 1e6
     if args.check:
         # decomposed run vs one oracle run of the global grid, gathered on rank 0
-        eng = D.SlabGpuEngine(gdims, z0, z1, opts)
+        eng = make_engine()
         host = eng.local_host_problem(KIND, SEED)
         eng.upload_local(host)
         D.run_distributed(eng, args.check, ex)
@@ -449,7 +458,10 @@ def run_native_multi(P, args, opts, iters, world, rank, local):
     line = _line(P, args, world, P.GridDims(*GRID), engine_ran, dev_secs, launches, e2e, clk,
                  {"global_grid": [gdims.nx, gdims.ny, gdims.nz],
                   "halo_bytes_per_rank_per_step": halo // max(1, args.steps),
-                  "exchange": "torch.distributed %s batch_isend_irecv after every %d-step pass"
+                  "exchange": ("peer stores into the neighbours' halos from the kernel "
+                               "(CUDA IPC over NVLink), a barrier per %d-step pass" % period)
+                              if peer else
+                              "torch.distributed %s batch_isend_irecv after every %d-step pass"
                               % (backend, period)})
     dist.destroy_process_group()
     return line if rank == 0 else None

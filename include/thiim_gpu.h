@@ -253,6 +253,27 @@ typedef struct {
 } thiim_slab_info;
 int thiim_gpu_slab_info(thiim_gpu_ctx* ctx, thiim_slab_info* info);
 
+/* Multi-process peer stores (ranks on one node, NVLink / NVSwitch): each rank
+ * exports its slab (CUDA IPC handle + layout), imports its neighbours' exports,
+ * and from then on every TBLOCK pass stores its boundary planes straight into
+ * the neighbours' halo planes -- no halo exchange after 2-step passes.  The
+ * caller orders passes across processes: thiim_gpu_step(ctx, k <= 2), then a
+ * barrier of all ranks (covers both the halo writes and the neighbours' reads
+ * of halos the next pass overwrites).  Odd remainder steps (k = 1) still need
+ * the view exchange.  TBLOCK deep-halo slab contexts only. */
+typedef struct {
+  unsigned char ipc[64]; /* cudaIpcMemHandle_t of the slab state */
+  long long stride;      /* elements per array */
+  int nz_local, ext_lo, ext_hi, nfield_sets, device;
+  int px;
+  long long pxy;
+} thiim_slab_export;
+enum { THIIM_PEER_LOWER = 0, THIIM_PEER_UPPER = 1 };
+int thiim_gpu_slab_export(thiim_gpu_ctx* ctx, thiim_slab_export* out);
+int thiim_gpu_slab_import(thiim_gpu_ctx* ctx, int which, const thiim_slab_export* peer);
+/* Unmaps imported neighbours: back to exchange after every pass. */
+int thiim_gpu_slab_detach(thiim_gpu_ctx* ctx);
+
 /* Plane-range variants for rank-local host buffers: the host arrays hold the
  * global padded planes [p0, ...) only (plane p = global interior z p-1); a
  * slab reads padded planes [local_z0, local_z1 + 2) and writes back its owned

@@ -300,7 +300,8 @@ EXPORTED_SYMBOLS = [
     "thiim_gpu_upload_planes", "thiim_gpu_download_fields_planes", "thiim_generate_host_planes",
     "thiim_gpu_upload_table", "thiim_gpu_download_table", "thiim_gpu_set_sanitize",
     "thiim_gpu_coverage", "thiim_scheme_default", "thiim_gpu_init_benchmark",
-    "thiim_gpu_init_materials", "thiim_gpu_selftest_cdiv",
+    "thiim_gpu_init_materials", "thiim_gpu_selftest_cdiv", "thiim_gpu_slab_export",
+    "thiim_gpu_slab_import", "thiim_gpu_slab_detach",
 ]
 
 _LIB = None

@@ -72,6 +72,13 @@ struct Slab {
   int own0 = 0, own1 = 0, ext_lo = 0, ext_hi = 0;
   bool deep = false;
   unsigned* cnt = nullptr;                 // sanitizer store counts [12][stride] (or null)
+  bool ipc_buf = false;  // buf from cudaMalloc (exportable by IPC), not the pool
+  // neighbour slabs of other processes, imported by IPC (multi-process peer stores)
+  struct Peer {
+    double2* base = nullptr;
+    long long stride = 0;
+    int nz = 0, ext_lo = 0, ext_hi = 0;
+  } peer[2];
   unsigned long long* cov_bad = nullptr;   // sanitizer violations (device)
   double2* buf = nullptr;
   size_t stride = 0;   // elements per array
@@ -479,6 +486,22 @@ PeerOut peer_out(const thiim_gpu_ctx* ctx, int k) {
   po.st1 = sl.deep ? sl.g.nz - sl.ext_hi : sl.g.nz;
   if (!ctx->peer_stores) return po;
   const long long pxy = sl.g.pxy;
+  if (ctx->slabs.size() == 1) {  // neighbours in other processes (IPC), same cur parity
+    const int out = sl.cur ^ 1;
+    if (const Slab::Peer& p = sl.peer[0]; p.base) {  // lower: its RECV_UP = its plane nz
+      for (int c = 0; c < 12; ++c) po.lo[c] = p.base + (size_t)(out * 12 + c) * p.stride;
+      po.lo_r0 = sl.ext_lo;
+      po.lo_r1 = sl.ext_lo + 2;
+      po.lo_shift = (long long)(p.nz - deep_first_plane(sl, THIIM_HALO_SEND_DOWN)) * pxy;
+    }
+    if (const Slab::Peer& p = sl.peer[1]; p.base) {  // upper: its RECV_DOWN = its plane 0
+      for (int c = 0; c < 12; ++c) po.hi[c] = p.base + (size_t)(out * 12 + c) * p.stride;
+      po.hi_r0 = sl.g.nz - 2 - sl.ext_hi;
+      po.hi_r1 = sl.g.nz - sl.ext_hi;
+      po.hi_shift = (long long)(0 - deep_first_plane(sl, THIIM_HALO_SEND_UP)) * pxy;
+    }
+    return po;
+  }
   if (k > 0) {
     const Slab& lo = ctx->slabs[k - 1];
     for (int c = 0; c < 12; ++c) po.lo[c] = lo.field(lo.cur ^ 1, c);
@@ -1035,7 +1058,7 @@ static cudaError_t pool_alloc(void** p, size_t bytes, int dev, cudaStream_t st) 
 
 // Shared by thiim_gpu_create (n_gpus slabs split like the reference's z_slab,
 // reference_engines.cpp:26-30) and thiim_gpu_create_slab (one explicit slab).
-static int create_impl(const thiim_dims* dims, const thiim_gpu_opts* opts,
+static int create_impl(const thiim_dims* dims, const thiim_gpu_opts* opts, bool ipc_alloc,
                        const std::vector<std::pair<int, int>>& ranges, thiim_gpu_ctx** out) {
   g_err.clear();
   if (!out) return fail(THIIM_ERR_CONFIG, "out pointer is null");
@@ -1125,7 +1148,11 @@ static int create_impl(const thiim_dims* dims, const thiim_gpu_opts* opts,
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&sl.stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) {
       device_pool(sl.device);
-      e = pool_alloc(reinterpret_cast<void**>(&sl.buf), bytes, sl.device, sl.stream);
+      // slab contexts of a multi-process decomposition: cudaMalloc, so that
+      // neighbours in other processes can map the state (thiim_gpu_slab_export)
+      sl.ipc_buf = ipc_alloc;
+      e = ipc_alloc ? cudaMalloc(reinterpret_cast<void**>(&sl.buf), bytes)
+                    : pool_alloc(reinterpret_cast<void**>(&sl.buf), bytes, sl.device, sl.stream);
       if (e == cudaSuccess) e = cudaMemsetAsync(sl.buf, 0, bytes, sl.stream);
       if (e == cudaSuccess) e = cudaStreamSynchronize(sl.stream);
       if (e != cudaSuccess) sl.buf = nullptr;
@@ -1195,7 +1222,7 @@ int thiim_gpu_create(const thiim_dims* dims, const thiim_gpu_opts* opts, thiim_g
       ranges.push_back({z0, z0 + base + (s < rem ? 1 : 0)});
     }
   }
-  return create_impl(dims, opts, ranges, out);
+  return create_impl(dims, opts, false, ranges, out);
 }
 
 int thiim_gpu_create_slab(const thiim_dims* global, int z0, int z1, const thiim_gpu_opts* opts,
@@ -1210,7 +1237,7 @@ int thiim_gpu_create_slab(const thiim_dims* global, int z0, int z1, const thiim_
     g_err = "slab contexts with halos need a fused engine (the split engine exchanges mid-step)";
     return THIIM_ERR_CONFIG;
   }
-  return create_impl(global, &o, {{z0, z1}}, out);
+  return create_impl(global, &o, true, {{z0, z1}}, out);
 }
 
 int thiim_gpu_halo_view(thiim_gpu_ctx* ctx, int which, thiim_halo_view* v) {
@@ -1258,6 +1285,76 @@ int thiim_gpu_slab_info(thiim_gpu_ctx* ctx, thiim_slab_info* info) {
   return THIIM_OK;
 }
 
+int thiim_gpu_slab_export(thiim_gpu_ctx* ctx, thiim_slab_export* out) {
+  g_err.clear();
+  if (!ctx || !out) return fail(THIIM_ERR_CONFIG, "null argument");
+  if (ctx->slabs.size() != 1 || !ctx->slabs[0].ipc_buf)
+    return fail(THIIM_ERR_CONFIG, "export needs a slab context (thiim_gpu_create_slab)");
+  const Slab& sl = ctx->slabs[0];
+  std::memset(out, 0, sizeof(*out));
+  cudaIpcMemHandle_t h;
+  CK(cudaSetDevice(sl.device));
+  CK(cudaIpcGetMemHandle(&h, sl.buf));
+  static_assert(sizeof(h) <= sizeof(out->ipc), "IPC handle size");
+  std::memcpy(out->ipc, &h, sizeof(h));
+  out->stride = (long long)sl.stride;
+  out->nz_local = sl.g.nz;
+  out->ext_lo = sl.ext_lo;
+  out->ext_hi = sl.ext_hi;
+  out->nfield_sets = sl.nfield_sets;
+  out->device = sl.device;
+  out->px = sl.g.px;
+  out->pxy = sl.g.pxy;
+  return THIIM_OK;
+}
+
+int thiim_gpu_slab_import(thiim_gpu_ctx* ctx, int which, const thiim_slab_export* peer) {
+  g_err.clear();
+  if (!ctx || !peer) return fail(THIIM_ERR_CONFIG, "null argument");
+  if (ctx->slabs.size() != 1) return fail(THIIM_ERR_CONFIG, "import needs a slab context");
+  Slab& sl = ctx->slabs[0];
+  if (!sl.deep || ctx->engine != THIIM_ENGINE_TBLOCK)
+    return fail(THIIM_ERR_CONFIG, "peer stores need a deep-halo (TBLOCK) slab");
+  if (which != THIIM_PEER_LOWER && which != THIIM_PEER_UPPER)
+    return fail(THIIM_ERR_CONFIG, "unknown neighbour");
+  if ((which == THIIM_PEER_LOWER && !sl.ext_lo) || (which == THIIM_PEER_UPPER && !sl.ext_hi))
+    return fail(THIIM_ERR_CONFIG, "no neighbour on that side");
+  if (peer->nfield_sets != sl.nfield_sets || peer->px != sl.g.px || peer->pxy != sl.g.pxy ||
+      (which == THIIM_PEER_LOWER ? !peer->ext_hi : !peer->ext_lo))
+    return fail(THIIM_ERR_CONFIG, "neighbour layout does not match");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, peer->ipc, sizeof(h));
+  CK(cudaSetDevice(sl.device));
+  void* base = nullptr;
+  cudaError_t e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(THIIM_ERR_COMM, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+  }
+  Slab::Peer& p = sl.peer[which == THIIM_PEER_LOWER ? 0 : 1];
+  if (p.base) cudaIpcCloseMemHandle(p.base);
+  p.base = static_cast<double2*>(base);
+  p.stride = peer->stride;
+  p.nz = peer->nz_local;
+  p.ext_lo = peer->ext_lo;
+  p.ext_hi = peer->ext_hi;
+  // peer stores once every neighbour this slab has is mapped
+  ctx->peer_stores = (!sl.ext_lo || sl.peer[0].base) && (!sl.ext_hi || sl.peer[1].base);
+  return THIIM_OK;
+}
+
+int thiim_gpu_slab_detach(thiim_gpu_ctx* ctx) {
+  g_err.clear();
+  if (!ctx) return fail(THIIM_ERR_CONFIG, "null context");
+  for (auto& sl : ctx->slabs)
+    for (auto& p : sl.peer) {
+      if (p.base) cudaIpcCloseMemHandle(p.base);
+      p = Slab::Peer{};
+    }
+  if (ctx->slabs.size() == 1) ctx->peer_stores = false;
+  return THIIM_OK;
+}
+
 int thiim_gpu_sync(thiim_gpu_ctx* ctx) {
   g_err.clear();
   if (!ctx) return fail(THIIM_ERR_CONFIG, "null context");
@@ -1273,7 +1370,11 @@ void thiim_gpu_destroy(thiim_gpu_ctx* ctx) {
   for (auto& sl : ctx->slabs) {
     cudaSetDevice(sl.device);
     if (sl.stream) cudaStreamSynchronize(sl.stream);
-    if (sl.buf) {  // back to the pool; the sync lets the next context reuse it at once
+    for (auto& p : sl.peer)
+      if (p.base) cudaIpcCloseMemHandle(p.base);
+    if (sl.buf && sl.ipc_buf) {
+      cudaFree(sl.buf);
+    } else if (sl.buf) {  // back to the pool; the sync lets the next context reuse it at once
       cudaFreeAsync(sl.buf, sl.stream);
       cudaStreamSynchronize(sl.stream);
     }
@@ -1651,6 +1752,9 @@ int thiim_gpu_step(thiim_gpu_ctx* ctx, int steps, thiim_gpu_stats* stats) {
   if (!ctx) return fail(THIIM_ERR_CONFIG, "null context");
   if (steps < 0) return fail(THIIM_ERR_CONFIG, "steps must be >= 0");
   if (!ctx->loaded) return fail(THIIM_ERR_STATE, "no problem uploaded or generated");
+  if (ctx->peer_stores && ctx->slabs.size() == 1 && steps > 2)
+    return fail(THIIM_ERR_CONFIG,
+                "a slab with IPC peer stores advances <= 2 steps per call (barrier in between)");
   long long launches = 0;
   const bool multi = ctx->slabs.size() > 1;
   for (auto& sl : ctx->slabs) {

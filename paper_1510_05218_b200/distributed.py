@@ -60,6 +60,14 @@ class _SlabInfo(ctypes.Structure):
                 ("engine", ctypes.c_int)]
 
 
+class _SlabExport(ctypes.Structure):
+    """thiim_slab_export (include/thiim_gpu.h)."""
+    _fields_ = [("ipc", ctypes.c_ubyte * 64), ("stride", ctypes.c_longlong),
+                ("nz_local", ctypes.c_int), ("ext_lo", ctypes.c_int), ("ext_hi", ctypes.c_int),
+                ("nfield_sets", ctypes.c_int), ("device", ctypes.c_int), ("px", ctypes.c_int),
+                ("pxy", ctypes.c_longlong)]
+
+
 class SlabGpuEngine:
     """One rank's slab of the global grid on its GPU (AUTO: TBLOCK deep-halo slab)."""
 
@@ -83,6 +91,7 @@ class SlabGpuEngine:
         self.local_z0, self.local_z1 = info.local_z0, info.local_z1
         self.exchange_period = info.exchange_period
         self.engine = info.engine
+        self.peer_stores = False
 
     def close(self):
         if self._ctx:
@@ -140,12 +149,46 @@ class SlabGpuEngine:
     def sync(self):
         _check(lib().thiim_gpu_sync(self._ctx))
 
+    def enable_peer_stores(self, rank: int, world: int, group=None) -> bool:
+        """Map the neighbour ranks' slabs (CUDA IPC) so that every TBLOCK pass
+        writes their halo planes itself -- no exchange after 2-step passes, a
+        barrier instead (run_distributed).  Collective: all ranks call it; all
+        end up enabled or all stay on the exchange."""
+        import torch
+        import torch.distributed as dist
+        L = lib()
+        L.thiim_gpu_slab_export.argtypes = [ctypes.c_void_p, ctypes.POINTER(_SlabExport)]
+        L.thiim_gpu_slab_import.argtypes = [ctypes.c_void_p, ctypes.c_int,
+                                            ctypes.POINTER(_SlabExport)]
+        L.thiim_gpu_slab_detach.argtypes = [ctypes.c_void_p]
+        mine = _SlabExport()
+        ok = self.exchange_period == 2 and L.thiim_gpu_slab_export(self._ctx, ctypes.byref(mine)) == 0
+        parts = [None] * world
+        dist.all_gather_object(parts, bytes(mine) if ok else None, group=group)
+        ok = all(p is not None for p in parts)
+        if ok:
+            for which, nb in ((0, rank - 1), (1, rank + 1)):
+                if 0 <= nb < world:
+                    ex = _SlabExport.from_buffer_copy(parts[nb])
+                    ok = ok and L.thiim_gpu_slab_import(self._ctx, which, ctypes.byref(ex)) == 0
+        flag = torch.tensor([1 if ok else 0], dtype=torch.int32,
+                            device="cuda" if dist.get_backend(group) == "nccl" else "cpu")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+        self.peer_stores = bool(flag.item())
+        if not self.peer_stores:
+            L.thiim_gpu_slab_detach(self._ctx)
+        return self.peer_stores
+
 
 class HaloExchanger:
     """Between-step halo exchange of one rank with its z-neighbours."""
 
     def __init__(self, rank: int, world: int, group=None):
         self.rank, self.world, self.group = rank, world, group
+
+    def barrier(self) -> None:
+        import torch.distributed as dist
+        dist.barrier(group=self.group)
 
     def exchange(self, engine) -> int:
         """Returns the number of bytes this rank sent."""
@@ -202,6 +245,9 @@ def run_distributed(engine, steps: int, exchanger: HaloExchanger) -> dict:
         k = min(period, steps - done)
         st = engine.step(k)
         launches += getattr(st, "kernel_launches", 0)
-        sent += exchanger.exchange(engine)
+        if getattr(engine, "peer_stores", False) and k == 2:
+            exchanger.barrier()  # the pass wrote the neighbours' halos itself
+        else:
+            sent += exchanger.exchange(engine)
         done += k
     return {"halo_bytes_sent": sent, "kernel_launches": launches}

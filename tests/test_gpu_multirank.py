@@ -23,8 +23,12 @@ def _port():
     return p
 
 
-def test_bench_two_ranks_one_gpu():
-    env = dict(os.environ, THIIM_DIST_BACKEND="gloo", THIIM_SAME_DEVICE="1")
+@pytest.mark.parametrize("peer", ["1", "0"])
+def test_bench_two_ranks_one_gpu(peer):
+    """peer = 1: the ranks map each other's slabs by CUDA IPC and every TBLOCK
+    pass writes the neighbour's halos itself (a barrier per pass); 0: halo
+    exchange after every pass."""
+    env = dict(os.environ, THIIM_DIST_BACKEND="gloo", THIIM_SAME_DEVICE="1", THIIM_PEER_STORES=peer)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), "bench.py", "--gpus", "2",
            "--config", "c0", "--steps", "1", "--warmup", "1", "--iters", "4", "--check", "3"]
@@ -35,4 +39,9 @@ def test_bench_two_ranks_one_gpu():
     bench = [l for l in lines if "metric" in l]
     assert check and check[0]["bitwise_equal"], lines
     assert bench and bench[0]["n_gpus"] == 2 and bench[0]["value"] > 0
-    assert bench[0]["config"]["halo_bytes_per_rank_per_step"] > 0
+    cfg = bench[0]["config"]
+    if peer == "1":
+        assert cfg["exchange"].startswith("peer stores"), cfg
+        assert cfg["halo_bytes_per_rank_per_step"] == 0  # iters even: no exchange at all
+    else:
+        assert cfg["halo_bytes_per_rank_per_step"] > 0
