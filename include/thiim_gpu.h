@@ -59,7 +59,9 @@ enum {
   THIIM_ERR_STATE = 6   /* call order (step before upload, ...) */
 };
 
-/* Engines (all bitwise-equal to step_reference). */
+/* Engines (all bitwise-equal to step_reference).  AUTO picks TBLOCK (two steps
+ * per HBM pass, 416 B/LUP; odd remainders run one fused step) when the
+ * ping-pong state fits, else SPLIT. */
 enum {
   THIIM_ENGINE_AUTO = 0,
   THIIM_ENGINE_SPLIT = 1, /* H sweep + E sweep, in place, z-streamed: 1024 B/LUP */

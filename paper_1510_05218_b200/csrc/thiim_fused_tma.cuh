@@ -1,4 +1,4 @@
-// thiim_fused_tma.cuh -- engine FUSED (default): one z-streamed H->E sweep per
+// thiim_fused_tma.cuh -- engine FUSED: one z-streamed H->E sweep per
 // THIIM step, operands staged by TMA.
 //
 // Each CTA owns a 30 x (BY-2) x-y tile and streams z over a chunk.  At plane z
