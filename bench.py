@@ -10,8 +10,10 @@ seed 1, zero ghosts.  One bench "step" = one full configs[1] run.
 
   value   MLUP/s with the problem resident in HBM (device time, CUDA events on
           the launching stream), max over ranks.
-  e2e     same metric through the public API (run_gpu: upload from pinned host
-          memory -> 100 iterations -> download of the 12 fields), every step.
+  e2e     same metric through the public API, every step's inputs uploaded
+          from pinned host memory and its 12 result fields downloaded: the
+          pipelined stream call run_gpu_batch (copies of neighbouring steps
+          overlap the sweep), with the serial run_gpu sequence beside it.
   roofline  dominant kernel (one THIIM iteration per launch) vs measured HBM.
   cpu_baseline  the reference's own run_naive (oracle/_ref, compiled from
           /root/reference unmodified) on the host cores, bounded sample.
@@ -326,16 +328,34 @@ def run_native_single(P, args, opts, iters):
     engine_ran = st.engine
     eng.close()
 
-    # e2e: the public API call a user makes (upload from pinned host memory,
-    # `iters` iterations, download of the 12 fields), every step
+    # e2e: the public API a user calls, with every step's inputs copied from
+    # pinned host memory and its 12 result fields copied back.  Headline: the
+    # pipelined stream API (run_gpu_batch: step i uploads while i-1 computes and
+    # i-2 downloads, all inside one timed call incl. context create/destroy).
+    # Beside it the one-problem call sequence (create, upload, step, download,
+    # destroy), serial, with its phases.
     e2e = None
+    e2e_extra = {}
     if not args.no_e2e:
         host = P.generate_problem(dims, KIND, SEED)
-        for a in host.arrays:
+        out = [np.zeros_like(a) for a in host.fields]
+        pinned = host.arrays + out
+        for a in pinned:
             P.lib().thiim_gpu_pin_host(a.ctypes.data, a.nbytes)
+        P.run_gpu_batch([host] * 2, iters, opts, outputs=[out] * 2)  # untimed warm-up
+        rep = P.run_gpu_batch([host] * args.steps, iters, opts, outputs=[out] * args.steps)
+        e2e = dims.interior_cells() * iters * args.steps / rep.seconds / 1e6
+        e2e_extra = {
+            "api": "run_gpu_batch (thiim_gpu_run_batch), depth %d, one problem per step" % rep.depth,
+            "device_ms_per_step": {
+                "upload": round(1e3 * rep.upload_seconds / args.steps, 2),
+                "sweep": round(1e3 * rep.kernel_seconds / args.steps, 2),
+                "download": round(1e3 * rep.download_seconds / args.steps, 2)},
+        }
         secs = 0.0
         phases = [0.0] * 5
-        for k in range(1 + args.steps):  # 1 untimed warm-up
+        nser = max(1, min(args.steps, 3))
+        for k in range(1 + nser):  # 1 untimed warm-up
             t = [time.perf_counter()]
             e = P.GpuEngine(dims, opts)
             t.append(time.perf_counter())
@@ -351,14 +371,16 @@ def run_native_single(P, args, opts, iters):
                 secs += t[-1] - t[0]
                 for j in range(5):
                     phases[j] += t[j + 1] - t[j]
-        for a in host.arrays:
+        for a in pinned:
             P.lib().thiim_gpu_unpin_host(a.ctypes.data)
-        e2e = dims.interior_cells() * iters * args.steps / secs / 1e6
-        e2e_phases = dict(zip(["create", "upload", "step", "download", "destroy"],
-                              [round(1e3 * v / args.steps, 2) for v in phases]))
+        e2e_extra["serial_value"] = round(dims.interior_cells() * iters * nser / secs / 1e6, 2)
+        e2e_extra["serial_api"] = "run_gpu call sequence, %d steps" % nser
+        e2e_extra["serial_phases_ms_per_step"] = dict(
+            zip(["create", "upload", "step", "download", "destroy"],
+                [round(1e3 * v / nser, 2) for v in phases]))
     line = _line(P, args, 1, dims, engine_ran, dev_secs, launches, e2e, clk, {})
     if e2e:
-        line["e2e"]["phases_ms_per_step"] = e2e_phases
+        line["e2e"].update(e2e_extra)
     return line
 
 

@@ -186,6 +186,34 @@ typedef struct {
 int thiim_gpu_compare_fields(thiim_gpu_ctx* ctx, const thiim_c128* const ref_fields[12],
                              thiim_gpu_diff* out);
 
+/* A stream of independent problems on one GPU (e.g. the paper's sweep over
+ * wavelengths): for each problem i, == run_naive(problem i, steps)
+ * (reference_engines.cpp:34-67) with the result's 12 fields written to
+ * outputs[12*i .. 12*i+11] (NULL outputs: back into the problem's own field
+ * arrays, in place like run_naive).  inputs[40*i .. 40*i+39] are problem i's
+ * arrays in thiim_gpu_upload order (12 fields, 12 t, 12 c, 4 src).
+ * Problems are pipelined over `depth` device contexts (<= 0: 3): problem i
+ * uploads while i-1 computes and i-2 downloads, each resource in problem
+ * order.  Host buffers should be pinned (thiim_gpu_pin_host) for the copies to
+ * overlap.  An output may be shared by several problems but must not overlap
+ * another problem's inputs (THIIM_ERR_CONFIG).  Blocking; reference layout,
+ * n_gpus = 1. */
+typedef struct {
+  double seconds;          /* host wall clock of the whole call, contexts included */
+  double device_seconds;   /* first upload start .. last download end (device events) */
+  double upload_seconds;   /* sums over problems of each phase's device time */
+  double kernel_seconds;
+  double download_seconds;
+  double mlups;            /* n_problems x interior cells x steps / seconds / 1e6 */
+  long long kernel_launches;
+  long long h2d_bytes, d2h_bytes;
+  int n_problems, depth, engine;
+  int reserved[5];
+} thiim_gpu_batch_stats;
+int thiim_gpu_run_batch(const thiim_dims* dims, const thiim_gpu_opts* opts, int n_problems,
+                        const thiim_c128* const* inputs, thiim_c128* const* outputs, int steps,
+                        int depth, thiim_gpu_batch_stats* stats);
+
 /* Host-side generator for the same synthetic problem (for CPU oracles and for
  * uploading); arrays must be zeroed or are fully overwritten (ghosts -> 0). */
 int thiim_generate_host(const thiim_dims* dims, int kind, uint64_t seed,

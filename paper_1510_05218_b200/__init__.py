@@ -40,6 +40,7 @@ __all__ = [
     "ENGINE_FUSED", "ENGINE_TBLOCK", "GpuOptions", "RunReport", "StateDiff", "GpuEngine",
     "run_gpu", "generate_problem", "compare_states", "balance_model", "lib",
     "compress_coefficients", "expand_coefficients", "COEFF_FULL", "COEFF_TABLE",
+    "run_gpu_batch", "BatchReport",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -285,6 +286,15 @@ class _Stats(ctypes.Structure):
                 ("reserved", ctypes.c_int * 5)]
 
 
+class _BatchStats(ctypes.Structure):
+    _fields_ = [("seconds", ctypes.c_double), ("device_seconds", ctypes.c_double),
+                ("upload_seconds", ctypes.c_double), ("kernel_seconds", ctypes.c_double),
+                ("download_seconds", ctypes.c_double), ("mlups", ctypes.c_double),
+                ("kernel_launches", ctypes.c_longlong), ("h2d_bytes", ctypes.c_longlong),
+                ("d2h_bytes", ctypes.c_longlong), ("n_problems", ctypes.c_int),
+                ("depth", ctypes.c_int), ("engine", ctypes.c_int), ("reserved", ctypes.c_int * 5)]
+
+
 class _Diff(ctypes.Structure):
     _fields_ = [("differing_values", ctypes.c_ulonglong), ("max_rel_l2", ctypes.c_double),
                 ("rel_l2", ctypes.c_double * 12)]
@@ -301,7 +311,7 @@ EXPORTED_SYMBOLS = [
     "thiim_gpu_upload_table", "thiim_gpu_download_table", "thiim_gpu_set_sanitize",
     "thiim_gpu_coverage", "thiim_scheme_default", "thiim_gpu_init_benchmark",
     "thiim_gpu_init_materials", "thiim_gpu_selftest_cdiv", "thiim_gpu_slab_export",
-    "thiim_gpu_slab_import", "thiim_gpu_slab_detach",
+    "thiim_gpu_slab_import", "thiim_gpu_slab_detach", "thiim_gpu_run_batch",
 ]
 
 _LIB = None
@@ -344,6 +354,9 @@ def lib() -> ctypes.CDLL:
     L.thiim_gpu_selftest_cdiv.argtypes = [ctypes.c_int, P, P]
     L.thiim_gpu_coverage.argtypes = [P, ctypes.POINTER(ctypes.c_ulonglong),
                                      ctypes.POINTER(ctypes.c_ulonglong)]
+    L.thiim_gpu_run_batch.argtypes = [ctypes.POINTER(_Dims), ctypes.POINTER(_Opts), ctypes.c_int,
+                                      PP, PP, ctypes.c_int, ctypes.c_int,
+                                      ctypes.POINTER(_BatchStats)]
     if L.thiim_gpu_abi_version() != 1:
         raise GpuError("libthiim_gpu.so ABI mismatch")
     _LIB = L
@@ -607,3 +620,63 @@ def run_gpu(state: ProblemState, steps: int, opts: Optional[GpuOptions] = None) 
     if steps > 0 and st.seconds > 0:
         r.mlups = state.dims.interior_cells() * steps / st.seconds / 1e6
     return r
+
+
+@dataclass
+class BatchReport:
+    """Result of run_gpu_batch: host wall clock of the whole call plus the
+    device time of each phase summed over the problems."""
+
+    engine: str = ""
+    n_problems: int = 0
+    depth: int = 0
+    steps: int = 0
+    seconds: float = 0.0
+    device_seconds: float = 0.0
+    upload_seconds: float = 0.0
+    kernel_seconds: float = 0.0
+    download_seconds: float = 0.0
+    mlups: float = 0.0
+    kernel_launches: int = 0
+    h2d_bytes: int = 0
+    d2h_bytes: int = 0
+
+
+def run_gpu_batch(states: List[ProblemState], steps: int, opts: Optional[GpuOptions] = None,
+                  outputs: Optional[List[List[np.ndarray]]] = None, depth: int = 0) -> BatchReport:
+    """run_naive (reference_engines.cpp:34-67) over a stream of independent
+    problems on one GPU, pipelined (thiim_gpu_run_batch): problem i uploads
+    while i-1 computes and i-2 downloads.  ``outputs[i]`` (12 complex128
+    arrays of padded_cells()) receives problem i's fields; without it each
+    state is updated in place, and then the states must not share arrays.
+    Pin the host arrays (lib().thiim_gpu_pin_host) for the copies to overlap."""
+    if steps < 0:
+        raise ConfigError("steps must be >= 0")
+    opts = opts or GpuOptions()
+    if not states:
+        return BatchReport(n_problems=0, steps=steps)
+    dims = states[0].dims
+    n = dims.padded_cells()
+    for s in states:
+        if s.dims != dims:
+            raise ConfigError("all problems of a batch need the same grid dims")
+    if outputs is not None:
+        if len(outputs) != len(states):
+            raise ConfigError("outputs needs one 12-array field set per problem")
+        for fs in outputs:
+            if len(fs) != 12 or any(a.shape != (n,) or a.dtype != np.complex128
+                                    or not a.flags.c_contiguous for a in fs):
+                raise ConfigError("outputs: 12 C-contiguous complex128 arrays of padded_cells()")
+    ins = _ptrs([a for s in states for a in s.arrays])
+    outs = _ptrs([a for fs in outputs for a in fs]) if outputs is not None else None
+    d = _Dims(dims.nx, dims.ny, dims.nz, dims.ghost)
+    o = opts._c()
+    st = _BatchStats()
+    _check(lib().thiim_gpu_run_batch(ctypes.byref(d), ctypes.byref(o), len(states), ins, outs,
+                                     steps, depth, ctypes.byref(st)))
+    return BatchReport(engine=ENGINE_NAMES.get(st.engine, "gpu"), n_problems=st.n_problems,
+                       depth=st.depth, steps=steps, seconds=st.seconds,
+                       device_seconds=st.device_seconds, upload_seconds=st.upload_seconds,
+                       kernel_seconds=st.kernel_seconds, download_seconds=st.download_seconds,
+                       mlups=st.mlups, kernel_launches=st.kernel_launches,
+                       h2d_bytes=st.h2d_bytes, d2h_bytes=st.d2h_bytes)

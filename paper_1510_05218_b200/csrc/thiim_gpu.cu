@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <complex>
 #include <cstdlib>
@@ -1397,7 +1398,7 @@ void thiim_gpu_destroy(thiim_gpu_ctx* ctx) {
 }
 
 static int upload_arrays(thiim_gpu_ctx* ctx, const thiim_c128* const* arrays, int first, int count,
-                         int p0 = 0) {
+                         int p0 = 0, bool sync = true) {
   const long long pxy = ctx->pxy();
   for (auto& sl : ctx->slabs) {
     CK(cudaSetDevice(sl.device));
@@ -1423,7 +1424,7 @@ static int upload_arrays(thiim_gpu_ctx* ctx, const thiim_c128* const* arrays, in
   }
   for (auto& sl : ctx->slabs) {
     CK(cudaSetDevice(sl.device));
-    CK(cudaStreamSynchronize(sl.stream));
+    if (sync) CK(cudaStreamSynchronize(sl.stream));
     sl.cur = 0;
   }
   return THIIM_OK;
@@ -1752,20 +1753,12 @@ int thiim_gpu_coverage(thiim_gpu_ctx* ctx, unsigned long long* passes,
   return THIIM_OK;
 }
 
-int thiim_gpu_step(thiim_gpu_ctx* ctx, int steps, thiim_gpu_stats* stats) {
-  g_err.clear();
-  if (!ctx) return fail(THIIM_ERR_CONFIG, "null context");
-  if (steps < 0) return fail(THIIM_ERR_CONFIG, "steps must be >= 0");
-  if (!ctx->loaded) return fail(THIIM_ERR_STATE, "no problem uploaded or generated");
-  if (ctx->peer_stores && ctx->slabs.size() == 1 && steps > 2)
-    return fail(THIIM_ERR_CONFIG,
-                "a slab with IPC peer stores advances <= 2 steps per call (barrier in between)");
+// Enqueues `steps` iterations on the context's stream(s) without waiting for
+// them; host-side bookkeeping (current field set, graphs) advances at enqueue
+// time, so calls on one context must stay in stream order.
+static int step_enqueue(thiim_gpu_ctx* ctx, int steps, long long* launches_out) {
   long long launches = 0;
   const bool multi = ctx->slabs.size() > 1;
-  for (auto& sl : ctx->slabs) {
-    CK(cudaSetDevice(sl.device));
-    CK(cudaEventRecord(sl.ev0, sl.stream));
-  }
   int r;
   int n = 0;
   if (ctx->engine == THIIM_ENGINE_TBLOCK) {
@@ -1839,6 +1832,25 @@ int thiim_gpu_step(thiim_gpu_ctx* ctx, int steps, thiim_gpu_stats* stats) {
     }
     if (ctx->sanitize && (r = coverage_pass(ctx))) return r;
   }
+  *launches_out += launches;
+  return THIIM_OK;
+}
+
+int thiim_gpu_step(thiim_gpu_ctx* ctx, int steps, thiim_gpu_stats* stats) {
+  g_err.clear();
+  if (!ctx) return fail(THIIM_ERR_CONFIG, "null context");
+  if (steps < 0) return fail(THIIM_ERR_CONFIG, "steps must be >= 0");
+  if (!ctx->loaded) return fail(THIIM_ERR_STATE, "no problem uploaded or generated");
+  if (ctx->peer_stores && ctx->slabs.size() == 1 && steps > 2)
+    return fail(THIIM_ERR_CONFIG,
+                "a slab with IPC peer stores advances <= 2 steps per call (barrier in between)");
+  for (auto& sl : ctx->slabs) {
+    CK(cudaSetDevice(sl.device));
+    CK(cudaEventRecord(sl.ev0, sl.stream));
+  }
+  long long launches = 0;
+  int r;
+  if ((r = step_enqueue(ctx, steps, &launches))) return r;
   double secs = 0.0;
   for (auto& sl : ctx->slabs) {
     CK(cudaSetDevice(sl.device));
@@ -1866,7 +1878,8 @@ int thiim_gpu_step(thiim_gpu_ctx* ctx, int steps, thiim_gpu_stats* stats) {
   return THIIM_OK;
 }
 
-static int download_impl(thiim_gpu_ctx* ctx, int a, thiim_c128* dst, int hp0 = 0) {
+static int download_impl(thiim_gpu_ctx* ctx, int a, thiim_c128* dst, int hp0 = 0,
+                         bool sync = true) {
   const long long pxy = ctx->pxy();
   for (auto& sl : ctx->slabs) {
     CK(cudaSetDevice(sl.device));
@@ -1879,6 +1892,7 @@ static int download_impl(thiim_gpu_ctx* ctx, int a, thiim_c128* dst, int hp0 = 0
                        (size_t)(p1 - p0) * (size_t)pxy * sizeof(double2), cudaMemcpyDeviceToHost,
                        sl.stream));
   }
+  if (!sync) return THIIM_OK;
   for (auto& sl : ctx->slabs) {
     CK(cudaSetDevice(sl.device));
     CK(cudaStreamSynchronize(sl.stream));
@@ -1916,6 +1930,148 @@ int thiim_gpu_download_fields_planes(thiim_gpu_ctx* ctx, thiim_c128* const field
     if (!fields[k]) return fail(THIIM_ERR_CONFIG, "null host array");
     int r = download_impl(ctx, k, fields[k], p0);
     if (r) return r;
+  }
+  return THIIM_OK;
+}
+
+// A stream of independent problems through `depth` device contexts: problem i
+// uploads while problem i-1 computes and problem i-2 downloads.  Three event
+// chains keep each resource in problem order (H2D copies, sweeps, D2H copies),
+// so the PCIe directions and the SMs each work on one problem at a time, and a
+// context is reused only after its previous problem's download (same stream).
+int thiim_gpu_run_batch(const thiim_dims* dims, const thiim_gpu_opts* opts, int n_problems,
+                        const thiim_c128* const* inputs, thiim_c128* const* outputs, int steps,
+                        int depth, thiim_gpu_batch_stats* stats) {
+  g_err.clear();
+  if (!dims || !inputs) return fail(THIIM_ERR_CONFIG, "null argument");
+  if (n_problems < 0 || steps < 0) return fail(THIIM_ERR_CONFIG, "n_problems and steps must be >= 0");
+  thiim_gpu_opts o;
+  if (opts)
+    o = *opts;
+  else
+    thiim_gpu_default_opts(&o);
+  if (o.n_gpus != 1) return fail(THIIM_ERR_CONFIG, "run_batch drives one GPU (n_gpus = 1)");
+  if (o.coeff_layout != THIIM_COEFF_FULL)
+    return fail(THIIM_ERR_CONFIG, "run_batch takes the reference layout (40 arrays per problem)");
+  if (depth <= 0) depth = 3;
+  depth = std::max(1, std::min(depth, std::max(n_problems, 1)));
+  const size_t bytes = (size_t)(dims->nx + 2) * (size_t)(dims->ny + 2) * (size_t)(dims->nz + 2) *
+                       sizeof(thiim_c128);
+  auto out_ptr = [&](int i, int k) -> thiim_c128* {
+    return outputs ? outputs[(size_t)i * 12 + k] : const_cast<thiim_c128*>(inputs[(size_t)i * 40 + k]);
+  };
+  for (int i = 0; i < n_problems; ++i) {
+    for (int a = 0; a < 40; ++a)
+      if (!inputs[(size_t)i * 40 + a]) return fail(THIIM_ERR_CONFIG, "null host array");
+    for (int k = 0; k < 12; ++k)
+      if (!out_ptr(i, k)) return fail(THIIM_ERR_CONFIG, "null host array");
+  }
+  // problem i's download may run while problem j's upload reads its inputs:
+  // outputs must not overlap another problem's inputs (shared outputs are fine,
+  // downloads are serialised; writing back over the problem's own inputs is fine)
+  for (int i = 0; i < n_problems; ++i)
+    for (int k = 0; k < 12; ++k) {
+      const char* o0 = (const char*)out_ptr(i, k);
+      for (int j = 0; j < n_problems; ++j) {
+        if (j == i) continue;
+        for (int a = 0; a < 40; ++a) {
+          const char* i0 = (const char*)inputs[(size_t)j * 40 + a];
+          if (o0 < i0 + bytes && i0 < o0 + bytes) {
+            char msg[160];
+            std::snprintf(msg, sizeof msg,
+                          "output field %d of problem %d overlaps input array %d of problem %d", k,
+                          i, a, j);
+            return fail(THIIM_ERR_CONFIG, msg);
+          }
+        }
+      }
+    }
+  const auto t0 = std::chrono::steady_clock::now();
+  std::vector<thiim_gpu_ctx*> ctxs(depth, nullptr);
+  // per problem: upload, sweep and download brackets
+  std::vector<cudaEvent_t> ev((size_t)n_problems * 6, nullptr);
+  auto cleanup = [&]() {
+    for (auto* c : ctxs)
+      if (c) thiim_gpu_destroy(c);  // waits for the context's stream
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+  };
+  auto bail = [&](int rc) {
+    const std::string msg = g_err;
+    cleanup();
+    g_err = msg;
+    return rc;
+  };
+  int r;
+  for (int d = 0; d < depth; ++d)
+    if ((r = thiim_gpu_create(dims, &o, &ctxs[d]))) return bail(r);
+  {
+    const cudaError_t e = cudaSetDevice(ctxs[0]->slabs[0].device);
+    for (auto& x : ev)
+      if (e != cudaSuccess || cudaEventCreate(&x) != cudaSuccess)
+        return bail(fail(THIIM_ERR_CUDA, "cudaEventCreate failed"));
+  }
+  long long launches = 0;
+  auto E = [&](int i, int k) { return ev[(size_t)i * 6 + k]; };
+  for (int i = 0; i < n_problems; ++i) {
+    thiim_gpu_ctx* ctx = ctxs[i % depth];
+    cudaStream_t st = ctx->slabs[0].stream;
+    auto ck = [&](cudaError_t e) { return e == cudaSuccess ? THIIM_OK : fail(THIIM_ERR_CUDA, cudaGetErrorString(e)); };
+    if (i > 0 && (r = ck(cudaStreamWaitEvent(st, E(i - 1, 1), 0)))) return bail(r);
+    if ((r = ck(cudaEventRecord(E(i, 0), st)))) return bail(r);
+    const thiim_c128* const* in = inputs + (size_t)i * 40;
+    if ((r = upload_arrays(ctx, in, 0, 12, 0, false)) || (r = upload_arrays(ctx, in + 12, 12, 12, 0, false)) ||
+        (r = upload_arrays(ctx, in + 24, 24, 12, 0, false)) ||
+        (r = upload_arrays(ctx, in + 36, 36, 4, 0, false)))
+      return bail(r);
+    ctx->loaded = true;
+    if ((r = ck(cudaEventRecord(E(i, 1), st)))) return bail(r);
+    if (i > 0 && (r = ck(cudaStreamWaitEvent(st, E(i - 1, 3), 0)))) return bail(r);
+    if ((r = ck(cudaEventRecord(E(i, 2), st)))) return bail(r);
+    if ((r = step_enqueue(ctx, steps, &launches))) return bail(r);
+    if ((r = ck(cudaEventRecord(E(i, 3), st)))) return bail(r);
+    if (i > 0 && (r = ck(cudaStreamWaitEvent(st, E(i - 1, 5), 0)))) return bail(r);
+    if ((r = ck(cudaEventRecord(E(i, 4), st)))) return bail(r);
+    for (int k = 0; k < 12; ++k)
+      if ((r = download_impl(ctx, k, out_ptr(i, k), 0, false))) return bail(r);
+    if ((r = ck(cudaEventRecord(E(i, 5), st)))) return bail(r);
+  }
+  for (auto* c : ctxs) {
+    const cudaError_t e = cudaStreamSynchronize(c->slabs[0].stream);
+    if (e != cudaSuccess) return bail(fail(THIIM_ERR_CUDA, cudaGetErrorString(e)));
+  }
+  double up = 0, sw = 0, down = 0, span = 0;
+  for (int i = 0; i < n_problems; ++i) {
+    float a = 0, b = 0, c = 0, w = 0;
+    cudaEventElapsedTime(&a, E(i, 0), E(i, 1));
+    cudaEventElapsedTime(&b, E(i, 2), E(i, 3));
+    cudaEventElapsedTime(&c, E(i, 4), E(i, 5));
+    up += a * 1e-3;
+    sw += b * 1e-3;
+    down += c * 1e-3;
+    if (i == n_problems - 1) {
+      cudaEventElapsedTime(&w, E(0, 0), E(i, 5));
+      span = w * 1e-3;
+    }
+  }
+  const int engine_ran = ctxs[0] ? ctxs[0]->engine : o.engine;
+  cleanup();
+  const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  if (stats) {
+    std::memset(stats, 0, sizeof(*stats));
+    stats->seconds = secs;
+    stats->device_seconds = span;
+    stats->upload_seconds = up;
+    stats->kernel_seconds = sw;
+    stats->download_seconds = down;
+    stats->kernel_launches = launches;
+    stats->h2d_bytes = (long long)n_problems * 40 * (long long)bytes;
+    stats->d2h_bytes = (long long)n_problems * 12 * (long long)bytes;
+    stats->n_problems = n_problems;
+    stats->depth = depth;
+    stats->engine = engine_ran;
+    const double lups = (double)dims->nx * dims->ny * dims->nz * steps * n_problems;
+    stats->mlups = secs > 0 ? lups / secs / 1e6 : 0.0;
   }
   return THIIM_OK;
 }
