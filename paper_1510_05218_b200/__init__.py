@@ -44,7 +44,8 @@ __all__ = [
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libthiim_gpu.so")
+# THIIM_LIB: load an alternative build (A/B experiments, tools/build_variant.sh)
+LIB_PATH = os.environ.get("THIIM_LIB") or os.path.join(HERE, "libthiim_gpu.so")
 
 
 # ---------------------------------------------------------------- errors
