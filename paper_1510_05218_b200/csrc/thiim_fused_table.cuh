@@ -139,11 +139,14 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
   const bool upd_z = own || (ring_x && x >= 0) || (ring_y && y >= 0);
   const int xs = inpad ? x : 0, ys = inpad ? y : 0;
   long long i = g.idx(xs, ys, z0);
-  // material id of this thread's cell at local padded plane zp
-  auto mat_at = [&](int zp) -> int {
-    const int m = __ldg(T.mat + (long long)zp * T.mplane + (long long)(ys + 1) * T.mp + (xs + 1));
-    return m < T.n_mat ? m : 0;
+  // material id of this thread's cell at local padded plane zp: the raw byte
+  // (loaded one plane ahead) and its range check at the point of use, so the
+  // load's latency is not exposed by a compare right after it
+  auto mat_raw = [&](int zp) -> int {
+    return __ldg(T.mat + (long long)zp * T.mplane + (long long)(ys + 1) * T.mp + (xs + 1));
   };
+  auto mat_ok = [&](int m) -> int { return m < T.n_mat ? m : 0; };
+  auto mat_at = [&](int zp) -> int { return mat_ok(mat_raw(zp)); };
 
   double2 e[6];
 #pragma unroll
@@ -184,10 +187,10 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
   auto& R = sm.ring;
   RingCursor rc = ring_cursor(R);
 #define RD(k, b) ring_read<true>(R, rc, k, b, tx, ty)
-  int mid_next = inpad ? mat_at(z0 + 1) : 0;  // material id, one plane ahead
+  int mid_next = inpad ? mat_raw(z0 + 1) : 0;  // material id, one plane ahead
   for (int z = z0; z < z1; ++z, i += pxy) {
-    int mid = mid_next;
-    if (inpad && z + 1 < z1) mid_next = mat_at(z + 2);
+    const int mid = mat_ok(mid_next);
+    if (inpad && z + 1 < z1) mid_next = mat_raw(z + 2);
     double2 en[6];
     ring_wait(R, rc);
 #pragma unroll

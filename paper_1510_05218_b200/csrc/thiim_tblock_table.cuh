@@ -96,11 +96,14 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
   const bool upd2_y = (own2 || rx2) && interior;
   const bool upd2_z = (own2 || rx2 || ry2) && interior;
   // material id of this thread's cell at interior plane z (padded plane z+1)
-  auto mat_at = [&](int z) -> int {
+  // (raw byte loaded one plane ahead, range-checked where it is used, so no
+  // compare right after the load exposes its latency)
+  auto mat_raw = [&](int z) -> int {
     if (!inpad) return 0;
-    const int m = __ldg(T.mat + (long long)(z + 1) * T.mplane + (long long)(ys + 1) * T.mp + (xs + 1));
-    return m < T.n_mat ? m : 0;
+    return __ldg(T.mat + (long long)(z + 1) * T.mplane + (long long)(ys + 1) * T.mp + (xs + 1));
   };
+  auto mat_ok = [&](int m) -> int { return m < T.n_mat ? m : 0; };
+  auto mat_at = [&](int z) -> int { return mat_ok(mat_raw(z)); };
 
   auto& R = sm.ring;
   RingCursor rc = ring_cursor(R);
@@ -154,7 +157,7 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
   double2 pH2x = make_double2(0.0, 0.0), pH2y = make_double2(0.0, 0.0);
   double2 nE2x = make_double2(0.0, 0.0), nE2y = make_double2(0.0, 0.0);
   const uint64_t first = policy_evict_first();
-  int mid1_next = mat_at(qs);  // level-1 material id, one plane ahead
+  int mid1_next = mat_raw(qs);  // level-1 material id (raw), one plane ahead
   int mid_last = 0;            // material id of the last level-1 plane
 
   for (int q = qs; q <= qe; ++q) {
@@ -162,9 +165,9 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
     const int mid2 = mid_last;
     // ================= level 1 at plane q (step n) -> TMEM slot q&1
     if (q <= q1) {
-      const int mid1 = mid1_next;
+      const int mid1 = mat_ok(mid1_next);
       mid_last = mid1;
-      if (q + 1 <= q1) mid1_next = mat_at(q + 1);
+      if (q + 1 <= q1) mid1_next = mat_raw(q + 1);
       const double2* C = sm.tab[mid1];
       const uint32_t tslot = tcar + 48 * (q & 1);
       double2 e[6];
