@@ -4,7 +4,7 @@
 // against run_naive with compare_states (verifier.cpp:13-44), bitwise, the way
 // test_reference_engines.cpp:32-55 and test_mwd.cpp:14-26 check their engines.
 // Built by adapter/Makefile against the UNMODIFIED reference library objects
-// (oracle/_ref/obj) into build/test_run_gpu; run by tests/test_gpu_adapter.py.
+// (oracle/_ref/obj) into build/test_run_gpu; run by tests/test_gpu_slabs.py.
 #include <cstdio>
 #include <cstring>
 #include <functional>
@@ -142,6 +142,26 @@ void test_layered_material() {
   CHECK(compare_states(a, b).bitwise_equal);
 }
 
+void test_batch_matches_run_naive() {
+  // a stream of distinct problems, each == run_naive on its own copy
+  const GridDims d(40, 33, 24);
+  std::vector<ProblemState> want, got;
+  for (int k = 0; k < 4; ++k) {
+    want.push_back(random_state(d, 100 + k, k % 2 ? THIIM_GEN_LAYERED : THIIM_GEN_RANDOM));
+    got.push_back(clone_state(want.back()));
+  }
+  for (auto& s : want) run_naive(s, 5, 4);
+  std::vector<ProblemState*> ptrs;
+  for (auto& s : got) ptrs.push_back(&s);
+  const RunReport r = run_gpu_batch(ptrs, 5);
+  for (int k = 0; k < 4; ++k) CHECK(compare_states(want[k], got[k]).bitwise_equal);
+  CHECK(r.steps == 5 && r.mlups.has_value() && r.engine == "gpu-tblock");
+  // the same state twice would be read while being written back
+  std::vector<ProblemState*> twice{&got[0], &got[0]};
+  CHECK(throws_as<ConfigError>([&] { run_gpu_batch(twice, 1); }));
+  CHECK(throws_as<ConfigError>([&] { run_gpu_batch(ptrs, -1); }));
+}
+
 }  // namespace
 
 int main() {
@@ -152,6 +172,7 @@ int main() {
       {"empty run and argument validation", test_empty_run_and_validation},
       {"single-cell known answer 1.35", test_single_cell_kat},
       {"layered thin-film material", test_layered_material},
+      {"run_gpu_batch: stream of problems == run_naive each", test_batch_matches_run_naive},
   };
   for (const auto& [name, fn] : cases) {
     const int before = g_fail;

@@ -114,4 +114,49 @@ RunReport run_gpu(ProblemState& state, int steps, const GpuOptions& opts, GpuRun
   return report;
 }
 
+RunReport run_gpu_batch(const std::vector<ProblemState*>& states, int steps, const GpuOptions& opts) {
+  if (steps < 0) throw ConfigError("steps must be >= 0");
+  if (opts.n_gpus != 1) throw ConfigError("run_gpu_batch drives one GPU (n_gpus = 1)");
+  RunReport report;
+  report.steps = report.steps_executed = steps;
+  report.threads = 1;
+  if (states.empty()) return report;
+  const GridDims dims = states[0]->dims;
+  report.dims = dims;
+  const std::size_t bytes = dims.padded_cells() * sizeof(ComplexScalar);
+  std::vector<const thiim_c128*> in;
+  in.reserve(states.size() * 40);
+  PinGuard pins;
+  auto add = [&](const FieldArray& a) {
+    in.push_back(reinterpret_cast<const thiim_c128*>(a.data()));
+    if (opts.pin_host) pins.pin(const_cast<ComplexScalar*>(a.data()), bytes);
+  };
+  for (ProblemState* st : states) {
+    if (!st) throw ConfigError("null state");
+    if (st->dims.nx != dims.nx || st->dims.ny != dims.ny || st->dims.nz != dims.nz)
+      throw ConfigError("all problems of a batch need the same grid dims");
+    for (int i = 0; i < kNumComponents; ++i) add(st->fields[i]);
+    for (int i = 0; i < kNumComponents; ++i) add(st->coeff_t[i]);
+    for (int i = 0; i < kNumComponents; ++i) add(st->coeff_c[i]);
+    for (int i = 0; i < kNumSourceComponents; ++i) add(st->coeff_src[i]);
+  }
+  thiim_dims d{dims.nx, dims.ny, dims.nz, dims.ghost};
+  thiim_gpu_opts o;
+  thiim_gpu_default_opts(&o);
+  o.device = opts.device;
+  o.engine = opts.engine;
+  o.time_block = opts.time_block;
+  o.z_chunk = opts.z_chunk;
+  o.tile_y = opts.tile_y;
+  thiim_gpu_batch_stats bs{};
+  check(thiim_gpu_run_batch(&d, &o, int(states.size()), in.data(), nullptr, steps, 0, &bs),
+        "thiim_gpu_run_batch");
+  report.engine = engine_name(bs.engine);
+  report.seconds = bs.seconds;
+  report.balance_model = thiim_gpu_balance_model(bs.engine, opts.time_block);
+  if (steps > 0 && bs.seconds > 0.0) report.mlups = bs.mlups;
+  report.verification = "skipped";
+  return report;
+}
+
 }  // namespace thiim

@@ -20,6 +20,8 @@
 #include "thiim/state.hpp"
 #include "thiim_gpu.h"
 
+#include <vector>
+
 namespace thiim {
 
 struct GpuOptions {
@@ -47,5 +49,15 @@ struct GpuRunExtras {
   long long kernel_launches = 0;
 };
 RunReport run_gpu(ProblemState& state, int steps, const GpuOptions& opts, GpuRunExtras* extras);
+
+// A stream of independent problems of one shape (e.g. the paper's sweep over
+// wavelengths): every state advanced `steps` iterations in place, each bitwise
+// == run_naive(*state, steps).  One GPU; uploads, sweeps and downloads of
+// consecutive problems overlap (thiim_gpu_run_batch).  The states must be
+// distinct objects (ConfigError otherwise).  RunReport of the whole stream:
+// seconds = wall clock of the call (copies included), mlups =
+// states x interior x steps / seconds, threads = 1.
+RunReport run_gpu_batch(const std::vector<ProblemState*>& states, int steps,
+                        const GpuOptions& opts = {});
 
 }  // namespace thiim
