@@ -526,8 +526,12 @@ class GpuEngine:
         _check(lib().thiim_gpu_step(self._ctx, steps, ctypes.byref(st)))
         return st
 
-    def download_fields(self, s: ProblemState) -> None:
-        _check(lib().thiim_gpu_download_fields(self._ctx, _ptrs(s.arrays[0:12])))
+    def download_fields(self, s) -> None:
+        """Into a ProblemState's fields, or into a list of 12 padded arrays."""
+        fs = s.arrays[0:12] if isinstance(s, ProblemState) else list(s)
+        if len(fs) != 12:
+            raise ConfigError("download_fields needs 12 arrays")
+        _check(lib().thiim_gpu_download_fields(self._ctx, _ptrs(fs)))
 
     def set_sanitize(self, on: bool = True) -> None:
         """Exactly-once store coverage check after every pass (debug mode)."""
@@ -564,9 +568,13 @@ class GpuEngine:
             self.download_array(a, s.arrays[a])
         return s
 
-    def compare_fields(self, ref: ProblemState) -> StateDiff:
+    def compare_fields(self, ref) -> StateDiff:
+        """On-device comparison with a ProblemState's fields or 12 padded arrays."""
+        fs = ref.arrays[0:12] if isinstance(ref, ProblemState) else list(ref)
+        if len(fs) != 12:
+            raise ConfigError("compare_fields needs 12 arrays")
         out = _Diff()
-        _check(lib().thiim_gpu_compare_fields(self._ctx, _ptrs(ref.arrays[0:12]), ctypes.byref(out)))
+        _check(lib().thiim_gpu_compare_fields(self._ctx, _ptrs(fs), ctypes.byref(out)))
         d = StateDiff()
         d.differing_values = int(out.differing_values)
         d.bitwise_equal = d.differing_values == 0
