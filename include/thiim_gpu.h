@@ -192,7 +192,8 @@ int thiim_gpu_compare_fields(thiim_gpu_ctx* ctx, const thiim_c128* const ref_fie
  * outputs[12*i .. 12*i+11] (NULL outputs: back into the problem's own field
  * arrays, in place like run_naive).  inputs[40*i .. 40*i+39] are problem i's
  * arrays in thiim_gpu_upload order (12 fields, 12 t, 12 c, 4 src).
- * Problems are pipelined over `depth` device contexts (<= 0: 3): problem i
+ * Problems are pipelined over `depth` device contexts (<= 0: 3; fewer when
+ * device memory holds fewer, stats->depth says how many ran): problem i
  * uploads while i-1 computes and i-2 downloads, each resource in problem
  * order.  Host buffers should be pinned (thiim_gpu_pin_host) for the copies to
  * overlap.  An output may be shared by several problems but must not overlap
@@ -335,6 +336,13 @@ int thiim_gpu_coverage(thiim_gpu_ctx* ctx, unsigned long long* passes,
 
 /* Blocks until all work queued on the context's streams has finished. */
 int thiim_gpu_sync(thiim_gpu_ctx* ctx);
+
+/* Contexts take their state from the device's stream-ordered memory pool and
+ * give it back on destroy; the pool keeps the pages for the next context
+ * (creating a 14 GB context costs ~2 ms instead of a fresh allocation).  This
+ * returns the cached, unused pages of `device`'s pool to the driver, e.g.
+ * before another library allocates device memory. */
+int thiim_gpu_release_cached(int device);
 
 /* Message of the last failing call on this thread ("" if none). */
 const char* thiim_gpu_last_error(void);

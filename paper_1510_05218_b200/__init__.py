@@ -40,7 +40,7 @@ __all__ = [
     "ENGINE_FUSED", "ENGINE_TBLOCK", "GpuOptions", "RunReport", "StateDiff", "GpuEngine",
     "run_gpu", "generate_problem", "compare_states", "balance_model", "lib",
     "compress_coefficients", "expand_coefficients", "COEFF_FULL", "COEFF_TABLE",
-    "run_gpu_batch", "BatchReport",
+    "run_gpu_batch", "BatchReport", "release_cached",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -313,6 +313,7 @@ EXPORTED_SYMBOLS = [
     "thiim_gpu_coverage", "thiim_scheme_default", "thiim_gpu_init_benchmark",
     "thiim_gpu_init_materials", "thiim_gpu_selftest_cdiv", "thiim_gpu_slab_export",
     "thiim_gpu_slab_import", "thiim_gpu_slab_detach", "thiim_gpu_run_batch",
+    "thiim_gpu_release_cached",
 ]
 
 _LIB = None
@@ -355,6 +356,7 @@ def lib() -> ctypes.CDLL:
     L.thiim_gpu_selftest_cdiv.argtypes = [ctypes.c_int, P, P]
     L.thiim_gpu_coverage.argtypes = [P, ctypes.POINTER(ctypes.c_ulonglong),
                                      ctypes.POINTER(ctypes.c_ulonglong)]
+    L.thiim_gpu_release_cached.argtypes = [ctypes.c_int]
     L.thiim_gpu_run_batch.argtypes = [ctypes.POINTER(_Dims), ctypes.POINTER(_Opts), ctypes.c_int,
                                       PP, PP, ctypes.c_int, ctypes.c_int,
                                       ctypes.POINTER(_BatchStats)]
@@ -649,6 +651,11 @@ class BatchReport:
     kernel_launches: int = 0
     h2d_bytes: int = 0
     d2h_bytes: int = 0
+
+
+def release_cached(device: int = 0) -> None:
+    """Return the device pool's cached, unused pages to the driver."""
+    _check(lib().thiim_gpu_release_cached(device))
 
 
 def run_gpu_batch(states: List[ProblemState], steps: int, opts: Optional[GpuOptions] = None,

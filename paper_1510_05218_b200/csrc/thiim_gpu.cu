@@ -1369,6 +1369,17 @@ int thiim_gpu_sync(thiim_gpu_ctx* ctx) {
   return THIIM_OK;
 }
 
+int thiim_gpu_release_cached(int device) {
+  g_err.clear();
+  int n = 0;
+  CK(cudaGetDeviceCount(&n));
+  if (device < 0 || device >= n) return fail(THIIM_ERR_CONFIG, "no such device");
+  CK(cudaSetDevice(device));
+  CK(cudaDeviceSynchronize());
+  if (cudaMemPool_t pool = device_pool(device)) CK(cudaMemPoolTrimTo(pool, 0));
+  return THIIM_OK;
+}
+
 void thiim_gpu_destroy(thiim_gpu_ctx* ctx) {
   if (!ctx) return;
   for (auto& sl : ctx->slabs) {
@@ -2004,7 +2015,15 @@ int thiim_gpu_run_batch(const thiim_dims* dims, const thiim_gpu_opts* opts, int 
   };
   int r;
   for (int d = 0; d < depth; ++d)
-    if ((r = thiim_gpu_create(dims, &o, &ctxs[d]))) return bail(r);
+    if ((r = thiim_gpu_create(dims, &o, &ctxs[d]))) {
+      // device memory for fewer contexts: a shallower pipeline (depth 1 still
+      // runs, one problem at a time); any other failure is an error
+      if (d == 0 || r != THIIM_ERR_SETUP) return bail(r);
+      depth = d;
+      ctxs.resize(d);
+      g_err.clear();
+      break;
+    }
   {
     const cudaError_t e = cudaSetDevice(ctxs[0]->slabs[0].device);
     for (auto& x : ev)

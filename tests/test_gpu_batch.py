@@ -116,3 +116,27 @@ def test_batch_pinned_large():
     assert fields_equal(outs[0], one.fields) and fields_equal(outs[1], one.fields)
     # pipelining: the whole batch takes less than the phases run back to back
     assert rep.device_seconds < rep.upload_seconds + rep.kernel_seconds + rep.download_seconds
+
+
+@pytest.mark.gpu
+def test_batch_depth_shrinks_to_fit_memory():
+    """With device memory for one context only, the stream runs at depth 1
+    (one problem at a time) instead of failing; results unchanged."""
+    import torch
+
+    d = P.GridDims(128, 128, 128)
+    ctx_bytes = d.padded_cells() * 16 * 52  # 2 field sets + 28 coefficient arrays
+    states = [P.generate_problem(d, P.GEN_RANDOM, seed=s) for s in (1, 2, 3)]
+    want = [oracle_run(s, 2) for s in states]
+    outs = [[np.zeros_like(a) for a in s.fields] for s in states]
+    P.release_cached(0)
+    free, _ = torch.cuda.mem_get_info(0)
+    hog = torch.empty(free - int(1.5 * ctx_bytes), dtype=torch.uint8, device="cuda:0")
+    try:
+        rep = P.run_gpu_batch(states, 2, outputs=outs, depth=3)
+    finally:
+        del hog
+        torch.cuda.empty_cache()
+    assert rep.depth == 1, rep
+    for o, w in zip(outs, want):
+        assert fields_equal(o, w.fields)
