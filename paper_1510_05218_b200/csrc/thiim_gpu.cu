@@ -1980,23 +1980,35 @@ int thiim_gpu_run_batch(const thiim_dims* dims, const thiim_gpu_opts* opts, int 
   // problem i's download may run while problem j's upload reads its inputs:
   // outputs must not overlap another problem's inputs (shared outputs are fine,
   // downloads are serialised; writing back over the problem's own inputs is fine)
-  for (int i = 0; i < n_problems; ++i)
-    for (int k = 0; k < 12; ++k) {
-      const char* o0 = (const char*)out_ptr(i, k);
-      for (int j = 0; j < n_problems; ++j) {
-        if (j == i) continue;
-        for (int a = 0; a < 40; ++a) {
-          const char* i0 = (const char*)inputs[(size_t)j * 40 + a];
-          if (o0 < i0 + bytes && i0 < o0 + bytes) {
-            char msg[160];
-            std::snprintf(msg, sizeof msg,
-                          "output field %d of problem %d overlaps input array %d of problem %d", k,
-                          i, a, j);
-            return fail(THIIM_ERR_CONFIG, msg);
-          }
+  // (all arrays have the same length, so input starts sorted once and a
+  // window search per output keep this O(n log n) for distinct inputs)
+  {
+    struct In {
+      uintptr_t start;
+      int problem, array;
+    };
+    std::vector<In> ins;
+    ins.reserve((size_t)n_problems * 40);
+    for (int j = 0; j < n_problems; ++j)
+      for (int a = 0; a < 40; ++a) ins.push_back({(uintptr_t)inputs[(size_t)j * 40 + a], j, a});
+    std::sort(ins.begin(), ins.end(), [](const In& x, const In& y) { return x.start < y.start; });
+    for (int i = 0; i < n_problems; ++i)
+      for (int k = 0; k < 12; ++k) {
+        const uintptr_t o0 = (uintptr_t)out_ptr(i, k);
+        // inputs overlapping [o0, o0 + bytes) start in (o0 - bytes, o0 + bytes)
+        const uintptr_t lo = o0 > bytes ? o0 - bytes : 0;
+        auto it = std::upper_bound(ins.begin(), ins.end(), lo,
+                                   [](uintptr_t v, const In& x) { return v < x.start; });
+        for (; it != ins.end() && it->start < o0 + bytes; ++it) {
+          if (it->problem == i) continue;
+          char msg[160];
+          std::snprintf(msg, sizeof msg,
+                        "output field %d of problem %d overlaps input array %d of problem %d", k, i,
+                        it->array, it->problem);
+          return fail(THIIM_ERR_CONFIG, msg);
         }
       }
-    }
+  }
   const auto t0 = std::chrono::steady_clock::now();
   std::vector<thiim_gpu_ctx*> ctxs(depth, nullptr);
   // per problem: upload, sweep and download brackets
