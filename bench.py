@@ -313,6 +313,30 @@ def _line(P, args, world, dims_rank, engine_ran, dev_secs, launches, e2e, clk, e
     }
 
 
+def host_available_bytes() -> int:
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemAvailable:"):
+                    return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return 0
+
+
+def e2e_skip_reason(args, dims):
+    """Why the host-memory e2e leg cannot run for this configuration, or None."""
+    if args.coeff == "table":
+        return ("table layout: its inputs (material ids + table) are this engine's own format, "
+                "generated on the device; e2e is measured on the reference layout")
+    need = 52 * dims.padded_cells() * 16  # 40 input arrays + 12 result fields, pinned
+    avail = host_available_bytes()
+    if avail and need > 0.8 * avail:
+        return "host RAM: %.0f GB of pinned inputs/outputs, %.0f GB available" % (need / 1e9,
+                                                                               avail / 1e9)
+    return None
+
+
 def run_native_single(P, args, opts, iters):
     dims = P.GridDims(*GRID)
     eng = P.GpuEngine(dims, opts)
@@ -336,7 +360,10 @@ def run_native_single(P, args, opts, iters):
     # destroy), serial, with its phases.
     e2e = None
     e2e_extra = {}
-    if not args.no_e2e:
+    skip = e2e_skip_reason(args, dims)
+    if skip:
+        e2e_extra = {"skipped": skip}
+    if not args.no_e2e and not skip:
         host = P.generate_problem(dims, KIND, SEED)
         out = [np.zeros_like(a) for a in host.fields]
         pinned = host.arrays + out
@@ -346,9 +373,10 @@ def run_native_single(P, args, opts, iters):
         # three contexts the timed call reuses
         P.run_gpu_batch([host] * 3, iters, opts, outputs=[out] * 3)
         rep = P.run_gpu_batch([host] * args.steps, iters, opts, outputs=[out] * args.steps)
-        e2e = dims.interior_cells() * iters * args.steps / rep.seconds / 1e6
-        e2e_extra = {
+        stream = {
+            "value": round(dims.interior_cells() * iters * args.steps / rep.seconds / 1e6, 2),
             "api": "run_gpu_batch (thiim_gpu_run_batch), depth %d, one problem per step" % rep.depth,
+            "depth": rep.depth,
             "call_ms": round(1e3 * rep.seconds, 1),
             "device_span_ms": round(1e3 * rep.device_seconds, 1),
             "device_ms_per_step": {
@@ -367,7 +395,7 @@ def run_native_single(P, args, opts, iters):
             t.append(time.perf_counter())
             e.step(iters)
             t.append(time.perf_counter())
-            e.download_fields(host)
+            e.download_fields(out)
             t.append(time.perf_counter())
             e.close()
             t.append(time.perf_counter())
@@ -377,14 +405,21 @@ def run_native_single(P, args, opts, iters):
                     phases[j] += t[j + 1] - t[j]
         for a in pinned:
             P.lib().thiim_gpu_unpin_host(a.ctypes.data)
-        e2e_extra["serial_value"] = round(dims.interior_cells() * iters * nser / secs / 1e6, 2)
-        e2e_extra["serial_api"] = "run_gpu call sequence, %d steps" % nser
-        e2e_extra["serial_phases_ms_per_step"] = dict(
-            zip(["create", "upload", "step", "download", "destroy"],
-                [round(1e3 * v / nser, 2) for v in phases]))
+        serial = {
+            "value": round(dims.interior_cells() * iters * nser / secs / 1e6, 2),
+            "api": "run_gpu call sequence (create, upload, step, download, destroy), %d steps"
+                   % nser,
+            "phases_ms_per_step": dict(zip(["create", "upload", "step", "download", "destroy"],
+                                           [round(1e3 * v / nser, 2) for v in phases])),
+        }
+        # headline: the faster of the two public-API paths (the stream overlaps
+        # copies with sweeps when the device holds >= 2 contexts; with one it
+        # cannot, and the plain call sequence is the better way to run)
+        best = stream if stream["value"] >= serial["value"] else serial
+        e2e = best["value"]
+        e2e_extra = {"api": best["api"], "stream": stream, "serial": serial}
     line = _line(P, args, 1, dims, engine_ran, dev_secs, launches, e2e, clk, {})
-    if e2e:
-        line["e2e"].update(e2e_extra)
+    line["e2e"].update(e2e_extra)
     return line
 
 

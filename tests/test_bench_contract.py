@@ -38,8 +38,10 @@ def test_native_line():
     assert d["config"]["workload"].startswith("configs[0]")
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
-    assert e["api"].startswith("run_gpu_batch") and e["serial_value"] > 0
-    assert set(e["device_ms_per_step"]) == {"upload", "sweep", "download"}
+    assert e["stream"]["value"] > 0 and e["serial"]["value"] > 0
+    assert e["value"] == max(e["stream"]["value"], e["serial"]["value"])
+    assert e["api"] in (e["stream"]["api"], e["serial"]["api"])
+    assert set(e["stream"]["device_ms_per_step"]) == {"upload", "sweep", "download"}
     assert d["gpu_launches"] >= 3
     r = d["roofline"]
     assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0 < r["frac"] < 1.2
