@@ -33,6 +33,10 @@
 #include "thiim_producer.cuh"
 #include "thiim_tmem.cuh"
 
+#ifndef THIIM_PATTERN_ONLY
+#define THIIM_PATTERN_ONLY 0
+#endif
+
 namespace thiim_gpu {
 
 // Level-2 sequence (11 groups); src 2 = level-1 output of plane r (component in
@@ -611,12 +615,57 @@ __device__ __forceinline__ void tblock_tm_body(TmSmem<BY, NG>& sm, const Grid& g
         // level 1 keeps coefficients in L2 for level 2 (their last use)
         if (q <= q1) produce_plane_ct<true>(P, fb, cb, q, pf1, pc1);
         const int r = q - LAG;
-        if (r >= z0 - 1 && r < z1) produce_level2_coef_ct(P, cb, r, pc2);
+        if (r >= z0 - 1 && r < z1) {
+#if THIIM_PATTERN_ONLY == 2  // experiment: level 2 re-reads no coefficients
+          for (int k = 0; k < 8; ++k) {
+            P.template begin<0>();
+            P.end();
+          }
+#else
+          produce_level2_coef_ct(P, cb, r, pc2);
+#endif
+        }
       }
     }
     return;
   }
 
+#if THIIM_PATTERN_ONLY
+  // Experiment builds only (tools/build_variant.sh NAME -DTHIIM_PATTERN_ONLY=1):
+  // the same producer stream, ring protocol and output stores with no compute,
+  // i.e. the memory-system ceiling of this access pattern.  Results are garbage.
+  {
+    const int x = xb + lx, y = yb + ty;
+    const bool own2 = lx >= 2 && lx <= W - 3 && ty >= 2 && ty <= BY - 3;
+    const bool interior = (x >= 0) && (x < g.nx) && (y >= 0) && (y < g.ny);
+    auto& R = sm.ring;
+    RingCursor rc = ring_cursor(R);
+    const uint64_t first = policy_evict_first();
+    for (int q = qs; q <= qe; ++q) {
+      if (q <= q1)
+        for (int k = 0; k < 12; ++k) {
+          ring_wait(R, rc);
+          ring_release(R, rc, tx, 0u);
+        }
+      const int r = q - LAG;
+      if (r >= z0 - 1 && r < z1) {
+        for (int k = 0; k < 8; ++k) {
+          ring_wait(R, rc);
+          ring_release(R, rc, tx, 0u);
+        }
+        if (r >= z0 && own2 && interior && r >= po.st0 && r < po.st1) {
+          const long long i = g.idx(x, y, r);
+          for (int k = 0; k < 12; ++k) st_hint(A.fo[k] + i, make_double2(0.0, 0.0), first);
+        }
+      }
+    }
+    tm_fence_before();
+    named_sync(1, NCOMP);
+    tm_fence_after();
+    if (ty == 0) tm_dealloc<512>(sm.tmem_base);
+    return;
+  }
+#endif
   // -------------------------------------------------------------- consumers
   const uint32_t tcar = tm_warp_addr(sm.tmem_base, ty, 128 * (ty >> 2));
   const uint32_t tnext = tcar + 96;
