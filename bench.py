@@ -158,6 +158,8 @@ def reference_engines_sample(grid, threads):
         secs, executed = O.ref_run_mwd(grid, s.arrays, 4, 8, 1, 1, 1, 1, threads)
         out["mwd_mlups"] = round(cells * executed / secs / 1e6, 3)
         out["mwd_params"] = "dw 8, bz 1, shape 1x1x1, %d threads" % threads
+        # the reference's own host triad (its `bandwidth` subcommand), SURVEY s8d
+        out["host_triad_gbs"] = round(O.ref_measure_bandwidth(threads), 1)
     except Exception as e:  # report, never fail the bench line
         out["reference_engines_error"] = str(e)[:200]
     return out
@@ -244,17 +246,24 @@ def _roofline(P, dims, engine_ran, dev_secs, launches, table=False):
         bytes_launch = 832.0 * dims.interior_cells()
         kname = "k_fused_tma<15,6>"
     achieved = bytes_launch / per_launch_s / 1e9
+    # ncu DRAM bytes per launch of this kernel on this grid (profiles/traffic.json,
+    # written by tools/summarize_ncu.py); null for a grid that was not captured
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
-            traffic = json.load(f).get(kname)
+            traffic = json.load(f).get("%s@%dx%dx%d" % (kname, dims.nx, dims.ny, dims.nz))
     balance = (385.0 / (2 if engine_ran == P.ENGINE_TBLOCK else 1)) if table \
         else P.balance_model(engine_ran)
+    steps_per_launch = 2 if engine_ran == P.ENGINE_TBLOCK else 1
+    if engine_ran == P.ENGINE_SPLIT:
+        steps_per_launch = 0.5
     return {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
             "frac": round(achieved / hbm, 4), "traffic": traffic, "kernel": kname,
             "algorithmic_bytes_per_launch": bytes_launch, "peak_kind": peak_kind,
             "bytes_per_lup_model": balance,
+            "traffic_bytes_per_lup": (round(traffic / (dims.interior_cells() * steps_per_launch), 1)
+                                      if traffic else None),
             "lup_roofline_mlups": round(hbm * 1e3 / balance, 1)}
 
 

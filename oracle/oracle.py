@@ -212,6 +212,15 @@ def ref_run_mwd(dims, arrays, steps, dw, bz, tgz, tgx, tgc, threads):
     return sec.value, ex.value
 
 
+def ref_measure_bandwidth(threads: int, cache_bytes: int = 45 << 20) -> float:
+    """reference measure_bandwidth (bandwidth.cpp:12-44): host triad GB/s, best of
+    five; cache_bytes defaults to the reference's profile (perf_models.hpp:10)."""
+    gbs = ctypes.c_double()
+    _ref_check(ref_lib().ref_measure_bandwidth(threads, ctypes.c_ulonglong(cache_bytes),
+                                               ctypes.byref(gbs)))
+    return gbs.value
+
+
 def ref_benchmark_problem(dims, omega=0.4, tau=1.0, delta=1.0):
     arrays = new_arrays(dims)
     nx, ny, nz = dims

@@ -16,6 +16,7 @@
 #include <exception>
 #include <string>
 
+#include "thiim/bandwidth.hpp"
 #include "thiim/coefficients.hpp"
 #include "thiim/kernels.hpp"
 #include "thiim/mwd.hpp"
@@ -199,5 +200,11 @@ int ref_compare_states(int nx, int ny, int nz, double* const* a, double* const* 
 }
 
 double ref_code_balance_naive() { return code_balance_naive(); }
+
+// the reference's host triad (bandwidth.cpp:12-44; the CLI's `bandwidth`
+// subcommand, tools/main.cpp:433-436), GB/s best of five
+int ref_measure_bandwidth(int threads, unsigned long long cache_bytes, double* gbs) {
+  return guarded([&] { *gbs = measure_bandwidth(threads, cache_bytes); });
+}
 
 }  // extern "C"

@@ -46,6 +46,11 @@ def test_native_line():
     r = d["roofline"]
     assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0 < r["frac"] < 1.2
     assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-3
+    assert "traffic_bytes_per_lup" in r  # null unless this grid was captured under ncu
+    cb = d["cpu_baseline"]
+    assert cb["value"] > 0 and cb["cores"] >= 1
+    if cb["kind"] == "reference":
+        assert cb["host_triad_gbs"] > 0  # the reference's own measure_bandwidth
     c = d["clocks"]
     assert c["sm_max_mhz"] and isinstance(c["reasons"], list)
     b = d["cpu_baseline"]

@@ -1,7 +1,7 @@
 """Summarize ncu captures into profiles/ (run in the dev container).
 
     python tools/summarize_ncu.py --rep gpurun_out/prof.ncu-rep --launches gpurun_out/launches.csv \
-        --tag r01 --kernel k_fused_tma --traffic-key "k_fused_tma<16,20>"
+        --tag r01 --kernel k_fused_tma --traffic-key "k_fused_tma<15,6>@256x256x256"
 
 Writes profiles/<tag>_<kernel>_ncu.md (key metrics + stall reasons of the
 --set full capture), profiles/<tag>_launches.md (per-kernel share of the
@@ -66,7 +66,7 @@ def main():
     ap.add_argument("--launches")
     ap.add_argument("--tag", required=True)
     ap.add_argument("--kernel", default="k_fused_tma")
-    ap.add_argument("--traffic-key", default=None)
+    ap.add_argument("--traffic-key", default=None, help="kernel<..>@NXxNYxNZ (bench.py looks it up per grid)")
     ap.add_argument("--algorithmic-bytes", type=float, default=None)
     ap.add_argument("--note", default="")
     a = ap.parse_args()
