@@ -101,7 +101,7 @@ class Clocks:
         except Exception:
             self.proc.kill()
             out = ""
-        sm, mx, reasons = [], None, set()
+        sm, pw, mx, reasons = [], [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         post = False
         if not out.strip():  # timed region shorter than the sampler's first tick
@@ -121,12 +121,17 @@ class Clocks:
                 mx = float(f[2])
             except ValueError:
                 continue
+            try:
+                pw.append(float(f[3]))
+            except ValueError:
+                pass
             for n, v in zip(names, f[5:9]):
                 if v.lower() == "active":
                     reasons.add(n)
         if sm:
             self.result = {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx,
-                           "reasons": sorted(reasons), "samples": 0 if post else len(sm)}
+                           "reasons": sorted(reasons), "samples": 0 if post else len(sm),
+                           "power_w": float(np.median(pw)) if pw else None}
             if post:
                 self.result["note"] = "timed region shorter than one sampling tick: post-run sample"
 

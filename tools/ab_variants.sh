@@ -8,6 +8,6 @@ for i in $(seq "$reps"); do
     name=${v%%=*}; lib=${v#*=}
     [ "$lib" = product ] && lib=paper_1510_05218_b200/libthiim_gpu.so
     timeout 600 env THIIM_LIB=$lib python bench.py $args --no-e2e --no-cpu-baseline 2>/dev/null | tail -1 |
-      python -c "import json,sys;d=json.loads(sys.stdin.read());print('$name',d['value'],d['roofline']['frac'],d['clocks']['sm_mhz'])"
+      python -c "import json,sys;d=json.loads(sys.stdin.read());print('$name',d['value'],d['roofline']['frac'],d['clocks']['sm_mhz'],d['clocks'].get('power_w'))"
   done
 done
