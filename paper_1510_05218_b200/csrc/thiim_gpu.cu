@@ -23,6 +23,11 @@
 #include <string>
 #include <vector>
 
+// ring depth (slots) of the default TBLOCK kernel (experiment builds override)
+#ifndef THIIM_TB_NG
+#define THIIM_TB_NG 6
+#endif
+
 #include "../../include/thiim_gpu.h"
 #include "thiim_common.cuh"
 #include "thiim_complex.cuh"
@@ -790,7 +795,7 @@ int launch_tblock2_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches, const Pee
   const size_t smem = scratch ? sizeof(TbSmem<BY, NG>) : sizeof(TmSmem<BY, NG>);
   static std::atomic<unsigned> attr_set{0};
   if (setup_needed(attr_set, s.device)) {
-    if constexpr (BY == 15)
+    if constexpr (BY == 15 && sizeof(TbSmem<BY, NG>) <= 232448)
       CK(cudaFuncSetAttribute(k_tblock2<BY, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)sizeof(TbSmem<BY, NG>)));
     const int tm_smem = (int)sizeof(TmSmem<BY, NG>);
@@ -918,12 +923,12 @@ int launch_tblock_table_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches, cons
 int launch_tblock2(thiim_gpu_ctx* ctx, Slab& s, long long* launches, const PeerOut& po) {
   CK(cudaSetDevice(s.device));
   if (s.table) return launch_tblock_table_t<15, 5>(ctx, s, launches, po);
-  if (s.deep) return launch_tblock2_t<15, 6>(ctx, s, launches, po);
+  if (s.deep) return launch_tblock2_t<15, THIIM_TB_NG>(ctx, s, launches, po);
   switch (ctx->opts.tile_y) {  // CTA height incl. the 4 halo rows; ring depth fills the smem
     case 16: return launch_tblock2_t<16, 5>(ctx, s, launches, po);
     case 14: return launch_tblock2_t<14, 6>(ctx, s, launches, po);
     case 12: return launch_tblock2_t<12, 7>(ctx, s, launches, po);
-    default: return launch_tblock2_t<15, 6>(ctx, s, launches, po);
+    default: return launch_tblock2_t<15, THIIM_TB_NG>(ctx, s, launches, po);
   }
 }
 

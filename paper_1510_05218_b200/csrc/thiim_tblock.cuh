@@ -560,9 +560,14 @@ inline void seq_level2_coef(GroupSeq& S, CS cslot) {
 
 template <int BY, int NG>
 struct TmSmem {
+#if THIIM_PATTERN_ONLY
+  static constexpr int SROWS = 1;  // pattern builds exchange nothing (room for a deeper ring)
+#else
+  static constexpr int SROWS = BY;
+#endif
   Ring<BY, NG> ring;
-  double2 sE[3][BY][32];
-  double2 sH[3][BY][32];
+  double2 sE[3][SROWS][32];
+  double2 sH[3][SROWS][32];
   uint32_t tmem_base;
 };
 
@@ -591,14 +596,44 @@ __device__ __forceinline__ void tblock_tm_body(TmSmem<BY, NG>& sm, const Grid& g
   const int qe = z1 + LAG - 1;
 
   if (ty == 0) tm_alloc<512>(&sm.tmem_base);
+#if THIIM_PATTERN_ONLY == 3
+  // experiment: level-1 (DRAM) groups and level-2 coefficient (L2) groups in
+  // two rings of 4 + 2 slots, each with its own producer lane
+  using RingA = Ring<BY, 4>;
+  using RingB = Ring<BY, NG - 4>;
+  RingA& RA = *reinterpret_cast<RingA*>(&sm.ring);
+  RingB& RB = *reinterpret_cast<RingB*>(reinterpret_cast<char*>(&sm.ring) + sizeof(RingA));
+  if (tx == 0 && ty == 0) {
+    ring_init(RA, BY);
+    ring_init(RB, BY);
+    fence_mbar_init();
+  }
+#else
   if (tx == 0 && ty == 0) {
     ring_init(sm.ring, BY);
     fence_mbar_init();
   }
+#endif
   tm_fence_before();
   __syncthreads();
   tm_fence_after();
 
+#if THIIM_PATTERN_ONLY == 3
+  if (ty == BY) {
+    const uint64_t keep = policy_evict_last(), drop = policy_evict_first();
+    if (tx == 0) {
+      RingProducer<BY, 4, W> PA(RA, maps, xb, yb0);
+      for (int q = qs; q <= q1; ++q) produce_plane_ct<true>(PA, fb, cb, q, drop, keep);
+    } else if (tx == 1) {
+      RingProducer<BY, NG - 4, W> PB(RB, maps, xb, yb0);
+      for (int q = qs; q <= qe; ++q) {
+        const int r = q - LAG;
+        if (r >= z0 - 1 && r < z1) produce_level2_coef_ct(PB, cb, r, drop);
+      }
+    }
+    return;
+  }
+#endif
   if (ty == BY) {
     // ------------------------------------------------------------ producer
     if (tx == 0) {
@@ -638,8 +673,16 @@ __device__ __forceinline__ void tblock_tm_body(TmSmem<BY, NG>& sm, const Grid& g
     const int x = xb + lx, y = yb + ty;
     const bool own2 = lx >= 2 && lx <= W - 3 && ty >= 2 && ty <= BY - 3;
     const bool interior = (x >= 0) && (x < g.nx) && (y >= 0) && (y < g.ny);
+#if THIIM_PATTERN_ONLY == 3
+    auto& R = RA;
+    auto& R2 = RB;
+    RingCursor rc = ring_cursor(R), rc2 = ring_cursor(R2);
+#else
     auto& R = sm.ring;
+    auto& R2 = sm.ring;
     RingCursor rc = ring_cursor(R);
+    RingCursor& rc2 = rc;
+#endif
     const uint64_t first = policy_evict_first();
     for (int q = qs; q <= qe; ++q) {
       if (q <= q1)
@@ -650,8 +693,8 @@ __device__ __forceinline__ void tblock_tm_body(TmSmem<BY, NG>& sm, const Grid& g
       const int r = q - LAG;
       if (r >= z0 - 1 && r < z1) {
         for (int k = 0; k < 8; ++k) {
-          ring_wait(R, rc);
-          ring_release(R, rc, tx, 0u);
+          ring_wait(R2, rc2);
+          ring_release(R2, rc2, tx, 0u);
         }
         if (r >= z0 && own2 && interior && r >= po.st0 && r < po.st1) {
           const long long i = g.idx(x, y, r);
