@@ -55,3 +55,54 @@ def test_native_line():
     assert c["sm_max_mhz"] and isinstance(c["reasons"], list)
     b = d["cpu_baseline"]
     assert b["value"] > 0 and b["unit"] == "MLUP/s" and b["cores"] >= 1
+
+
+def _bench_module():
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("thiim_bench", os.path.join(ROOT, "bench.py"))
+    m = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(m)
+    return m
+
+
+def test_roofline_helper_keys_traffic_by_kernel_and_grid():
+    """Host logic only: the roofline of a TBLOCK launch (two iterations) uses the
+    algorithmic 832 B per cell, reports ncu traffic only for a captured grid."""
+    import paper_1510_05218_b200 as P
+    B = _bench_module()
+    dims = P.GridDims(256, 256, 256)
+    r = B._roofline(P, dims, P.ENGINE_TBLOCK, dev_secs=0.15, launches=50)
+    cells = 256 ** 3
+    assert r["algorithmic_bytes_per_launch"] == 832.0 * cells
+    assert abs(r["achieved"] - 832.0 * cells / (0.15 / 50) / 1e9) < 0.1
+    assert r["bytes_per_lup_model"] == 416.0 and r["kernel"] == "k_tblock_tm<15,6>"
+    with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+        t = json.load(f)
+    if "k_tblock_tm<15,6>@256x256x256" in t:
+        assert r["traffic"] == t["k_tblock_tm<15,6>@256x256x256"]
+        assert abs(r["traffic_bytes_per_lup"] - r["traffic"] / (2 * cells)) < 0.1
+    other = B._roofline(P, P.GridDims(512, 512, 512), P.ENGINE_TBLOCK, 1.0, 100)
+    assert other["traffic"] is None and other["traffic_bytes_per_lup"] is None
+
+
+def test_clock_sampler_parses_reasons_and_power():
+    """Host logic only: the nvidia-smi sampler's parsing (median SM clock and
+    power, throttle reasons) on canned output."""
+    B = _bench_module()
+
+    class FakeProc:
+        def terminate(self):
+            pass
+
+        def communicate(self, timeout=None):
+            return ("0, 1530, 1965, 990.5, 0x4, Not Active, Not Active, Not Active, Active\n"
+                    "0, 1545, 1965, 998.1, 0x4, Not Active, Not Active, Not Active, Active\n"
+                    "0, 1560, 1965, 994.0, 0x0, Not Active, Not Active, Not Active, Not Active\n",
+                    "")
+
+    c = B.Clocks(0)
+    c.proc = FakeProc()
+    c.__exit__(None, None, None)
+    assert c.result["sm_mhz"] == 1545.0 and c.result["sm_max_mhz"] == 1965.0
+    assert c.result["reasons"] == ["sw_power_cap"] and c.result["samples"] == 3
+    assert abs(c.result["power_w"] - 994.0) < 1e-9
