@@ -81,7 +81,10 @@ def test_roofline_helper_keys_traffic_by_kernel_and_grid():
     if "k_tblock_tm<15,6>@256x256x256" in t:
         assert r["traffic"] == t["k_tblock_tm<15,6>@256x256x256"]
         assert abs(r["traffic_bytes_per_lup"] - r["traffic"] / (2 * cells)) < 0.1
-    other = B._roofline(P, P.GridDims(512, 512, 512), P.ENGINE_TBLOCK, 1.0, 100)
+    if "k_tblock_tm<15,6>@512x512x512" in t:
+        big = B._roofline(P, P.GridDims(512, 512, 512), P.ENGINE_TBLOCK, 1.0, 100)
+        assert big["traffic"] == t["k_tblock_tm<15,6>@512x512x512"]
+    other = B._roofline(P, P.GridDims(384, 320, 96), P.ENGINE_TBLOCK, 1.0, 100)
     assert other["traffic"] is None and other["traffic_bytes_per_lup"] is None
 
 
