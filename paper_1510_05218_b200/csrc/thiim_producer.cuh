@@ -207,8 +207,9 @@ __device__ __forceinline__ void produce_level2_coef_ct(PR& P, int cb, int r, uin
   P.end();
 }
 
-// Table-layout plane z (seq_table): E_old(z+1) x6, H_old(z) x6 -- the only
-// HBM-streamed arrays when coefficients come from the material table.
+// Table-layout plane z (seq_table's 12 arrays, in three full groups instead of
+// its four): E_old(z+1) x6, H_old(z) x6 -- the only HBM-streamed arrays when
+// coefficients come from the material table.
 template <int BY, int NG>
 __device__ __forceinline__ void produce_table_plane_ct(RingProducer<BY, NG>& P, int fb, int z,
                                                        uint64_t pol) {
@@ -222,19 +223,18 @@ __device__ __forceinline__ void produce_table_plane_ct(RingProducer<BY, NG>& P, 
   P.template box<BOX_A>(2, fb + EYX, p1, pol);
   P.template box<BOX_A>(3, fb + EYZ, p1, pol);
   P.end();
-  P.template begin<2 * SA>();
+  // three full groups per plane: the z-components of E_old ride with Hzx/Hzy
+  P.template begin<2 * SA + 2 * SB>();
   P.template box<BOX_A>(0, fb + EZX, p1, pol);
   P.template box<BOX_A>(1, fb + EZY, p1, pol);
+  P.template box<BOX_B>(2, fb + HZX, p0, pol);
+  P.template box<BOX_B>(3, fb + HZY, p0, pol);
   P.end();
   P.template begin<2 * SBY + 2 * SBX>();
   P.template box<BOX_BY>(0, fb + HXY, p0, pol);
   P.template box<BOX_BY>(1, fb + HXZ, p0, pol);
   P.template box<BOX_BX>(2, fb + HYX, p0, pol);
   P.template box<BOX_BX>(3, fb + HYZ, p0, pol);
-  P.end();
-  P.template begin<2 * SB>();
-  P.template box<BOX_B>(0, fb + HZX, p0, pol);
-  P.template box<BOX_B>(1, fb + HZY, p0, pol);
   P.end();
 }
 

@@ -173,6 +173,7 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
       double2 e[6];
       tm_ld6(tnext, e);  // E_old(q)
       double2 nEx, nEy;
+      double2 h45[2];
       {
         double2 en[6];
         ring_wait(R, rc);
@@ -182,7 +183,9 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
         ring_wait(R, rc);
         en[4] = RD(0, BOX_A);
         en[5] = RD(1, BOX_A);
-        ring_release(R, rc, tx, ring_dep(en[4], en[5]));
+        h45[0] = RD(2, BOX_B);
+        h45[1] = RD(3, BOX_B);
+        ring_release(R, rc, tx, ring_dep(en[4], en[5], h45[0], h45[1]));
         tm_st6(tnext, en);  // E_old(q+1) for the next plane
         nEx = csum(en[EXY], en[EXZ]);
         nEy = csum(en[EYX], en[EYZ]);
@@ -203,10 +206,8 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
       h[2] = RD(2, BOX_BX);
       h[3] = RD(3, BOX_BX);
       ring_release(R, rc, tx, ring_dep(h[0], h[1], h[2], h[3]));
-      ring_wait(R, rc);
-      h[4] = RD(0, BOX_B);
-      h[5] = RD(1, BOX_B);
-      ring_release(R, rc, tx, ring_dep(h[4], h[5]));
+      h[4] = h45[0];
+      h[5] = h45[1];
       if (upd1_x) {
         h[0] = upd(h[0], C[HXY], C[12 + HXY], sm.sE[2][ty + 1][tx], sEz);
         h[1] = upd_src(h[1], C[HXZ], C[12 + HXZ], nEy, sEy, C[24 + SRC_HXZ]);
