@@ -288,10 +288,12 @@ int thiim_gpu_slab_info(thiim_gpu_ctx* ctx, thiim_slab_info* info);
  * exports its slab (CUDA IPC handle + layout), imports its neighbours' exports,
  * and from then on every TBLOCK pass stores its boundary planes straight into
  * the neighbours' halo planes -- no halo exchange after 2-step passes.  The
- * caller orders passes across processes: thiim_gpu_step(ctx, k <= 2), then a
- * barrier of all ranks (covers both the halo writes and the neighbours' reads
- * of halos the next pass overwrites).  Odd remainder steps (k = 1) still need
- * the view exchange.  TBLOCK deep-halo slab contexts only. */
+ * caller orders passes across processes: a barrier of all ranks after any
+ * upload / generate (they write both field sets, halos included, which a
+ * neighbour's first pass stores into), then thiim_gpu_step(ctx, k <= 2) and a
+ * barrier of all ranks after each pass (covers both the halo writes and the
+ * neighbours' reads of halos the next pass overwrites).  Odd remainder steps
+ * (k = 1) still need the view exchange.  TBLOCK deep-halo slab contexts only. */
 typedef struct {
   unsigned char ipc[64]; /* cudaIpcMemHandle_t of the slab state */
   long long stride;      /* elements per array */

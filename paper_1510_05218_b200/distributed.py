@@ -241,6 +241,10 @@ def run_distributed(engine, steps: int, exchanger: HaloExchanger) -> dict:
     sent = 0
     launches = 0
     done = 0
+    if getattr(engine, "peer_stores", False) and steps > 0:
+        # upload / generate write both field sets of this slab, halos included:
+        # no neighbour's pass may store into them before every rank is done
+        exchanger.barrier()
     while done < steps:
         k = min(period, steps - done)
         st = engine.step(k)

@@ -167,3 +167,35 @@ def test_missing_halo_exchange_is_detected(tmp_path):
     pxy = 64
     got = np.concatenate([lo.local[0][pxy:6 * pxy], hi.local[0][pxy:6 * pxy]])
     assert not np.array_equal(got, ref[0][pxy:11 * pxy])
+
+
+def test_peer_store_protocol_orders_upload_before_first_pass():
+    """Host logic only: with IPC peer stores, run_distributed barriers once on
+    entry (an upload / generate rewrites the halos a neighbour's first pass
+    stores into -- the race the 2-rank GPU test caught) and after every 2-step
+    pass; the odd remainder step still exchanges."""
+    calls = []
+
+    class Eng:
+        exchange_period = 2
+        peer_stores = True
+
+        def step(self, k):
+            calls.append(("step", k))
+            return type("S", (), {"kernel_launches": 1})()
+
+    class Ex:
+        def barrier(self):
+            calls.append(("barrier",))
+
+        def exchange(self, eng):
+            calls.append(("exchange",))
+            return 8
+
+    st = D.run_distributed(Eng(), 5, Ex())
+    assert calls == [("barrier",), ("step", 2), ("barrier",), ("step", 2), ("barrier",),
+                     ("step", 1), ("exchange",)]
+    assert st == {"halo_bytes_sent": 8, "kernel_launches": 3}
+    calls.clear()
+    D.run_distributed(Eng(), 0, Ex())
+    assert calls == []
