@@ -310,7 +310,8 @@ def _line(P, args, world, dims_rank, engine_ran, dev_secs, launches, e2e, clk, e
            "iterations_per_step": args.iters, "engine": P.ENGINE_NAMES.get(engine_ran),
            "parallelism": "z-slab x%d" % world if world > 1 else "single GPU",
            "l2": "inputs (%.1f GB state per GPU) larger than the 126 MB L2; no flush needed"
-                 % (dims_rank.padded_cells() * (832 if engine_ran != P.ENGINE_SPLIT else 640) / 1e9)}
+                 % (dims_rank.padded_cells() * (385 if args.coeff == "table" else
+                                                832 if engine_ran != P.ENGINE_SPLIT else 640) / 1e9)}
     cfg.update(extra_cfg)
     return {
         "metric": METRIC, "value": round(value, 2), "unit": "MLUP/s", "n_gpus": world,
