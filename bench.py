@@ -228,12 +228,17 @@ def run_reference_arm(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
-def _roofline(P, dims, engine_ran, dev_secs, launches, table=False):
+def _roofline(P, dims, engine_ran, dev_secs, launches, table=False, iters_total=0):
     """Roofline of the dominant kernel: one THIIM iteration (fused) or one
-    half-step sweep (split) per launch over the rank's grid."""
+    half-step sweep (split) per launch over the rank's grid.  TBLOCK in place:
+    one two-step pass (its sub-range launches + copy-back) is the unit."""
     hbm, peak_kind = load_peaks()
     per_launch_s = dev_secs / max(1, launches)
-    if engine_ran == P.ENGINE_SPLIT:
+    if engine_ran == P.ENGINE_TBLOCK_INPLACE:
+        per_launch_s = dev_secs / max(1, iters_total / 2)
+        bytes_launch = 1216.0 * dims.interior_cells()  # 832 B pass + 384 B copy-back
+        kname = "k_tblock_tm<15,6> sub-ranges + k_copy_interior"
+    elif engine_ran == P.ENGINE_SPLIT:
         bytes_launch = 512.0 * dims.interior_cells()  # one half-step sweep: 32 x 16 B per cell
         kname = "k_split_h/k_split_e"
     elif table and engine_ran == P.ENGINE_TBLOCK:
@@ -260,7 +265,7 @@ def _roofline(P, dims, engine_ran, dev_secs, launches, table=False):
             traffic = json.load(f).get("%s@%dx%dx%d" % (kname, dims.nx, dims.ny, dims.nz))
     balance = (385.0 / (2 if engine_ran == P.ENGINE_TBLOCK else 1)) if table \
         else P.balance_model(engine_ran)
-    steps_per_launch = 2 if engine_ran == P.ENGINE_TBLOCK else 1
+    steps_per_launch = 2 if engine_ran in (P.ENGINE_TBLOCK, P.ENGINE_TBLOCK_INPLACE) else 1
     if engine_ran == P.ENGINE_SPLIT:
         steps_per_launch = 0.5
     return {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
@@ -275,7 +280,7 @@ def _roofline(P, dims, engine_ran, dev_secs, launches, table=False):
 def run_native(args, world, rank, local):
     import paper_1510_05218_b200 as P
     engine = {"auto": P.ENGINE_AUTO, "split": P.ENGINE_SPLIT, "fused": P.ENGINE_FUSED,
-              "tblock": P.ENGINE_TBLOCK}[args.engine]
+              "tblock": P.ENGINE_TBLOCK, "tblock-inplace": P.ENGINE_TBLOCK_INPLACE}[args.engine]
     opts = P.GpuOptions(device=local if world > 1 else args.device, engine=engine,
                         tile_y=args.tile_y, z_chunk=args.z_chunk, min_blocks=args.min_blocks,
                         variant=args.variant, l2_promotion=args.l2_promotion,
@@ -311,7 +316,9 @@ def _line(P, args, world, dims_rank, engine_ran, dev_secs, launches, e2e, clk, e
            "parallelism": "z-slab x%d" % world if world > 1 else "single GPU",
            "l2": "inputs (%.1f GB state per GPU) larger than the 126 MB L2; no flush needed"
                  % (dims_rank.padded_cells() * (385 if args.coeff == "table" else
-                                                832 if engine_ran != P.ENGINE_SPLIT else 640) / 1e9)}
+                                                640 if engine_ran in (P.ENGINE_SPLIT,
+                                                                      P.ENGINE_TBLOCK_INPLACE)
+                                                else 832) / 1e9)}
     cfg.update(extra_cfg)
     return {
         "metric": METRIC, "value": round(value, 2), "unit": "MLUP/s", "n_gpus": world,
@@ -323,7 +330,8 @@ def _line(P, args, world, dims_rank, engine_ran, dev_secs, launches, e2e, clk, e
                 "h2d_bytes_per_step": 40 * padded, "d2h_bytes_per_step": 12 * padded},
         "gpu_launches": launches,
         "roofline": _roofline(P, dims_rank, engine_ran, dev_secs, launches,
-                              table=getattr(args, "coeff", "full") == "table"),
+                              table=getattr(args, "coeff", "full") == "table",
+                              iters_total=args.iters * args.steps),
         "clocks": clk.result,
     }
 
@@ -549,7 +557,8 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
-    ap.add_argument("--engine", default="auto", choices=["auto", "split", "fused", "tblock"])
+    ap.add_argument("--engine", default="auto",
+                    choices=["auto", "split", "fused", "tblock", "tblock-inplace"])
     ap.add_argument("--iters", type=int, default=None)
     ap.add_argument("--device", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -66,7 +66,12 @@ enum {
   THIIM_ENGINE_AUTO = 0,
   THIIM_ENGINE_SPLIT = 1, /* H sweep + E sweep, in place, z-streamed: 1024 B/LUP */
   THIIM_ENGINE_FUSED = 2, /* one z-streamed H->E sweep per step, ping-pong fields: 832 B/LUP */
-  THIIM_ENGINE_TBLOCK = 3 /* temporally blocked fused sweep, `time_block` steps per pass */
+  THIIM_ENGINE_TBLOCK = 3, /* temporally blocked fused sweep, `time_block` steps per pass */
+  /* TBLOCK on one field set (state that fits in place but not twice): z
+   * sub-ranges of L planes, outputs into spare planes, interior copy-back;
+   * 608 B/LUP.  One whole-z slab; AUTO picks it over SPLIT when >= 8 spare
+   * planes fit.  THIIM_INPLACE_TB=L (env) sets L, 0 disables it under AUTO. */
+  THIIM_ENGINE_TBLOCK_INPLACE = 4
 };
 
 /* Synthetic problem kinds for thiim_gpu_init_generated / thiim_generate_host

@@ -37,7 +37,7 @@ __all__ = [
     "ConfigError", "SetupError", "PlanError", "GpuError",
     "GridDims", "ProblemState", "allocate_state", "clone_state", "Component",
     "COMPONENT_TABLE", "GEN_RANDOM", "GEN_LAYERED", "ENGINE_AUTO", "ENGINE_SPLIT",
-    "ENGINE_FUSED", "ENGINE_TBLOCK", "GpuOptions", "RunReport", "StateDiff", "GpuEngine",
+    "ENGINE_FUSED", "ENGINE_TBLOCK", "ENGINE_TBLOCK_INPLACE", "GpuOptions", "RunReport", "StateDiff", "GpuEngine",
     "run_gpu", "generate_problem", "compare_states", "balance_model", "lib",
     "compress_coefficients", "expand_coefficients", "COEFF_FULL", "COEFF_TABLE",
     "run_gpu_batch", "BatchReport", "release_cached",
@@ -385,8 +385,9 @@ GEN_RANDOM = 0
 GEN_LAYERED = 1
 COEFF_FULL = 0
 COEFF_TABLE = 1
-ENGINE_AUTO, ENGINE_SPLIT, ENGINE_FUSED, ENGINE_TBLOCK = 0, 1, 2, 3
-ENGINE_NAMES = {ENGINE_SPLIT: "gpu-split", ENGINE_FUSED: "gpu-fused", ENGINE_TBLOCK: "gpu-tblock"}
+ENGINE_AUTO, ENGINE_SPLIT, ENGINE_FUSED, ENGINE_TBLOCK, ENGINE_TBLOCK_INPLACE = 0, 1, 2, 3, 4
+ENGINE_NAMES = {ENGINE_SPLIT: "gpu-split", ENGINE_FUSED: "gpu-fused", ENGINE_TBLOCK: "gpu-tblock",
+                ENGINE_TBLOCK_INPLACE: "gpu-tblock-inplace"}
 
 
 def selftest_cdiv(operands: np.ndarray) -> np.ndarray:

@@ -114,6 +114,16 @@ struct Slab {
   CUtensorMap smap;
   int smap_by = 0;
 
+  // TBLOCK in place (THIIM_ENGINE_TBLOCK_INPLACE, one whole-z slab, no second
+  // field set): spare output planes of one z sub-range (12 x ip_L padded
+  // planes) and a two-plane tail per field (see launch_tblock_inplace)
+  int ip_L = 0;
+  double2* ip_buf = nullptr;
+  // sub-range views only: where the TBLOCK pass stores its outputs (field k at
+  // fo_base + k * fo_stride - fo_shift) instead of the other field set
+  double2* fo_base = nullptr;
+  long long fo_stride = 0, fo_shift = 0;
+
   double2* field(int set, int k) const { return buf + (size_t)(set * 12 + k) * stride; }
   double2* coeff(int a) const {  // a in 12..39 (FULL layout only)
     return table ? nullptr : buf + (size_t)(nfield_sets * 12 + (a - 12)) * stride;
@@ -124,7 +134,7 @@ struct Slab {
     Arrays A;
     for (int k = 0; k < 12; ++k) {
       A.f[k] = field(in_set, k);
-      A.fo[k] = field(out_set, k);
+      A.fo[k] = fo_base ? fo_base + k * fo_stride - fo_shift : field(out_set, k);
       A.t[k] = coeff(12 + k);
       A.c[k] = coeff(24 + k);
     }
@@ -335,6 +345,28 @@ __global__ void k_selftest_cdiv(int n, const double* in, double* out) {
 // UpdateLog coverage, tools/main.cpp:20-41): every (component, interior cell) of
 // the slab's local grid was stored exactly once, no ghost ever; the counts are
 // reset for the next pass.
+// Interior cells (x/y ghost ring excluded) of `nplanes` consecutive padded
+// planes of the 12 fields, src -> dst: TBLOCK-in-place copy-back.  The ring is
+// input data the sweep never writes, and the spare planes never hold it.
+struct Planes12 {
+  double2* p[12];
+};
+__global__ void k_copy_interior(Planes12 dst, Planes12 src, int nplanes, int nx, int ny,
+                                long long px, long long pxy) {
+  const long long per = (long long)nx * ny;
+  const long long n = 12LL * nplanes * per;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int k = (int)(t / ((long long)nplanes * per));
+    const long long r = t - (long long)k * nplanes * per;
+    const int z = (int)(r / per);
+    const long long c = r - (long long)z * per;
+    const int y = (int)(c / nx), x = (int)(c - (long long)y * nx);
+    const long long i = (long long)z * pxy + (long long)(y + 1) * px + (x + 1);
+    dst.p[k][i] = src.p[k][i];
+  }
+}
+
 __global__ void k_coverage(Grid g, unsigned* cnt, long long cstride, int r0, int r1,
                            unsigned long long* bad) {
   const long long n = (long long)(g.nz + 2) * g.pxy;
@@ -932,6 +964,71 @@ int launch_tblock2(thiim_gpu_ctx* ctx, Slab& s, long long* launches, const PeerO
   }
 }
 
+// TBLOCK without a second field set (BASELINE c3 in the reference layout:
+// 40 arrays fit in HBM, the 52 of ping-pong TBLOCK do not).  The interior is
+// swept as z sub-ranges [a, b) of ip_L planes, in order; each is one deep-slab
+// TBLOCK pass (k_tblock_tm, owned-plane stores) over the view of interior
+// planes [a-1, b+1) plus the plane on either side -- exactly a z-slab whose
+// halos hold the neighbours' current values, here the not yet updated state
+// itself -- storing its two-step outputs into spare planes instead of the
+// other field set.  A later sub-range still reads the two planes below its
+// start, so after sub-range k its planes [a, b-2) are copied back at once and
+// [b-2, b) move to a two-plane tail, copied back once sub-range k+1 has run.
+// Traffic per two steps: one TBLOCK pass (832 B/cell + the ~4 planes each view
+// re-reads) and the 384-B interior copy-back of 12 fields.
+static int launch_tblock_inplace(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
+  const int nz = s.g.nz, L = s.ip_L;
+  const long long pxy = s.g.pxy;
+  const int blocks = 4 * sm_count(s.device);
+  Planes12 spare, tail;
+  for (int k = 0; k < 12; ++k) {
+    spare.p[k] = s.ip_buf + (size_t)k * L * pxy;
+    tail.p[k] = s.ip_buf + ((size_t)12 * L + 2 * k) * pxy;
+  }
+  auto main_at = [&](int z) {  // padded plane of interior plane z, field set 0
+    Planes12 m;
+    for (int k = 0; k < 12; ++k) m.p[k] = s.field(0, k) + (size_t)(z + 1) * pxy;
+    return m;
+  };
+  auto copy = [&](const Planes12& dst, const Planes12& src, int np) -> int {
+    k_copy_interior<<<blocks, 256, 0, s.stream>>>(dst, src, np, s.g.nx, s.g.ny, s.g.px, pxy);
+    CK(cudaGetLastError());
+    ++*launches;
+    return THIIM_OK;
+  };
+  int r;
+  for (int a = 0; a < nz; a += L) {
+    const int b = std::min(nz, a + L);
+    const int lo = a > 0 ? a - 1 : 0, hi = b < nz ? b + 1 : nz;
+    Slab v = s;  // view: interior planes [lo, hi) of the same allocation
+    v.buf = s.buf + (size_t)lo * pxy;
+    v.g.nz = hi - lo;
+    v.g.halo_lo = lo > 0 ? 1 : 0;
+    v.deep = true;
+    v.cur = 0;
+    v.cnt = nullptr;
+    for (auto& ok : v.maps_ok) ok = false;
+    for (auto& row : v.maps_seg_ok)
+      for (auto& ok : row) ok = false;
+    PeerOut po{};
+    po.st0 = a - lo;  // local plane st0 + j -> spare plane j (global a + j)
+    po.st1 = b - lo;
+    v.fo_base = s.ip_buf;
+    v.fo_stride = (long long)L * pxy;
+    v.fo_shift = (long long)(po.st0 + 1) * pxy;
+    if ((r = launch_tblock2(ctx, v, launches, po))) return r;
+    if (a > 0 && (r = copy(main_at(a - 2), tail, 2))) return r;  // read by this sub-range
+    const int keep = b < nz ? 2 : 0;
+    if (b - a - keep > 0 && (r = copy(main_at(a), spare, b - a - keep))) return r;
+    if (keep) {
+      Planes12 top = spare;
+      for (auto& q : top.p) q += (size_t)(b - a - 2) * pxy;
+      if ((r = copy(tail, top, 2))) return r;
+    }
+  }
+  return THIIM_OK;
+}
+
 template <int BY, int NG>
 int launch_fused_table_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
   static_assert(BY == 15, "material-id map box height is 15");
@@ -1017,6 +1114,8 @@ double thiim_gpu_balance_model(int engine, int time_block) {
   switch (engine) {
     case THIIM_ENGINE_SPLIT: return 1024.0;
     case THIIM_ENGINE_TBLOCK: return 832.0 / (time_block > 0 ? time_block : 2);
+    // one TBLOCK pass + the 12-field interior copy-back per two steps
+    case THIIM_ENGINE_TBLOCK_INPLACE: return (832.0 + 384.0) / 2;
     // table coefficient layout: 24 fields x 16 B + 1 B id per HBM pass of time_block steps
     case 100 + THIIM_COEFF_TABLE: return 385.0 / (time_block > 0 ? time_block : 1);
     default: return 832.0;
@@ -1080,14 +1179,14 @@ static int create_impl(const thiim_dims* dims, const thiim_gpu_opts* opts, bool 
   else
     thiim_gpu_default_opts(&o);
   if (o.n_gpus < 1 || o.n_gpus > 8) return fail(THIIM_ERR_CONFIG, "n_gpus must be in 1..8");
-  if (o.engine < THIIM_ENGINE_AUTO || o.engine > THIIM_ENGINE_TBLOCK)
+  if (o.engine < THIIM_ENGINE_AUTO || o.engine > THIIM_ENGINE_TBLOCK_INPLACE)
     return fail(THIIM_ERR_CONFIG, "unknown engine");
   if (o.engine == THIIM_ENGINE_TBLOCK && o.time_block != 0 && o.time_block != 2)
     return fail(THIIM_ERR_CONFIG, "engine TBLOCK supports time_block 2");
   const bool table = o.coeff_layout == THIIM_COEFF_TABLE;
   if (o.coeff_layout != THIIM_COEFF_FULL && !table)
     return fail(THIIM_ERR_CONFIG, "unknown coefficient layout");
-  if (table && o.engine == THIIM_ENGINE_SPLIT)
+  if (table && (o.engine == THIIM_ENGINE_SPLIT || o.engine == THIIM_ENGINE_TBLOCK_INPLACE))
     return fail(THIIM_ERR_CONFIG, "the table coefficient layout runs on the fused or TBLOCK engine");
   if (table && (o.n_materials < 1 || o.n_materials > kMaxMaterials))
     return fail(THIIM_ERR_CONFIG, "n_materials must be in 1..16 for the table layout");
@@ -1110,6 +1209,13 @@ static int create_impl(const thiim_dims* dims, const thiim_gpu_opts* opts, bool 
   const int n = (int)ranges.size();
   ctx->engine = o.engine;
   const bool whole_z = n == 1 && ranges[0].first == 0 && ranges[0].second == dims->nz;
+  // TBLOCK in place runs on a split (one field set) context plus spare planes
+  const bool want_ip = o.engine == THIIM_ENGINE_TBLOCK_INPLACE;
+  if (want_ip && !whole_z) {
+    delete ctx;
+    return fail(THIIM_ERR_CONFIG, "TBLOCK in place needs one whole-z slab");
+  }
+  if (want_ip) ctx->engine = THIIM_ENGINE_SPLIT;
   // AUTO: TBLOCK (two steps per HBM pass, odd remainders fused; z-slabs keep
   // deep two-plane halos exchanged per pass); the table layout has no split form
   if (table && o.engine == THIIM_ENGINE_AUTO) ctx->engine = THIIM_ENGINE_TBLOCK;
@@ -1123,6 +1229,7 @@ static int create_impl(const thiim_dims* dims, const thiim_gpu_opts* opts, bool 
       if (need > freeb) ctx->engine = THIIM_ENGINE_SPLIT;
     }
   }
+  const bool auto_split = o.engine == THIIM_ENGINE_AUTO && ctx->engine == THIIM_ENGINE_SPLIT;
   const int nf = ctx->engine == THIIM_ENGINE_SPLIT ? 1 : 2;
   for (int s = 0; s < n; ++s) {
     Slab sl;
@@ -1186,6 +1293,35 @@ static int create_impl(const thiim_dims* dims, const thiim_gpu_opts* opts, bool 
       cudaGetLastError();
       thiim_gpu_destroy(ctx);
       return fail(THIIM_ERR_SETUP, msg);
+    }
+  }
+  if ((want_ip || auto_split) && whole_z && !table) {
+    // spare planes for TBLOCK in place: THIIM_INPLACE_TB=L forces the sub-range
+    // length (0: plain split); default the most planes free memory holds, <= 64
+    Slab& sl = ctx->slabs[0];
+    const size_t plane = (size_t)pxy * sizeof(double2);
+    const char* env = std::getenv("THIIM_INPLACE_TB");
+    int L = env ? std::atoi(env) : -1;
+    if (L < 0) {
+      const size_t freeb = device_available(sl.device), margin = (size_t)512 << 20;
+      L = freeb > margin ? (int)std::min<size_t>(66, (freeb - margin) / (12 * plane)) - 2 : 0;
+      if (!want_ip && L < 8) L = 0;  // too short to beat split
+    }
+    L = std::min(L, dims->nz);
+    if (L >= 2 || (L >= 1 && L == dims->nz)) {
+      cudaSetDevice(sl.device);
+      cudaError_t e = pool_alloc(reinterpret_cast<void**>(&sl.ip_buf), (size_t)12 * (L + 2) * plane,
+                                 sl.device, sl.stream);
+      if (e == cudaSuccess) {
+        sl.ip_L = L;
+      } else {
+        cudaGetLastError();
+        sl.ip_buf = nullptr;
+      }
+    }
+    if (want_ip && !sl.ip_L) {
+      thiim_gpu_destroy(ctx);
+      return fail(THIIM_ERR_SETUP, "TBLOCK in place: no device memory for the spare planes");
     }
   }
   if (n > 1) {
@@ -1392,6 +1528,7 @@ void thiim_gpu_destroy(thiim_gpu_ctx* ctx) {
     if (sl.stream) cudaStreamSynchronize(sl.stream);
     for (auto& p : sl.peer)
       if (p.base) cudaIpcCloseMemHandle(p.base);
+    if (sl.ip_buf) cudaFreeAsync(sl.ip_buf, sl.stream);
     if (sl.buf && sl.ipc_buf) {
       cudaFree(sl.buf);
     } else if (sl.buf) {  // back to the pool; the sync lets the next context reuse it at once
@@ -1833,6 +1970,11 @@ static int step_enqueue(thiim_gpu_ctx* ctx, int steps, long long* launches_out) 
       if (multi && (r = exchange_deep(ctx))) return r;
     }
   }
+  if (ctx->engine == THIIM_ENGINE_SPLIT && !multi && ctx->slabs[0].ip_L > 0 && !ctx->sanitize) {
+    // TBLOCK in place: two steps per sub-range sweep, an odd remainder split
+    for (; n + 2 <= steps; n += 2)
+      if ((r = launch_tblock_inplace(ctx, ctx->slabs[0], &launches))) return r;
+  }
   for (; n < steps; ++n) {
     if (ctx->engine == THIIM_ENGINE_SPLIT) {
       if (multi && (r = exchange(ctx, 0))) return r;
@@ -1881,13 +2023,14 @@ int thiim_gpu_step(thiim_gpu_ctx* ctx, int steps, thiim_gpu_stats* stats) {
     stats->seconds = secs;
     stats->kernel_seconds = secs;
     stats->steps = steps;
-    stats->engine = ctx->engine;
+    const bool ip = ctx->engine == THIIM_ENGINE_SPLIT && ctx->slabs[0].ip_L > 0 && !ctx->sanitize;
+    stats->engine = ip ? THIIM_ENGINE_TBLOCK_INPLACE : ctx->engine;
     stats->n_gpus = (int)ctx->slabs.size();
     stats->kernel_launches = launches;
     stats->balance_model = ctx->slabs[0].table
                                ? thiim_gpu_balance_model(100 + THIIM_COEFF_TABLE,
                                                          ctx->engine == THIIM_ENGINE_TBLOCK ? 2 : 1)
-                               : thiim_gpu_balance_model(ctx->engine, ctx->opts.time_block);
+                               : thiim_gpu_balance_model(stats->engine, ctx->opts.time_block);
     const double lups = (double)ctx->dims.nx * ctx->dims.ny * ctx->dims.nz * steps;
     stats->mlups = (steps > 0 && secs > 0) ? lups / secs / 1e6 : 0.0;
   }
