@@ -353,18 +353,13 @@ struct Planes12 {
 };
 __global__ void k_copy_interior(Planes12 dst, Planes12 src, int nplanes, int nx, int ny,
                                 long long px, long long pxy) {
-  const long long per = (long long)nx * ny;
-  const long long n = 12LL * nplanes * per;
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
-       t += (long long)gridDim.x * blockDim.x) {
-    const int k = (int)(t / ((long long)nplanes * per));
-    const long long r = t - (long long)k * nplanes * per;
-    const int z = (int)(r / per);
-    const long long c = r - (long long)z * per;
-    const int y = (int)(c / nx), x = (int)(c - (long long)y * nx);
-    const long long i = (long long)z * pxy + (long long)(y + 1) * px + (x + 1);
-    dst.p[k][i] = src.p[k][i];
-  }
+  // grid: x = rows of one plane (grid-stride), y = plane, z = field; no divisions
+  const int k = blockIdx.z, z = blockIdx.y;
+  double2* __restrict__ d = dst.p[k] + (long long)z * pxy + px + 1;
+  const double2* __restrict__ sp = src.p[k] + (long long)z * pxy + px + 1;
+  for (int y = blockIdx.x; y < ny; y += gridDim.x)
+#pragma unroll 4
+    for (int x = threadIdx.x; x < nx; x += blockDim.x) d[(long long)y * px + x] = sp[(long long)y * px + x];
 }
 
 __global__ void k_coverage(Grid g, unsigned* cnt, long long cstride, int r0, int r1,
@@ -979,7 +974,6 @@ int launch_tblock2(thiim_gpu_ctx* ctx, Slab& s, long long* launches, const PeerO
 static int launch_tblock_inplace(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
   const int nz = s.g.nz, L = s.ip_L;
   const long long pxy = s.g.pxy;
-  const int blocks = 4 * sm_count(s.device);
   Planes12 spare, tail;
   for (int k = 0; k < 12; ++k) {
     spare.p[k] = s.ip_buf + (size_t)k * L * pxy;
@@ -991,7 +985,10 @@ static int launch_tblock_inplace(thiim_gpu_ctx* ctx, Slab& s, long long* launche
     return m;
   };
   auto copy = [&](const Planes12& dst, const Planes12& src, int np) -> int {
-    k_copy_interior<<<blocks, 256, 0, s.stream>>>(dst, src, np, s.g.nx, s.g.ny, s.g.px, pxy);
+    // 12 x np x up to 64 CTAs of whole rows (full occupancy, 4 loads in flight per thread)
+    const int rows = std::min(s.g.ny, 64);
+    k_copy_interior<<<dim3(rows, np, 12), 256, 0, s.stream>>>(dst, src, np, s.g.nx, s.g.ny,
+                                                              s.g.px, pxy);
     CK(cudaGetLastError());
     ++*launches;
     return THIIM_OK;
