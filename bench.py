@@ -2,26 +2,27 @@
 """bench.py -- THIIM sweep throughput (MLUP/s) on B200, per the driver contract.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl native|reference]
+                    [--config c0..c4]
 
-Workload (BASELINE.json configs[1]): 256^3 grid, complex128, 100 THIIM
-iterations (H half-step then E half-step, reference step_reference order) per
-bench step, fields U[-1,1]^2 and 28 coefficient arrays uniform in |z|<=0.45,
-seed 1, zero ghosts.  One bench "step" = one full configs[1] run.
+Workload: the largest single-GPU BASELINE.json config, configs[2] (512^3 grid,
+complex128, 200 THIIM iterations -- H half-step then E half-step in the
+reference's step_reference order -- per bench step; fields U[-1,1]^2, 28
+coefficient arrays uniform in |z|<=0.45, seed 1, zero ghosts) at N=1, and
+configs[4] (a 1024x1024x128 z-slab per GPU, 100 iterations, weak scaling) at
+N>1.  One bench "step" = one full run of that config.
 
   value   MLUP/s with the problem resident in HBM (device time, CUDA events on
           the launching stream), max over ranks.
   e2e     same metric through the public API, every step's inputs uploaded
-          from pinned host memory and its 12 result fields downloaded: the
-          pipelined stream call run_gpu_batch (copies of neighbouring steps
-          overlap the sweep), with the serial run_gpu sequence beside it.
-  roofline  dominant kernel (one THIIM iteration per launch) vs measured HBM.
+          from pinned host memory and its 12 result fields downloaded.
+  roofline  dominant kernel vs measured HBM.
   cpu_baseline  the reference's own run_naive (oracle/_ref, compiled from
           /root/reference unmodified) on the host cores, bounded sample.
 
---impl reference runs the reference CPU implementation alone (rank 0 only).
-Multi-rank (torchrun): weak scaling, rank r owns z-slab r (256^3 cells) of a
-256x256x(256N) grid; the halo planes move over NCCL before every iteration
-(paper_1510_05218_b200/distributed.py).
+--impl reference runs the reference CPU implementation alone (rank 0 only) on a
+bounded sample of the same config; its inputs come from the oracle's generator
+(oracle/), never from this package.  Multi-rank (torchrun): weak scaling, rank r
+owns z-slab r of the global grid (paper_1510_05218_b200/distributed.py).
 """
 from __future__ import annotations
 
@@ -48,10 +49,17 @@ CONFIGS = {
     "c4": ((1024, 1024, 128), 100, 0, "configs[4]: weak-scaling slab 1024x1024x128 per GPU, 100 "
                                       "THIIM iterations"),
 }
-GRID, ITERS, KIND, _DESC = CONFIGS["c1"]
+DEFAULT_SINGLE, DEFAULT_MULTI = "c2", "c4"
+GRID, ITERS, KIND, _DESC = CONFIGS[DEFAULT_SINGLE]
 WORKLOAD = (_DESC + " (H then E half-step) per bench step, complex128, fields U[-1,1], "
             "coeffs |c|<=0.45, seed 1, zero halo")
 METRIC = "MLUP/s (double-complex E+H update) at N B200; % of HBM roofline"
+
+
+def default_config(world: int) -> str:
+    """configs[2] (the largest single-GPU config) at N=1, configs[4] (the
+    weak-scaling slab per GPU) at N>1."""
+    return DEFAULT_SINGLE if world == 1 else DEFAULT_MULTI
 
 
 def load_peaks():
@@ -143,25 +151,31 @@ def cpu_threads():
         return os.cpu_count() or 1
 
 
+def sample_grid(grid):
+    """Bounded CPU sample of a config: its x-y plane, with the z extent cut so
+    the sample holds about 2^25 cells (the whole grid when it is smaller)."""
+    nx, ny, nz = grid
+    return (nx, ny, max(8, min(nz, (1 << 25) // (nx * ny))))
+
+
 def reference_engines_sample(grid, threads):
     """The reference's other CPU engines on the same sample: its
     spatially blocked sweep (block_y 8) and its multicore wavefront-diamond
     engine (the paper's temporal blocking; dw 8, bz 1, one thread per group),
     4 iterations each -- context for the naive baseline `value`."""
     from oracle import oracle as O  # cpu baseline leg only
-    import paper_1510_05218_b200 as P
     if not O.ref_available():
         return {}
-    dims = P.GridDims(*grid)
-    cells = dims.interior_cells()
+    cells = grid[0] * grid[1] * grid[2]
     out = {}
     try:
-        s = P.generate_problem(dims, P.GEN_RANDOM, SEED)
-        secs = O.ref_run_spatial(grid, s.arrays, 4, 8, 0, threads)
-        out["spatial_blocked_mlups"] = round(cells * 4 / secs / 1e6, 3)
-        s = P.generate_problem(dims, P.GEN_RANDOM, SEED)
-        secs, executed = O.ref_run_mwd(grid, s.arrays, 4, 8, 1, 1, 1, 1, threads)
-        out["mwd_mlups"] = round(cells * executed / secs / 1e6, 3)
+        with O.RefState(grid) as r:
+            r.generate(SEED, bool(KIND), threads)
+            secs = r.run_spatial(4, 8, 0, threads)
+            out["spatial_blocked_mlups"] = round(cells * 4 / secs / 1e6, 3)
+            r.generate(SEED, bool(KIND), threads)
+            secs, executed = r.run_mwd(4, 8, 1, 1, 1, 1, threads)
+            out["mwd_mlups"] = round(cells * executed / secs / 1e6, 3)
         out["mwd_params"] = "dw 8, bz 1, shape 1x1x1, %d threads" % threads
         # the reference's own host triad (its `bandwidth` subcommand), SURVEY s8d
         out["host_triad_gbs"] = round(O.ref_measure_bandwidth(threads), 1)
@@ -170,58 +184,75 @@ def reference_engines_sample(grid, threads):
     return out
 
 
-def reference_sample(grid, iters, threads):
-    """Time the reference's run_naive (oracle/_ref) on a host problem."""
-    from oracle import oracle as O  # cpu baseline leg only
-    import paper_1510_05218_b200 as P
-    dims = P.GridDims(*grid)
-    s = P.generate_problem(dims, P.GEN_RANDOM, SEED)
-    if O.ref_available():
-        secs = O.ref_run_naive(grid, s.arrays, iters, threads)
-        kind = "reference"
-    else:
+class _CpuRef:
+    """The reference's run_naive on a problem generated inside oracle/_ref
+    (ref_shim.cpp: the seeded generator restated there, so only the reference
+    library is loaded); the oracle's C port when oracle/_ref is absent."""
+
+    def __init__(self, grid, threads):
+        from oracle import oracle as O  # cpu baseline / reference arm only
+        self.O, self.grid, self.threads = O, grid, threads
+        self.kind = "reference" if O.ref_available() else "port"
+        if self.kind == "reference":
+            self.r = O.RefState(grid)
+            self.r.generate(SEED, bool(KIND), threads)
+        else:
+            self.a = O.c_generate(grid, SEED, layered=bool(KIND))
+
+    def run(self, iters):
+        if self.kind == "reference":
+            return self.r.run_naive(iters, self.threads)
         t0 = time.perf_counter()
-        O.c_step(grid, s.arrays, iters, threads=threads)
-        secs = time.perf_counter() - t0
-        kind = "port"
-    lups = dims.interior_cells() * iters
-    return lups / secs / 1e6, kind
+        self.O.c_step(self.grid, self.a, iters, threads=self.threads)
+        return time.perf_counter() - t0
+
+    def close(self):
+        if self.kind == "reference":
+            self.r.close()
+
+
+def reference_sample(grid, iters, threads):
+    """Time the reference's run_naive (oracle/_ref) on the sample problem."""
+    c = _CpuRef(grid, threads)
+    secs = c.run(iters)
+    c.close()
+    return grid[0] * grid[1] * grid[2] * iters / secs / 1e6, c.kind
 
 
 def run_reference_arm(args, world, rank):
+    """The reference's own CPU path (oracle/_ref run_naive, all host threads)
+    on a bounded sample of the bench config: the config's x-y planes, ~2^25
+    cells, one THIIM iteration per step.  The problem is generated inside the
+    reference library's shim (bitwise the product's generator,
+    tests/test_oracle.py); this arm never imports or loads the product package."""
     if rank != 0:
         return
     threads = cpu_threads()
-    # bounded sample per step: 1 THIIM iteration of the full 256^3 grid
     sample_iters = 1
-    import paper_1510_05218_b200 as P
-    from oracle import oracle as O
-    dims = P.GridDims(*GRID)
-    s = P.generate_problem(dims, P.GEN_RANDOM, SEED)
-    kind = "reference" if O.ref_available() else "port"
+    grid = sample_grid(GRID)
+    c = _CpuRef(grid, threads)
     vals = []
     for k in range(args.warmup + args.steps):
-        if kind == "reference":
-            secs = O.ref_run_naive(GRID, s.arrays, sample_iters, threads)
-        else:
-            t0 = time.perf_counter()
-            O.c_step(GRID, s.arrays, sample_iters, threads=threads)
-            secs = time.perf_counter() - t0
+        secs = c.run(sample_iters)
         if k >= args.warmup:
             vals.append(secs)
+    c.close()
     secs = sum(vals)
-    v = dims.interior_cells() * sample_iters * len(vals) / secs / 1e6
+    cells = grid[0] * grid[1] * grid[2]
+    v = cells * sample_iters * len(vals) / secs / 1e6
+    sample = ("%dx%dx%d x %d iteration(s) per step (the config's x-y planes, z cut to a bounded "
+              "sample), run_naive threads=%d, problem generated in oracle/_ref"
+              % (grid + (sample_iters, threads)))
     line = {
         "impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "MLUP/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(1e3 * secs / max(1, len(vals)), 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "c128 (f64)", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "grid": list(GRID),
-                   "iterations_per_step": sample_iters,
-                   "note": "reference run_naive on host cores; each step a 1-iteration sample"},
-        "cpu_baseline": {"value": round(v, 3), "unit": "MLUP/s", "cores": threads, "kind": kind,
-                         "sample": "256^3 x %d iteration(s) per step, run_naive threads=%d"
-                                   % (sample_iters, threads)},
+        "config": {"workload": WORKLOAD, "config": args.config, "grid": list(GRID),
+                   "sample_grid": list(grid), "iterations_per_step": sample_iters,
+                   "note": "reference run_naive on host cores; each step a bounded sample"},
+        "cpu_baseline": {"value": round(v, 3), "unit": "MLUP/s", "cores": threads, "kind": c.kind,
+                         "sample": sample},
         "e2e": {"value": round(v, 3), "unit": "MLUP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -296,12 +327,13 @@ def run_native(args, world, rank, local):
         return
     if world == 1 and not args.no_cpu_baseline:
         threads = cpu_threads()
-        grid = (256, 256, 64)
+        grid = sample_grid(GRID)
         v, kind = reference_sample(grid, 2, threads)
         line["cpu_baseline"] = {"value": round(v, 3), "unit": "MLUP/s", "cores": threads,
                                 "kind": kind,
                                 "sample": "reference run_naive (oracle/_ref, compiled unmodified), "
-                                          "256x256x64 x 2 iterations, %d threads" % threads}
+                                          "%dx%dx%d x 2 iterations, %d threads, problem "
+                                          "generated in oracle/_ref" % (grid + (threads,))}
         line["cpu_baseline"].update(reference_engines_sample(grid, threads))
     print(json.dumps(line), flush=True)
 
@@ -392,21 +424,27 @@ def run_native_single(P, args, opts, iters):
         pinned = host.arrays + out
         for a in pinned:
             P.lib().thiim_gpu_pin_host(a.ctypes.data, a.nbytes)
-        # untimed warm-up; 3 problems so the device pool already holds the
-        # three contexts the timed call reuses
-        P.run_gpu_batch([host] * 3, iters, opts, outputs=[out] * 3)
-        rep = P.run_gpu_batch([host] * args.steps, iters, opts, outputs=[out] * args.steps)
-        stream = {
-            "value": round(dims.interior_cells() * iters * args.steps / rep.seconds / 1e6, 2),
-            "api": "run_gpu_batch (thiim_gpu_run_batch), depth %d, one problem per step" % rep.depth,
-            "depth": rep.depth,
-            "call_ms": round(1e3 * rep.seconds, 1),
-            "device_span_ms": round(1e3 * rep.device_seconds, 1),
-            "device_ms_per_step": {
-                "upload": round(1e3 * rep.upload_seconds / args.steps, 2),
-                "sweep": round(1e3 * rep.kernel_seconds / args.steps, 2),
-                "download": round(1e3 * rep.download_seconds / args.steps, 2)},
-        }
+        # the stream overlaps problem i's upload with i-1's sweep only when the
+        # device holds >= 2 contexts (52 arrays each with ping-pong fields);
+        # configs[2]/[4] hold one, so there the serial sequence is the API
+        stream = None
+        if 2 * 52 * dims.padded_cells() * 16 < 170e9:
+            # untimed warm-up; 3 problems so the device pool already holds the
+            # three contexts the timed call reuses
+            P.run_gpu_batch([host] * 3, iters, opts, outputs=[out] * 3)
+            rep = P.run_gpu_batch([host] * args.steps, iters, opts, outputs=[out] * args.steps)
+            stream = {
+                "value": round(dims.interior_cells() * iters * args.steps / rep.seconds / 1e6, 2),
+                "api": "run_gpu_batch (thiim_gpu_run_batch), depth %d, one problem per step"
+                       % rep.depth,
+                "depth": rep.depth,
+                "call_ms": round(1e3 * rep.seconds, 1),
+                "device_span_ms": round(1e3 * rep.device_seconds, 1),
+                "device_ms_per_step": {
+                    "upload": round(1e3 * rep.upload_seconds / args.steps, 2),
+                    "sweep": round(1e3 * rep.kernel_seconds / args.steps, 2),
+                    "download": round(1e3 * rep.download_seconds / args.steps, 2)},
+            }
         secs = 0.0
         phases = [0.0] * 5
         nser = max(1, min(args.steps, 3))
@@ -428,6 +466,7 @@ def run_native_single(P, args, opts, iters):
                     phases[j] += t[j + 1] - t[j]
         for a in pinned:
             P.lib().thiim_gpu_unpin_host(a.ctypes.data)
+        del host, out, pinned
         serial = {
             "value": round(dims.interior_cells() * iters * nser / secs / 1e6, 2),
             "api": "run_gpu call sequence (create, upload, step, download, destroy), %d steps"
@@ -438,17 +477,22 @@ def run_native_single(P, args, opts, iters):
         # headline: the faster of the two public-API paths (the stream overlaps
         # copies with sweeps when the device holds >= 2 contexts; with one it
         # cannot, and the plain call sequence is the better way to run)
-        best = stream if stream["value"] >= serial["value"] else serial
+        best = stream if stream and stream["value"] >= serial["value"] else serial
         e2e = best["value"]
-        e2e_extra = {"api": best["api"], "stream": stream, "serial": serial}
+        e2e_extra = {"api": best["api"], "serial": serial}
+        if stream:
+            e2e_extra["stream"] = stream
+        else:
+            e2e_extra["stream"] = "not run: the device holds one context of this size"
     line = _line(P, args, 1, dims, engine_ran, dev_secs, launches, e2e, clk, {})
     line["e2e"].update(e2e_extra)
     return line
 
 
 def run_native_multi(P, args, opts, iters, world, rank, local):
-    """Weak scaling: rank r owns the 256^3 z-slab r of a 256x256x(256*N) grid;
-    halo planes move over NCCL (torch.distributed) before every iteration."""
+    """Weak scaling: rank r owns z-slab r (the config's grid, configs[4] by
+    default: 1024x1024x128) of an nx x ny x (nz*N) grid; TBLOCK slabs store
+    their boundary planes into the neighbours' halos (CUDA IPC peer stores)."""
     import torch
     import torch.distributed as dist
     from paper_1510_05218_b200 import distributed as D
@@ -508,8 +552,10 @@ def run_native_multi(P, args, opts, iters, world, rank, local):
         for a in host:
             P.lib().thiim_gpu_pin_host(a.ctypes.data, a.nbytes)
 
+        n_e2e = max(1, min(args.steps, 3))
+
         def e2e_run():
-            for _ in range(args.steps):
+            for _ in range(n_e2e):
                 eng.upload_local(host)
                 D.run_distributed(eng, iters, ex)
                 eng.download_local(host)
@@ -517,7 +563,7 @@ def run_native_multi(P, args, opts, iters, world, rank, local):
         for a in host:
             P.lib().thiim_gpu_unpin_host(a.ctypes.data)
         eng.close()
-        e2e = world * 256 ** 3 * iters * args.steps / e2e_run_secs / 1e6
+        e2e = world * P.GridDims(*GRID).interior_cells() * iters * n_e2e / e2e_run_secs / 1e6
     if args.check:
         # decomposed run vs one oracle run of the global grid, gathered on rank 0
         eng = make_engine()
@@ -571,7 +617,8 @@ def main():
     ap.add_argument("--y-fastest", type=int, default=0)
     ap.add_argument("--runtime-seq", type=int, default=0)
     ap.add_argument("--pol-mode", type=int, default=0)
-    ap.add_argument("--config", default="c1", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default=None, choices=sorted(CONFIGS),
+                    help="default: configs[2] at N=1, configs[4] (per rank) at N>1")
     ap.add_argument("--check", type=int, default=0,
                     help="multi-rank: also run CHECK steps and compare with the oracle (rank 0)")
     ap.add_argument("--coeff", default="full", choices=["full", "table"],
@@ -579,12 +626,14 @@ def main():
                          "reported separately from the reference-layout roofline")
     args = ap.parse_args()
     global GRID, ITERS, KIND, WORKLOAD
+    world, rank, local = dist_env()
+    if args.config is None:
+        args.config = default_config(world)
     GRID, ITERS, KIND, desc = CONFIGS[args.config]
     if args.iters is None:
         args.iters = ITERS
     WORKLOAD = (desc + " (H then E half-step) per bench step, complex128, fields U[-1,1], "
                 + ("per-layer coeffs" if KIND else "coeffs") + " |c|<=0.45, seed 1, zero halo")
-    world, rank, local = dist_env()
     if args.impl == "reference":
         run_reference_arm(args, world, rank)
     else:

@@ -271,3 +271,85 @@ def ref_compare(dims, a, b):
     return {"bitwise_equal": bool(out[0]), "differing_values": int(out[1]),
             "first_component": int(out[2]), "x": int(out[3]), "y": int(out[4]), "z": int(out[5]),
             "max_abs_diff": mx.value}
+
+
+class RefState:
+    """A reference ProblemState held inside oracle/_ref (ref_shim.cpp): generated
+    there (the seeded synthetic problem, bitwise c_generate's), stepped with the
+    reference's engines in place, compared there -- no host copies of 87-174 GB
+    states.  Only libthiim_ref.so is loaded."""
+
+    def __init__(self, dims):
+        L = ref_lib()
+        L.ref_state_new.restype = ctypes.c_void_p
+        L.ref_state_new.argtypes = [ctypes.c_int] * 3
+        for f in ("ref_state_generate", "ref_state_run_naive", "ref_state_run_spatial",
+                  "ref_state_run_mwd", "ref_state_get", "ref_state_set",
+                  "ref_state_compare_fields"):
+            getattr(L, f).restype = ctypes.c_int
+        L.ref_state_free.argtypes = [ctypes.c_void_p]
+        self.dims = tuple(dims)
+        self.h = L.ref_state_new(*self.dims)
+        if not self.h:
+            raise RuntimeError("ref_state_new: " + L.ref_last_error().decode())
+
+    def close(self):
+        if self.h:
+            ref_lib().ref_state_free(ctypes.c_void_p(self.h))
+            self.h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def generate(self, seed: int, layered: bool = False, threads: int = 1):
+        _ref_check(ref_lib().ref_state_generate(ctypes.c_void_p(self.h), ctypes.c_ulonglong(seed),
+                                                int(layered), threads))
+
+    def run_naive(self, steps: int, threads: int = 1) -> float:
+        sec = ctypes.c_double()
+        _ref_check(ref_lib().ref_state_run_naive(ctypes.c_void_p(self.h), steps, threads,
+                                                 ctypes.byref(sec)))
+        return sec.value
+
+    def run_spatial(self, steps, block_y=8, block_x=0, threads=1) -> float:
+        sec = ctypes.c_double()
+        _ref_check(ref_lib().ref_state_run_spatial(ctypes.c_void_p(self.h), steps, block_y,
+                                                   block_x, threads, ctypes.byref(sec)))
+        return sec.value
+
+    def run_mwd(self, steps, dw, bz, tgz, tgx, tgc, threads):
+        sec = ctypes.c_double()
+        ex = ctypes.c_int()
+        _ref_check(ref_lib().ref_state_run_mwd(ctypes.c_void_p(self.h), steps, dw, bz, tgz, tgx,
+                                               tgc, threads, ctypes.byref(sec), ctypes.byref(ex)))
+        return sec.value, ex.value
+
+    def get(self, a: int):
+        import numpy as np
+        nx, ny, nz = self.dims
+        out = np.empty((nx + 2) * (ny + 2) * (nz + 2), dtype=np.complex128)
+        _ref_check(ref_lib().ref_state_get(ctypes.c_void_p(self.h), a,
+                                           ctypes.c_void_p(out.ctypes.data)))
+        return out
+
+    def set(self, a: int, arr):
+        _ref_check(ref_lib().ref_state_set(ctypes.c_void_p(self.h), a,
+                                           ctypes.c_void_p(arr.ctypes.data)))
+
+    def compare_fields(self, fields):
+        """compare_states' field loop vs 12 host arrays (padded layout)."""
+        out = (ctypes.c_longlong * 5)()
+        mx = ctypes.c_double()
+        _ref_check(ref_lib().ref_state_compare_fields(ctypes.c_void_p(self.h), _ptrs(fields), out,
+                                                      ctypes.byref(mx)))
+        return {"differing_values": int(out[0]), "first_component": int(out[1]),
+                "x": int(out[2]), "y": int(out[3]), "z": int(out[4]), "max_abs_diff": mx.value}

@@ -12,9 +12,14 @@
 // padded layout (grid.hpp:12-48) in ProblemState order (state.hpp:49-66):
 // [0..11] fields, [12..23] t, [24..35] c, [36..39] src.
 
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
 #include <cstring>
 #include <exception>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "thiim/bandwidth.hpp"
 #include "thiim/coefficients.hpp"
@@ -71,6 +76,79 @@ int guarded(F&& f) {
     g_err = e.what();
     return 1;
   }
+}
+
+// ---- seeded synthetic inputs, restated here
+// so the CPU baseline arm generates its problem without loading any other
+// library; bitwise equal to oracle/thiim_oracle.c (tests/test_oracle.py).
+std::uint64_t sm64(std::uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+std::uint64_t gen_key(std::uint64_t seed, int array_id) {
+  return sm64(sm64(seed) ^ ((std::uint64_t)(array_id + 1) * 0x9E3779B97F4A7C15ull));
+}
+double gen_u(std::uint64_t key, std::uint64_t counter, int draw) {
+  return (double)(sm64(key + (counter << 8) + (std::uint64_t)draw) >> 11) * 0x1.0p-53;
+}
+ComplexScalar gen_field(std::uint64_t key, std::uint64_t i) {
+  return {2.0 * gen_u(key, i, 0) - 1.0, 2.0 * gen_u(key, i, 1) - 1.0};
+}
+ComplexScalar gen_disk(std::uint64_t key, std::uint64_t i) {
+  const double r = 0.45;
+  for (int k = 0; k < 64; ++k) {
+    const double re = r * (2.0 * gen_u(key, i, 2 * k) - 1.0);
+    const double im = r * (2.0 * gen_u(key, i, 2 * k + 1) - 1.0);
+    if (re * re + im * im <= r * r) return {re, im};
+  }
+  return {0.0, 0.0};
+}
+int gen_layer(std::uint64_t seed, int nx, int nz, int x, int y, int z) {
+  const std::uint64_t c = (std::uint64_t)y * (std::uint64_t)nx + (std::uint64_t)x;
+  int layer = 0;
+  for (int k = 1; k <= 5; ++k) {
+    const std::uint64_t b = sm64(gen_key(seed, 64 + k) + (c << 8));
+    const int h = (int)((b >> 11) % 17ull) - 8;
+    if (z >= k * nz / 6 + h) ++layer;
+  }
+  return layer;
+}
+
+ComplexScalar* array_of(ProblemState& s, int a) {
+  return a < 12 ? s.fields[a].data()
+         : a < 24 ? s.coeff_t[a - 12].data()
+         : a < 36 ? s.coeff_c[a - 24].data()
+                  : s.coeff_src[a - 36].data();
+}
+
+void generate_into(ProblemState& s, std::uint64_t seed, bool layered, int threads) {
+  const int nx = s.dims.nx, ny = s.dims.ny, nz = s.dims.nz;
+  std::uint64_t key[40];
+  for (int a = 0; a < 40; ++a) key[a] = gen_key(seed, a);
+  ComplexScalar table[28][6];
+  for (int a = 12; a < 40; ++a)
+    for (int L = 0; L < 6; ++L) table[a - 12][L] = gen_disk(key[a], (std::uint64_t)L);
+  ComplexScalar* arr[40];
+  for (int a = 0; a < 40; ++a) arr[a] = array_of(s, a);
+  auto work = [&](int w, int nw) {
+    for (int z = w; z < nz; z += nw)
+      for (int y = 0; y < ny; ++y)
+        for (int x = 0; x < nx; ++x) {
+          const std::size_t i = s.dims.linear_index(x, y, z);
+          const int L = layered ? gen_layer(seed, nx, nz, x, y, z) : 0;
+          for (int a = 0; a < 40; ++a)
+            arr[a][i] = a < 12 ? gen_field(key[a], i)
+                        : layered ? table[a - 12][L]
+                                  : gen_disk(key[a], i);
+        }
+  };
+  threads = std::max(1, std::min(threads, nz));
+  std::vector<std::thread> pool;
+  for (int w = 1; w < threads; ++w) pool.emplace_back(work, w, threads);
+  work(0, threads);
+  for (auto& t : pool) t.join();
 }
 
 }  // namespace
@@ -196,6 +274,99 @@ int ref_compare_states(int nx, int ny, int nz, double* const* a, double* const* 
     out_i[4] = d.y;
     out_i[5] = d.z;
     *max_abs_diff = d.max_abs_diff;
+  });
+}
+
+// ---- a reference ProblemState held by the shim (no copies per call): the
+// CPU baseline arm and the full-size parity tests run the reference on
+// 87-174 GB states, which must not be duplicated in host memory.
+void* ref_state_new(int nx, int ny, int nz) {
+  ProblemState* p = nullptr;
+  const int rc = guarded([&] { p = new ProblemState(allocate_state(GridDims(nx, ny, nz))); });
+  return rc ? nullptr : p;
+}
+
+void ref_state_free(void* h) { delete static_cast<ProblemState*>(h); }
+
+int ref_state_generate(void* h, unsigned long long seed, int layered, int threads) {
+  return guarded([&] { generate_into(*static_cast<ProblemState*>(h), seed, layered != 0, threads); });
+}
+
+int ref_state_run_naive(void* h, int steps, int threads, double* seconds) {
+  return guarded([&] {
+    const RunReport r = run_naive(*static_cast<ProblemState*>(h), steps, threads);
+    if (seconds) *seconds = r.seconds;
+  });
+}
+
+int ref_state_run_spatial(void* h, int steps, int block_y, int block_x, int threads,
+                          double* seconds) {
+  return guarded([&] {
+    const RunReport r =
+        run_spatial_blocked(*static_cast<ProblemState*>(h), steps, block_y, block_x, threads);
+    if (seconds) *seconds = r.seconds;
+  });
+}
+
+int ref_state_run_mwd(void* h, int steps, int dw, int bz, int tgz, int tgx, int tgc, int threads,
+                      double* seconds, int* steps_executed) {
+  return guarded([&] {
+    ThreadGroupShape shape;
+    shape.tgz = tgz;
+    shape.tgx = tgx;
+    shape.tgc = tgc;
+    const MwdResult r = run_mwd(*static_cast<ProblemState*>(h), steps, dw, bz, shape, threads);
+    if (seconds) *seconds = r.report.seconds;
+    if (steps_executed) *steps_executed = r.report.steps_executed;
+  });
+}
+
+// copy array a (0..39, ProblemState order) of the held state out / in
+int ref_state_get(void* h, int a, double* out) {
+  return guarded([&] {
+    ProblemState& s = *static_cast<ProblemState*>(h);
+    std::memcpy(out, array_of(s, a), s.dims.padded_cells() * sizeof(ComplexScalar));
+  });
+}
+
+int ref_state_set(void* h, int a, const double* in) {
+  return guarded([&] {
+    ProblemState& s = *static_cast<ProblemState*>(h);
+    std::memcpy(array_of(s, a), in, s.dims.padded_cells() * sizeof(ComplexScalar));
+  });
+}
+
+// compare_states' field loop (verifier.cpp:13-44) between the held state's
+// fields and 12 host field arrays: out_i = {differing_values, first_component,
+// x, y, z} (first_component -1 when equal), *max_abs_diff.
+int ref_state_compare_fields(void* h, double* const* fields, long long* out_i,
+                             double* max_abs_diff) {
+  return guarded([&] {
+    const ProblemState& s = *static_cast<ProblemState*>(h);
+    long long n = 0;
+    double mx = 0.0;
+    out_i[1] = -1;
+    for (int c = 0; c < 12; ++c) {
+      const ComplexScalar* a = s.fields[c].data();
+      const ComplexScalar* b = reinterpret_cast<const ComplexScalar*>(fields[c]);
+      for (int z = 0; z < s.dims.nz; ++z)
+        for (int y = 0; y < s.dims.ny; ++y)
+          for (int x = 0; x < s.dims.nx; ++x) {
+            const std::size_t i = s.dims.linear_index(x, y, z);
+            if (std::memcmp(&a[i], &b[i], sizeof(ComplexScalar)) != 0) {
+              if (n == 0) {
+                out_i[1] = c;
+                out_i[2] = x;
+                out_i[3] = y;
+                out_i[4] = z;
+              }
+              ++n;
+              mx = std::max(mx, std::max(std::abs(a[i].re - b[i].re), std::abs(a[i].im - b[i].im)));
+            }
+          }
+    }
+    out_i[0] = n;
+    *max_abs_diff = mx;
   });
 }
 

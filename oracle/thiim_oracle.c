@@ -321,8 +321,11 @@ static orc_c128 orc_disk_value(uint64_t seed, int array_id, uint64_t counter) {
   return z;
 }
 
+/* Every value is a pure function of (seed, array, padded index), so the
+   planes are filled in parallel (OpenMP; same values for any thread count). */
 void orc_generate_random(orc_state* s, uint64_t seed) {
   for (int a = 0; a < 40; ++a)
+#pragma omp parallel for schedule(static)
     for (int z = 0; z < s->nz; ++z)
       for (int y = 0; y < s->ny; ++y)
         for (int x = 0; x < s->nx; ++x) {
@@ -345,6 +348,7 @@ void orc_generate_layered(orc_state* s, uint64_t seed) {
   orc_c128 table[28][6];
   for (int a = 12; a < 40; ++a)
     for (int L = 0; L < 6; ++L) table[a - 12][L] = orc_disk_value(seed, a, (uint64_t)L);
+#pragma omp parallel for schedule(static)
   for (int z = 0; z < s->nz; ++z)
     for (int y = 0; y < s->ny; ++y)
       for (int x = 0; x < s->nx; ++x) {

@@ -22,12 +22,42 @@ def _line(args, timeout=900):
 
 
 def test_reference_arm_line():
-    d = _line(["--impl", "reference", "--steps", "1", "--warmup", "1"])
+    d = _line(["--impl", "reference", "--config", "c0", "--steps", "1", "--warmup", "1"])
     assert BASE_KEYS <= set(d) and d["impl"] == "reference"
     assert d["value"] > 0 and d["higher_is_better"] is True and d["unit"] == "MLUP/s"
     assert d["cpu_baseline"]["kind"] in ("reference", "port") and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}
+
+
+def test_reference_arm_loads_only_the_reference_library():
+    """The reference arm generates its problem inside oracle/_ref and times the
+    reference's run_naive there: no product library (and no C port) is mapped."""
+    code = ("import runpy, sys\n"
+            "sys.argv = ['bench.py', '--impl', 'reference', '--config', 'c0', '--steps', '1',"
+            " '--warmup', '0']\n"
+            "runpy.run_path('bench.py', run_name='__main__')\n"
+            "print('MAPS', sorted({l.split()[-1] for l in open('/proc/self/maps')"
+            " if l.rstrip().endswith('.so') and '/root' in l or 'repo' in l.split()[-1]}))\n")
+    r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    maps = eval(r.stdout.split("MAPS", 1)[1].strip())
+    mine = [m for m in maps if m.startswith(ROOT)]
+    from oracle import oracle as O
+    if O.ref_available():
+        assert mine == [os.path.join(ROOT, "oracle", "_ref", "libthiim_ref.so")], mine
+    assert not any("paper_1510_05218_b200" in m for m in mine), mine
+
+
+def test_default_configs():
+    m = _bench_module()
+    assert m.default_config(1) == "c2" and m.default_config(2) == "c4"
+    assert m.default_config(8) == "c4"
+    assert m.CONFIGS["c2"][:2] == ((512, 512, 512), 200)
+    assert m.CONFIGS["c4"][:2] == ((1024, 1024, 128), 100)
+    assert m.sample_grid((512, 512, 512)) == (512, 512, 128)
+    assert m.sample_grid((64, 64, 64)) == (64, 64, 64)
 
 
 @pytest.mark.gpu

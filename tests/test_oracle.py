@@ -206,3 +206,26 @@ def test_generator_distributions():
     lay = P.generate_problem(P.GridDims(8, 8, 60), P.GEN_LAYERED, 3)
     col = lay.interior(12)[:, 2, 3]
     assert 2 <= len(np.unique(col)) <= 6  # piecewise constant along z
+
+
+@need_ref
+@pytest.mark.parametrize("dims,layered,threads", [((9, 7, 6), False, 1), ((13, 5, 11), False, 4),
+                                                  ((16, 12, 30), True, 3), ((6, 9, 14), True, 1)])
+def test_reference_shim_generator_matches_oracle(dims, layered, threads):
+    """The generator restated inside oracle/_ref (used by bench.py's CPU arms and
+    the full-size parity tests) is bitwise the oracle's, and a held reference
+    state steps exactly like the reference's run_naive on copied arrays."""
+    a = O.c_generate(dims, 11, layered=layered)
+    with O.RefState(dims) as r:
+        r.generate(11, layered, threads)
+        for k in range(40):
+            assert same(r.get(k), a[k]), k
+        O.ref_run_naive(dims, a, 3, 1)
+        r.run_naive(3, threads)
+        d = r.compare_fields(a[:12])
+        assert d["differing_values"] == 0 and d["first_component"] == -1
+        i = dims[0] + 2 + 1 + (dims[0] + 2) * (dims[1] + 2) * 2  # interior (0, 0, 1)
+        a[5][i] += 1.0
+        d = r.compare_fields(a[:12])
+        assert (d["differing_values"], d["first_component"], d["x"], d["y"], d["z"]) == \
+            (1, 5, 0, 0, 1)
