@@ -265,6 +265,10 @@ def _roofline(P, dims, engine_ran, dev_secs, launches, table=False, iters_total=
     one two-step pass (its sub-range launches + copy-back) is the unit."""
     hbm, peak_kind = load_peaks()
     per_launch_s = dev_secs / max(1, launches)
+    if engine_ran == P.ENGINE_TBLOCK:
+        # a TBLOCK pass (two iterations) is one launch per round of <= 148 CTAs:
+        # the unit is the pass
+        per_launch_s = dev_secs / max(1, iters_total / 2)
     if engine_ran == P.ENGINE_TBLOCK_INPLACE:
         per_launch_s = dev_secs / max(1, iters_total / 2)
         bytes_launch = 1216.0 * dims.interior_cells()  # 832 B pass + 384 B copy-back
@@ -313,9 +317,8 @@ def run_native(args, world, rank, local):
     engine = {"auto": P.ENGINE_AUTO, "split": P.ENGINE_SPLIT, "fused": P.ENGINE_FUSED,
               "tblock": P.ENGINE_TBLOCK, "tblock-inplace": P.ENGINE_TBLOCK_INPLACE}[args.engine]
     opts = P.GpuOptions(device=local if world > 1 else args.device, engine=engine,
-                        tile_y=args.tile_y, z_chunk=args.z_chunk, min_blocks=args.min_blocks,
-                        variant=args.variant, l2_promotion=args.l2_promotion,
-                        y_fastest=args.y_fastest, runtime_seq=args.runtime_seq, pol_mode=args.pol_mode,
+                        tile_y=args.tile_y, z_chunk=args.z_chunk, schedule=args.schedule,
+                        band=args.band,
                         coeff_layout=P.COEFF_TABLE if args.coeff == "table" else P.COEFF_FULL,
                         n_materials=6 if args.coeff == "table" else 0)
     iters = args.iters
@@ -611,12 +614,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--tile-y", type=int, default=0)
     ap.add_argument("--z-chunk", type=int, default=0)
-    ap.add_argument("--min-blocks", type=int, default=0)
-    ap.add_argument("--variant", type=int, default=0)
-    ap.add_argument("--l2-promotion", type=int, default=0)
-    ap.add_argument("--y-fastest", type=int, default=0)
-    ap.add_argument("--runtime-seq", type=int, default=0)
-    ap.add_argument("--pol-mode", type=int, default=0)
+    ap.add_argument("--schedule", type=int, default=0,
+                    help="TBLOCK CTA schedule: 0 auto (rounds, banded tiles), 1 one launch")
+    ap.add_argument("--band", type=int, default=0, help="TBLOCK rounds: tile columns per band")
     ap.add_argument("--config", default=None, choices=sorted(CONFIGS),
                     help="default: configs[2] at N=1, configs[4] (per rank) at N>1")
     ap.add_argument("--check", type=int, default=0,

@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define THIIM_GPU_ABI_VERSION 1
+#define THIIM_GPU_ABI_VERSION 2
 
 /* == thiim::ComplexScalar (include/thiim/complex.hpp:11-20). */
 typedef struct { double re, im; } thiim_c128;
@@ -89,8 +89,13 @@ typedef struct {
   int tile_y;       /* 0 = auto */
   int z_chunk;      /* planes per CTA along the z-stream, 0 = auto */
   int time_block;   /* TBLOCK: steps per HBM pass, 0 = auto */
-  int reserved[7];  /* experiment / test knobs (0 = defaults); reserved[6] = 1 places
-                       every slab on `device` (exercises multi-slab paths on one GPU) */
+  int schedule;     /* TBLOCK CTA schedule: 0 = auto (rounds of <= one CTA per SM,
+                       tiles in bands, so neighbouring tiles stream the same planes at
+                       the same time), 1 = one launch of all tiles (x-fastest order) */
+  int band;         /* TBLOCK rounds: tile columns per band, 0 = auto */
+  int same_device;  /* test knob: 1 places every slab on `device` (exercises the
+                       multi-slab paths on one GPU) */
+  int reserved[4];  /* 0 */
   int coeff_layout; /* THIIM_COEFF_FULL (28 arrays) or THIIM_COEFF_TABLE (material ids) */
   int n_materials;  /* THIIM_COEFF_TABLE: rows of the coefficient table (<= 64) */
 } thiim_gpu_opts;

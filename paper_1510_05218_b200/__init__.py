@@ -275,7 +275,8 @@ class _Dims(ctypes.Structure):
 class _Opts(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int), ("n_gpus", ctypes.c_int), ("engine", ctypes.c_int),
                 ("tile_x", ctypes.c_int), ("tile_y", ctypes.c_int), ("z_chunk", ctypes.c_int),
-                ("time_block", ctypes.c_int), ("reserved", ctypes.c_int * 7),
+                ("time_block", ctypes.c_int), ("schedule", ctypes.c_int), ("band", ctypes.c_int),
+                ("same_device", ctypes.c_int), ("reserved", ctypes.c_int * 4),
                 ("coeff_layout", ctypes.c_int), ("n_materials", ctypes.c_int)]
 
 
@@ -360,7 +361,7 @@ def lib() -> ctypes.CDLL:
     L.thiim_gpu_run_batch.argtypes = [ctypes.POINTER(_Dims), ctypes.POINTER(_Opts), ctypes.c_int,
                                       PP, PP, ctypes.c_int, ctypes.c_int,
                                       ctypes.POINTER(_BatchStats)]
-    if L.thiim_gpu_abi_version() != 1:
+    if L.thiim_gpu_abi_version() != 2:
         raise GpuError("libthiim_gpu.so ABI mismatch")
     _LIB = L
     return L
@@ -415,13 +416,9 @@ class GpuOptions:
     tile_y: int = 0
     z_chunk: int = 0
     time_block: int = 0
-    min_blocks: int = 0  # experimental register cap knob (reserved[0])
-    variant: int = 0     # fused kernel variant (reserved[1]): 0 bulk-async staged, 1 register-staged
-    l2_promotion: int = 0  # TMA L2 promotion (reserved[2]): 0 none, 1 64B, 2 128B, 3 256B
-    y_fastest: int = 0   # CTA order (reserved[3]): 0 x-tiles fastest (default), 1 y-tiles fastest
-    runtime_seq: int = 0  # experiment (reserved[4]): 1 = fused producer interprets its box sequence at run time
-    pol_mode: int = 0  # experiment (reserved[5]): TBLOCK L2 policy set
-    same_device: int = 0  # test knob (reserved[6]): all slabs of a multi-slab context on `device`
+    schedule: int = 0  # TBLOCK CTA schedule: 0 auto (rounds, tiles in bands), 1 one launch
+    band: int = 0      # TBLOCK rounds: tile columns per band, 0 = auto
+    same_device: int = 0  # test knob: all slabs of a multi-slab context on `device`
     coeff_layout: int = 0  # COEFF_FULL (reference layout) or COEFF_TABLE (material ids)
     n_materials: int = 0
 
@@ -430,13 +427,7 @@ class GpuOptions:
         lib().thiim_gpu_default_opts(ctypes.byref(o))
         o.device, o.n_gpus, o.engine = self.device, self.n_gpus, self.engine
         o.tile_x, o.tile_y, o.z_chunk, o.time_block = self.tile_x, self.tile_y, self.z_chunk, self.time_block
-        o.reserved[0] = self.min_blocks
-        o.reserved[1] = self.variant
-        o.reserved[2] = self.l2_promotion
-        o.reserved[3] = self.y_fastest
-        o.reserved[4] = self.runtime_seq
-        o.reserved[5] = self.pol_mode
-        o.reserved[6] = self.same_device
+        o.schedule, o.band, o.same_device = self.schedule, self.band, self.same_device
         o.coeff_layout, o.n_materials = self.coeff_layout, self.n_materials
         return o
 

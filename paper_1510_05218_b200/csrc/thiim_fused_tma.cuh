@@ -28,56 +28,6 @@
 
 namespace thiim_gpu {
 
-// Level-1 / fused plane sequence (12 groups).  The consumer code below reads
-// the groups in exactly this order; the order of updates within one family is
-// free (H reads only E, E reads only H: components.hpp:55-66).
-template <class FS, class CS>
-inline void seq_plane(GroupSeq& S, FS fslot, CS cslot) {
-  S.ngroups = 0;
-  S.nelem = 0;
-  auto add = [&](int slot, int box, int src, int coef) {
-    SeqElem& e = S.e[S.nelem++];
-    e.slot = (short)slot;
-    e.box = (char)box;
-    e.src = (char)src;
-    e.coef = (char)coef;
-    S.gsize[S.ngroups - 1]++;
-  };
-  auto group = [&]() { S.gsize[S.ngroups++] = 0; };
-  group();  // G0: E_old(z+1) Exy Exz Eyx Eyz
-  for (int c : {EXY, EXZ, EYX, EYZ}) add(fslot(c), BOX_A, 1, 0);
-  group();  // G1: E_old(z+1) Ezx Ezy
-  for (int c : {EZX, EZY}) add(fslot(c), BOX_A, 1, 0);
-  const int hbox[6] = {BOX_BY, BOX_BY, BOX_BX, BOX_BX, BOX_B, BOX_B};
-  const int hsrc[6] = {-1, SRC_HXZ, -1, SRC_HYZ, -1, -1};
-  for (int c = HXY; c <= HZY; ++c) {  // G2..G7: F, t, c (, src) per H component
-    group();
-    const int b = hbox[c - HXY];
-    add(fslot(c), b, 0, 0);
-    add(cslot(12 + c), b, 0, 1);
-    add(cslot(24 + c), b, 0, 1);
-    if (hsrc[c - HXY] >= 0) add(cslot(36 + hsrc[c - HXY]), b, 0, 1);
-  }
-  group();  // G8: Exy t c, Eyx t c
-  for (int c : {EXY, EYX}) {
-    add(cslot(12 + c), BOX_C, 0, 1);
-    add(cslot(24 + c), BOX_C, 0, 1);
-  }
-  group();  // G9: Exz t c src
-  add(cslot(12 + EXZ), BOX_C, 0, 1);
-  add(cslot(24 + EXZ), BOX_C, 0, 1);
-  add(cslot(36 + SRC_EXZ), BOX_C, 0, 1);
-  group();  // G10: Eyz t c src
-  add(cslot(12 + EYZ), BOX_C, 0, 1);
-  add(cslot(24 + EYZ), BOX_C, 0, 1);
-  add(cslot(36 + SRC_EYZ), BOX_C, 0, 1);
-  group();  // G11: Ezx t c, Ezy t c
-  for (int c : {EZX, EZY}) {
-    add(cslot(12 + c), BOX_C, 0, 1);
-    add(cslot(24 + c), BOX_C, 0, 1);
-  }
-}
-
 template <int BY, int NG>
 struct FusedSmem {
   Ring<BY, NG> ring;
@@ -85,46 +35,17 @@ struct FusedSmem {
   double2 sH[3][BY][32];  // H_new sums at plane z
 };
 
-// Producer: issue the groups of `seq` for one plane (level plane z, local
-// padded planes z+1 / z+2 for src 0 / 1).
-template <int BY, int NG>
-__device__ __forceinline__ void produce_plane(Ring<BY, NG>& r, int& g, uint32_t& ph,
-                                              const GroupSeq& S, const TmaMaps& maps, int xb,
-                                              int yb, int z) {
-  using Gm = BoxGeom<BY>;
-  int e = 0;
-  for (int gi = 0; gi < S.ngroups; ++gi) {
-    const int n = S.gsize[gi];
-    int bytes = 0;
-    for (int k = 0; k < n; ++k) bytes += Gm::bytes(S.e[e + k].box);
-    mbar_wait(&r.empty[g], ph ^ 1);
-    mbar_arrive_expect_tx(&r.full[g], (uint32_t)bytes);
-    for (int k = 0; k < n; ++k, ++e) {
-      const SeqElem el = S.e[e];
-      const int b = el.box;
-      tma_load_4d(&r.buf[g][k][0], &maps.m[b], 2 * (xb + 1 + Gm::x0(b)), yb + 1 + Gm::y0(b),
-                  z + 1 + el.src, el.slot, &r.full[g]);
-    }
-    if (++g == NG) {
-      g = 0;
-      ph ^= 1;
-    }
-  }
-}
-
 template <int BY, int NG, bool COUNT = false>
 __global__ void __launch_bounds__(32 * (BY + 1), 1)
-    k_fused_tma(Grid g, Arrays A, const __grid_constant__ TmaMaps maps,
-                const __grid_constant__ GroupSeq S, int zc, int tiles_y, int tiles_x,
-                int x_fastest, int fb, int cb, int ct) {
+    k_fused_tma(Grid g, Arrays A, const __grid_constant__ TmaMaps maps, int zc, int tiles_x,
+                int fb, int cb) {
   constexpr int BX = 32, TX = BX - 2, TY = BY - 2, NCOMP = 32 * BY;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   FusedSmem<BY, NG>& sm = *reinterpret_cast<FusedSmem<BY, NG>*>(smem_raw);
-  // x-tiles enumerate fastest by default: x-neighbours share the DRAM blocks
-  // at their (unaligned) box edges, so running them together lets the second
-  // fetch hit in L2 (measured: 5.7% excess DRAM reads vs 19% y-fastest)
-  const int bty = x_fastest ? blockIdx.x / tiles_x : blockIdx.x % tiles_y;
-  const int btx = x_fastest ? blockIdx.x % tiles_x : blockIdx.x / tiles_y;
+  // x-tiles enumerate fastest: x-neighbours share the DRAM blocks at their
+  // (unaligned) box edges, so running them together lets the second fetch hit
+  // in L2 (measured: 5.7% excess DRAM reads vs 19% y-fastest)
+  const int bty = blockIdx.x / tiles_x, btx = blockIdx.x % tiles_x;
   const int xb = btx * TX - 1, yb = bty * TY - 1;
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int z0 = blockIdx.z * zc;
@@ -141,14 +62,9 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
     if (tx == 0) {
 #pragma unroll
       for (int b = 0; b < NBOX; ++b) tma_prefetch_desc(&maps.m[b]);
-      int gi = 0;
-      uint32_t ph = 0;
-      if (ct) {  // compile-time sequence (thiim_producer.cuh)
-        RingProducer<BY, NG> P(sm.ring, maps, xb, yb);
-        for (int z = z0; z < z1; ++z) produce_plane_ct<false>(P, fb, cb, z);
-      } else {
-        for (int z = z0; z < z1; ++z) produce_plane(sm.ring, gi, ph, S, maps, xb, yb, z);
-      }
+      // straight-line sequence (thiim_producer.cuh): 40 boxes in 12 groups
+      RingProducer<BY, NG> P(sm.ring, maps, xb, yb);
+      for (int z = z0; z < z1; ++z) produce_plane_ct<false>(P, fb, cb, z);
     }
     return;
   }

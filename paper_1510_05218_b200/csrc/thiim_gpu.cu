@@ -31,7 +31,6 @@
 #include "../../include/thiim_gpu.h"
 #include "thiim_common.cuh"
 #include "thiim_complex.cuh"
-#include "thiim_fused.cuh"
 #include "thiim_fused_table.cuh"
 #include "thiim_fused_tma.cuh"
 #include "thiim_split.cuh"
@@ -108,11 +107,6 @@ struct Slab {
   bool maps_ok[6] = {false, false, false, false, false, false};
   TmaMaps maps_seg[6][2];  // the same for 16- / 8-lane segments (folded TBLOCK tiles)
   bool maps_seg_ok[6][2] = {};
-  // TBLOCK: per-SM scratch ring (3 planes x 12 fields x tile) and its tensor map
-  double2* scratch = nullptr;
-  size_t scratch_bytes = 0;
-  CUtensorMap smap;
-  int smap_by = 0;
 
   // TBLOCK in place (THIIM_ENGINE_TBLOCK_INPLACE, one whole-z slab, no second
   // field set): spare output planes of one z sub-range (12 x ip_L padded
@@ -613,21 +607,6 @@ int launch_split(thiim_gpu_ctx* ctx, Slab& s, int fam, long long* launches) {
   return THIIM_OK;
 }
 
-template <int BX, int BY, int MINB>
-int launch_fused_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
-  const Arrays A = s.arrays(s.cur, s.cur ^ 1);
-  constexpr int TX = BX - 2, TY = BY - 2;
-  const dim3 block(BX, BY);
-  const long long cols = (long long)((s.g.nx + TX - 1) / TX) * ((s.g.ny + TY - 1) / TY);
-  const int zc = pick_zchunk(ctx, s, cols, ctx->opts.z_chunk);
-  const dim3 grid((s.g.nx + TX - 1) / TX, (s.g.ny + TY - 1) / TY, (s.g.nz + zc - 1) / zc);
-  k_fused<BX, BY, MINB><<<grid, block, 0, s.stream>>>(s.g, A, zc);
-  CK(cudaGetLastError());
-  s.cur ^= 1;
-  ++*launches;
-  return THIIM_OK;
-}
-
 // z-chunk count for a grid of `cols` column tiles with `per_sm` resident CTAs
 // per SM: minimise (waves x planes-per-CTA incl. ~1.5 planes of prologue).
 int balanced_zchunk(const Slab& s, long long cols, int per_sm, int user) {
@@ -673,16 +652,14 @@ TmaMaps& tmaps(Slab& s, int by, int width = 32) {
   return width == 32 ? s.maps[w] : s.maps_seg[w][width == 16 ? 0 : 1];
 }
 
-int ensure_tmap(Slab& s, int by, int promo, int width = 32) {
+// L2 promotion stays off: 256-B promotion inflated DRAM reads by 7%
+int ensure_tmap(Slab& s, int by, int width = 32) {
   const int w = map_index(by);
   if (w < 0) return fail(THIIM_ERR_CONFIG, "no tensor maps for tile height " + std::to_string(by));
   if (width != 32 && width != 16 && width != 8)
     return fail(THIIM_ERR_CONFIG, "no tensor maps for tile width " + std::to_string(width));
   bool& ok = width == 32 ? s.maps_ok[w] : s.maps_seg_ok[w][width == 16 ? 0 : 1];
   if (ok) return THIIM_OK;
-  const CUtensorMapL2promotion pr[4] = {CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_64B,
-                                        CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B};
   auto fn = get_encode_fn();
   if (!fn) return fail(THIIM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   const cuuint64_t dims[4] = {(cuuint64_t)(2 * s.g.px), (cuuint64_t)(s.g.pxy / s.g.px),
@@ -699,7 +676,7 @@ int ensure_tmap(Slab& s, int by, int promo, int width = 32) {
     CUresult r = fn(&tmaps(s, by, width).m[b], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, s.buf, dims,
                     strides, box,
                     estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                    pr[promo & 3], CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                    CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS)
       return fail(THIIM_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
   }
@@ -711,10 +688,7 @@ template <int BY, int NG>
 int launch_fused_tma_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
   const Arrays A = s.arrays(s.cur, s.cur ^ 1);
   const int cur = s.cur, nf = s.nfield_sets;
-  GroupSeq S;
-  seq_plane(S, [&](int k) { return cur * 12 + k; }, [&](int a) { return nf * 12 + (a - 12); });
-  // reserved[2]: L2 promotion of the TMA fills (0 none, 1 64B, 2 128B, 3 256B)
-  int r = ensure_tmap(s, BY, ctx->opts.reserved[2]);
+  int r = ensure_tmap(s, BY);
   if (r) return r;
   constexpr int TX = 30, TY = BY - 2;
   const size_t smem = sizeof(FusedSmem<BY, NG>);
@@ -733,54 +707,14 @@ int launch_fused_tma_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
   const dim3 grid(tiles_x * tiles_y, 1, (s.g.nz + zc - 1) / zc);
   const dim3 block(32, BY + 1);
   (s.cnt ? k_fused_tma<BY, NG, true> : k_fused_tma<BY, NG, false>)<<<grid, block, smem, s.stream>>>(
-      s.g, A, tmaps(s, BY), S, zc,
-                                                       tiles_y, tiles_x, ctx->opts.reserved[3] == 0,
-                                                       cur * 12, nf * 12, ctx->opts.reserved[4] == 0);
+      s.g, A, tmaps(s, BY), zc, tiles_x, cur * 12, nf * 12);
   CK(cudaGetLastError());
   s.cur ^= 1;
   ++*launches;
   return THIIM_OK;
 }
 
-// ---- TBLOCK (two steps per launch)
-int smid_count() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    n = std::max(256, 2 * sms);  // %smid < %nsmid <= this bound on sm_100
-  }
-  return n;
-}
-
-template <int BY>
-int ensure_scratch(Slab& s) {
-  const size_t tile = (size_t)BY * 32;
-  const int nsm = smid_count();
-  const size_t bytes = (size_t)nsm * 24 * tile * sizeof(double2);  // 2 planes x 12 fields
-  if (s.scratch && s.scratch_bytes >= bytes && s.smap_by == BY) return THIIM_OK;
-  if (s.scratch) cudaFree(s.scratch);
-  s.scratch = nullptr;
-  CK(cudaMalloc(&s.scratch, bytes));
-  CK(cudaMemsetAsync(s.scratch, 0, bytes, s.stream));
-  CK(cudaStreamSynchronize(s.stream));
-  s.scratch_bytes = bytes;
-  auto fn = get_encode_fn();
-  if (!fn) return fail(THIIM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-  const cuuint64_t dims[3] = {64, (cuuint64_t)BY, (cuuint64_t)nsm * 24};
-  const cuuint64_t strides[2] = {32 * 16, (cuuint64_t)BY * 32 * 16};
-  const cuuint32_t box[3] = {64, (cuuint32_t)BY, 1};
-  const cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = fn(&s.smap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, s.scratch, dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                  CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(THIIM_ERR_CUDA, "scratch tensor map failed");
-  s.smap_by = BY;
-  return THIIM_OK;
-}
-
+// ---- TBLOCK (two steps per pass)
 // z-chunks of a TBLOCK launch: each CTA re-does ~2 planes of level-1/level-2
 // work at its start; minimise waves x (planes + 2) over one CTA per SM
 int tblock_zchunk(const Slab& s, long long cols) {
@@ -799,47 +733,39 @@ int tblock_zchunk(const Slab& s, long long cols) {
   return (s.g.nz + best_c - 1) / best_c;
 }
 
+// Tile columns per band of a round-scheduled TBLOCK pass (TileOrder,
+// thiim_tblock.cuh).  A round of G tiles as a band x (G / band) block re-fetches
+// the y-overlap of its `band` bottom tiles (~50 KB per tile-plane of level-1
+// boxes: 105 array-rows of ~30 cells) and the x-overlap of its G / band side
+// tiles (~23 KB: 1445 cells); band ~ sqrt(G * 23 / 50) ~ 8 minimises the sum.
+// Bands are made equal-width.
+int tblock_band(int tiles_x, int per_round, int user) {
+  if (user > 0) return std::min(user, tiles_x);
+  const double b = std::sqrt((double)per_round * 23.0 / 50.0);
+  const int nb = std::max(1, (int)std::ceil(tiles_x / b));
+  return (tiles_x + nb - 1) / nb;
+}
+
 template <int BY, int NG>
 int launch_tblock2_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches, const PeerOut& po) {
   if (!s.deep && (s.g.halo_lo || s.z1 < ctx->dims.nz))
     return fail(THIIM_ERR_CONFIG, "TBLOCK on a slab needs a deep-halo slab context");
   const Arrays A = s.arrays(s.cur, s.cur ^ 1);
   const int cur = s.cur, nf = s.nfield_sets;
-  auto fslot = [&](int k) { return cur * 12 + k; };
-  auto cslot = [&](int a) { return nf * 12 + (a - 12); };
-  // reserved[1] = 2 selects the L2-scratch hand-off kernel (k_tblock2);
-  // default: the TMEM hand-off (k_tblock_tm)
-  const bool scratch = ctx->opts.reserved[1] == 2;
-  GroupSeq S1, S2;
-  seq_plane(S1, fslot, cslot);
-  if (scratch)
-    seq_level2(S2, cslot);
-  else
-    seq_level2_coef(S2, cslot);
-  int r = ensure_tmap(s, BY, ctx->opts.reserved[2]);
+  int r = ensure_tmap(s, BY);
   if (r) return r;
-  if (scratch && (r = ensure_scratch<BY>(s))) return r;
-  const size_t smem = scratch ? sizeof(TbSmem<BY, NG>) : sizeof(TmSmem<BY, NG>);
+  const size_t smem = sizeof(TmSmem<BY, NG>);
   static std::atomic<unsigned> attr_set{0};
   if (setup_needed(attr_set, s.device)) {
-    if constexpr (BY == 15 && sizeof(TbSmem<BY, NG>) <= 232448)
-      CK(cudaFuncSetAttribute(k_tblock2<BY, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)sizeof(TbSmem<BY, NG>)));
-    const int tm_smem = (int)sizeof(TmSmem<BY, NG>);
+    const int tm_smem = (int)smem;
     CK(cudaFuncSetAttribute(k_tblock_tm<BY, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             tm_smem));
     CK(cudaFuncSetAttribute(k_tblock_tm<BY, NG, true>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, tm_smem));
     if constexpr (BY == 15) {
-      CK(cudaFuncSetAttribute(k_tblock_tm<BY, NG, false, 8>,
-                              cudaFuncAttributeMaxDynamicSharedMemorySize, tm_smem));
-      CK(cudaFuncSetAttribute(k_tblock_tm<BY, NG, true, 8>,
-                              cudaFuncAttributeMaxDynamicSharedMemorySize, tm_smem));
-      CK(cudaFuncSetAttribute(k_tblock_tm<BY, NG, false, 16>,
-                              cudaFuncAttributeMaxDynamicSharedMemorySize, tm_smem));
-      CK(cudaFuncSetAttribute(k_tblock_tm<BY, NG, true, 16>,
-                              cudaFuncAttributeMaxDynamicSharedMemorySize, tm_smem));
-      for (auto f : {k_tblock_tm<BY, NG, false, 0, true>, k_tblock_tm<BY, NG, true, 0, true>,
+      for (auto f : {k_tblock_tm<BY, NG, false, 8>, k_tblock_tm<BY, NG, true, 8>,
+                     k_tblock_tm<BY, NG, false, 16>, k_tblock_tm<BY, NG, true, 16>,
+                     k_tblock_tm<BY, NG, false, 0, true>, k_tblock_tm<BY, NG, true, 0, true>,
                      k_tblock_tm<BY, NG, false, 8, true>, k_tblock_tm<BY, NG, true, 8, true>,
                      k_tblock_tm<BY, NG, false, 16, true>, k_tblock_tm<BY, NG, true, 16, true>})
         CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, tm_smem));
@@ -855,54 +781,57 @@ int launch_tblock2_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches, const Pee
   const int rem = s.g.nx - (s.g.nx / TX2) * TX2;
   static const bool no_fold = std::getenv("THIIM_NO_FOLD") != nullptr;  // A/B knob
   if constexpr (BY == 15) {
-    if (!scratch && !no_fold && s.g.nx >= TX2 && rem > 0 && rem <= 12) {
+    if (!no_fold && s.g.nx >= TX2 && rem > 0 && rem <= 12) {
       wf = rem <= 4 ? 8 : 16;
       tiles_x = s.g.nx / TX2;
       n_fold = (tiles_y + 32 / wf - 1) / (32 / wf);
-      if ((r = ensure_tmap(s, BY, ctx->opts.reserved[2], wf))) return r;
+      if ((r = ensure_tmap(s, BY, wf))) return r;
     }
   }
-  const int n_main = tiles_x * tiles_y;
+  const int n_main = tiles_x * tiles_y, nbt = n_main + n_fold;
   int zc = ctx->opts.z_chunk;
-  if (zc <= 0) zc = tblock_zchunk(s, (long long)n_main + n_fold);
-  const dim3 grid(n_main + n_fold, 1, (s.g.nz + zc - 1) / zc);
+  if (zc <= 0) zc = tblock_zchunk(s, (long long)nbt);
+  const int nchunks = (s.g.nz + zc - 1) / zc;
+  const long long items = (long long)nbt * nchunks;
+  // CTA schedule: rounds of at most one CTA per SM in band order (default), or
+  // (schedule 1) one launch of every item in x-fastest order
+  const int sms = sm_count(s.device);
+  const bool one_launch = ctx->opts.schedule == 1;
+  const long long rounds = one_launch ? 1 : (items + sms - 1) / sms;
+  const long long per_round = (items + rounds - 1) / rounds;
+  TileOrder ord;
+  ord.nbt = nbt;
+  ord.tiles_y = tiles_y;
+  ord.band = one_launch ? tiles_x : tblock_band(tiles_x, (int)std::min<long long>(per_round, sms),
+                                                 ctx->opts.band);
   const dim3 block(32, BY + 1);
-  if (scratch && s.deep) return fail(THIIM_ERR_CONFIG, "the scratch TBLOCK variant is whole-z only");
-  if (scratch) {
-    if constexpr (BY == 15) {
-      TbParams P;
-      P.zc = zc;
-      P.tiles_x = tiles_x;
-      for (int k = 0; k < 12; ++k) P.field_in[k] = fslot(k);
-      P.scratch = s.scratch;
-      k_tblock2<BY, NG><<<grid, block, smem, s.stream>>>(s.g, A, tmaps(s, BY), s.smap,
-                                                         S1, S2, P);
+  // sanitizer negative control (tests only): THIIM_SANITIZE_UNCOUNTED=1 runs the
+  // uninstrumented instances while the sanitizer is on, so every store must be
+  // reported missing
+  const bool c = s.cnt != nullptr && !std::getenv("THIIM_SANITIZE_UNCOUNTED");
+  auto kern = c ? k_tblock_tm<BY, NG, true> : k_tblock_tm<BY, NG, false>;
+  if constexpr (BY == 15) {
+    if (s.deep) {  // owned-plane stores + peer stores (multi-GPU slabs)
+      kern = wf == 8    ? (c ? k_tblock_tm<BY, NG, true, 8, true> : k_tblock_tm<BY, NG, false, 8, true>)
+             : wf == 16 ? (c ? k_tblock_tm<BY, NG, true, 16, true>
+                             : k_tblock_tm<BY, NG, false, 16, true>)
+                        : (c ? k_tblock_tm<BY, NG, true, 0, true> : k_tblock_tm<BY, NG, false, 0, true>);
     } else {
-      return fail(THIIM_ERR_CONFIG, "the scratch TBLOCK variant has tile height 15 only");
+      if (wf == 8) kern = c ? k_tblock_tm<BY, NG, true, 8> : k_tblock_tm<BY, NG, false, 8>;
+      if (wf == 16) kern = c ? k_tblock_tm<BY, NG, true, 16> : k_tblock_tm<BY, NG, false, 16>;
     }
-  } else {
-    auto kern = s.cnt ? k_tblock_tm<BY, NG, true> : k_tblock_tm<BY, NG, false>;
-    if constexpr (BY == 15) {
-      const bool c = s.cnt != nullptr;
-      if (s.deep) {  // owned-plane stores + peer stores (multi-GPU slabs)
-        kern = wf == 8    ? (c ? k_tblock_tm<BY, NG, true, 8, true> : k_tblock_tm<BY, NG, false, 8, true>)
-               : wf == 16 ? (c ? k_tblock_tm<BY, NG, true, 16, true>
-                               : k_tblock_tm<BY, NG, false, 16, true>)
-                          : (c ? k_tblock_tm<BY, NG, true, 0, true> : k_tblock_tm<BY, NG, false, 0, true>);
-      } else {
-        if (wf == 8) kern = c ? k_tblock_tm<BY, NG, true, 8> : k_tblock_tm<BY, NG, false, 8>;
-        if (wf == 16) kern = c ? k_tblock_tm<BY, NG, true, 16> : k_tblock_tm<BY, NG, false, 16>;
-      }
-    } else if (s.deep) {
-      return fail(THIIM_ERR_CONFIG, "deep-halo slabs run TBLOCK at tile height 15");
-    }
-    kern<<<grid, block, smem, s.stream>>>(s.g, A, tmaps(s, BY), tmaps(s, BY, wf ? wf : 32), po,
-                                          cur * 12, nf * 12, zc, tiles_x, n_main,
-                                          ctx->opts.reserved[5]);
+  } else if (s.deep) {
+    return fail(THIIM_ERR_CONFIG, "deep-halo slabs run TBLOCK at tile height 15");
   }
-  CK(cudaGetLastError());
+  for (long long it0 = 0; it0 < items; it0 += per_round) {
+    ord.item0 = (int)it0;
+    const unsigned n = (unsigned)std::min<long long>(per_round, items - it0);
+    kern<<<n, block, smem, s.stream>>>(s.g, A, tmaps(s, BY), tmaps(s, BY, wf ? wf : 32), po,
+                                       cur * 12, nf * 12, zc, tiles_x, n_main, ord);
+    CK(cudaGetLastError());
+    ++*launches;
+  }
   s.cur ^= 1;
-  ++*launches;
   return THIIM_OK;
 }
 
@@ -911,7 +840,7 @@ int launch_tblock_table_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches, cons
   if (!s.deep && (s.g.halo_lo || s.z1 < ctx->dims.nz))
     return fail(THIIM_ERR_CONFIG, "TBLOCK on a slab needs a deep-halo slab context");
   const Arrays A = s.arrays(s.cur, s.cur ^ 1);
-  int r = ensure_tmap(s, BY, 0);
+  int r = ensure_tmap(s, BY);
   if (r) return r;
   TableGrid T;
   T.mat = s.mat;
@@ -1033,7 +962,7 @@ int launch_fused_table_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
   const int cur = s.cur;
   GroupSeq S;
   seq_table(S, [&](int k) { return cur * 12 + k; });
-  int r = ensure_tmap(s, BY, 0);
+  int r = ensure_tmap(s, BY);
   if (r) return r;
   TableMaps maps;
   maps.f = tmaps(s, BY);
@@ -1068,17 +997,6 @@ int launch_fused_table_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
 int launch_fused(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
   CK(cudaSetDevice(s.device));
   if (s.table) return launch_fused_table_t<15, 5>(ctx, s, launches);
-  // reserved[1] = 1 selects the register-staged kernel (thiim_fused.cuh);
-  // default is the bulk-async staged one (thiim_fused_tma.cuh).
-  if (ctx->opts.reserved[1] == 1) {
-    // tile_y selects the CTA height (rows incl. the 2-row ring); reserved[0] the
-    // minimum resident CTAs per SM requested from ptxas (register cap).
-    const int by = ctx->opts.tile_y, minb = ctx->opts.reserved[0];
-    if (by == 16) return launch_fused_t<32, 16, 1>(ctx, s, launches);
-    if (by == 4) return launch_fused_t<32, 4, 4>(ctx, s, launches);
-    if (minb == 1) return launch_fused_t<32, 8, 1>(ctx, s, launches);
-    return launch_fused_t<32, 8, 2>(ctx, s, launches);
-  }
   if (ctx->opts.tile_y == 8) return launch_fused_tma_t<8, 12>(ctx, s, launches);
   if (ctx->opts.tile_y == 16) return launch_fused_tma_t<16, 5>(ctx, s, launches);
   if (ctx->opts.tile_y == 116) return launch_fused_tma_t<16, 2>(ctx, s, launches);  // stress: tiny ring
@@ -1193,9 +1111,9 @@ static int create_impl(const thiim_dims* dims, const thiim_gpu_opts* opts, bool 
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1)
     return fail(THIIM_ERR_CUDA, "no CUDA device visible");
-  // reserved[6] = 1 (test knob): put every slab on opts->device, so the
+  // same_device = 1 (test knob): put every slab on opts->device, so the
   // multi-slab exchange paths can be exercised with one GPU
-  const int dev_step = o.reserved[6] == 1 ? 0 : 1;
+  const int dev_step = o.same_device == 1 ? 0 : 1;
   if (o.device < 0 || o.device + dev_step * ((int)ranges.size() - 1) >= ndev)
     return fail(THIIM_ERR_CONFIG, "device range exceeds visible devices");
 
@@ -1532,7 +1450,6 @@ void thiim_gpu_destroy(thiim_gpu_ctx* ctx) {
       cudaFreeAsync(sl.buf, sl.stream);
       cudaStreamSynchronize(sl.stream);
     }
-    if (sl.scratch) cudaFree(sl.scratch);
     if (sl.cnt) cudaFree(sl.cnt);
     if (sl.cov_bad) cudaFree(sl.cov_bad);
     if (sl.mat) cudaFree(sl.mat);

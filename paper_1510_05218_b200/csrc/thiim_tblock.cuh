@@ -12,16 +12,14 @@
 // identical); chunk starts recompute one level-1 plane and one level-2 H plane
 // below.  DRAM traffic: 832 / 2 = 416 B/LUP plus tile-overlap re-fetch.
 //
-// Two kernels:
-//   k_tblock_tm (default): the level-1 -> level-2 hand-off (E^1 / H^1 of plane
-//     q-1, computed by the same thread) lives in the thread's TMEM lane; a
-//     remainder tile column of <= 12 grid columns runs as folded CTAs of 8- or
-//     16-lane segments; deep-halo slabs of multi-GPU contexts write their
-//     neighbours' halo planes directly (peer stores).  See the comments at
-//     k_tblock_tm and DESIGN.md "Temporal blocking".
-//   k_tblock2 (A/B only, `variant = 2`): the predecessor -- the hand-off through
-//     a per-SM scratch ring in global memory (L2-resident, evict_last stores,
-//     re-fetched by TMA behind a `ready` barrier); 5.4 vs 11.0 GLUP/s at 256^3.
+// k_tblock_tm: the level-1 -> level-2 hand-off (E^1 / H^1 of plane q-1,
+// computed by the same thread) lives in the thread's TMEM lane; a remainder
+// tile column of <= 12 grid columns runs as folded CTAs of 8- or 16-lane
+// segments; deep-halo slabs of multi-GPU contexts write their neighbours' halo
+// planes directly (peer stores).  See the comments at k_tblock_tm and
+// DESIGN.md "Temporal blocking".  (Its predecessor -- the hand-off through an
+// L2-resident scratch ring, 5.4 vs 11.0 GLUP/s at 256^3 -- and the
+// pattern-only ceiling builds are recorded in DESIGN.md, not shipped.)
 #pragma once
 
 #include <cuda.h>
@@ -33,498 +31,7 @@
 #include "thiim_producer.cuh"
 #include "thiim_tmem.cuh"
 
-#ifndef THIIM_PATTERN_ONLY
-#define THIIM_PATTERN_ONLY 0
-#endif
-
 namespace thiim_gpu {
-
-// Level-2 sequence (11 groups); src 2 = level-1 output of plane r (component in
-// `slot`), from scratch or, on a ghost plane, the input field set.
-template <class CS>
-inline void seq_level2(GroupSeq& S, CS cslot) {
-  S.ngroups = 0;
-  S.nelem = 0;
-  auto add = [&](int slot, int box, int src, int coef) {
-    SeqElem& e = S.e[S.nelem++];
-    e.slot = (short)slot;
-    e.box = (char)box;
-    e.src = (char)src;
-    e.coef = (char)coef;
-    S.gsize[S.ngroups - 1]++;
-  };
-  auto group = [&]() { S.gsize[S.ngroups++] = 0; };
-  group();  // G0: E^1 Exy Exz Eyx Eyz
-  for (int c : {EXY, EXZ, EYX, EYZ}) add(c, BOX_A, 2, 0);
-  group();  // G1: E^1 Ezx Ezy, H^1 Hzx Hzy
-  for (int c : {EZX, EZY, HZX, HZY}) add(c, BOX_A, 2, 0);
-  group();  // G2: H^1 Hxy Hxz Hyx Hyz
-  for (int c : {HXY, HXZ, HYX, HYZ}) add(c, BOX_A, 2, 0);
-  group();  // G3: Hxy t c, Hyx t c
-  add(cslot(12 + HXY), BOX_BY, 0, 1);
-  add(cslot(24 + HXY), BOX_BY, 0, 1);
-  add(cslot(12 + HYX), BOX_BX, 0, 1);
-  add(cslot(24 + HYX), BOX_BX, 0, 1);
-  group();  // G4: Hxz t c src
-  add(cslot(12 + HXZ), BOX_BY, 0, 1);
-  add(cslot(24 + HXZ), BOX_BY, 0, 1);
-  add(cslot(36 + SRC_HXZ), BOX_BY, 0, 1);
-  group();  // G5: Hyz t c src
-  add(cslot(12 + HYZ), BOX_BX, 0, 1);
-  add(cslot(24 + HYZ), BOX_BX, 0, 1);
-  add(cslot(36 + SRC_HYZ), BOX_BX, 0, 1);
-  group();  // G6: Hzx t c, Hzy t c
-  for (int c : {HZX, HZY}) {
-    add(cslot(12 + c), BOX_B, 0, 1);
-    add(cslot(24 + c), BOX_B, 0, 1);
-  }
-  group();  // G7: Exy t c, Eyx t c
-  for (int c : {EXY, EYX}) {
-    add(cslot(12 + c), BOX_C, 0, 1);
-    add(cslot(24 + c), BOX_C, 0, 1);
-  }
-  group();  // G8: Exz t c src
-  add(cslot(12 + EXZ), BOX_C, 0, 1);
-  add(cslot(24 + EXZ), BOX_C, 0, 1);
-  add(cslot(36 + SRC_EXZ), BOX_C, 0, 1);
-  group();  // G9: Eyz t c src
-  add(cslot(12 + EYZ), BOX_C, 0, 1);
-  add(cslot(24 + EYZ), BOX_C, 0, 1);
-  add(cslot(36 + SRC_EYZ), BOX_C, 0, 1);
-  group();  // G10: Ezx t c, Ezy t c
-  for (int c : {EZX, EZY}) {
-    add(cslot(12 + c), BOX_C, 0, 1);
-    add(cslot(24 + c), BOX_C, 0, 1);
-  }
-}
-
-struct TbParams {
-  int zc;          // level-2 planes per CTA chunk
-  int tiles_x;     // x-tiles (fastest CTA index)
-  int field_in[12];  // allocation slot of each input field (ghost-plane reads)
-  double2* scratch;  // [nsm][RING][12][BY*32]
-};
-
-template <int BY, int NG>
-struct TbSmem {
-  Ring<BY, NG> ring;
-  double2 sE[3][BY][32];  // E sums of the level being swept
-  double2 sH[3][BY][32];  // H sums of the level being swept
-  uint64_t ready[2];      // scratch ring slot written by level 1
-};
-
-__device__ __forceinline__ uint32_t smid_u32() {
-  uint32_t id;
-  asm volatile("mov.u32 %0, %%smid;" : "=r"(id));
-  return id;
-}
-
-template <int BY, int NG>
-__global__ void __launch_bounds__(32 * (BY + 1), 1)
-    k_tblock2(Grid g, Arrays A, const __grid_constant__ TmaMaps maps,
-              const __grid_constant__ CUtensorMap smap, const __grid_constant__ GroupSeq S1,
-              const __grid_constant__ GroupSeq S2, TbParams P) {
-  constexpr int NCOMP = 32 * BY;
-  constexpr int TX2 = 28, TY2 = BY - 4;  // level-2 (output) tile
-  constexpr int TILE = BY * 32;
-  constexpr int LAG = 1, RING = 2;
-  extern __shared__ __align__(1024) unsigned char smem_raw[];
-  TbSmem<BY, NG>& sm = *reinterpret_cast<TbSmem<BY, NG>*>(smem_raw);
-  const int tx = threadIdx.x, ty = threadIdx.y;
-  const int btx = blockIdx.x % P.tiles_x, bty = blockIdx.x / P.tiles_x;
-  const int xb = btx * TX2 - 2, yb = bty * TY2 - 2;  // interior coords of thread (0,0)
-  const int z0 = blockIdx.z * P.zc;
-  const int z1 = min(g.nz, z0 + P.zc);
-  const long long pxy = g.pxy;
-  const int qs = max(z0 - 1, 0);      // first level-1 plane
-  const int q1 = min(z1, g.nz - 1);   // last level-1 plane
-  const int qe = z1 + LAG - 1;        // last iteration
-  // one CTA per SM (shared memory), so the SM id owns a private scratch ring
-  const uint32_t sid = smid_u32();
-  double2* scr = P.scratch + (size_t)sid * (RING * 12 * TILE);
-
-  if (tx == 0 && ty == 0) {
-    ring_init(sm.ring, BY);
-    for (int k = 0; k < RING; ++k) mbar_init(&sm.ready[k], BY);
-    fence_mbar_init();
-  }
-  __syncthreads();
-
-  if (ty == BY) {
-    // ------------------------------------------------------------ producer
-    if (tx == 0) {
-#pragma unroll
-      for (int b = 0; b < NBOX; ++b) tma_prefetch_desc(&maps.m[b]);
-      tma_prefetch_desc(&smap);
-      using Gm = BoxGeom<BY>;
-      const uint64_t keep = policy_evict_last(), drop = policy_evict_first();
-      auto& R = sm.ring;
-      int gi = 0;
-      uint32_t ph = 0;
-      // level: 1 or 2; plane: that level's plane
-      auto produce = [&](const GroupSeq& S, int level, int plane) {
-        int e = 0;
-        for (int gr = 0; gr < S.ngroups; ++gr) {
-          const int n = S.gsize[gr];
-          int bytes = 0;
-          for (int k = 0; k < n; ++k) bytes += Gm::bytes(S.e[e + k].box);
-          mbar_wait(&R.empty[gi], ph ^ 1);
-          mbar_arrive_expect_tx(&R.full[gi], (uint32_t)bytes);
-          for (int k = 0; k < n; ++k, ++e) {
-            const SeqElem el = S.e[e];
-            const int b = el.box;
-            void* dst = &R.buf[gi][k][0];
-            if (el.src == 2) {
-              if (plane >= 0 && plane < g.nz) {  // level-1 output in scratch
-                const int sidx = (int)(sid * (RING * 12) + ((plane - qs) % RING) * 12 + el.slot);
-                tma_load_3d_hint(dst, &smap, 0, 0, sidx, &R.full[gi], drop);
-              } else {  // ghost plane: never updated, read the input set
-                tma_load_4d_hint(dst, &maps.m[BOX_A], 2 * (xb + 1), yb + 1, plane + 1,
-                                 P.field_in[el.slot], &R.full[gi], drop);
-              }
-            } else {
-              // level 1 keeps coefficients in L2 for level 2 (its last use)
-              const uint64_t pol = (level == 1 && el.coef) ? keep : drop;
-              tma_load_4d_hint(dst, &maps.m[b], 2 * (xb + 1 + Gm::x0(b)), yb + 1 + Gm::y0(b),
-                               plane + 1 + el.src, el.slot, &R.full[gi], pol);
-            }
-          }
-          if (++gi == NG) {
-            gi = 0;
-            ph ^= 1;
-          }
-        }
-      };
-      for (int q = qs; q <= qe; ++q) {
-        if (q <= q1) produce(S1, 1, q);
-        const int r = q - LAG;
-        if (r >= z0 - 1 && r < z1) {
-          if (r >= 0 && r < g.nz) mbar_wait(&sm.ready[(r - qs) % RING], ((r - qs) / RING) & 1);
-          produce(S2, 2, r);
-        }
-      }
-    }
-    return;
-  }
-
-  // -------------------------------------------------------------- consumers
-  const int x = xb + tx, y = yb + ty;
-  const bool inpad = (x >= -1) && (x <= g.nx) && (y >= -1) && (y <= g.ny);
-  const bool interior = (x >= 0) && (x < g.nx) && (y >= 0) && (y < g.ny);
-  const int xs = inpad ? x : 0, ys = inpad ? y : 0;
-  // level-1 geometry (the tile grown by one ring)
-  const bool own1 = tx >= 1 && tx <= 30 && ty >= 1 && ty <= BY - 2;
-  const bool rx1 = (tx == 0) && (ty >= 1) && (ty <= BY - 2);
-  const bool ry1 = (ty == 0) && (tx >= 1) && (tx <= 30);
-  // level-2 geometry
-  const bool own2 = tx >= 2 && tx <= 29 && ty >= 2 && ty <= BY - 3;
-  const bool rx2 = (tx == 1) && (ty >= 2) && (ty <= BY - 3);
-  const bool ry2 = (ty == 1) && (tx >= 2) && (tx <= 29);
-  const bool upd1_x = (own1 || ry1) && interior;
-  const bool upd1_y = (own1 || rx1) && interior;
-  const bool upd1_z = (own1 || rx1 || ry1) && interior;
-  const bool upd2_x = (own2 || ry2) && interior;
-  const bool upd2_y = (own2 || rx2) && interior;
-  const bool upd2_z = (own2 || rx2 || ry2) && interior;
-
-  auto& R = sm.ring;
-  RingCursor rc = ring_cursor(R);
-#define RD(k, b) ring_read(R, rc, k, b, tx, ty)
-
-  // ---- level-1 prologue: E^0 splits at qs (carried), H^1 sums at qs-1
-  double2 e[6];
-  {
-    const long long i1 = g.idx(xs, ys, qs);
-#pragma unroll
-    for (int k = 0; k < 6; ++k) e[k] = inpad ? __ldg(A.f[k] + i1) : make_double2(0.0, 0.0);
-  }
-  double2 pH1x = make_double2(0.0, 0.0), pH1y = make_double2(0.0, 0.0);
-  {
-    const long long im = g.idx(xs, ys, qs) - pxy;
-    if (qs == 0 && !g.halo_lo) {
-      if (own1 && inpad) {  // ghost plane below the grid: H never updated
-        pH1x = csum(__ldg(A.f[HXY] + im), __ldg(A.f[HXZ] + im));
-        pH1y = csum(__ldg(A.f[HYX] + im), __ldg(A.f[HYZ] + im));
-      }
-    } else {
-      if (inpad) {
-        double2 m[6];
-#pragma unroll
-        for (int k = 0; k < 6; ++k) m[k] = __ldg(A.f[k] + im);
-        sm.sE[0][ty][tx] = csum(m[EXY], m[EXZ]);
-        sm.sE[1][ty][tx] = csum(m[EYX], m[EYZ]);
-        sm.sE[2][ty][tx] = csum(m[EZX], m[EZY]);
-      }
-      named_sync(1, NCOMP);
-      if (own1 && inpad) {
-        if (interior) {
-          const double2 sEx = sm.sE[0][ty][tx], sEy = sm.sE[1][ty][tx], sEz = sm.sE[2][ty][tx];
-          const double2 nEx = csum(e[EXY], e[EXZ]), nEy = csum(e[EYX], e[EYZ]);
-          const double2 hxy = upd(__ldg(A.f[HXY] + im), __ldg(A.t[HXY] + im),
-                                  __ldg(A.c[HXY] + im), sm.sE[2][ty + 1][tx], sEz);
-          const double2 hxz = upd_src(__ldg(A.f[HXZ] + im), __ldg(A.t[HXZ] + im),
-                                      __ldg(A.c[HXZ] + im), nEy, sEy, __ldg(A.src[SRC_HXZ] + im));
-          const double2 hyx = upd(__ldg(A.f[HYX] + im), __ldg(A.t[HYX] + im),
-                                  __ldg(A.c[HYX] + im), sm.sE[2][ty][tx + 1], sEz);
-          const double2 hyz = upd_src(__ldg(A.f[HYZ] + im), __ldg(A.t[HYZ] + im),
-                                      __ldg(A.c[HYZ] + im), nEx, sEx, __ldg(A.src[SRC_HYZ] + im));
-          pH1x = csum(hxy, hxz);
-          pH1y = csum(hyx, hyz);
-        } else {  // ghost column/row: H never updated
-          pH1x = csum(__ldg(A.f[HXY] + im), __ldg(A.f[HXZ] + im));
-          pH1y = csum(__ldg(A.f[HYX] + im), __ldg(A.f[HYZ] + im));
-        }
-      }
-      named_sync(1, NCOMP);
-    }
-  }
-  double2 pH2x = make_double2(0.0, 0.0), pH2y = make_double2(0.0, 0.0);
-  double2 nE2x = make_double2(0.0, 0.0), nE2y = make_double2(0.0, 0.0);
-  const uint64_t keep = policy_evict_last(), first = policy_evict_first();
-
-  for (int q = qs; q <= qe; ++q) {
-    // ================= level 1 at plane q (step n) -> scratch
-    if (q <= q1) {
-      double2 en[6];
-      ring_wait(R, rc);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) en[k] = RD(k, BOX_A);
-      ring_release(R, rc, tx, ring_dep(en[0], en[1], en[2], en[3]));
-      ring_wait(R, rc);
-      en[4] = RD(0, BOX_A);
-      en[5] = RD(1, BOX_A);
-      ring_release(R, rc, tx, ring_dep(en[4], en[5]));
-      // own sums from registers; neighbours read them from shared memory
-      const double2 sEx = csum(e[EXY], e[EXZ]), sEy = csum(e[EYX], e[EYZ]),
-                    sEz = csum(e[EZX], e[EZY]);
-      if (inpad) {
-        sm.sE[0][ty][tx] = sEx;
-        sm.sE[1][ty][tx] = sEy;
-        sm.sE[2][ty][tx] = sEz;
-      }
-      named_sync(1, NCOMP);
-      const double2 nEx = csum(en[EXY], en[EXZ]), nEy = csum(en[EYX], en[EYZ]);
-      double2 h[6];
-      {
-        ring_wait(R, rc);
-        h[0] = RD(0, BOX_BY);
-        const double2 t = RD(1, BOX_BY), c = RD(2, BOX_BY);
-        ring_release(R, rc, tx, ring_dep(h[0], c, t));
-        if (upd1_x) h[0] = upd(h[0], t, c, sm.sE[2][ty + 1][tx], sEz);
-      }
-      {
-        ring_wait(R, rc);
-        h[1] = RD(0, BOX_BY);
-        const double2 t = RD(1, BOX_BY), c = RD(2, BOX_BY), s = RD(3, BOX_BY);
-        ring_release(R, rc, tx, ring_dep(h[1], s, c, t));
-        if (upd1_x) h[1] = upd_src(h[1], t, c, nEy, sEy, s);
-      }
-      {
-        ring_wait(R, rc);
-        h[2] = RD(0, BOX_BX);
-        const double2 t = RD(1, BOX_BX), c = RD(2, BOX_BX);
-        ring_release(R, rc, tx, ring_dep(h[2], c, t));
-        if (upd1_y) h[2] = upd(h[2], t, c, sm.sE[2][ty][tx + 1], sEz);
-      }
-      {
-        ring_wait(R, rc);
-        h[3] = RD(0, BOX_BX);
-        const double2 t = RD(1, BOX_BX), c = RD(2, BOX_BX), s = RD(3, BOX_BX);
-        ring_release(R, rc, tx, ring_dep(h[3], s, c, t));
-        if (upd1_y) h[3] = upd_src(h[3], t, c, nEx, sEx, s);
-      }
-      {
-        ring_wait(R, rc);
-        h[4] = RD(0, BOX_B);
-        const double2 t = RD(1, BOX_B), c = RD(2, BOX_B);
-        ring_release(R, rc, tx, ring_dep(h[4], c, t));
-        if (upd1_z) h[4] = upd(h[4], t, c, sm.sE[1][ty][tx + 1], sEy);
-      }
-      {
-        ring_wait(R, rc);
-        h[5] = RD(0, BOX_B);
-        const double2 t = RD(1, BOX_B), c = RD(2, BOX_B);
-        ring_release(R, rc, tx, ring_dep(h[5], c, t));
-        if (upd1_z) h[5] = upd(h[5], t, c, sm.sE[0][ty + 1][tx], sEx);
-      }
-      const double2 sHx = csum(h[0], h[1]), sHy = csum(h[2], h[3]), sHz = csum(h[4], h[5]);
-      if (own1 || rx1 || ry1) {
-        sm.sH[0][ty][tx] = sHx;
-        sm.sH[1][ty][tx] = sHy;
-        sm.sH[2][ty][tx] = sHz;
-      }
-      named_sync(1, NCOMP);
-      double2 eo[6];
-      const bool ue = own1 && interior;
-      {
-        ring_wait(R, rc);
-        const double2 t0 = RD(0, BOX_C), c0 = RD(1, BOX_C), t1 = RD(2, BOX_C), c1 = RD(3, BOX_C);
-        ring_release(R, rc, tx, ring_dep(c1, t1, c0, t0));
-        eo[EXY] = ue ? upd(e[EXY], t0, c0, sm.sH[2][ty - 1][tx], sHz) : e[EXY];
-        eo[EYX] = ue ? upd(e[EYX], t1, c1, sm.sH[2][ty][tx - 1], sHz) : e[EYX];
-      }
-      {
-        ring_wait(R, rc);
-        const double2 t = RD(0, BOX_C), c = RD(1, BOX_C), s = RD(2, BOX_C);
-        ring_release(R, rc, tx, ring_dep(s, c, t));
-        eo[EXZ] = ue ? upd_src(e[EXZ], t, c, pH1y, sHy, s) : e[EXZ];
-      }
-      {
-        ring_wait(R, rc);
-        const double2 t = RD(0, BOX_C), c = RD(1, BOX_C), s = RD(2, BOX_C);
-        ring_release(R, rc, tx, ring_dep(s, c, t));
-        eo[EYZ] = ue ? upd_src(e[EYZ], t, c, pH1x, sHx, s) : e[EYZ];
-      }
-      {
-        ring_wait(R, rc);
-        const double2 t0 = RD(0, BOX_C), c0 = RD(1, BOX_C), t1 = RD(2, BOX_C), c1 = RD(3, BOX_C);
-        ring_release(R, rc, tx, ring_dep(c1, t1, c0, t0));
-        eo[EZX] = ue ? upd(e[EZX], t0, c0, sm.sH[1][ty][tx - 1], sHy) : e[EZX];
-        eo[EZY] = ue ? upd(e[EZY], t1, c1, sm.sH[0][ty - 1][tx], sHx) : e[EZY];
-      }
-      // scratch: level-1 E/H of the grown tile (ghost cells pass through)
-      double2* sp = scr + (size_t)(((q - qs) % RING) * 12) * TILE + ty * 32 + tx;
-      if (own1) {
-#pragma unroll
-        for (int k = 0; k < 6; ++k) st_hint(sp + (size_t)k * TILE, eo[k], keep);
-#pragma unroll
-        for (int k = 0; k < 6; ++k) st_hint(sp + (size_t)(6 + k) * TILE, h[k], keep);
-      }
-      asm volatile("fence.proxy.async.global;" ::: "memory");
-      __syncwarp();
-      if (tx == 0) mbar_arrive(&sm.ready[(q - qs) % RING]);
-      nE2x = csum(eo[EXY], eo[EXZ]);
-      nE2y = csum(eo[EYX], eo[EYZ]);
-      pH1x = sHx;
-      pH1y = sHy;
-#pragma unroll
-      for (int k = 0; k < 6; ++k) e[k] = en[k];
-    }
-
-    // ================= level 2 at plane r = q-1 (step n+1) -> output set
-    const int r = q - LAG;
-    if (r >= z0 - 1 && r < z1) {
-      const long long i = g.idx(xs, ys, r);
-      const bool plane_ok = r >= 0;  // plane -1 is the ghost plane: never updated
-      double2 nEx = nE2x, nEy = nE2y;
-      if (q > q1) {  // plane r+1 is the top ghost plane: level 1 did not run
-        nEx = csum(e[EXY], e[EXZ]);
-        nEy = csum(e[EYX], e[EYZ]);
-      }
-      double2 e1[6], h[6];
-      ring_wait(R, rc);
-      e1[EXY] = RD(0, BOX_A);
-      e1[EXZ] = RD(1, BOX_A);
-      e1[EYX] = RD(2, BOX_A);
-      e1[EYZ] = RD(3, BOX_A);
-      ring_release(R, rc, tx, ring_dep(e1[EXY], e1[EXZ], e1[EYX], e1[EYZ]));
-      ring_wait(R, rc);
-      e1[EZX] = RD(0, BOX_A);
-      e1[EZY] = RD(1, BOX_A);
-      h[4] = RD(2, BOX_A);
-      h[5] = RD(3, BOX_A);
-      ring_release(R, rc, tx, ring_dep(e1[EZX], e1[EZY], h[4], h[5]));
-      ring_wait(R, rc);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) h[k] = RD(k, BOX_A);
-      ring_release(R, rc, tx, ring_dep(h[0], h[1], h[2], h[3]));
-      // own sums from registers; neighbours read them from shared memory
-      const double2 sEx = csum(e1[EXY], e1[EXZ]), sEy = csum(e1[EYX], e1[EYZ]),
-                    sEz = csum(e1[EZX], e1[EZY]);
-      if (inpad) {
-        sm.sE[0][ty][tx] = sEx;
-        sm.sE[1][ty][tx] = sEy;
-        sm.sE[2][ty][tx] = sEz;
-      }
-      named_sync(1, NCOMP);
-      const bool u2x = upd2_x && plane_ok, u2y = upd2_y && plane_ok, u2z = upd2_z && plane_ok;
-      {  // Hxy, Hyx
-        ring_wait(R, rc);
-        const double2 t0 = RD(0, BOX_BY), c0 = RD(1, BOX_BY), t1 = RD(2, BOX_BX), c1 = RD(3, BOX_BX);
-        ring_release(R, rc, tx, ring_dep(c1, t1, c0, t0));
-        if (u2x) h[0] = upd(h[0], t0, c0, sm.sE[2][ty + 1][tx], sEz);
-        if (u2y) h[2] = upd(h[2], t1, c1, sm.sE[2][ty][tx + 1], sEz);
-      }
-      {  // Hxz
-        ring_wait(R, rc);
-        const double2 t = RD(0, BOX_BY), c = RD(1, BOX_BY), s = RD(2, BOX_BY);
-        ring_release(R, rc, tx, ring_dep(s, c, t));
-        if (u2x) h[1] = upd_src(h[1], t, c, nEy, sEy, s);
-      }
-      {  // Hyz
-        ring_wait(R, rc);
-        const double2 t = RD(0, BOX_BX), c = RD(1, BOX_BX), s = RD(2, BOX_BX);
-        ring_release(R, rc, tx, ring_dep(s, c, t));
-        if (u2y) h[3] = upd_src(h[3], t, c, nEx, sEx, s);
-      }
-      {  // Hzx, Hzy
-        ring_wait(R, rc);
-        const double2 t0 = RD(0, BOX_B), c0 = RD(1, BOX_B), t1 = RD(2, BOX_B), c1 = RD(3, BOX_B);
-        ring_release(R, rc, tx, ring_dep(c1, t1, c0, t0));
-        if (u2z) h[4] = upd(h[4], t0, c0, sm.sE[1][ty][tx + 1], sEy);
-        if (u2z) h[5] = upd(h[5], t1, c1, sm.sE[0][ty + 1][tx], sEx);
-      }
-      if (r == z0 - 1) {
-        // chunk prologue: only the H_new sums of the plane below the chunk
-        if (own2) {
-          pH2x = csum(h[0], h[1]);
-          pH2y = csum(h[2], h[3]);
-        }
-        for (int k = 0; k < 4; ++k) {  // E-coefficient groups, unused here
-          ring_wait(R, rc);
-          ring_release(R, rc, tx, ring_dep());
-        }
-        named_sync(1, NCOMP);  // sE reads done before the next level-1 writes
-        continue;
-      }
-      if (own2 && interior) {
-#pragma unroll
-        for (int k = 0; k < 6; ++k) st_hint(A.fo[HXY + k] + i, h[k], first);
-      }
-      const double2 sHx = csum(h[0], h[1]), sHy = csum(h[2], h[3]), sHz = csum(h[4], h[5]);
-      if (own2 || rx2 || ry2) {
-        sm.sH[0][ty][tx] = sHx;
-        sm.sH[1][ty][tx] = sHy;
-        sm.sH[2][ty][tx] = sHz;
-      }
-      named_sync(1, NCOMP);
-      const bool ue = own2 && interior;
-      {  // Exy, Eyx
-        ring_wait(R, rc);
-        const double2 t0 = RD(0, BOX_C), c0 = RD(1, BOX_C), t1 = RD(2, BOX_C), c1 = RD(3, BOX_C);
-        ring_release(R, rc, tx, ring_dep(c1, t1, c0, t0));
-        if (ue) {
-          st_hint(A.fo[EXY] + i, upd(e1[EXY], t0, c0, sm.sH[2][ty - 1][tx], sHz), first);
-          st_hint(A.fo[EYX] + i, upd(e1[EYX], t1, c1, sm.sH[2][ty][tx - 1], sHz), first);
-        }
-      }
-      {  // Exz
-        ring_wait(R, rc);
-        const double2 t = RD(0, BOX_C), c = RD(1, BOX_C), s = RD(2, BOX_C);
-        ring_release(R, rc, tx, ring_dep(s, c, t));
-        if (ue) st_hint(A.fo[EXZ] + i, upd_src(e1[EXZ], t, c, pH2y, sHy, s), first);
-      }
-      {  // Eyz
-        ring_wait(R, rc);
-        const double2 t = RD(0, BOX_C), c = RD(1, BOX_C), s = RD(2, BOX_C);
-        ring_release(R, rc, tx, ring_dep(s, c, t));
-        if (ue) st_hint(A.fo[EYZ] + i, upd_src(e1[EYZ], t, c, pH2x, sHx, s), first);
-      }
-      {  // Ezx, Ezy
-        ring_wait(R, rc);
-        const double2 t0 = RD(0, BOX_C), c0 = RD(1, BOX_C), t1 = RD(2, BOX_C), c1 = RD(3, BOX_C);
-        ring_release(R, rc, tx, ring_dep(c1, t1, c0, t0));
-        if (ue) {
-          st_hint(A.fo[EZX] + i, upd(e1[EZX], t0, c0, sm.sH[1][ty][tx - 1], sHy), first);
-          st_hint(A.fo[EZY] + i, upd(e1[EZY], t1, c1, sm.sH[0][ty - 1][tx], sHx), first);
-        }
-      }
-      pH2x = sHx;
-      pH2y = sHy;
-    }
-  }
-#undef RD
-}
 
 // ---------------------------------------------------------------------------
 // k_tblock_tm: the same two-level wavefront with the level-1 -> level-2
@@ -541,30 +48,9 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
 //   [0,48)   slot 0: E^1 (24 cols), H^1 (24 cols)   -- planes with r even
 //   [48,96)  slot 1: same                            -- r odd
 //   [96,120) E_old splits of the next level-1 plane
-template <class CS>
-inline void seq_level2_coef(GroupSeq& S, CS cslot) {
-  GroupSeq full;
-  seq_level2(full, cslot);
-  S.ngroups = 0;
-  S.nelem = 0;
-  int e = 0;
-  for (int gr = 0; gr < full.ngroups; ++gr) {
-    const int n = full.gsize[gr];
-    if (full.e[e].src != 2) {  // drop the three scratch groups
-      S.gsize[S.ngroups++] = (unsigned char)n;
-      for (int k = 0; k < n; ++k) S.e[S.nelem++] = full.e[e + k];
-    }
-    e += n;
-  }
-}
-
 template <int BY, int NG>
 struct TmSmem {
-#if THIIM_PATTERN_ONLY
-  static constexpr int SROWS = 1;  // pattern builds exchange nothing (room for a deeper ring)
-#else
   static constexpr int SROWS = BY;
-#endif
   Ring<BY, NG> ring;
   double2 sE[3][SROWS][32];
   double2 sH[3][SROWS][32];
@@ -580,7 +66,7 @@ struct TmSmem {
 template <int BY, int NG, bool COUNT, int W, bool DEEP>
 __device__ __forceinline__ void tblock_tm_body(TmSmem<BY, NG>& sm, const Grid& g, const Arrays& A,
                                                const TmaMaps& maps, const PeerOut& po, int fb, int cb,
-                                               int zc, int xb, int yb0, int pol_mode) {
+                                               int zc, int chunk, int xb, int yb0) {
   constexpr int NCOMP = 32 * BY;
   constexpr int TY2 = BY - 4;
   constexpr int LAG = 1;
@@ -588,7 +74,7 @@ __device__ __forceinline__ void tblock_tm_body(TmSmem<BY, NG>& sm, const Grid& g
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int lx = W == 32 ? tx : tx % W, seg = W == 32 ? 0 : tx / W;
   const int yb = yb0 + seg * TY2;
-  const int z0 = blockIdx.z * zc;
+  const int z0 = chunk * zc;
   const int z1 = min(g.nz, z0 + zc);
   const long long pxy = g.pxy;
   const int qs = max(z0 - 1, 0);
@@ -596,119 +82,36 @@ __device__ __forceinline__ void tblock_tm_body(TmSmem<BY, NG>& sm, const Grid& g
   const int qe = z1 + LAG - 1;
 
   if (ty == 0) tm_alloc<512>(&sm.tmem_base);
-#if THIIM_PATTERN_ONLY == 3
-  // experiment: level-1 (DRAM) groups and level-2 coefficient (L2) groups in
-  // two rings of 4 + 2 slots, each with its own producer lane
-  using RingA = Ring<BY, 4>;
-  using RingB = Ring<BY, NG - 4>;
-  RingA& RA = *reinterpret_cast<RingA*>(&sm.ring);
-  RingB& RB = *reinterpret_cast<RingB*>(reinterpret_cast<char*>(&sm.ring) + sizeof(RingA));
-  if (tx == 0 && ty == 0) {
-    ring_init(RA, BY);
-    ring_init(RB, BY);
-    fence_mbar_init();
-  }
-#else
   if (tx == 0 && ty == 0) {
     ring_init(sm.ring, BY);
     fence_mbar_init();
   }
-#endif
   tm_fence_before();
   __syncthreads();
   tm_fence_after();
 
-#if THIIM_PATTERN_ONLY == 3
-  if (ty == BY) {
-    const uint64_t keep = policy_evict_last(), drop = policy_evict_first();
-    if (tx == 0) {
-      RingProducer<BY, 4, W> PA(RA, maps, xb, yb0);
-      for (int q = qs; q <= q1; ++q) produce_plane_ct<true>(PA, fb, cb, q, drop, keep);
-    } else if (tx == 1) {
-      RingProducer<BY, NG - 4, W> PB(RB, maps, xb, yb0);
-      for (int q = qs; q <= qe; ++q) {
-        const int r = q - LAG;
-        if (r >= z0 - 1 && r < z1) produce_level2_coef_ct(PB, cb, r, drop);
-      }
-    }
-    return;
-  }
-#endif
   if (ty == BY) {
     // ------------------------------------------------------------ producer
     if (tx == 0) {
 #pragma unroll
       for (int b = 0; b < NBOX; ++b) tma_prefetch_desc(&maps.m[b]);
-      const uint64_t keep = policy_evict_last(), drop = policy_evict_first(),
-                     norm = policy_evict_normal();
-      // experiment knob: L2 policies (level-1 fields, level-1 coefs, level-2 coefs)
-      const uint64_t pf1 = pol_mode == 3 ? norm : drop;
-      const uint64_t pc1 = pol_mode == 2 ? norm : keep;
-      const uint64_t pc2 = pol_mode == 1 || pol_mode == 2 ? norm : pol_mode == 4 ? keep : drop;
+      // L2 policies: level-1 fields evict_first (read once), level-1
+      // coefficients evict_last (level 2 re-reads them one plane later, their
+      // last use: evict_first) -- the best of the measured policy sets
+      const uint64_t pf1 = policy_evict_first(), pc1 = policy_evict_last(), pc2 = pf1;
       RingProducer<BY, NG, W> P(sm.ring, maps, xb, yb0);
       for (int q = qs; q <= qe; ++q) {
         // level 1 keeps coefficients in L2 for level 2 (their last use)
         if (q <= q1) produce_plane_ct<true>(P, fb, cb, q, pf1, pc1);
         const int r = q - LAG;
         if (r >= z0 - 1 && r < z1) {
-#if THIIM_PATTERN_ONLY == 2  // experiment: level 2 re-reads no coefficients
-          for (int k = 0; k < 8; ++k) {
-            P.template begin<0>();
-            P.end();
-          }
-#else
           produce_level2_coef_ct(P, cb, r, pc2);
-#endif
         }
       }
     }
     return;
   }
 
-#if THIIM_PATTERN_ONLY
-  // Experiment builds only (tools/build_variant.sh NAME -DTHIIM_PATTERN_ONLY=1):
-  // the same producer stream, ring protocol and output stores with no compute,
-  // i.e. the memory-system ceiling of this access pattern.  Results are garbage.
-  {
-    const int x = xb + lx, y = yb + ty;
-    const bool own2 = lx >= 2 && lx <= W - 3 && ty >= 2 && ty <= BY - 3;
-    const bool interior = (x >= 0) && (x < g.nx) && (y >= 0) && (y < g.ny);
-#if THIIM_PATTERN_ONLY == 3
-    auto& R = RA;
-    auto& R2 = RB;
-    RingCursor rc = ring_cursor(R), rc2 = ring_cursor(R2);
-#else
-    auto& R = sm.ring;
-    auto& R2 = sm.ring;
-    RingCursor rc = ring_cursor(R);
-    RingCursor& rc2 = rc;
-#endif
-    const uint64_t first = policy_evict_first();
-    for (int q = qs; q <= qe; ++q) {
-      if (q <= q1)
-        for (int k = 0; k < 12; ++k) {
-          ring_wait(R, rc);
-          ring_release(R, rc, tx, 0u);
-        }
-      const int r = q - LAG;
-      if (r >= z0 - 1 && r < z1) {
-        for (int k = 0; k < 8; ++k) {
-          ring_wait(R2, rc2);
-          ring_release(R2, rc2, tx, 0u);
-        }
-        if (r >= z0 && own2 && interior && r >= po.st0 && r < po.st1) {
-          const long long i = g.idx(x, y, r);
-          for (int k = 0; k < 12; ++k) st_hint(A.fo[k] + i, make_double2(0.0, 0.0), first);
-        }
-      }
-    }
-    tm_fence_before();
-    named_sync(1, NCOMP);
-    tm_fence_after();
-    if (ty == 0) tm_dealloc<512>(sm.tmem_base);
-    return;
-  }
-#endif
   // -------------------------------------------------------------- consumers
   const uint32_t tcar = tm_warp_addr(sm.tmem_base, ty, 128 * (ty >> 2));
   const uint32_t tnext = tcar + 96;
@@ -1054,21 +457,57 @@ __device__ __forceinline__ void tblock_tm_body(TmSmem<BY, NG>& sm, const Grid& g
 }
 
 
+// Which (tile, z-chunk) a CTA sweeps.  Items are numbered chunk-major; within
+// a chunk the n_main full tiles come in vertical BANDS of `band` tile columns
+// (row by row inside a band), then the folded remainder CTAs.  A launch covers
+// items [item0, item0 + gridDim.x).  The host launches a pass as ROUNDS of at
+// most one CTA per SM, so every CTA of a round starts at once and a round's
+// tiles form a compact band x rows block whose y- and x-neighbours stream the
+// same z-planes at the same time: their overlapping box rows are fetched from
+// DRAM once and hit in L2 for the neighbour.  (One launch of all items lets
+// the hardware start CTAs as SMs free up: y-neighbours then run tiles_x/148 of
+// a CTA lifetime apart -- tens of planes -- and re-fetch every overlap row.)
+// band = tiles_x with one launch is the plain x-fastest order.
+struct TileOrder {
+  int item0;    // first item of this launch
+  int nbt;      // items per z-chunk (n_main + folded CTAs)
+  int band;     // tile columns per band (1..tiles_x)
+  int tiles_y;  // tile rows
+};
+
+__device__ __forceinline__ int band_tile(int t, int tiles_x, const TileOrder& o) {
+  const int full = tiles_x / o.band, per = o.band * o.tiles_y;
+  int row, col;
+  if (t < full * per) {
+    const int bi = t / per, r = t - bi * per;
+    row = r / o.band;
+    col = bi * o.band + (r - row * o.band);
+  } else {
+    const int w = tiles_x - full * o.band, r = t - full * per;
+    row = r / w;
+    col = full * o.band + (r - row * w);
+  }
+  return row * tiles_x + col;
+}
+
 template <int BY, int NG, bool COUNT = false, int WF = 0, bool DEEP = false>
 __global__ void __launch_bounds__(32 * (BY + 1), 1)
     k_tblock_tm(Grid g, Arrays A, const __grid_constant__ TmaMaps maps,
                 const __grid_constant__ TmaMaps maps_f, const __grid_constant__ PeerOut po, int fb,
-                int cb, int zc, int tiles_x, int n_main, int pol_mode) {
+                int cb, int zc, int tiles_x, int n_main, TileOrder ord) {
   constexpr int TX2 = 28, TY2 = BY - 4;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   TmSmem<BY, NG>& sm = *reinterpret_cast<TmSmem<BY, NG>*>(smem_raw);
-  const int b = blockIdx.x;
-  if (b < n_main) {  // full tiles, x-fastest
-    tblock_tm_body<BY, NG, COUNT, 32, DEEP>(sm, g, A, maps, po, fb, cb, zc, (b % tiles_x) * TX2 - 2,
-                                      (b / tiles_x) * TY2 - 2, pol_mode);
+  const int it = ord.item0 + (int)blockIdx.x;
+  const int chunk = it / ord.nbt;
+  const int t = it - chunk * ord.nbt;
+  if (t < n_main) {  // full tiles
+    const int b = band_tile(t, tiles_x, ord);
+    tblock_tm_body<BY, NG, COUNT, 32, DEEP>(sm, g, A, maps, po, fb, cb, zc, chunk,
+                                            (b % tiles_x) * TX2 - 2, (b / tiles_x) * TY2 - 2);
   } else if constexpr (WF > 0) {  // folded remainder column: 32/WF y-tiles per CTA
-    tblock_tm_body<BY, NG, COUNT, WF, DEEP>(sm, g, A, maps_f, po, fb, cb, zc, tiles_x * TX2 - 2,
-                                      (b - n_main) * (32 / WF) * TY2 - 2, pol_mode);
+    tblock_tm_body<BY, NG, COUNT, WF, DEEP>(sm, g, A, maps_f, po, fb, cb, zc, chunk,
+                                            tiles_x * TX2 - 2, (t - n_main) * (32 / WF) * TY2 - 2);
   }
 }
 

@@ -45,6 +45,12 @@ def test_library_is_sm100a_cubin():
     assert "sm_100a" in out
     sass = subprocess.run(["cuobjdump", "-sass", P.LIB_PATH], capture_output=True, text=True).stdout
     assert "UTMALDG" in sass, "TMA tensor loads expected in the fused sweep"
+    # the TBLOCK level-1 -> level-2 hand-off lives in TMEM: tcgen05.st / .ld
+    # (SASS STTM / LDTM) in every k_tblock_tm instance
+    tm = [blk for blk in sass.split("Function :")[1:] if blk.split()[0].startswith("_ZN9thiim_gpu11k_tblock_tm")]
+    assert tm, "no k_tblock_tm instances"
+    for blk in tm:
+        assert "UTMALDG" in blk and "LDTM" in blk and "STTM" in blk, blk.split()[0]
     # -fmad=false: no contracted FP64 multiply-add in any stencil / setup kernel.  Only
     # the kernels that divide (IEEE division is an FMA-refined sequence, still correctly
     # rounded -- test_gpu_materials.py pins them bitwise against libgcc) contain DFMA.
@@ -59,7 +65,10 @@ def test_library_is_sm100a_cubin():
 
 
 def test_abi_version_and_models():
-    assert P.lib().thiim_gpu_abi_version() == 1
+    assert P.lib().thiim_gpu_abi_version() == 2
+    # thiim_gpu_opts: 7 ints of geometry/engine, schedule, band, same_device,
+    # 4 reserved, coeff_layout, n_materials
+    assert ctypes.sizeof(P._Opts) == 16 * 4
     assert P.balance_model(P.ENGINE_SPLIT) == 1024.0
     assert P.balance_model(P.ENGINE_FUSED) == 832.0
     assert P.balance_model(P.ENGINE_TBLOCK, 2) == 416.0

@@ -58,11 +58,13 @@ def test_exactly_once_multi_slab(engine):
         assert e.coverage() == (_passes(engine, 5), 0)
 
 
-def test_uninstrumented_schedule_is_reported():
-    """The A/B scratch TBLOCK kernel stores without counting: every interior
-    (component, cell) of every pass must show up as a violation."""
+def test_uninstrumented_schedule_is_reported(monkeypatch):
+    """Negative control: the uninstrumented TBLOCK instances store without
+    counting, so every interior (component, cell) of every pass must show up
+    as a violation."""
+    monkeypatch.setenv("THIIM_SANITIZE_UNCOUNTED", "1")
     d = P.GridDims(30, 20, 16)
-    with P.GpuEngine(d, P.GpuOptions(engine=P.ENGINE_TBLOCK, variant=2)) as e:
+    with P.GpuEngine(d, P.GpuOptions(engine=P.ENGINE_TBLOCK)) as e:
         e.generate(P.GEN_RANDOM, 1)
         e.set_sanitize(True)
         e.step(4)
