@@ -101,6 +101,7 @@ struct Slab {
   // CUDA graph of two TBLOCK passes (4 steps) per starting field set, replayed
   // by thiim_gpu_step on whole-z contexts (launch-bound small grids)
   cudaGraphExec_t pass_graph[2] = {nullptr, nullptr};
+  long long pass_graph_launches[2] = {0, 0};  // kernel launches one replay runs
   // 4-D tensor maps over the allocation {x (doubles), y, plane, array slot},
   // one set of box shapes per tile height (8 / 16 rows), built lazily
   TmaMaps maps[6];  // tile heights 8, 16, 15, 12, 14, 13 (map_index)
@@ -1852,6 +1853,7 @@ static int step_enqueue(thiim_gpu_ctx* ctx, int steps, long long* launches_out) 
         CK(cudaStreamBeginCapture(sl.stream, cudaStreamCaptureModeThreadLocal));
         int rc = launch_tblock2(ctx, sl, &dummy, po0);
         if (!rc) rc = launch_tblock2(ctx, sl, &dummy, po0);
+        sl.pass_graph_launches[cur0] = dummy;
         const cudaError_t ec = cudaStreamEndCapture(sl.stream, &graph);
         sl.cur = cur0;  // the capture ran no kernels; both launches flipped cur
         if (rc) return rc;
@@ -1862,13 +1864,20 @@ static int step_enqueue(thiim_gpu_ctx* ctx, int steps, long long* launches_out) 
       }
       for (; n + 4 <= steps; n += 4) {
         CK(cudaGraphLaunch(gx, sl.stream));
-        launches += 2;
+        launches += sl.pass_graph_launches[sl.cur];
       }
     }
     for (; n + 2 <= steps; n += 2) {
       for (int k = 0; k < ns; ++k) po[k] = peer_out(ctx, k);
+      // every slab's pass waits for its neighbours' PREVIOUS pass (their halo
+      // reads of the set this pass stores into, and their stores into this
+      // slab's input halos): all waits are enqueued before any of this
+      // iteration's records, or slab k+1 would wait for slab k's current pass
+      // and the slabs would run one after another
+      if (ctx->peer_stores)
+        for (int k = 0; k < ns; ++k)
+          if ((r = wait_neighbours(ctx, k))) return r;
       for (int k = 0; k < ns; ++k) {
-        if (ctx->peer_stores && (r = wait_neighbours(ctx, k))) return r;
         if ((r = launch_tblock2(ctx, ctx->slabs[k], &launches, po[k]))) return r;
         if (multi) CK(cudaEventRecord(ctx->slabs[k].ev_pass, ctx->slabs[k].stream));
       }
@@ -1876,10 +1885,11 @@ static int step_enqueue(thiim_gpu_ctx* ctx, int steps, long long* launches_out) 
       if (multi && !ctx->peer_stores && (r = exchange_deep(ctx))) return r;
     }
     for (; n < steps; ++n) {
-      for (int k = 0; k < ns; ++k) {
-        if (ctx->peer_stores && (r = wait_neighbours(ctx, k))) return r;
+      if (ctx->peer_stores)
+        for (int k = 0; k < ns; ++k)
+          if ((r = wait_neighbours(ctx, k))) return r;
+      for (int k = 0; k < ns; ++k)
         if ((r = launch_fused(ctx, ctx->slabs[k], &launches))) return r;
-      }
       if (ctx->sanitize && (r = coverage_pass(ctx, false))) return r;
       if (multi && (r = exchange_deep(ctx))) return r;
     }

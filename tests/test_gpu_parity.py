@@ -124,7 +124,8 @@ def test_tblock_full_config1_grid_vs_fused():
     with P.GpuEngine(d, P.GpuOptions(engine=P.ENGINE_TBLOCK)) as b:
         b.generate(P.GEN_RANDOM, 1)
         st = b.step(6)
-        assert st.kernel_launches == 3
+        # three passes, each one launch per round of <= one CTA per SM
+        assert st.kernel_launches >= 3 and st.kernel_launches % 3 == 0
         diff = b.compare_fields(ref)
     assert diff.bitwise_equal, diff
 
