@@ -259,16 +259,16 @@ def run_reference_arm(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
-def _roofline(P, dims, engine_ran, dev_secs, launches, table=False, iters_total=0):
+def _roofline(P, dims, engine_ran, dev_secs, launches, table=False, iters_total=0, depth=2):
     """Roofline of the dominant kernel: one THIIM iteration (fused) or one
     half-step sweep (split) per launch over the rank's grid.  TBLOCK in place:
     one two-step pass (its sub-range launches + copy-back) is the unit."""
     hbm, peak_kind = load_peaks()
     per_launch_s = dev_secs / max(1, launches)
     if engine_ran == P.ENGINE_TBLOCK:
-        # a TBLOCK pass (two iterations) is one launch per round of <= 148 CTAs:
-        # the unit is the pass
-        per_launch_s = dev_secs / max(1, iters_total / 2)
+        # a TBLOCK pass (`depth` iterations) is one launch per round of <= 148
+        # CTAs: the unit is the pass
+        per_launch_s = dev_secs / max(1, iters_total / depth)
     if engine_ran == P.ENGINE_TBLOCK_INPLACE:
         per_launch_s = dev_secs / max(1, iters_total / 2)
         bytes_launch = 1216.0 * dims.interior_cells()  # 832 B pass + 384 B copy-back
@@ -284,9 +284,9 @@ def _roofline(P, dims, engine_ran, dev_secs, launches, table=False, iters_total=
         bytes_launch = 385.0 * dims.interior_cells()  # 24 fields x 16 B + 1 B material id
         kname = "k_fused_table<15,5>"
     elif engine_ran == P.ENGINE_TBLOCK:
-        # one launch = two THIIM iterations in one HBM pass: 832 B per cell = 416 B/LUP
+        # one pass = `depth` THIIM iterations: 832 B per cell = 832/depth B/LUP
         bytes_launch = 832.0 * dims.interior_cells()
-        kname = "k_tblock_tm<15,6>"
+        kname = "k_tblock3_tm<15,6>" if depth == 3 else "k_tblock_tm<15,6>"
     else:
         bytes_launch = 832.0 * dims.interior_cells()
         kname = "k_fused_tma<15,6>"
@@ -299,8 +299,10 @@ def _roofline(P, dims, engine_ran, dev_secs, launches, table=False, iters_total=
         with open(tp) as f:
             traffic = json.load(f).get("%s@%dx%dx%d" % (kname, dims.nx, dims.ny, dims.nz))
     balance = (385.0 / (2 if engine_ran == P.ENGINE_TBLOCK else 1)) if table \
-        else P.balance_model(engine_ran)
+        else P.balance_model(engine_ran, depth if engine_ran == P.ENGINE_TBLOCK else 0)
     steps_per_launch = 2 if engine_ran in (P.ENGINE_TBLOCK, P.ENGINE_TBLOCK_INPLACE) else 1
+    if engine_ran == P.ENGINE_TBLOCK and not table:
+        steps_per_launch = depth
     if engine_ran == P.ENGINE_SPLIT:
         steps_per_launch = 0.5
     return {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
@@ -318,7 +320,7 @@ def run_native(args, world, rank, local):
               "tblock": P.ENGINE_TBLOCK, "tblock-inplace": P.ENGINE_TBLOCK_INPLACE}[args.engine]
     opts = P.GpuOptions(device=local if world > 1 else args.device, engine=engine,
                         tile_y=args.tile_y, z_chunk=args.z_chunk, schedule=args.schedule,
-                        band=args.band,
+                        band=args.band, time_block=args.time_block,
                         coeff_layout=P.COEFF_TABLE if args.coeff == "table" else P.COEFF_FULL,
                         n_materials=6 if args.coeff == "table" else 0)
     iters = args.iters
@@ -366,7 +368,8 @@ def _line(P, args, world, dims_rank, engine_ran, dev_secs, launches, e2e, clk, e
         "gpu_launches": launches,
         "roofline": _roofline(P, dims_rank, engine_ran, dev_secs, launches,
                               table=getattr(args, "coeff", "full") == "table",
-                              iters_total=args.iters * args.steps),
+                              iters_total=args.iters * args.steps,
+                              depth=getattr(args, "depth_ran", 2)),
         "clocks": clk.result,
     }
 
@@ -408,6 +411,8 @@ def run_native_single(P, args, opts, iters):
             dev_secs += st.seconds
             launches += st.kernel_launches
     engine_ran = st.engine
+    if engine_ran == P.ENGINE_TBLOCK and args.coeff != "table" and st.balance_model > 0:
+        args.depth_ran = int(round(832.0 / st.balance_model))  # time-block depth that ran
     eng.close()
 
     # e2e: the public API a user calls, with every step's inputs copied from
@@ -617,6 +622,8 @@ def main():
     ap.add_argument("--schedule", type=int, default=0,
                     help="TBLOCK CTA schedule: 0 auto (rounds, banded tiles), 1 one launch")
     ap.add_argument("--band", type=int, default=0, help="TBLOCK rounds: tile columns per band")
+    ap.add_argument("--time-block", type=int, default=0,
+                    help="TBLOCK steps per HBM pass: 0 auto, 2, 3")
     ap.add_argument("--config", default=None, choices=sorted(CONFIGS),
                     help="default: configs[2] at N=1, configs[4] (per rank) at N>1")
     ap.add_argument("--check", type=int, default=0,

@@ -35,6 +35,7 @@
 #include "thiim_fused_tma.cuh"
 #include "thiim_split.cuh"
 #include "thiim_tblock.cuh"
+#include "thiim_tblock3.cuh"
 #include "thiim_tblock_table.cuh"
 
 using namespace thiim_gpu;
@@ -102,6 +103,7 @@ struct Slab {
   // by thiim_gpu_step on whole-z contexts (launch-bound small grids)
   cudaGraphExec_t pass_graph[2] = {nullptr, nullptr};
   long long pass_graph_launches[2] = {0, 0};  // kernel launches one replay runs
+  int pass_graph_depth[2] = {0, 0};           // time-block depth of the captured passes
   // 4-D tensor maps over the allocation {x (doubles), y, plane, array slot},
   // one set of box shapes per tile height (8 / 16 rows), built lazily
   TmaMaps maps[6];  // tile heights 8, 16, 15, 12, 14, 13 (map_index)
@@ -145,6 +147,7 @@ struct Slab {
 struct thiim_gpu_ctx {
   thiim_dims dims{};
   thiim_gpu_opts opts{};
+  int depth = 2;  // TBLOCK time-block depth (3: one whole-z slab, reference layout)
   int engine = THIIM_ENGINE_FUSED;
   std::vector<Slab> slabs;
   bool loaded = false;
@@ -667,9 +670,9 @@ int ensure_tmap(Slab& s, int by, int width = 32) {
                               (cuuint64_t)(s.g.nz + 2), (cuuint64_t)s.n_arrays()};
   const cuuint64_t strides[3] = {(cuuint64_t)s.g.px * 16, (cuuint64_t)s.g.pxy * 16,
                                  (cuuint64_t)s.stride * 16};
-  int bw[NBOX] = {32, 31, 31, 30, 30, 29, 28};  // BoxGeom
-  for (int b = 0; b < NBOX; ++b) bw[b] -= 32 - width;
-  int bh[NBOX] = {by, by - 1, by - 2, by - 1, by - 2, by - 3, by - 4};
+  int bw[NBOX] = {32, 31, 31, 30, 30, 29, 28, 27, 26};  // BoxGeom
+  for (int b = 0; b < NBOX; ++b) bw[b] = std::max(1, bw[b] - (32 - width));
+  int bh[NBOX] = {by, by - 1, by - 2, by - 1, by - 2, by - 3, by - 4, by - 5, by - 6};
   for (int b = 0; b < NBOX; ++b) bh[b] += (32 / width - 1) * (by - 4);  // folded: all segments
   for (int b = 0; b < NBOX; ++b) {
     const cuuint32_t box[4] = {(cuuint32_t)(2 * bw[b]), (cuuint32_t)bh[b], 1, 1};
@@ -718,14 +721,14 @@ int launch_fused_tma_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
 // ---- TBLOCK (two steps per pass)
 // z-chunks of a TBLOCK launch: each CTA re-does ~2 planes of level-1/level-2
 // work at its start; minimise waves x (planes + 2) over one CTA per SM
-int tblock_zchunk(const Slab& s, long long cols) {
+int tblock_zchunk(const Slab& s, long long cols, double overhead = 2.0) {
   const long long slots = sm_count(s.device);
   double best = 1e300;
   int best_c = 1;
   for (int c = 1; c <= std::max(1, s.g.nz / 8); ++c) {
     const int planes = (s.g.nz + c - 1) / c;
     const long long waves = (cols * c + slots - 1) / slots;
-    const double t = (double)waves * (planes + 2.0);
+    const double t = (double)waves * (planes + overhead);
     if (t < best - 1e-9) {
       best = t;
       best_c = c;
@@ -733,6 +736,10 @@ int tblock_zchunk(const Slab& s, long long cols) {
   }
   return (s.g.nz + best_c - 1) / best_c;
 }
+
+// slot bases of the 4-D tensor maps: current field set, first coefficient
+int cur_slot(const Slab& s) { return s.cur * 12; }
+int nf_slot(const Slab& s) { return s.nfield_sets * 12; }
 
 // Tile columns per band of a round-scheduled TBLOCK pass (TileOrder,
 // thiim_tblock.cuh).  A round of G tiles as a band x (G / band) block re-fetches
@@ -875,6 +882,59 @@ int launch_tblock_table_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches, cons
   s.cur ^= 1;
   ++*launches;
   return THIIM_OK;
+}
+
+// Depth-3 TBLOCK pass (k_tblock3_tm, thiim_tblock3.cuh): whole-z slabs only.
+template <int BY, int NG>
+int launch_tblock3_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
+  if (s.deep || s.g.halo_lo || s.z1 < ctx->dims.nz || s.table)
+    return fail(THIIM_ERR_CONFIG, "time_block 3 runs on whole-z contexts in the reference layout");
+  const Arrays A = s.arrays(s.cur, s.cur ^ 1);
+  int r = ensure_tmap(s, BY);
+  if (r) return r;
+  const size_t smem = sizeof(TmSmem<BY, NG>);
+  static std::atomic<unsigned> attr_set{0};
+  if (setup_needed(attr_set, s.device)) {
+    CK(cudaFuncSetAttribute(k_tblock3_tm<BY, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)smem));
+    CK(cudaFuncSetAttribute(k_tblock3_tm<BY, NG, true>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    setup_done(attr_set, s.device);
+  }
+  constexpr int TX3 = 26, TY3 = BY - 6;
+  const int tiles_x = (s.g.nx + TX3 - 1) / TX3, tiles_y = (s.g.ny + TY3 - 1) / TY3;
+  const int nbt = tiles_x * tiles_y;
+  int zc = ctx->opts.z_chunk;
+  // a chunk start re-does ~3 planes of level work (prologues of three levels)
+  if (zc <= 0) zc = tblock_zchunk(s, (long long)nbt, 3.0);
+  const int nchunks = (s.g.nz + zc - 1) / zc;
+  const long long items = (long long)nbt * nchunks;
+  const int sms = sm_count(s.device);
+  const bool one_launch = ctx->opts.schedule == 1;
+  const long long rounds = one_launch ? 1 : (items + sms - 1) / sms;
+  const long long per_round = (items + rounds - 1) / rounds;
+  TileOrder ord;
+  ord.nbt = nbt;
+  ord.tiles_y = tiles_y;
+  ord.band = one_launch ? tiles_x : tblock_band(tiles_x, (int)std::min<long long>(per_round, sms),
+                                                 ctx->opts.band);
+  const bool c = s.cnt != nullptr && !std::getenv("THIIM_SANITIZE_UNCOUNTED");
+  auto kern = c ? k_tblock3_tm<BY, NG, true> : k_tblock3_tm<BY, NG, false>;
+  for (long long it0 = 0; it0 < items; it0 += per_round) {
+    ord.item0 = (int)it0;
+    const unsigned n = (unsigned)std::min<long long>(per_round, items - it0);
+    kern<<<n, dim3(32, BY + 1), smem, s.stream>>>(s.g, A, tmaps(s, BY), cur_slot(s), nf_slot(s), zc,
+                                                   tiles_x, ord);
+    CK(cudaGetLastError());
+    ++*launches;
+  }
+  s.cur ^= 1;
+  return THIIM_OK;
+}
+
+int launch_tblock3(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
+  CK(cudaSetDevice(s.device));
+  return launch_tblock3_t<15, THIIM_TB_NG>(ctx, s, launches);
 }
 
 int launch_tblock2(thiim_gpu_ctx* ctx, Slab& s, long long* launches, const PeerOut& po) {
@@ -1097,8 +1157,12 @@ static int create_impl(const thiim_dims* dims, const thiim_gpu_opts* opts, bool 
   if (o.n_gpus < 1 || o.n_gpus > 8) return fail(THIIM_ERR_CONFIG, "n_gpus must be in 1..8");
   if (o.engine < THIIM_ENGINE_AUTO || o.engine > THIIM_ENGINE_TBLOCK_INPLACE)
     return fail(THIIM_ERR_CONFIG, "unknown engine");
-  if (o.engine == THIIM_ENGINE_TBLOCK && o.time_block != 0 && o.time_block != 2)
-    return fail(THIIM_ERR_CONFIG, "engine TBLOCK supports time_block 2");
+  if ((o.engine == THIIM_ENGINE_TBLOCK || o.engine == THIIM_ENGINE_AUTO) && o.time_block != 0 &&
+      o.time_block != 2 && o.time_block != 3)
+    return fail(THIIM_ERR_CONFIG, "engine TBLOCK supports time_block 2 or 3");
+  if (o.time_block == 3 && (o.n_gpus > 1 || o.coeff_layout != THIIM_COEFF_FULL))
+    return fail(THIIM_ERR_CONFIG,
+                "time_block 3 runs on one whole-z slab in the reference coefficient layout");
   const bool table = o.coeff_layout == THIIM_COEFF_TABLE;
   if (o.coeff_layout != THIIM_COEFF_FULL && !table)
     return fail(THIIM_ERR_CONFIG, "unknown coefficient layout");
@@ -1124,6 +1188,7 @@ static int create_impl(const thiim_dims* dims, const thiim_gpu_opts* opts, bool 
   const long long pxy = ctx->pxy();
   const int n = (int)ranges.size();
   ctx->engine = o.engine;
+  ctx->depth = o.time_block == 3 ? 3 : 2;
   const bool whole_z = n == 1 && ranges[0].first == 0 && ranges[0].second == dims->nz;
   // TBLOCK in place runs on a split (one field set) context plus spare planes
   const bool want_ip = o.engine == THIIM_ENGINE_TBLOCK_INPLACE;
@@ -1824,6 +1889,12 @@ int thiim_gpu_coverage(thiim_gpu_ctx* ctx, unsigned long long* passes,
 // Enqueues `steps` iterations on the context's stream(s) without waiting for
 // them; host-side bookkeeping (current field set, graphs) advances at enqueue
 // time, so calls on one context must stay in stream order.
+static int tb_depth(const thiim_gpu_ctx* ctx) {
+  const bool whole = ctx->slabs.size() == 1 && !ctx->slabs[0].deep && !ctx->slabs[0].table &&
+                     ctx->slabs[0].z0 == 0 && ctx->slabs[0].z1 == ctx->dims.nz;
+  return whole ? ctx->depth : 2;
+}
+
 static int step_enqueue(thiim_gpu_ctx* ctx, int steps, long long* launches_out) {
   long long launches = 0;
   const bool multi = ctx->slabs.size() > 1;
@@ -1837,22 +1908,30 @@ static int step_enqueue(thiim_gpu_ctx* ctx, int steps, long long* launches_out) 
     // exchange step, only stream-event ordering between adjacent slabs
     const int ns = (int)ctx->slabs.size();
     std::vector<PeerOut> po(ns);
+    // time-block depth of the passes: 3 on one whole-z slab when asked for
+    // (thiim_tblock3.cuh), else 2
+    const int depth = tb_depth(ctx);
+    auto pass = [&](Slab& sl, long long* l, const PeerOut& p) {
+      return depth == 3 ? launch_tblock3(ctx, sl, l) : launch_tblock2(ctx, sl, l, p);
+    };
     // whole-z context: after one plain pass (one-time setup outside any capture),
-    // 4-step cycles replay a captured graph of two passes
-    if (ns == 1 && !multi && !ctx->slabs[0].deep && !ctx->sanitize && steps - n >= 6 &&
+    // cycles of two passes replay a captured graph
+    if (ns == 1 && !multi && !ctx->slabs[0].deep && !ctx->sanitize && steps - n >= 3 * depth &&
         std::getenv("THIIM_NO_GRAPHS") == nullptr) {
       Slab& sl = ctx->slabs[0];
       const PeerOut po0 = peer_out(ctx, 0);
-      if ((r = launch_tblock2(ctx, sl, &launches, po0))) return r;
-      n += 2;
+      if ((r = pass(sl, &launches, po0))) return r;
+      n += depth;
       cudaGraphExec_t& gx = sl.pass_graph[sl.cur];
-      if (!gx) {
+      if (!gx || sl.pass_graph_depth[sl.cur] != depth) {
+        if (gx) cudaGraphExecDestroy(gx);
+        gx = nullptr;
         const int cur0 = sl.cur;
         cudaGraph_t graph = nullptr;
         long long dummy = 0;
         CK(cudaStreamBeginCapture(sl.stream, cudaStreamCaptureModeThreadLocal));
-        int rc = launch_tblock2(ctx, sl, &dummy, po0);
-        if (!rc) rc = launch_tblock2(ctx, sl, &dummy, po0);
+        int rc = pass(sl, &dummy, po0);
+        if (!rc) rc = pass(sl, &dummy, po0);
         sl.pass_graph_launches[cur0] = dummy;
         const cudaError_t ec = cudaStreamEndCapture(sl.stream, &graph);
         sl.cur = cur0;  // the capture ran no kernels; both launches flipped cur
@@ -1861,10 +1940,18 @@ static int step_enqueue(thiim_gpu_ctx* ctx, int steps, long long* launches_out) 
         const cudaError_t ei = cudaGraphInstantiate(&gx, graph, 0);
         cudaGraphDestroy(graph);
         CK(ei);
+        sl.pass_graph_depth[cur0] = depth;
       }
-      for (; n + 4 <= steps; n += 4) {
+      for (; n + 2 * depth <= steps; n += 2 * depth) {
         CK(cudaGraphLaunch(gx, sl.stream));
         launches += sl.pass_graph_launches[sl.cur];
+      }
+    }
+    if (depth == 3) {
+      Slab& sl = ctx->slabs[0];
+      for (; n + 3 <= steps; n += 3) {
+        if ((r = launch_tblock3(ctx, sl, &launches))) return r;
+        if (ctx->sanitize && (r = coverage_pass(ctx, true))) return r;
       }
     }
     for (; n + 2 <= steps; n += 2) {

@@ -156,55 +156,61 @@ __device__ __forceinline__ void produce_plane_ct(PR& P, int fb, int cb, int z, u
 #undef BOXC
 }
 
-// Level-2 coefficient groups of plane r, policy `pol`: seq_level2_coef's
-// grouping, boxed to the level-2 regions (BOX_H2 / BOX_E2).
+// The 28 coefficient planes of a deeper level at plane r, policy `pol`, in 8
+// groups (the consumer's read order), boxed to that level's regions: BH / BE =
+// BOX_H2 / BOX_E2 (level 2) or BOX_H3 / BOX_E3 (level 3).
+template <int BH, int BE, class PR>
+__device__ __forceinline__ void produce_levelj_coef_ct(PR& P, int cb, int r, uint64_t pol) {
+  const int p0 = r + 1;
+  P.template begin_group<BH, 4>();  // Hxy t c, Hyx t c
+  P.template box<BH>(0, cb + HXY, p0, pol);
+  P.template box<BH>(1, cb + 12 + HXY, p0, pol);
+  P.template box<BH>(2, cb + HYX, p0, pol);
+  P.template box<BH>(3, cb + 12 + HYX, p0, pol);
+  P.end();
+  P.template begin_group<BH, 3>();  // Hxz t c src
+  P.template box<BH>(0, cb + HXZ, p0, pol);
+  P.template box<BH>(1, cb + 12 + HXZ, p0, pol);
+  P.template box<BH>(2, cb + 24 + SRC_HXZ, p0, pol);
+  P.end();
+  P.template begin_group<BH, 3>();  // Hyz t c src
+  P.template box<BH>(0, cb + HYZ, p0, pol);
+  P.template box<BH>(1, cb + 12 + HYZ, p0, pol);
+  P.template box<BH>(2, cb + 24 + SRC_HYZ, p0, pol);
+  P.end();
+  P.template begin_group<BH, 4>();  // Hzx t c, Hzy t c
+  P.template box<BH>(0, cb + HZX, p0, pol);
+  P.template box<BH>(1, cb + 12 + HZX, p0, pol);
+  P.template box<BH>(2, cb + HZY, p0, pol);
+  P.template box<BH>(3, cb + 12 + HZY, p0, pol);
+  P.end();
+  P.template begin_group<BE, 4>();  // Exy t c, Eyx t c
+  P.template box<BE>(0, cb + EXY, p0, pol);
+  P.template box<BE>(1, cb + 12 + EXY, p0, pol);
+  P.template box<BE>(2, cb + EYX, p0, pol);
+  P.template box<BE>(3, cb + 12 + EYX, p0, pol);
+  P.end();
+  P.template begin_group<BE, 3>();  // Exz t c src
+  P.template box<BE>(0, cb + EXZ, p0, pol);
+  P.template box<BE>(1, cb + 12 + EXZ, p0, pol);
+  P.template box<BE>(2, cb + 24 + SRC_EXZ, p0, pol);
+  P.end();
+  P.template begin_group<BE, 3>();  // Eyz t c src
+  P.template box<BE>(0, cb + EYZ, p0, pol);
+  P.template box<BE>(1, cb + 12 + EYZ, p0, pol);
+  P.template box<BE>(2, cb + 24 + SRC_EYZ, p0, pol);
+  P.end();
+  P.template begin_group<BE, 4>();  // Ezx t c, Ezy t c
+  P.template box<BE>(0, cb + EZX, p0, pol);
+  P.template box<BE>(1, cb + 12 + EZX, p0, pol);
+  P.template box<BE>(2, cb + EZY, p0, pol);
+  P.template box<BE>(3, cb + 12 + EZY, p0, pol);
+  P.end();
+}
+
 template <class PR>
 __device__ __forceinline__ void produce_level2_coef_ct(PR& P, int cb, int r, uint64_t pol) {
-  const int p0 = r + 1;
-  P.template begin_group<BOX_H2, 4>();  // Hxy t c, Hyx t c
-  P.template box<BOX_H2>(0, cb + HXY, p0, pol);
-  P.template box<BOX_H2>(1, cb + 12 + HXY, p0, pol);
-  P.template box<BOX_H2>(2, cb + HYX, p0, pol);
-  P.template box<BOX_H2>(3, cb + 12 + HYX, p0, pol);
-  P.end();
-  P.template begin_group<BOX_H2, 3>();  // Hxz t c src
-  P.template box<BOX_H2>(0, cb + HXZ, p0, pol);
-  P.template box<BOX_H2>(1, cb + 12 + HXZ, p0, pol);
-  P.template box<BOX_H2>(2, cb + 24 + SRC_HXZ, p0, pol);
-  P.end();
-  P.template begin_group<BOX_H2, 3>();  // Hyz t c src
-  P.template box<BOX_H2>(0, cb + HYZ, p0, pol);
-  P.template box<BOX_H2>(1, cb + 12 + HYZ, p0, pol);
-  P.template box<BOX_H2>(2, cb + 24 + SRC_HYZ, p0, pol);
-  P.end();
-  P.template begin_group<BOX_H2, 4>();  // Hzx t c, Hzy t c
-  P.template box<BOX_H2>(0, cb + HZX, p0, pol);
-  P.template box<BOX_H2>(1, cb + 12 + HZX, p0, pol);
-  P.template box<BOX_H2>(2, cb + HZY, p0, pol);
-  P.template box<BOX_H2>(3, cb + 12 + HZY, p0, pol);
-  P.end();
-  P.template begin_group<BOX_E2, 4>();  // Exy t c, Eyx t c
-  P.template box<BOX_E2>(0, cb + EXY, p0, pol);
-  P.template box<BOX_E2>(1, cb + 12 + EXY, p0, pol);
-  P.template box<BOX_E2>(2, cb + EYX, p0, pol);
-  P.template box<BOX_E2>(3, cb + 12 + EYX, p0, pol);
-  P.end();
-  P.template begin_group<BOX_E2, 3>();  // Exz t c src
-  P.template box<BOX_E2>(0, cb + EXZ, p0, pol);
-  P.template box<BOX_E2>(1, cb + 12 + EXZ, p0, pol);
-  P.template box<BOX_E2>(2, cb + 24 + SRC_EXZ, p0, pol);
-  P.end();
-  P.template begin_group<BOX_E2, 3>();  // Eyz t c src
-  P.template box<BOX_E2>(0, cb + EYZ, p0, pol);
-  P.template box<BOX_E2>(1, cb + 12 + EYZ, p0, pol);
-  P.template box<BOX_E2>(2, cb + 24 + SRC_EYZ, p0, pol);
-  P.end();
-  P.template begin_group<BOX_E2, 4>();  // Ezx t c, Ezy t c
-  P.template box<BOX_E2>(0, cb + EZX, p0, pol);
-  P.template box<BOX_E2>(1, cb + 12 + EZX, p0, pol);
-  P.template box<BOX_E2>(2, cb + EZY, p0, pol);
-  P.template box<BOX_E2>(3, cb + 12 + EZY, p0, pol);
-  P.end();
+  produce_levelj_coef_ct<BOX_H2, BOX_E2>(P, cb, r, pol);
 }
 
 // Table-layout plane z (seq_table's 12 arrays, in three full groups instead of

@@ -40,14 +40,17 @@ namespace thiim_gpu {
 //   BOX_BX 31 x (BY-2) own + ring_x (x0-1 column)   (Hyx, Hyz operands)
 //   BOX_BY 30 x (BY-1) own + ring_y (y0-1 row)      (Hxy, Hxz operands)
 //   BOX_C  30 x (BY-2) own only                     (E-phase coefficients)
-// and for the second level of the temporally blocked sweep, whose output tile
-// is one ring smaller (28 x (BY-4) at thread (2,2)):
+// and for the deeper levels of the temporally blocked sweep, whose regions
+// shrink by one ring per level (level j: own cells [j, 31-j] x [j, BY-1-j],
+// H updated also on the -x/-y ring at j-1):
 //   BOX_H2 29 x (BY-3) level-2 own + its -x/-y ring  (level-2 H coefficients)
 //   BOX_E2 28 x (BY-4) level-2 own                   (level-2 E coefficients)
+//   BOX_H3 27 x (BY-5), BOX_E3 26 x (BY-6)           (level 3, depth-3 sweep)
 // Fetching only what each group needs keeps the tile overlap (re-read by the
 // neighbouring CTA) at ~7% instead of ~22%.
 enum : int {
-  BOX_A = 0, BOX_B = 1, BOX_BX = 2, BOX_BY = 3, BOX_C = 4, BOX_H2 = 5, BOX_E2 = 6, NBOX = 7
+  BOX_A = 0, BOX_B = 1, BOX_BX = 2, BOX_BY = 3, BOX_C = 4, BOX_H2 = 5, BOX_E2 = 6,
+  BOX_H3 = 7, BOX_E3 = 8, NBOX = 9
 };
 
 // W: width of the thread tile the boxes belong to -- 32 (one warp row), or a
@@ -58,20 +61,25 @@ enum : int {
 template <int BY, int W = 32>
 struct BoxGeom {
   __host__ __device__ static constexpr int x0(int b) {
-    return b == BOX_E2 ? 2 : (b == BOX_BY || b == BOX_C || b == BOX_H2) ? 1 : 0;
+    return b == BOX_E3 ? 3
+           : (b == BOX_E2 || b == BOX_H3) ? 2
+           : (b == BOX_BY || b == BOX_C || b == BOX_H2) ? 1
+                                                        : 0;
   }
   __host__ __device__ static constexpr int y0(int b) {
-    return b == BOX_E2 ? 2 : (b == BOX_BX || b == BOX_C || b == BOX_H2) ? 1 : 0;
+    return b == BOX_E3 ? 3
+           : (b == BOX_E2 || b == BOX_H3) ? 2
+           : (b == BOX_BX || b == BOX_C || b == BOX_H2) ? 1
+                                                        : 0;
   }
   __host__ __device__ static constexpr int w(int b) {
-    return (b == BOX_A ? 32 : b <= BOX_BX ? 31 : b <= BOX_C ? 30 : b == BOX_H2 ? 29 : 28) - (32 - W);
+    return (b == BOX_A ? 32 : b <= BOX_BX ? 31 : b <= BOX_C ? 30 : 34 - b) - (32 - W);
   }
   __host__ __device__ static constexpr int h_seg(int b) {  // rows one segment reads
     return b == BOX_A                      ? BY
            : (b == BOX_B || b == BOX_BY)   ? BY - 1
            : (b == BOX_BX || b == BOX_C)   ? BY - 2
-           : b == BOX_H2                   ? BY - 3
-                                           : BY - 4;
+                                           : BY + 2 - b;
   }
   __host__ __device__ static constexpr int h(int b) {  // box rows
     return h_seg(b) + (32 / W - 1) * (BY - 4);

@@ -88,6 +88,45 @@ __device__ __forceinline__ void tm_ld6(uint32_t a, double2* v) {
                         __hiloint2double((int)r[4 * k + 3], (int)r[4 * k + 2]));
 }
 
+// two double2 = 8 columns
+__device__ __forceinline__ void tm_st2(uint32_t a, const double2* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n\t"
+      "tcgen05.wait::st.sync.aligned;" ::"r"(a),
+      "r"(THIIM_LO(v[0].x)), "r"(THIIM_HI(v[0].x)), "r"(THIIM_LO(v[0].y)), "r"(THIIM_HI(v[0].y)),
+      "r"(THIIM_LO(v[1].x)), "r"(THIIM_HI(v[1].x)), "r"(THIIM_LO(v[1].y)), "r"(THIIM_HI(v[1].y))
+      : "memory");
+}
+
+__device__ __forceinline__ void tm_ld2(uint32_t a, double2* v) {
+  uint32_t r[8];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n\t"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7])
+      : "r"(a)
+      : "memory");
+#pragma unroll
+  for (int k = 0; k < 2; ++k)
+    v[k] = make_double2(__hiloint2double((int)r[4 * k + 1], (int)r[4 * k]),
+                        __hiloint2double((int)r[4 * k + 3], (int)r[4 * k + 2]));
+}
+
+// Single-buffered hand-off: exchange the six values in `v` with the six
+// parked at `a`, two at a time (the register peak is the six values plus one
+// pair).
+__device__ __forceinline__ void tm_xchg6(uint32_t a, double2* v) {
+#pragma unroll
+  for (int p = 0; p < 3; ++p) {
+    double2 t[2];
+    tm_ld2(a + 8 * p, t);
+    tm_st2(a + 8 * p, v + 2 * p);
+    v[2 * p] = t[0];
+    v[2 * p + 1] = t[1];
+  }
+}
+
 #undef THIIM_LO
 #undef THIIM_HI
 
