@@ -22,7 +22,7 @@
 // swapped: level j reads its plane's values out of the slot and parks the
 // values level j-1 just computed in the same columns (tm_swap6, two values at a
 // time), before level j overwrites the registers.  TMEM per warp: stash 1
-// [0,48), stash 2 [48,96), E_old carry [96,120).
+// [0,48), stash 2 [48,96), E_old carry [96,120), level 3's H sums [120,128).
 //
 // Chunk z-range [z0, z1): level j's full planes are [z0-(3-j), z1+(3-j)-1]
 // (clamped to the grid) and one plane below them is its prologue (H sums only,
@@ -79,6 +79,24 @@ __device__ __forceinline__ void coef_level(TmSmem<BY, NG>& sm, RingCursor& rc, i
                                            double2& pHy) {
   constexpr int NCOMP = 32 * BY;
   auto& R = sm.ring;
+  if (ty < J - 1 || ty > BY - J) {
+    // a warp row outside the level's region (H rows [J-1, BY-1-J], their +y
+    // neighbours' E sums up to BY-J): nothing to compute or exchange -- keep
+    // the ring and barrier protocol only (its values pass through unchanged
+    // and are never read at this level or the next)
+    named_sync(1, NCOMP);
+    for (int k = 0; k < 4; ++k) {
+      ring_wait(R, rc);
+      ring_release(R, rc, tx, ring_dep());
+    }
+    if (mode == 2) named_sync(1, NCOMP);
+    for (int k = 0; k < 4; ++k) {
+      ring_wait(R, rc);
+      ring_release(R, rc, tx, ring_dep());
+    }
+    if (mode != 2) named_sync(1, NCOMP);
+    return;
+  }
 #define RD(k, b) ring_read<false>(R, rc, k, b, tx, ty)
   const double2 sEx = csum(e[EXY], e[EXZ]), sEy = csum(e[EYX], e[EYZ]), sEz = csum(e[EZX], e[EZY]);
   if (inpad) {
@@ -226,7 +244,7 @@ __device__ __forceinline__ void tblock3_body(TmSmem<BY, NG>& sm, const Grid& g, 
 
   // -------------------------------------------------------------- consumers
   const uint32_t tcar = tm_warp_addr(sm.tmem_base, ty, 128 * (ty >> 2));
-  const uint32_t ts1 = tcar, ts2 = tcar + 48, tnext = tcar + 96;
+  const uint32_t ts1 = tcar, ts2 = tcar + 48, tnext = tcar + 96, tph3 = tcar + 120;
   const int x = xb + tx, y = yb + ty;
   const bool inpad = (x >= -1) && (x <= g.nx) && (y >= -1) && (y <= g.ny);
   const bool interior = (x >= 0) && (x < g.nx) && (y >= 0) && (y < g.ny);
@@ -285,7 +303,11 @@ __device__ __forceinline__ void tblock3_body(TmSmem<BY, NG>& sm, const Grid& g, 
       named_sync(1, NCOMP);
     }
   }
-  double2 pH2x = make_double2(0.0, 0.0), pH2y = pH2x, pH3x = pH2x, pH3y = pH2x;
+  double2 pH2x = make_double2(0.0, 0.0), pH2y = pH2x;
+  {  // level 3's carried H sums live in TMEM [120,128) between its planes
+    const double2 z2[2] = {pH2x, pH2x};
+    tm_st2(tph3, z2);
+  }
   double2 nE2x = pH2x, nE2y = pH2x, nE3x = pH2x, nE3y = pH2x;
   const uint64_t first = policy_evict_first();
 
@@ -464,8 +486,11 @@ __device__ __forceinline__ void tblock3_body(TmSmem<BY, NG>& sm, const Grid& g, 
       double2 nEx = nE3x, nEy = nE3y;
       if (!full2) top_ghost_sums(tnext, nEx, nEy);  // plane r3+1 is the top ghost plane
       const bool full3 = r3 > p3;
+      double2 pH3[2];
+      tm_ld2(tph3, pH3);
       coef_level<BY, NG, 3, BOX_H3, BOX_E3>(sm, rc, tx, ty, m3, inpad, r3 < 0 ? 0 : full3 ? 2 : 1, e,
-                                            h, nEx, nEy, pH3x, pH3y);
+                                            h, nEx, nEy, pH3[0], pH3[1]);
+      tm_st2(tph3, pH3);
       if (full3 && m3.ue()) {
         const long long i = g.idx(xs, ys, r3);
 #pragma unroll
