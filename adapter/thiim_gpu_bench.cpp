@@ -3,11 +3,13 @@
 // (/root/reference/proj/tools/main.cpp:78-151, 165-208) with `--engine gpu`.
 //
 //   thiim-gpu-bench run  [--config F] [--grid N|NXxNYxNZ] [--steps S]
-//                        [--engine gpu|gpu-tblock|gpu-fused|gpu-split] [--threads G]
-//                        [--tile-y R] [--z-chunk Z] [--bandwidth GBs]
+//                        [--engine gpu|gpu-tblock|gpu-tblock-inplace|gpu-fused|gpu-split]
+//                        [--threads G] [--time-block K] [--tile-y R] [--z-chunk Z]
+//                        [--band B] [--schedule S] [--bandwidth GBs]
 //                        [--report-dir D] [--check] [--sanitize]
-//   thiim-gpu-bench tune [--config F] [--grid ..] [--steps S] [--threads G]
-//                        [--bandwidth GBs] [--table tune_trials.csv] [--winner W.json]
+//   thiim-gpu-bench tune [--config F] [--grid ..] [--steps S] [--bandwidth GBs]
+//                        [--trials N] [--min-seconds T] [--table tune_trials.csv]
+//                        [--winner W.json]
 //
 // The problem is the reference's build_benchmark_problem (coefficients.cpp:94-111)
 // for the configured grid and scheme; `--threads` is the number of GPUs (z-slabs
@@ -15,16 +17,22 @@
 // checks against run_naive like check_against_naive (main.cpp:43-61: `--check`,
 // or automatically for grids up to 96^3), runs the exactly-once coverage
 // sanitizer with `--sanitize`, and appends the run to <report-dir>/reports.jsonl
-// and reports.csv through the reference's emit_reports.  tune times every
-// (engine, time block, tile height) candidate, writes the trial table CSV --
-// the reference's trial_table_csv layout (autotuner.cpp:165-177) with the GPU's
-// knobs as columns -- and verifies the winner against run_naive (grids up to
-// 96^3) or against the split engine on the GPU.  Exit codes follow main.cpp:
-// 0 ok, 1 verification / sanitizer failure or other error, 2 bad configuration.
+// and reports.csv through the reference's emit_reports.  tune is the library's
+// thiim_gpu_tune (the reference's enumerate_candidates + tune,
+// autotuner.cpp:15-142, over time block x tile height x z-chunk x band x
+// schedule, ranked by the GPU models): it times the model's best candidates,
+// writes the trial table CSV -- trial_table_csv's layout (autotuner.cpp:165-177)
+// with the GPU's knobs and model columns -- and the winner JSON; the winner is
+// verified bitwise by the library against the fused engine and here, on the
+// reference's benchmark problem, against run_naive (grids up to 96^3).  The
+// `--bandwidth` default is MEASURED_PEAKS.json's hbm_gbs when that file is in
+// the working directory.  Exit codes follow main.cpp: 0 ok, 1 verification /
+// sanitizer failure or other error, 2 bad configuration.
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <fstream>
+#include <iterator>
 #include <stdexcept>
 #include <string>
 #include <thread>
@@ -46,7 +54,9 @@ using namespace thiim;
 struct Args {
   BenchConfig cfg;
   std::string engine = "gpu";
-  int tile_y = 0, z_chunk = 0;
+  int tile_y = 0, z_chunk = 0, time_block = 0, band = 0, schedule = 0;
+  int trials = 8;
+  double min_seconds = 0.5;
   bool check = false, sanitize = false;
   std::string table = "tune_trials.csv", winner;
 };
@@ -54,9 +64,10 @@ struct Args {
 [[noreturn]] void usage(const char* msg, int code = 2) {
   std::fprintf(stderr,
                "%s%susage: thiim-gpu-bench run|tune [--config F] [--grid N|NXxNYxNZ] "
-               "[--steps S] [--engine gpu|gpu-tblock|gpu-fused|gpu-split] [--threads G] "
-               "[--tile-y R] [--z-chunk Z] [--bandwidth GBs] [--report-dir D] [--check] "
-               "[--sanitize] [--table CSV] [--winner JSON]\n",
+               "[--steps S] [--engine gpu|gpu-tblock|gpu-tblock-inplace|gpu-fused|gpu-split] "
+               "[--threads G] [--time-block K] [--tile-y R] [--z-chunk Z] [--band B] "
+               "[--schedule S] [--bandwidth GBs] [--report-dir D] [--check] [--sanitize] "
+               "[--trials N] [--min-seconds T] [--table CSV] [--winner JSON]\n",
                msg ? msg : "", msg ? "\n" : "");
   std::exit(code);
 }
@@ -64,9 +75,11 @@ struct Args {
 int engine_id(const std::string& e) {
   if (e == "gpu") return THIIM_ENGINE_AUTO;
   if (e == "gpu-tblock") return THIIM_ENGINE_TBLOCK;
+  if (e == "gpu-tblock-inplace") return THIIM_ENGINE_TBLOCK_INPLACE;
   if (e == "gpu-fused") return THIIM_ENGINE_FUSED;
   if (e == "gpu-split") return THIIM_ENGINE_SPLIT;
-  throw ConfigError("unknown engine: " + e + " (gpu | gpu-tblock | gpu-fused | gpu-split)");
+  throw ConfigError("unknown engine: " + e +
+                    " (gpu | gpu-tblock | gpu-tblock-inplace | gpu-fused | gpu-split)");
 }
 
 // the reference's report line (tools/main.cpp:63-76)
@@ -111,6 +124,9 @@ GpuOptions gpu_options(const Args& a, int engine, int tile_y) {
   o.engine = engine;
   o.tile_y = tile_y;
   o.z_chunk = a.z_chunk;
+  o.time_block = a.time_block;
+  o.band = a.band;
+  o.schedule = a.schedule;
   o.sanitize = a.sanitize;
   o.hbm_gbs = a.cfg.profile.bandwidth_gbs;
   return o;
@@ -138,92 +154,89 @@ int do_run(const Args& a) {
   return rc;
 }
 
-struct Trial {
-  std::string engine;
-  int time_block, tile_y;
-  double balance, seconds, mlups;
-  bool ok;
-  std::string note;
-};
-
+// tune (autotuner.cpp:62-142) over the GPU knobs: thiim_gpu_tune ranks the
+// candidates by the GPU models, times the best, verifies the winner against
+// the fused engine; here the winner is also checked against run_naive on the
+// reference's benchmark problem (grids up to 96^3, like check_against_naive).
 int do_tune(const Args& a) {
   const BenchConfig& cfg = a.cfg;
   if (cfg.steps < 1) throw ConfigError("tune needs --steps >= 1");
-  const ProblemState base = build_benchmark_problem(cfg.grid, cfg.scheme);
-  struct Cand {
-    int engine, tile_y;
-  };
-  const std::vector<Cand> cands = {
-      {THIIM_ENGINE_TBLOCK, 15}, {THIIM_ENGINE_TBLOCK, 14}, {THIIM_ENGINE_TBLOCK, 12},
-      {THIIM_ENGINE_FUSED, 15},  {THIIM_ENGINE_FUSED, 16},  {THIIM_ENGINE_FUSED, 8},
-      {THIIM_ENGINE_SPLIT, 0}};
-  std::vector<Trial> table;
-  int best = -1;
-  for (const Cand& c : cands) {
-    ProblemState s = clone_state(base);
-    Trial t{"", c.engine == THIIM_ENGINE_TBLOCK ? 2 : 1, c.tile_y, 0, 0, 0, false, ""};
-    try {
-      GpuOptions o = gpu_options(a, c.engine, c.tile_y);
-      o.sanitize = false;
-      run_gpu(s, cfg.steps, o);  // warm-up (module load, pool, tensor maps)
-      s = clone_state(base);
-      const RunReport r = run_gpu(s, cfg.steps, o);
-      t.engine = r.engine;
-      t.balance = r.balance_model;
-      t.seconds = r.seconds;
-      t.mlups = r.mlups ? *r.mlups : 0.0;
-      t.ok = true;
-    } catch (const std::exception& e) {
-      t.engine = c.engine == THIIM_ENGINE_TBLOCK  ? "gpu-tblock"
-                 : c.engine == THIIM_ENGINE_FUSED ? "gpu-fused"
-                                                  : "gpu-split";
-      t.note = e.what();
-      for (char& ch : t.note)
-        if (ch == ',' || ch == '\n') ch = ';';
-    }
-    table.push_back(t);
-    if (t.ok && (best < 0 || t.mlups > table[best].mlups)) best = (int)table.size() - 1;
-  }
+  if (cfg.threads != 1) throw ConfigError("tune runs on one GPU (--threads 1)");
+  const thiim_dims d{cfg.grid.nx, cfg.grid.ny, cfg.grid.nz, cfg.grid.ghost};
+  thiim_gpu_opts base;
+  thiim_gpu_default_opts(&base);
+  std::vector<thiim_gpu_trial> table((std::size_t)a.trials + 2);
+  int n = 0, verified = 0;
+  thiim_gpu_opts w;
+  const int rc = thiim_gpu_tune(&d, &base, cfg.steps, a.min_seconds, a.trials, table.data(),
+                                (int)table.size(), &n, &w, &verified);
+  if (rc == THIIM_ERR_CONFIG) throw ConfigError(thiim_gpu_last_error());
+  if (rc) throw std::runtime_error(std::string("thiim_gpu_tune: ") + thiim_gpu_last_error());
   {
     std::ofstream out(a.table);
     if (!out) throw ConfigError("cannot write " + a.table);
-    out << "engine,time_block,tile_y,z_chunk,n_gpus,balance_model,steps,seconds,mlups,ok,note\n";
-    for (const Trial& t : table)
-      out << t.engine << ',' << t.time_block << ',' << t.tile_y << ',' << a.z_chunk << ','
-          << cfg.threads << ',' << t.balance << ',' << cfg.steps << ',' << t.seconds << ','
-          << t.mlups << ',' << (t.ok ? 1 : 0) << ',' << t.note << '\n';
+    out << "engine,time_block,tile_y,z_chunk,band,schedule,tiles,rounds,balance_model,"
+           "model_bytes_per_lup,model_mlups,l2_set_bytes,steps,seconds,mlups,ok,note\n";
+    for (int i = 0; i < n; ++i) {
+      const thiim_gpu_trial& t = table[i];
+      const thiim_gpu_candidate& c = t.cand;
+      out << "gpu-tblock," << c.time_block << ',' << c.tile_y << ',' << c.z_chunk << ','
+          << c.band << ',' << c.schedule << ',' << c.tiles << ',' << c.rounds << ','
+          << c.balance_model << ',' << c.model_bytes_per_lup << ',' << c.model_mlups << ','
+          << c.l2_set_bytes << ',' << t.steps << ',' << t.seconds << ',' << t.mlups << ','
+          << t.ok << ',' << t.note << '\n';
+    }
   }
-  if (best < 0) {
-    std::printf("tuner: no candidate ran\n");
-    return 1;
-  }
-  const Trial& w = table[best];
-  // winner verification: run_naive on small grids, else the split engine on the GPU
-  ProblemState got = clone_state(base);
-  run_gpu(got, cfg.steps, gpu_options(a, engine_id(w.engine), w.tile_y));
-  std::string verification;
-  if (cfg.grid.interior_cells() <= 96ull * 96 * 96) {
-    ProblemState ref = clone_state(base);
+  double best = 0.0;
+  for (int i = 0; i < n; ++i)
+    if (table[i].ok && table[i].cand.time_block == w.time_block && table[i].cand.tile_y == w.tile_y &&
+        table[i].cand.z_chunk == w.z_chunk && table[i].cand.band == w.band &&
+        table[i].cand.schedule == w.schedule)
+      best = table[i].mlups;
+  std::string verification = verified ? "bitwise-equal vs gpu-fused" : "failed";
+  if (verified && cfg.grid.interior_cells() <= 96ull * 96 * 96) {
+    const ProblemState base_state = build_benchmark_problem(cfg.grid, cfg.scheme);
+    ProblemState got = clone_state(base_state), ref = clone_state(base_state);
+    GpuOptions go;
+    go.engine = THIIM_ENGINE_TBLOCK;
+    go.time_block = w.time_block;
+    go.tile_y = w.tile_y;
+    go.z_chunk = std::min(w.z_chunk, cfg.grid.nz);
+    go.band = w.band;
+    go.schedule = w.schedule;
+    run_gpu(got, cfg.steps, go);
     run_naive(ref, cfg.steps, host_threads());
     verification = compare_states(ref, got).bitwise_equal ? "bitwise-equal vs naive" : "failed";
-  } else {
-    ProblemState ref = clone_state(base);
-    run_gpu(ref, cfg.steps, gpu_options(a, THIIM_ENGINE_SPLIT, 0));
-    verification =
-        compare_states(ref, got).bitwise_equal ? "bitwise-equal vs gpu-split" : "failed";
   }
   char js[512];
   std::snprintf(js, sizeof js,
-                "{\"engine\":\"%s\",\"time_block\":%d,\"tile_y\":%d,\"z_chunk\":%d,\"n_gpus\":%d,"
-                "\"balance_model\":%g,\"mlups\":%.2f}",
-                w.engine.c_str(), w.time_block, w.tile_y, a.z_chunk, cfg.threads, w.balance,
-                w.mlups);
+                "{\"engine\":\"gpu-tblock\",\"time_block\":%d,\"tile_y\":%d,\"z_chunk\":%d,"
+                "\"band\":%d,\"schedule\":%d,\"balance_model\":%g,\"mlups\":%.2f,"
+                "\"trials\":%d}",
+                w.time_block, w.tile_y, w.z_chunk, w.band, w.schedule,
+                thiim_gpu_balance_model(THIIM_ENGINE_TBLOCK, w.time_block), best, n);
   std::printf("winner: %s (verification: %s)\n", js, verification.c_str());
   if (!a.winner.empty()) {
     std::ofstream out(a.winner);
     out << js << '\n';
   }
   return verification == "failed" ? 1 : 0;
+}
+
+// MEASURED_PEAKS.json hbm_gbs (driver-written, in the working directory), else
+// 6536 GB/s (the measured B200 copy peak of this pool)
+double measured_hbm_gbs() {
+  std::ifstream f("MEASURED_PEAKS.json");
+  std::string s((std::istreambuf_iterator<char>(f)), std::istreambuf_iterator<char>());
+  const std::size_t k = s.find("\"hbm_gbs\"");
+  if (k != std::string::npos) {
+    const std::size_t c = s.find(':', k);
+    if (c != std::string::npos) {
+      const double v = std::atof(s.c_str() + c + 1);
+      if (v > 0) return v;
+    }
+  }
+  return 6536.0;
 }
 
 Args parse(int argc, char** argv) {
@@ -242,6 +255,11 @@ Args parse(int argc, char** argv) {
     else if (k == "--engine") a.engine = val();
     else if (k == "--threads") a.cfg.threads = std::stoi(val());
     else if (k == "--tile-y") a.tile_y = std::stoi(val());
+    else if (k == "--time-block") a.time_block = std::stoi(val());
+    else if (k == "--band") a.band = std::stoi(val());
+    else if (k == "--schedule") a.schedule = std::stoi(val());
+    else if (k == "--trials") a.trials = std::stoi(val());
+    else if (k == "--min-seconds") a.min_seconds = std::stod(val());
     else if (k == "--z-chunk") a.z_chunk = std::stoi(val());
     else if (k == "--bandwidth") a.cfg.profile.bandwidth_gbs = std::stod(val());
     else if (k == "--report-dir") a.cfg.report_dir = val();
@@ -262,7 +280,7 @@ Args parse(int argc, char** argv) {
   if (!grid_spec.empty()) a.cfg.grid = parse_grid(grid_spec);
   // (no THIIM_THREADS override: --threads counts GPUs here)
   if (a.cfg.profile.bandwidth_gbs == MachineProfile{}.bandwidth_gbs)
-    a.cfg.profile.bandwidth_gbs = 6542.4;  // MEASURED_PEAKS.json hbm_gbs (B200)
+    a.cfg.profile.bandwidth_gbs = measured_hbm_gbs();
   if (a.cfg.threads < 1) throw ConfigError("--threads must be >= 1");
   return a;
 }

@@ -21,8 +21,20 @@ const char* engine_name(int e) {
   switch (e) {
     case THIIM_ENGINE_SPLIT: return "gpu-split";
     case THIIM_ENGINE_TBLOCK: return "gpu-tblock";
+    case THIIM_ENGINE_TBLOCK_INPLACE: return "gpu-tblock-inplace";
     default: return "gpu-fused";
   }
+}
+
+void apply(const GpuOptions& opts, thiim_gpu_opts& o) {
+  o.device = opts.device;
+  o.n_gpus = opts.n_gpus;
+  o.engine = opts.engine;
+  o.time_block = opts.time_block;
+  o.z_chunk = opts.z_chunk;
+  o.tile_y = opts.tile_y;
+  o.band = opts.band;
+  o.schedule = opts.schedule;
 }
 
 // RAII over the page-lock of the 40 host arrays.
@@ -57,12 +69,7 @@ RunReport run_gpu(ProblemState& state, int steps, const GpuOptions& opts, GpuRun
   thiim_dims d{state.dims.nx, state.dims.ny, state.dims.nz, state.dims.ghost};
   thiim_gpu_opts o;
   thiim_gpu_default_opts(&o);
-  o.device = opts.device;
-  o.n_gpus = opts.n_gpus;
-  o.engine = opts.engine;
-  o.time_block = opts.time_block;
-  o.z_chunk = opts.z_chunk;
-  o.tile_y = opts.tile_y;
+  apply(opts, o);
 
   CtxGuard g;
   check(thiim_gpu_create(&d, &o, &g.ctx), "thiim_gpu_create");
@@ -143,11 +150,8 @@ RunReport run_gpu_batch(const std::vector<ProblemState*>& states, int steps, con
   thiim_dims d{dims.nx, dims.ny, dims.nz, dims.ghost};
   thiim_gpu_opts o;
   thiim_gpu_default_opts(&o);
-  o.device = opts.device;
-  o.engine = opts.engine;
-  o.time_block = opts.time_block;
-  o.z_chunk = opts.z_chunk;
-  o.tile_y = opts.tile_y;
+  apply(opts, o);
+  o.n_gpus = 1;
   thiim_gpu_batch_stats bs{};
   check(thiim_gpu_run_batch(&d, &o, int(states.size()), in.data(), nullptr, steps, 0, &bs),
         "thiim_gpu_run_batch");

@@ -31,13 +31,16 @@ struct GpuOptions {
   int time_block = 0;              // TBLOCK: steps per HBM pass (0 = auto)
   int z_chunk = 0;                 // planes per CTA along z (0 = auto)
   int tile_y = 0;                  // CTA height in rows (0 = the engine default)
+  int band = 0;                    // TBLOCK rounds: tile columns per band (0 = auto)
+  int schedule = 0;                // TBLOCK CTA schedule (0 = rounds, 1 = one launch)
   bool sanitize = false;           // exactly-once store coverage check per pass
   bool pin_host = true;            // page-lock the 40 arrays during the copies
   double hbm_gbs = 0.0;            // if > 0: predicted_mlups = hbm_gbs / balance
 };
 
 // Upload `state`, run `steps` THIIM iterations on the GPU(s), download the 12
-// fields back into `state`.  RunReport: engine "gpu-split|gpu-fused|gpu-tblock",
+// fields back into `state`.  RunReport: engine "gpu-split|gpu-fused|gpu-tblock|
+// gpu-tblock-inplace",
 // threads = #GPUs, seconds = device time of the step loop (CUDA events),
 // mlups = interior*steps/seconds/1e6, balance_model = algorithmic bytes/LUP.
 RunReport run_gpu(ProblemState& state, int steps, const GpuOptions& opts = {});

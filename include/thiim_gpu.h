@@ -356,6 +356,45 @@ int thiim_gpu_sync(thiim_gpu_ctx* ctx);
  * before another library allocates device memory. */
 int thiim_gpu_release_cached(int device);
 
+/* ---- auto-tuner (the reference's tune, autotuner.cpp:15-142, for the GPU
+ * knobs).  Candidates: time_block {2, 3} x tile_y x z-chunk count x band x
+ * schedule of the TBLOCK engine.  A GPU re-parameterisation of the
+ * reference's models ranks them: Eq. 12's code balance becomes the DRAM bytes
+ * per LUP of a candidate (832 / time_block, plus the tile-overlap rows the L2
+ * does not share across round / band edges and the chunk-start re-reads) times
+ * its wave quantisation; Eq. 11's cache-fit test becomes the L2 working set of
+ * the evict_last coefficient planes one round keeps for the deeper levels,
+ * which must fit 60% of the L2.  Sorted by model MLUP/s, best first. */
+typedef struct {
+  int time_block, tile_y, z_chunk, band, schedule;
+  int tiles, rounds;            /* CTAs and launches (rounds) per pass */
+  double balance_model;         /* 832 / time_block */
+  double model_bytes_per_lup;   /* incl. overlap re-fetch and chunk starts */
+  double quantization;          /* useful / scheduled CTA-planes */
+  double model_mlups;           /* hbm_gbs / model_bytes_per_lup * quantization */
+  double l2_set_bytes;          /* coefficient planes held in L2 by one round */
+} thiim_gpu_candidate;
+int thiim_gpu_enumerate_candidates(const thiim_dims* dims, const thiim_gpu_opts* base,
+                                   double hbm_gbs, thiim_gpu_candidate* out, int cap, int* n);
+
+typedef struct {
+  thiim_gpu_candidate cand;
+  int steps, ok;
+  double seconds, mlups;  /* device time of the timed runs, steps x interior / seconds */
+  char note[96];
+} thiim_gpu_trial;
+/* Times the `max_trials` best-ranked candidates (plus the default schedule)
+ * on the seeded random problem of `dims` (generated on the device), `steps`
+ * iterations per run, repeated until `min_seconds` of device time; the winner
+ * is the deepest time_block within 2% of the best (then the fastest), and is
+ * verified bitwise against the FUSED engine (one step per pass, an
+ * independent schedule) on `dims` if it has <= 2^24 cells, else on a
+ * 120 x 100 x 48 grid.  *verified = 1 if equal.  winner: base with the
+ * winning knobs. */
+int thiim_gpu_tune(const thiim_dims* dims, const thiim_gpu_opts* base, int steps,
+                   double min_seconds, int max_trials, thiim_gpu_trial* table, int cap,
+                   int* n_trials, thiim_gpu_opts* winner, int* verified);
+
 /* Message of the last failing call on this thread ("" if none). */
 const char* thiim_gpu_last_error(void);
 

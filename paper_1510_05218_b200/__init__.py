@@ -302,6 +302,19 @@ class _Diff(ctypes.Structure):
                 ("rel_l2", ctypes.c_double * 12)]
 
 
+class _Cand(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int) for n in ("time_block", "tile_y", "z_chunk", "band", "schedule",
+                                            "tiles", "rounds")] + \
+               [(n, ctypes.c_double) for n in ("balance_model", "model_bytes_per_lup",
+                                               "quantization", "model_mlups", "l2_set_bytes")]
+
+
+class _Trial(ctypes.Structure):
+    _fields_ = [("cand", _Cand), ("steps", ctypes.c_int), ("ok", ctypes.c_int),
+                ("seconds", ctypes.c_double), ("mlups", ctypes.c_double),
+                ("note", ctypes.c_char * 96)]
+
+
 EXPORTED_SYMBOLS = [
     "thiim_gpu_abi_version", "thiim_gpu_last_error", "thiim_gpu_default_opts",
     "thiim_gpu_balance_model", "thiim_gpu_create", "thiim_gpu_destroy", "thiim_gpu_upload",
@@ -314,7 +327,7 @@ EXPORTED_SYMBOLS = [
     "thiim_gpu_coverage", "thiim_scheme_default", "thiim_gpu_init_benchmark",
     "thiim_gpu_init_materials", "thiim_gpu_selftest_cdiv", "thiim_gpu_slab_export",
     "thiim_gpu_slab_import", "thiim_gpu_slab_detach", "thiim_gpu_run_batch",
-    "thiim_gpu_release_cached",
+    "thiim_gpu_release_cached", "thiim_gpu_enumerate_candidates", "thiim_gpu_tune",
 ]
 
 _LIB = None
@@ -361,6 +374,13 @@ def lib() -> ctypes.CDLL:
     L.thiim_gpu_run_batch.argtypes = [ctypes.POINTER(_Dims), ctypes.POINTER(_Opts), ctypes.c_int,
                                       PP, PP, ctypes.c_int, ctypes.c_int,
                                       ctypes.POINTER(_BatchStats)]
+    L.thiim_gpu_enumerate_candidates.argtypes = [ctypes.POINTER(_Dims), ctypes.POINTER(_Opts),
+                                                 ctypes.c_double, ctypes.POINTER(_Cand),
+                                                 ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
+    L.thiim_gpu_tune.argtypes = [ctypes.POINTER(_Dims), ctypes.POINTER(_Opts), ctypes.c_int,
+                                 ctypes.c_double, ctypes.c_int, ctypes.POINTER(_Trial),
+                                 ctypes.c_int, ctypes.POINTER(ctypes.c_int),
+                                 ctypes.POINTER(_Opts), ctypes.POINTER(ctypes.c_int)]
     if L.thiim_gpu_abi_version() != 2:
         raise GpuError("libthiim_gpu.so ABI mismatch")
     _LIB = L
@@ -688,3 +708,68 @@ def run_gpu_batch(states: List[ProblemState], steps: int, opts: Optional[GpuOpti
                        kernel_seconds=st.kernel_seconds, download_seconds=st.download_seconds,
                        mlups=st.mlups, kernel_launches=st.kernel_launches,
                        h2d_bytes=st.h2d_bytes, d2h_bytes=st.d2h_bytes)
+
+
+# ---------------------------------------------------------------- auto-tuner
+_CAND_KEYS = ("time_block", "tile_y", "z_chunk", "band", "schedule", "tiles", "rounds",
+              "balance_model", "model_bytes_per_lup", "quantization", "model_mlups",
+              "l2_set_bytes")
+
+
+def _cand_dict(c: _Cand) -> dict:
+    return {k: getattr(c, k) for k in _CAND_KEYS}
+
+
+def enumerate_candidates(dims: GridDims, opts: Optional[GpuOptions] = None,
+                         hbm_gbs: float = 0.0) -> List[dict]:
+    """TBLOCK candidates ranked by the GPU re-parameterisation of the
+    reference's models (enumerate_candidates, autotuner.cpp:15-50): modelled
+    DRAM bytes/LUP (Eq. 12 analogue) x wave quantisation, L2 fit of the
+    deeper levels' coefficient planes (Eq. 11 analogue).  No device needed."""
+    d = _Dims(dims.nx, dims.ny, dims.nz, dims.ghost)
+    o = (opts or GpuOptions())._c()
+    n = ctypes.c_int()
+    _check(lib().thiim_gpu_enumerate_candidates(ctypes.byref(d), ctypes.byref(o), hbm_gbs, None, 0,
+                                                ctypes.byref(n)))
+    arr = (_Cand * max(1, n.value))()
+    _check(lib().thiim_gpu_enumerate_candidates(ctypes.byref(d), ctypes.byref(o), hbm_gbs, arr,
+                                                n.value, ctypes.byref(n)))
+    return [_cand_dict(arr[i]) for i in range(n.value)]
+
+
+@dataclass
+class TuneResult:
+    """tune's result (autotuner.hpp TuneResult): the trial table, the winner
+    as GpuOptions and its bitwise verification."""
+    table: List[dict] = field(default_factory=list)
+    best: Optional[GpuOptions] = None
+    winner_verification: str = "skipped"
+
+
+def tune(dims: GridDims, steps: int = 8, opts: Optional[GpuOptions] = None,
+         min_seconds: float = 0.5, max_trials: int = 8) -> TuneResult:
+    """tune (autotuner.cpp:62-142) for the GPU knobs: times the model's best
+    candidates, picks the deepest time block within 2% of the fastest and
+    verifies it bitwise against the fused engine."""
+    d = _Dims(dims.nx, dims.ny, dims.nz, dims.ghost)
+    o = (opts or GpuOptions())._c()
+    cap = max_trials + 2
+    tab = (_Trial * cap)()
+    n = ctypes.c_int()
+    w = _Opts()
+    ver = ctypes.c_int()
+    _check(lib().thiim_gpu_tune(ctypes.byref(d), ctypes.byref(o), steps, min_seconds, max_trials,
+                                tab, cap, ctypes.byref(n), ctypes.byref(w), ctypes.byref(ver)))
+    rows = []
+    for i in range(n.value):
+        t = tab[i]
+        r = _cand_dict(t.cand)
+        r.update(steps=t.steps, ok=bool(t.ok), seconds=t.seconds, mlups=t.mlups,
+                 note=t.note.decode(errors="replace"))
+        rows.append(r)
+    best = GpuOptions(device=w.device, n_gpus=w.n_gpus, engine=w.engine, tile_x=w.tile_x,
+                      tile_y=w.tile_y, z_chunk=w.z_chunk, time_block=w.time_block,
+                      schedule=w.schedule, band=w.band, same_device=w.same_device,
+                      coeff_layout=w.coeff_layout, n_materials=w.n_materials)
+    return TuneResult(table=rows, best=best,
+                      winner_verification="bitwise-equal vs gpu-fused" if ver.value else "failed")

@@ -1289,6 +1289,12 @@ static int create_impl(const thiim_dims* dims, const thiim_gpu_opts* opts, bool 
       if (!want_ip && L < 8) L = 0;  // too short to beat split
     }
     L = std::min(L, dims->nz);
+    if (want_ip && env && !(L >= 2 || (L >= 1 && L == dims->nz))) {
+      thiim_gpu_destroy(ctx);
+      return fail(THIIM_ERR_CONFIG,
+                  "TBLOCK in place needs sub-ranges of >= 2 planes (THIIM_INPLACE_TB=" +
+                      std::to_string(L) + ")");
+    }
     if (L >= 2 || (L >= 1 && L == dims->nz)) {
       cudaSetDevice(sl.device);
       cudaError_t e = pool_alloc(reinterpret_cast<void**>(&sl.ip_buf), (size_t)12 * (L + 2) * plane,
@@ -1844,6 +1850,10 @@ static int coverage_pass(thiim_gpu_ctx* ctx, bool tblock_pass = false) {
 int thiim_gpu_set_sanitize(thiim_gpu_ctx* ctx, int on) {
   g_err.clear();
   if (!ctx) return fail(THIIM_ERR_CONFIG, "null context");
+  if (on && ctx->opts.engine == THIIM_ENGINE_TBLOCK_INPLACE)
+    return fail(THIIM_ERR_CONFIG,
+                "the sanitizer checks one-pass schedules; TBLOCK in place (sub-range passes with "
+                "copy-back) is not instrumented -- use engine AUTO, which then runs SPLIT");
   for (auto& sl : ctx->slabs) {
     CK(cudaSetDevice(sl.device));
     CK(cudaStreamSynchronize(sl.stream));
@@ -1889,6 +1899,15 @@ int thiim_gpu_coverage(thiim_gpu_ctx* ctx, unsigned long long* passes,
 // Enqueues `steps` iterations on the context's stream(s) without waiting for
 // them; host-side bookkeeping (current field set, graphs) advances at enqueue
 // time, so calls on one context must stay in stream order.
+// The engine a step call of `steps` runs: split contexts with spare planes run
+// TBLOCK in place (two-step sub-range passes) unless the sanitizer is on; a
+// call of fewer than 2 steps runs only the split remainder.
+static int engine_ran(const thiim_gpu_ctx* ctx, int steps) {
+  const bool ip = ctx->engine == THIIM_ENGINE_SPLIT && ctx->slabs.size() == 1 &&
+                  ctx->slabs[0].ip_L > 0 && !ctx->sanitize && steps >= 2;
+  return ip ? THIIM_ENGINE_TBLOCK_INPLACE : ctx->engine;
+}
+
 static int tb_depth(const thiim_gpu_ctx* ctx) {
   const bool whole = ctx->slabs.size() == 1 && !ctx->slabs[0].deep && !ctx->slabs[0].table &&
                      ctx->slabs[0].z0 == 0 && ctx->slabs[0].z1 == ctx->dims.nz;
@@ -2034,8 +2053,7 @@ int thiim_gpu_step(thiim_gpu_ctx* ctx, int steps, thiim_gpu_stats* stats) {
     stats->seconds = secs;
     stats->kernel_seconds = secs;
     stats->steps = steps;
-    const bool ip = ctx->engine == THIIM_ENGINE_SPLIT && ctx->slabs[0].ip_L > 0 && !ctx->sanitize;
-    stats->engine = ip ? THIIM_ENGINE_TBLOCK_INPLACE : ctx->engine;
+    stats->engine = engine_ran(ctx, steps);
     stats->n_gpus = (int)ctx->slabs.size();
     stats->kernel_launches = launches;
     stats->balance_model = ctx->slabs[0].table
@@ -2244,7 +2262,7 @@ int thiim_gpu_run_batch(const thiim_dims* dims, const thiim_gpu_opts* opts, int 
       span = w * 1e-3;
     }
   }
-  const int engine_ran = ctxs[0] ? ctxs[0]->engine : o.engine;
+  const int ran = ctxs[0] ? engine_ran(ctxs[0], steps) : o.engine;
   cleanup();
   const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   if (stats) {
@@ -2259,7 +2277,7 @@ int thiim_gpu_run_batch(const thiim_dims* dims, const thiim_gpu_opts* opts, int 
     stats->d2h_bytes = (long long)n_problems * 12 * (long long)bytes;
     stats->n_problems = n_problems;
     stats->depth = depth;
-    stats->engine = engine_ran;
+    stats->engine = ran;
     const double lups = (double)dims->nx * dims->ny * dims->nz * steps * n_problems;
     stats->mlups = secs > 0 ? lups / secs / 1e6 : 0.0;
   }
@@ -2433,3 +2451,4 @@ int thiim_gpu_unpin_host(void* ptr) {
 }
 
 }  // extern "C"
+#include "thiim_tune.cuh"

@@ -129,3 +129,28 @@ def test_compress_expand_roundtrip():
         assert np.array_equal(full.arrays[k].view(np.uint64), s.arrays[k].view(np.uint64))
     with pytest.raises(P.ConfigError):
         P.compress_coefficients(P.generate_problem(d, P.GEN_RANDOM, 1))
+
+
+def test_tuner_model_ranks_candidates_without_a_device():
+    """thiim_gpu_enumerate_candidates: the GPU re-parameterisation of the
+    reference's Eq. 11/12 models (autotuner.cpp:15-50) runs on the host."""
+    c = P.enumerate_candidates(P.GridDims(512, 512, 512))
+    assert len(c) > 20
+    assert {x["time_block"] for x in c} == {2, 3}
+    m = [x["model_mlups"] for x in c]
+    assert all(a >= b * 0.995 for a, b in zip(m, m[1:]))  # best first (0.5% tie window)
+    for x in c:
+        assert x["balance_model"] == pytest.approx(832.0 / x["time_block"])
+        # overlap re-fetch and chunk starts only add bytes
+        assert x["model_bytes_per_lup"] >= x["balance_model"]
+        assert 0 < x["quantization"] <= 1 and x["l2_set_bytes"] > 0
+    # one launch (y-neighbours desynchronised) models more DRAM bytes than rounds
+    one = [x for x in c if x["schedule"] == 1 and x["time_block"] == 2 and x["tile_y"] == 15]
+    rnd = [x for x in c if x["schedule"] == 0 and x["band"] == 0 and x["time_block"] == 2
+           and x["tile_y"] == 15 and x["z_chunk"] == one[0]["z_chunk"]]
+    assert one and rnd and one[0]["model_bytes_per_lup"] > rnd[0]["model_bytes_per_lup"]
+    # depth 3 is SM-bound in the model (calibrated): it must not rank first
+    assert c[0]["time_block"] == 2
+    # slabs and the table layout have no depth 3
+    c2 = P.enumerate_candidates(P.GridDims(256, 256, 256), P.GpuOptions(n_gpus=2))
+    assert {x["time_block"] for x in c2} == {2}

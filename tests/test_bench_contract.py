@@ -96,12 +96,13 @@ def _bench_module():
 
 
 def test_roofline_helper_keys_traffic_by_kernel_and_grid():
-    """Host logic only: the roofline of a TBLOCK launch (two iterations) uses the
-    algorithmic 832 B per cell, reports ncu traffic only for a captured grid."""
+    """Host logic only: the roofline of a TBLOCK pass (two iterations; one launch
+    per round of CTAs) uses the algorithmic 832 B per cell, reports ncu traffic
+    only for a captured grid; a depth-3 pass is three iterations."""
     import paper_1510_05218_b200 as P
     B = _bench_module()
     dims = P.GridDims(256, 256, 256)
-    r = B._roofline(P, dims, P.ENGINE_TBLOCK, dev_secs=0.15, launches=50)
+    r = B._roofline(P, dims, P.ENGINE_TBLOCK, dev_secs=0.15, launches=150, iters_total=100)
     cells = 256 ** 3
     assert r["algorithmic_bytes_per_launch"] == 832.0 * cells
     assert abs(r["achieved"] - 832.0 * cells / (0.15 / 50) / 1e9) < 0.1
@@ -112,10 +113,20 @@ def test_roofline_helper_keys_traffic_by_kernel_and_grid():
         assert r["traffic"] == t["k_tblock_tm<15,6>@256x256x256"]
         assert abs(r["traffic_bytes_per_lup"] - r["traffic"] / (2 * cells)) < 0.1
     if "k_tblock_tm<15,6>@512x512x512" in t:
-        big = B._roofline(P, P.GridDims(512, 512, 512), P.ENGINE_TBLOCK, 1.0, 100)
+        big = B._roofline(P, P.GridDims(512, 512, 512), P.ENGINE_TBLOCK, 1.0, 600, iters_total=200)
         assert big["traffic"] == t["k_tblock_tm<15,6>@512x512x512"]
     other = B._roofline(P, P.GridDims(384, 320, 96), P.ENGINE_TBLOCK, 1.0, 100)
     assert other["traffic"] is None and other["traffic_bytes_per_lup"] is None
+
+
+def test_roofline_helper_depth3():
+    import paper_1510_05218_b200 as P
+    B = _bench_module()
+    cells = 128 ** 3
+    r = B._roofline(P, P.GridDims(128, 128, 128), P.ENGINE_TBLOCK, dev_secs=0.3, launches=99,
+                    iters_total=99, depth=3)
+    assert r["kernel"] == "k_tblock3_tm<15,6>" and r["bytes_per_lup_model"] == pytest.approx(832 / 3)
+    assert abs(r["achieved"] - 832.0 * cells / (0.3 / 33) / 1e9) < 0.1
 
 
 def test_clock_sampler_parses_reasons_and_power():

@@ -40,7 +40,9 @@ def _same(a, b):
 
 @pytest.mark.parametrize("shape,L", [((33, 17, 12), 5), ((31, 29, 40), 7), ((70, 13, 37), 16),
                                      ((9, 7, 6), 2), ((40, 26, 9), 64), ((256, 24, 30), 8),
-                                     ((4, 4, 4), 2)])
+                                     ((4, 4, 4), 2),
+                                     # last sub-range of exactly one plane (nz % L == 1)
+                                     ((33, 17, 13), 4), ((20, 9, 9), 8)])
 def test_inplace_matches_oracle(shape, L, monkeypatch):
     s = P.generate_problem(P.GridDims(*shape), P.GEN_RANDOM, seed=5)
     for steps in (2, 3, 6):
@@ -69,3 +71,28 @@ def test_inplace_rejects_slabs_and_table():
     with pytest.raises(P.ConfigError):  # the table layout has no in-place form
         P.run_gpu(P.clone_state(s), 2, P.GpuOptions(engine=P.ENGINE_TBLOCK_INPLACE,
                                                     coeff_layout=P.COEFF_TABLE, n_materials=2))
+
+
+def test_inplace_single_step_runs_split_and_says_so(monkeypatch):
+    """One step has no two-step pass: the split remainder runs, and the report
+    names the engine that ran."""
+    monkeypatch.setenv("THIIM_INPLACE_TB", "4")
+    s = P.generate_problem(P.GridDims(21, 11, 10), P.GEN_RANDOM, seed=3)
+    out = P.clone_state(s)
+    rep = P.run_gpu(out, 1, P.GpuOptions(engine=P.ENGINE_TBLOCK_INPLACE))
+    assert rep.engine == "gpu-split"
+    _same(out, _oracle(s, 1))
+
+
+@pytest.mark.parametrize("L", ["0", "1"])
+def test_inplace_rejects_short_sub_ranges(L, monkeypatch):
+    monkeypatch.setenv("THIIM_INPLACE_TB", L)
+    with pytest.raises(P.ConfigError, match="sub-ranges"):
+        P.GpuEngine(P.GridDims(16, 16, 16), P.GpuOptions(engine=P.ENGINE_TBLOCK_INPLACE))
+
+
+def test_inplace_rejects_the_sanitizer(monkeypatch):
+    monkeypatch.setenv("THIIM_INPLACE_TB", "4")
+    with P.GpuEngine(P.GridDims(16, 16, 16), P.GpuOptions(engine=P.ENGINE_TBLOCK_INPLACE)) as e:
+        with pytest.raises(P.ConfigError):
+            e.set_sanitize(True)
