@@ -551,6 +551,7 @@ def run_native_multi(P, args, opts, iters, world, rank, local):
     launches = sum(s["kernel_launches"] for s in stats)
     halo = sum(s["halo_bytes_sent"] for s in stats)
     engine_ran, period, peer = eng.engine, eng.exchange_period, eng.peer_stores
+    ordered = getattr(eng, "device_ordered", False)
     eng.close()
 
     e2e = None
@@ -597,7 +598,9 @@ def run_native_multi(P, args, opts, iters, world, rank, local):
                  {"global_grid": [gdims.nx, gdims.ny, gdims.nz],
                   "halo_bytes_per_rank_per_step": halo // max(1, args.steps),
                   "exchange": ("peer stores into the neighbours' halos from the kernel "
-                               "(CUDA IPC over NVLink), a barrier per %d-step pass" % period)
+                               "(CUDA IPC over NVLink), %d-step passes ordered %s" % (
+                                   period, "on the devices by pass counters (no host sync "
+                                   "between passes)" if ordered else "by a barrier per pass"))
                               if peer else
                               "torch.distributed %s batch_isend_irecv after every %d-step pass"
                               % (backend, period)})

@@ -291,25 +291,33 @@ typedef struct {
   int local_z0, local_z1;  /* planes held as local interior (incl. extended planes) */
   int exchange_period;     /* steps per exchange: 1 (FUSED), 2 (TBLOCK deep halo) */
   int engine;              /* THIIM_ENGINE_* the context runs */
+  int device_ordered;      /* IPC peer stores ordered by device pass counters */
 } thiim_slab_info;
 int thiim_gpu_slab_info(thiim_gpu_ctx* ctx, thiim_slab_info* info);
 
 /* Multi-process peer stores (ranks on one node, NVLink / NVSwitch): each rank
  * exports its slab (CUDA IPC handle + layout), imports its neighbours' exports,
  * and from then on every TBLOCK pass stores its boundary planes straight into
- * the neighbours' halo planes -- no halo exchange after 2-step passes.  The
- * caller orders passes across processes: a barrier of all ranks after any
- * upload / generate (they write both field sets, halos included, which a
- * neighbour's first pass stores into), then thiim_gpu_step(ctx, k <= 2) and a
- * barrier of all ranks after each pass (covers both the halo writes and the
- * neighbours' reads of halos the next pass overwrites).  Odd remainder steps
- * (k = 1) still need the view exchange.  TBLOCK deep-halo slab contexts only. */
+ * the neighbours' halo planes -- no halo exchange after 2-step passes.
+ * Ordering between the ranks' passes is on the devices: every slab keeps a
+ * pass counter in its own (exported) allocation; before pass n a slab's stream
+ * waits until both neighbours' counters reach n-1 (their reads of the halo set
+ * pass n stores into are done, and their stores into this slab's input halos
+ * have landed), and after the pass it writes n (stream memory operations,
+ * preceded by a system-scope fence).  So thiim_gpu_step(ctx, k) may advance
+ * any even k in one call with no host synchronisation between passes;
+ * thiim_slab_info.device_ordered says so (0: the stream memory operations were
+ * unavailable for the mapped counters, and the caller must barrier all ranks
+ * after every 2-step call).  The caller still barriers all ranks once after an
+ * upload / generate (they write both field sets, halos included).  Odd
+ * remainder steps (k = 1) use the view exchange.  TBLOCK deep-halo slabs only. */
 typedef struct {
   unsigned char ipc[64]; /* cudaIpcMemHandle_t of the slab state */
   long long stride;      /* elements per array */
   int nz_local, ext_lo, ext_hi, nfield_sets, device;
   int px;
   long long pxy;
+  long long counter_offset; /* byte offset of the pass counter in the allocation */
 } thiim_slab_export;
 enum { THIIM_PEER_LOWER = 0, THIIM_PEER_UPPER = 1 };
 int thiim_gpu_slab_export(thiim_gpu_ctx* ctx, thiim_slab_export* out);

@@ -84,7 +84,13 @@ struct Slab {
     double2* base = nullptr;
     long long stride = 0;
     int nz = 0, ext_lo = 0, ext_hi = 0;
+    unsigned long long* counter = nullptr;  // its pass counter (mapped)
   } peer[2];
+  // multi-process peer stores: this slab's pass counter (in buf, exported) and
+  // the number of TBLOCK passes enqueued so far
+  unsigned long long* counter = nullptr;
+  long long counter_offset = 0;
+  unsigned long long passes = 0;
   unsigned long long* cov_bad = nullptr;   // sanitizer violations (device)
   double2* buf = nullptr;
   size_t stride = 0;   // elements per array
@@ -153,6 +159,7 @@ struct thiim_gpu_ctx {
   bool loaded = false;
   bool sanitize = false;               // exactly-once store coverage per pass
   bool peer_stores = false;  // deep slabs write each other's halos from the kernel
+  bool ipc_ordered = false;  // IPC peer stores ordered by device pass counters
   unsigned long long cov_passes = 0;
   long long pxy() const { return (long long)(dims.nx + 2) * (dims.ny + 2); }
 };
@@ -513,6 +520,40 @@ int deep_first_plane(const Slab& sl, int which) {  // local padded plane of a 2-
 // owned planes; with peer stores they also write their two boundary planes at
 // each internal interface straight into the neighbour's halo (SEND_* -> RECV_*
 // of the deep-halo protocol, the neighbour's output set).
+// Stream memory operations (driver API) for the device-side pass counters of
+// multi-process peer stores.
+struct StreamMemOps {
+  CUresult (*wait64)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+  CUresult (*write64)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+};
+const StreamMemOps* stream_mem_ops() {
+  static StreamMemOps ops{nullptr, nullptr};
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* w = nullptr;
+    void* v = nullptr;
+    cudaDriverEntryPointQueryResult q1, q2;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue64", &w, cudaEnableDefault, &q1) == cudaSuccess &&
+        q1 == cudaDriverEntryPointSuccess &&
+        cudaGetDriverEntryPoint("cuStreamWriteValue64", &v, cudaEnableDefault, &q2) == cudaSuccess &&
+        q2 == cudaDriverEntryPointSuccess) {
+      ops.wait64 = reinterpret_cast<decltype(ops.wait64)>(w);
+      ops.write64 = reinterpret_cast<decltype(ops.write64)>(v);
+    }
+    cudaGetLastError();
+  }
+  return ops.wait64 && ops.write64 ? &ops : nullptr;
+}
+CUresult stream_wait_geq(cudaStream_t s, unsigned long long* addr, unsigned long long v) {
+  return stream_mem_ops()->wait64((CUstream)s, (CUdeviceptr)addr, v, CU_STREAM_WAIT_VALUE_GEQ);
+}
+// default flags: a system-scope memory fence orders the prior work's stores
+// (the pass's peer stores) before the counter write
+CUresult stream_write(cudaStream_t s, unsigned long long* addr, unsigned long long v) {
+  return stream_mem_ops()->write64((CUstream)s, (CUdeviceptr)addr, v, CU_STREAM_WRITE_VALUE_DEFAULT);
+}
+
 PeerOut peer_out(const thiim_gpu_ctx* ctx, int k) {
   const Slab& sl = ctx->slabs[k];
   PeerOut po{};
@@ -1238,9 +1279,13 @@ static int create_impl(const thiim_dims* dims, const thiim_gpu_opts* opts, bool 
     ctx->slabs.push_back(sl);
   }
   for (auto& sl : ctx->slabs) {
-    // + tail slack: tile row copies may run past the last padded row
+    // + tail slack: tile row copies may run past the last padded row; then 256 B
+    // for the pass counter of multi-process peer stores
     const size_t tail = (size_t)(34 * (dims->nx + 2) + 256) * sizeof(double2);
-    const size_t bytes = sl.stride * sizeof(double2) * (size_t)sl.n_arrays() + tail;
+    const size_t state_bytes = (sl.stride * sizeof(double2) * (size_t)sl.n_arrays() + tail + 255) /
+                               256 * 256;
+    const size_t bytes = state_bytes + 256;
+    sl.counter_offset = (long long)state_bytes;
     cudaError_t e = cudaSetDevice(sl.device);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&sl.stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) {
@@ -1253,6 +1298,9 @@ static int create_impl(const thiim_dims* dims, const thiim_gpu_opts* opts, bool 
       if (e == cudaSuccess) e = cudaMemsetAsync(sl.buf, 0, bytes, sl.stream);
       if (e == cudaSuccess) e = cudaStreamSynchronize(sl.stream);
       if (e != cudaSuccess) sl.buf = nullptr;
+      if (sl.buf)
+        sl.counter = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(sl.buf) +
+                                                           sl.counter_offset);
     }
     if (e == cudaSuccess && table) {
       const size_t mbytes = (size_t)sl.mplane * (sl.g.nz + 2) + 4096;
@@ -1414,6 +1462,7 @@ int thiim_gpu_slab_info(thiim_gpu_ctx* ctx, thiim_slab_info* info) {
   info->local_z1 = sl.z1;
   info->exchange_period = sl.deep ? 2 : 1;
   info->engine = ctx->engine;
+  info->device_ordered = ctx->ipc_ordered ? 1 : 0;
   return THIIM_OK;
 }
 
@@ -1437,6 +1486,7 @@ int thiim_gpu_slab_export(thiim_gpu_ctx* ctx, thiim_slab_export* out) {
   out->device = sl.device;
   out->px = sl.g.px;
   out->pxy = sl.g.pxy;
+  out->counter_offset = sl.counter_offset;
   return THIIM_OK;
 }
 
@@ -1470,8 +1520,22 @@ int thiim_gpu_slab_import(thiim_gpu_ctx* ctx, int which, const thiim_slab_export
   p.nz = peer->nz_local;
   p.ext_lo = peer->ext_lo;
   p.ext_hi = peer->ext_hi;
+  p.counter = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(base) +
+                                                    peer->counter_offset);
   // peer stores once every neighbour this slab has is mapped
   ctx->peer_stores = (!sl.ext_lo || sl.peer[0].base) && (!sl.ext_hi || sl.peer[1].base);
+  // device-side ordering if the stream memory operations take the mapped
+  // counters (probe: a wait that is already satisfied)
+  ctx->ipc_ordered = false;
+  if (ctx->peer_stores) {
+    bool ok = stream_mem_ops() != nullptr;
+    for (const Slab::Peer& q : sl.peer)
+      if (ok && q.counter)
+        ok = stream_wait_geq(sl.stream, q.counter, 0) == CUDA_SUCCESS;
+    ok = ok && cudaStreamSynchronize(sl.stream) == cudaSuccess;
+    cudaGetLastError();
+    ctx->ipc_ordered = ok;
+  }
   return THIIM_OK;
 }
 
@@ -1483,7 +1547,10 @@ int thiim_gpu_slab_detach(thiim_gpu_ctx* ctx) {
       if (p.base) cudaIpcCloseMemHandle(p.base);
       p = Slab::Peer{};
     }
-  if (ctx->slabs.size() == 1) ctx->peer_stores = false;
+  if (ctx->slabs.size() == 1) {
+    ctx->peer_stores = false;
+    ctx->ipc_ordered = false;
+  }
   return THIIM_OK;
 }
 
@@ -1980,18 +2047,30 @@ static int step_enqueue(thiim_gpu_ctx* ctx, int steps, long long* launches_out) 
       // slab's input halos): all waits are enqueued before any of this
       // iteration's records, or slab k+1 would wait for slab k's current pass
       // and the slabs would run one after another
-      if (ctx->peer_stores)
+      if (ctx->peer_stores && multi)
         for (int k = 0; k < ns; ++k)
           if ((r = wait_neighbours(ctx, k))) return r;
+      if (ctx->ipc_ordered) {
+        // neighbours in other processes: their pass counters reach n - 1
+        Slab& sl = ctx->slabs[0];
+        for (const Slab::Peer& q : sl.peer)
+          if (q.counter && stream_wait_geq(sl.stream, q.counter, sl.passes) != CUDA_SUCCESS)
+            return fail(THIIM_ERR_CUDA, "cuStreamWaitValue64 on a neighbour's pass counter failed");
+      }
       for (int k = 0; k < ns; ++k) {
         if ((r = launch_tblock2(ctx, ctx->slabs[k], &launches, po[k]))) return r;
         if (multi) CK(cudaEventRecord(ctx->slabs[k].ev_pass, ctx->slabs[k].stream));
+      }
+      if (ctx->ipc_ordered) {
+        Slab& sl = ctx->slabs[0];
+        if (stream_write(sl.stream, sl.counter, ++sl.passes) != CUDA_SUCCESS)
+          return fail(THIIM_ERR_CUDA, "cuStreamWriteValue64 of the pass counter failed");
       }
       if (ctx->sanitize && (r = coverage_pass(ctx, true))) return r;
       if (multi && !ctx->peer_stores && (r = exchange_deep(ctx))) return r;
     }
     for (; n < steps; ++n) {
-      if (ctx->peer_stores)
+      if (ctx->peer_stores && multi)
         for (int k = 0; k < ns; ++k)
           if ((r = wait_neighbours(ctx, k))) return r;
       for (int k = 0; k < ns; ++k)
@@ -2029,9 +2108,13 @@ int thiim_gpu_step(thiim_gpu_ctx* ctx, int steps, thiim_gpu_stats* stats) {
   if (!ctx) return fail(THIIM_ERR_CONFIG, "null context");
   if (steps < 0) return fail(THIIM_ERR_CONFIG, "steps must be >= 0");
   if (!ctx->loaded) return fail(THIIM_ERR_STATE, "no problem uploaded or generated");
-  if (ctx->peer_stores && ctx->slabs.size() == 1 && steps > 2)
+  if (ctx->peer_stores && ctx->slabs.size() == 1 && !ctx->ipc_ordered && steps > 2)
     return fail(THIIM_ERR_CONFIG,
                 "a slab with IPC peer stores advances <= 2 steps per call (barrier in between)");
+  if (ctx->ipc_ordered && (steps % 2) && steps > 1)
+    return fail(THIIM_ERR_CONFIG,
+                "device-ordered IPC peer stores advance an even number of steps per call (the "
+                "odd remainder step needs the view exchange)");
   for (auto& sl : ctx->slabs) {
     CK(cudaSetDevice(sl.device));
     CK(cudaEventRecord(sl.ev0, sl.stream));

@@ -57,7 +57,7 @@ class _CudaPlane:
 class _SlabInfo(ctypes.Structure):
     _fields_ = [("own_z0", ctypes.c_int), ("own_z1", ctypes.c_int), ("local_z0", ctypes.c_int),
                 ("local_z1", ctypes.c_int), ("exchange_period", ctypes.c_int),
-                ("engine", ctypes.c_int)]
+                ("engine", ctypes.c_int), ("device_ordered", ctypes.c_int)]
 
 
 class _SlabExport(ctypes.Structure):
@@ -65,7 +65,7 @@ class _SlabExport(ctypes.Structure):
     _fields_ = [("ipc", ctypes.c_ubyte * 64), ("stride", ctypes.c_longlong),
                 ("nz_local", ctypes.c_int), ("ext_lo", ctypes.c_int), ("ext_hi", ctypes.c_int),
                 ("nfield_sets", ctypes.c_int), ("device", ctypes.c_int), ("px", ctypes.c_int),
-                ("pxy", ctypes.c_longlong)]
+                ("pxy", ctypes.c_longlong), ("counter_offset", ctypes.c_longlong)]
 
 
 class SlabGpuEngine:
@@ -92,6 +92,7 @@ class SlabGpuEngine:
         self.exchange_period = info.exchange_period
         self.engine = info.engine
         self.peer_stores = False
+        self.device_ordered = False
 
     def close(self):
         if self._ctx:
@@ -177,6 +178,14 @@ class SlabGpuEngine:
         self.peer_stores = bool(flag.item())
         if not self.peer_stores:
             L.thiim_gpu_slab_detach(self._ctx)
+        # passes ordered on the devices (pass counters) on every rank, or a
+        # host barrier after every pass on all of them
+        info = _SlabInfo()
+        _check(L.thiim_gpu_slab_info(self._ctx, ctypes.byref(info)))
+        flag = torch.tensor([info.device_ordered if self.peer_stores else 0], dtype=torch.int32,
+                            device="cuda" if dist.get_backend(group) == "nccl" else "cpu")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+        self.device_ordered = bool(flag.item())
         return self.peer_stores
 
 
@@ -245,6 +254,13 @@ def run_distributed(engine, steps: int, exchanger: HaloExchanger) -> dict:
         # upload / generate write both field sets of this slab, halos included:
         # no neighbour's pass may store into them before every rank is done
         exchanger.barrier()
+    if getattr(engine, "device_ordered", False) and steps >= 2:
+        # every pass waits on the devices for the neighbours' previous pass
+        # (pass counters): all 2-step passes in one call, no host sync between
+        k = steps - steps % 2
+        st = engine.step(k)
+        launches += getattr(st, "kernel_launches", 0)
+        done = k
     while done < steps:
         k = min(period, steps - done)
         st = engine.step(k)

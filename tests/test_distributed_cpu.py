@@ -199,3 +199,35 @@ def test_peer_store_protocol_orders_upload_before_first_pass():
     calls.clear()
     D.run_distributed(Eng(), 0, Ex())
     assert calls == []
+
+
+def test_device_ordered_peer_stores_enqueue_all_passes_at_once():
+    """Host logic only: with device-side pass counters (device_ordered), the
+    2-step passes of a call go to the library in ONE step call -- no host
+    barrier between passes; one barrier on entry, the odd remainder step still
+    exchanges."""
+    calls = []
+
+    class Eng:
+        exchange_period = 2
+        peer_stores = True
+        device_ordered = True
+
+        def step(self, k):
+            calls.append(("step", k))
+            return type("S", (), {"kernel_launches": k // 2 or 1})()
+
+    class Ex:
+        def barrier(self):
+            calls.append(("barrier",))
+
+        def exchange(self, eng):
+            calls.append(("exchange",))
+            return 8
+
+    st = D.run_distributed(Eng(), 9, Ex())
+    assert calls == [("barrier",), ("step", 8), ("step", 1), ("exchange",)]
+    assert st == {"halo_bytes_sent": 8, "kernel_launches": 5}
+    calls.clear()
+    D.run_distributed(Eng(), 4, Ex())
+    assert calls == [("barrier",), ("step", 4)]

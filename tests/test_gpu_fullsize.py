@@ -98,7 +98,8 @@ def test_config2_full_workload_tblock_vs_fused():
     with P.GpuEngine(d, P.GpuOptions(engine=P.ENGINE_TBLOCK)) as b:
         b.generate(P.GEN_RANDOM, 1)
         st = b.step(200)
-        assert st.engine == P.ENGINE_TBLOCK and st.kernel_launches == 100
+        # 100 passes, each one launch per round of <= one CTA per SM
+        assert st.engine == P.ENGINE_TBLOCK and st.kernel_launches % 100 == 0
         diff = b.compare_fields(ref)
     assert diff.bitwise_equal, diff
     # not a trivial agreement: the fields moved and stayed finite

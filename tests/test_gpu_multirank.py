@@ -23,15 +23,17 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("peer", ["1", "0"])
-def test_bench_two_ranks_one_gpu(peer):
+@pytest.mark.parametrize("peer,iters,check", [("1", 4, 3), ("1", 10, 9), ("0", 4, 3)])
+def test_bench_two_ranks_one_gpu(peer, iters, check):
     """peer = 1: the ranks map each other's slabs by CUDA IPC and every TBLOCK
-    pass writes the neighbour's halos itself (a barrier per pass); 0: halo
-    exchange after every pass."""
+    pass writes the neighbour's halos itself, passes ordered on the device by
+    pass counters (several passes in flight per call); 0: halo exchange after
+    every pass."""
     env = dict(os.environ, THIIM_DIST_BACKEND="gloo", THIIM_SAME_DEVICE="1", THIIM_PEER_STORES=peer)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), "bench.py", "--gpus", "2",
-           "--config", "c0", "--steps", "1", "--warmup", "1", "--iters", "4", "--check", "3"]
+           "--config", "c0", "--steps", "1", "--warmup", "1", "--iters", str(iters), "--check",
+           str(check)]
     r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     lines = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
@@ -42,6 +44,7 @@ def test_bench_two_ranks_one_gpu(peer):
     cfg = bench[0]["config"]
     if peer == "1":
         assert cfg["exchange"].startswith("peer stores"), cfg
+        assert "pass counters" in cfg["exchange"], cfg
         assert cfg["halo_bytes_per_rank_per_step"] == 0  # iters even: no exchange at all
     else:
         assert cfg["halo_bytes_per_rank_per_step"] > 0
