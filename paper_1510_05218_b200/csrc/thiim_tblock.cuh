@@ -98,7 +98,11 @@ __device__ __forceinline__ void tblock_tm_body(TmSmem<BY, NG>& sm, const Grid& g
       // L2 policies: level-1 fields evict_first (read once), level-1
       // coefficients evict_last (level 2 re-reads them one plane later, their
       // last use: evict_first) -- the best of the measured policy sets
-      const uint64_t pf1 = policy_evict_first(), pc1 = policy_evict_last(), pc2 = pf1;
+#ifndef THIIM_TB_FIELD_POL  // A/B builds only (tools/build_variant.sh): 1 = evict_normal fields
+#define THIIM_TB_FIELD_POL 0
+#endif
+      const uint64_t pf1 = THIIM_TB_FIELD_POL ? policy_evict_normal() : policy_evict_first(),
+                     pc1 = policy_evict_last(), pc2 = policy_evict_first();
       RingProducer<BY, NG, W> P(sm.ring, maps, xb, yb0);
       for (int q = qs; q <= qe; ++q) {
         // level 1 keeps coefficients in L2 for level 2 (their last use)

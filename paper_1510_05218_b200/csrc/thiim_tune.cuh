@@ -202,13 +202,10 @@ int thiim_gpu_tune(const thiim_dims* dims, const thiim_gpu_opts* base, int steps
     for (const auto& t : trials) dup = dup || same(t, c);
     if (!dup) trials.push_back(c);
   }
-  thiim_gpu_candidate def{};
+  thiim_gpu_candidate def{};  // z_chunk 0: the library's own choice
   def.time_block = 2;
   def.tile_y = 15;
-  bool have_def = false;
-  for (const auto& c : trials)
-    have_def = have_def || (c.time_block == 2 && c.tile_y == 15 && c.band == 0 && c.schedule == 0);
-  if (!have_def) trials.push_back(def);
+  trials.push_back(def);
   std::vector<thiim_gpu_trial> done;
   for (const auto& c : trials) {
     thiim_gpu_trial t{};
