@@ -202,10 +202,26 @@ int thiim_gpu_tune(const thiim_dims* dims, const thiim_gpu_opts* base, int steps
     for (const auto& t : trials) dup = dup || same(t, c);
     if (!dup) trials.push_back(c);
   }
-  thiim_gpu_candidate def{};  // z_chunk 0: the library's own choice
-  def.time_block = 2;
-  def.tile_y = 15;
-  trials.push_back(def);
+  {
+    // the library default: depth 2, 15 rows, rounds, auto band, and the z-chunk
+    // count tblock_zchunk picks (modelled with that count, run with z_chunk 0)
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, o.device);
+    cudaGetLastError();
+    const long long nbt = (long long)((dims->nx + 27) / 28) * ((dims->ny + 10) / 11);
+    double best_t = 1e300;
+    int best_c = 1;
+    for (int c = 1; c <= std::max(1, dims->nz / 8); ++c) {
+      const double t = (double)((nbt * c + sms - 1) / sms) * ((dims->nz + c - 1) / c + 2.0);
+      if (t < best_t - 1e-9) {
+        best_t = t;
+        best_c = c;
+      }
+    }
+    thiim_gpu_candidate def = model_candidate(*dims, sms, 0.0, 6536.0, 2, 15, best_c, 0, 0);
+    def.z_chunk = 0;  // run it as the library would
+    trials.push_back(def);
+  }
   std::vector<thiim_gpu_trial> done;
   for (const auto& c : trials) {
     thiim_gpu_trial t{};
