@@ -12,16 +12,6 @@
 // 1's 12 field boxes per plane: (12 x 16 read + 12 x 16 written + 1) / 2
 // = 192.5 B/LUP.  Arithmetic is operation for operation that of the other
 // engines on the same coefficient values, so results are bitwise equal.
-//
-// Exchanges.  A level's H update needs E sums of the x+1 / y+1 neighbours, its
-// E update H sums of the x-1 / y-1 neighbours.  x-neighbours are lanes of the
-// same warp (a warp is one tile row): warp shuffles.  y-neighbours go through
-// shared memory, two components each (Ex, Ez up; Hx, Hz down), in four
-// buffers: E_old sums (level 1's H), H^1 (level 1's E), H^2 (level 2's E) and
-// E^1 -- level 2's H phase reads the E^1 sums of its plane, which level 1
-// computed one iteration earlier and wrote right after that iteration's last
-// barrier.  So an iteration needs three CTA-wide barriers instead of four
-// (r01: the table kernel was barrier-bound, 2.3 stall cycles per instruction).
 #pragma once
 
 #include <cuda.h>
@@ -38,22 +28,11 @@ namespace thiim_gpu {
 template <int BY, int NG>
 struct TbTableSmem {
   Ring<BY, NG> ring;
-  double2 sEo[2][BY][32];  // E_old sums of level 1's plane: Ex, Ez
-  double2 sE1[2][BY][32];  // E^1 sums of the plane level 2 sweeps next: Ex, Ez
-  double2 sH1[2][BY][32];  // H^1 sums: Hx, Hz
-  double2 sH2[2][BY][32];  // H^2 sums: Hx, Hz
+  double2 sE[3][BY][32];
+  double2 sH[3][BY][32];
   double2 tab[kMaxMaterials][28];
   uint32_t tmem_base;
 };
-
-// the x+1 / x-1 neighbour's value of a warp-row quantity (tile edge lanes get
-// their own value, which no update uses)
-__device__ __forceinline__ double2 from_right(double2 v) {
-  return make_double2(__shfl_down_sync(0xffffffffu, v.x, 1), __shfl_down_sync(0xffffffffu, v.y, 1));
-}
-__device__ __forceinline__ double2 from_left(double2 v) {
-  return make_double2(__shfl_up_sync(0xffffffffu, v.x, 1), __shfl_up_sync(0xffffffffu, v.y, 1));
-}
 
 template <int BY, int NG, bool COUNT = false, bool DEEP = false>
 __global__ void __launch_bounds__(32 * (BY + 1), 1)
@@ -145,29 +124,26 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
         pH1y = csum(__ldg(A.f[HYX] + im), __ldg(A.f[HYZ] + im));
       }
     } else {
-      double2 mEx = make_double2(0.0, 0.0), mEy = mEx, mEz = mEx;
       if (inpad) {
         double2 m[6];
 #pragma unroll
         for (int k = 0; k < 6; ++k) m[k] = __ldg(A.f[k] + im);
-        mEx = csum(m[EXY], m[EXZ]);
-        mEy = csum(m[EYX], m[EYZ]);
-        mEz = csum(m[EZX], m[EZY]);
-        sm.sEo[0][ty][tx] = mEx;
-        sm.sEo[1][ty][tx] = mEz;
+        sm.sE[0][ty][tx] = csum(m[EXY], m[EXZ]);
+        sm.sE[1][ty][tx] = csum(m[EYX], m[EYZ]);
+        sm.sE[2][ty][tx] = csum(m[EZX], m[EZY]);
       }
-      const double2 rEy = from_right(mEy), rEz = from_right(mEz);
       named_sync(1, NCOMP);
       if (own1 && inpad) {
         if (interior) {
           const double2* C = sm.tab[mat_at(qs - 1)];
+          const double2 sEx = sm.sE[0][ty][tx], sEy = sm.sE[1][ty][tx], sEz = sm.sE[2][ty][tx];
           const double2 nEx = csum(e[EXY], e[EXZ]), nEy = csum(e[EYX], e[EYZ]);
-          const double2 hxy = upd(__ldg(A.f[HXY] + im), C[HXY], C[12 + HXY], sm.sEo[1][ty + 1][tx], mEz);
+          const double2 hxy = upd(__ldg(A.f[HXY] + im), C[HXY], C[12 + HXY], sm.sE[2][ty + 1][tx], sEz);
           const double2 hxz =
-              upd_src(__ldg(A.f[HXZ] + im), C[HXZ], C[12 + HXZ], nEy, mEy, C[24 + SRC_HXZ]);
-          const double2 hyx = upd(__ldg(A.f[HYX] + im), C[HYX], C[12 + HYX], rEz, mEz);
+              upd_src(__ldg(A.f[HXZ] + im), C[HXZ], C[12 + HXZ], nEy, sEy, C[24 + SRC_HXZ]);
+          const double2 hyx = upd(__ldg(A.f[HYX] + im), C[HYX], C[12 + HYX], sm.sE[2][ty][tx + 1], sEz);
           const double2 hyz =
-              upd_src(__ldg(A.f[HYZ] + im), C[HYZ], C[12 + HYZ], nEx, mEx, C[24 + SRC_HYZ]);
+              upd_src(__ldg(A.f[HYZ] + im), C[HYZ], C[12 + HYZ], nEx, sEx, C[24 + SRC_HYZ]);
           pH1x = csum(hxy, hxz);
           pH1y = csum(hyx, hyz);
         } else {
@@ -175,7 +151,6 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
           pH1y = csum(__ldg(A.f[HYX] + im), __ldg(A.f[HYZ] + im));
         }
       }
-      (void)rEy;
       named_sync(1, NCOMP);
     }
   }
@@ -188,12 +163,8 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
   for (int q = qs; q <= qe; ++q) {
     // level 2 sweeps plane q-1: the plane level 1 swept in the previous iteration
     const int mid2 = mid_last;
-    const bool run1 = q <= q1;
-    // E^1(q) sums (Ex = nE2x, Ez) for level 2's y-neighbours next iteration;
-    // written to sE1 once this iteration's level 2 has read the previous plane's
-    double2 pendEz = make_double2(0.0, 0.0);
     // ================= level 1 at plane q (step n) -> TMEM slot q&1
-    if (run1) {
+    if (q <= q1) {
       const int mid1 = mat_ok(mid1_next);
       mid_last = mid1;
       if (q + 1 <= q1) mid1_next = mat_raw(q + 1);
@@ -219,15 +190,15 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
         nEx = csum(en[EXY], en[EXZ]);
         nEy = csum(en[EYX], en[EYZ]);
       }
-      // own sums from registers; x+1 neighbours by shuffle, y+1 from shared memory
+      // own sums from registers; neighbours read them from shared memory
       const double2 sEx = csum(e[EXY], e[EXZ]), sEy = csum(e[EYX], e[EYZ]),
                     sEz = csum(e[EZX], e[EZY]);
       if (inpad) {
-        sm.sEo[0][ty][tx] = sEx;
-        sm.sEo[1][ty][tx] = sEz;
+        sm.sE[0][ty][tx] = sEx;
+        sm.sE[1][ty][tx] = sEy;
+        sm.sE[2][ty][tx] = sEz;
       }
-      const double2 rEy = from_right(sEy), rEz = from_right(sEz);
-      named_sync(1, NCOMP);  // barrier 1: E_old sums
+      named_sync(1, NCOMP);
       double2 h[6];
       ring_wait(R, rc);
       h[0] = RD(0, BOX_BY);
@@ -238,46 +209,39 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
       h[4] = h45[0];
       h[5] = h45[1];
       if (upd1_x) {
-        h[0] = upd(h[0], C[HXY], C[12 + HXY], sm.sEo[1][ty + 1][tx], sEz);
+        h[0] = upd(h[0], C[HXY], C[12 + HXY], sm.sE[2][ty + 1][tx], sEz);
         h[1] = upd_src(h[1], C[HXZ], C[12 + HXZ], nEy, sEy, C[24 + SRC_HXZ]);
       }
       if (upd1_y) {
-        h[2] = upd(h[2], C[HYX], C[12 + HYX], rEz, sEz);
+        h[2] = upd(h[2], C[HYX], C[12 + HYX], sm.sE[2][ty][tx + 1], sEz);
         h[3] = upd_src(h[3], C[HYZ], C[12 + HYZ], nEx, sEx, C[24 + SRC_HYZ]);
       }
       if (upd1_z) {
-        h[4] = upd(h[4], C[HZX], C[12 + HZX], rEy, sEy);
-        h[5] = upd(h[5], C[HZY], C[12 + HZY], sm.sEo[0][ty + 1][tx], sEx);
+        h[4] = upd(h[4], C[HZX], C[12 + HZX], sm.sE[1][ty][tx + 1], sEy);
+        h[5] = upd(h[5], C[HZY], C[12 + HZY], sm.sE[0][ty + 1][tx], sEx);
       }
       const double2 sHx = csum(h[0], h[1]), sHy = csum(h[2], h[3]), sHz = csum(h[4], h[5]);
       if (own1 || rx1 || ry1) {
-        sm.sH1[0][ty][tx] = sHx;
-        sm.sH1[1][ty][tx] = sHz;
+        sm.sH[0][ty][tx] = sHx;
+        sm.sH[1][ty][tx] = sHy;
+        sm.sH[2][ty][tx] = sHz;
       }
-      const double2 lHy = from_left(sHy), lHz = from_left(sHz);
       tm_st6(tslot + 24, h);  // H^1(q)
-      named_sync(1, NCOMP);  // barrier 2: H^1 sums
+      named_sync(1, NCOMP);
       if (own1 && interior) {
-        e[EXY] = upd(e[EXY], C[EXY], C[12 + EXY], sm.sH1[1][ty - 1][tx], sHz);
+        e[EXY] = upd(e[EXY], C[EXY], C[12 + EXY], sm.sH[2][ty - 1][tx], sHz);
         e[EXZ] = upd_src(e[EXZ], C[EXZ], C[12 + EXZ], pH1y, sHy, C[24 + SRC_EXZ]);
-        e[EYX] = upd(e[EYX], C[EYX], C[12 + EYX], lHz, sHz);
+        e[EYX] = upd(e[EYX], C[EYX], C[12 + EYX], sm.sH[2][ty][tx - 1], sHz);
         e[EYZ] = upd_src(e[EYZ], C[EYZ], C[12 + EYZ], pH1x, sHx, C[24 + SRC_EYZ]);
-        e[EZX] = upd(e[EZX], C[EZX], C[12 + EZX], lHy, sHy);
-        e[EZY] = upd(e[EZY], C[EZY], C[12 + EZY], sm.sH1[0][ty - 1][tx], sHx);
+        e[EZX] = upd(e[EZX], C[EZX], C[12 + EZX], sm.sH[1][ty][tx - 1], sHy);
+        e[EZY] = upd(e[EZY], C[EZY], C[12 + EZY], sm.sH[0][ty - 1][tx], sHx);
       }
       tm_st6(tslot, e);  // E^1(q) (ghost cells pass through unchanged)
       nE2x = csum(e[EXY], e[EXZ]);
       nE2y = csum(e[EYX], e[EYZ]);
-      pendEz = csum(e[EZX], e[EZY]);
       pH1x = sHx;
       pH1y = sHy;
     }
-    auto publish_e1 = [&]() {  // after every read of the previous plane's sE1
-      if (run1 && inpad) {
-        sm.sE1[0][ty][tx] = nE2x;
-        sm.sE1[1][ty][tx] = pendEz;
-      }
-    };
 
     // ================= level 2 at plane r = q-1 (step n+1) -> output set
     const int r = q - LAG;
@@ -322,24 +286,26 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
           h[k] = inpad ? __ldg(A.f[HXY + k] + i) : make_double2(0.0, 0.0);
         }
       }
-      // own sums from registers; x+1 by shuffle; y+1: the E^1 sums level 1
-      // published last iteration (sE1, ordered by this iteration's barrier 1;
-      // past the last level-1 plane there is none: barrier here)
-      if (!run1) named_sync(1, NCOMP);
+      // own sums from registers; neighbours read them from shared memory
       const double2 sEx = csum(e1[EXY], e1[EXZ]), sEy = csum(e1[EYX], e1[EYZ]),
                     sEz = csum(e1[EZX], e1[EZY]);
-      const double2 rEy = from_right(sEy), rEz = from_right(sEz);
+      if (inpad) {
+        sm.sE[0][ty][tx] = sEx;
+        sm.sE[1][ty][tx] = sEy;
+        sm.sE[2][ty][tx] = sEz;
+      }
+      named_sync(1, NCOMP);
       if (upd2_x && plane_ok) {
-        h[0] = upd(h[0], C[HXY], C[12 + HXY], sm.sE1[1][ty + 1][tx], sEz);
+        h[0] = upd(h[0], C[HXY], C[12 + HXY], sm.sE[2][ty + 1][tx], sEz);
         h[1] = upd_src(h[1], C[HXZ], C[12 + HXZ], nEy, sEy, C[24 + SRC_HXZ]);
       }
       if (upd2_y && plane_ok) {
-        h[2] = upd(h[2], C[HYX], C[12 + HYX], rEz, sEz);
+        h[2] = upd(h[2], C[HYX], C[12 + HYX], sm.sE[2][ty][tx + 1], sEz);
         h[3] = upd_src(h[3], C[HYZ], C[12 + HYZ], nEx, sEx, C[24 + SRC_HYZ]);
       }
       if (upd2_z && plane_ok) {
-        h[4] = upd(h[4], C[HZX], C[12 + HZX], rEy, sEy);
-        h[5] = upd(h[5], C[HZY], C[12 + HZY], sm.sE1[0][ty + 1][tx], sEx);
+        h[4] = upd(h[4], C[HZX], C[12 + HZX], sm.sE[1][ty][tx + 1], sEy);
+        h[5] = upd(h[5], C[HZY], C[12 + HZY], sm.sE[0][ty + 1][tx], sEx);
       }
       if (r == z0 - 1) {
         // chunk prologue: only the H_new sums of the plane below the chunk
@@ -347,8 +313,7 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
           pH2x = csum(h[0], h[1]);
           pH2y = csum(h[2], h[3]);
         }
-        named_sync(1, NCOMP);  // sE1 reads done before it is republished
-        publish_e1();
+        named_sync(1, NCOMP);  // sE reads done before the next level-1 writes
         continue;
       }
       if (own2 && interior) {
@@ -357,24 +322,21 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
       }
       const double2 sHx = csum(h[0], h[1]), sHy = csum(h[2], h[3]), sHz = csum(h[4], h[5]);
       if (own2 || rx2 || ry2) {
-        sm.sH2[0][ty][tx] = sHx;
-        sm.sH2[1][ty][tx] = sHz;
+        sm.sH[0][ty][tx] = sHx;
+        sm.sH[1][ty][tx] = sHy;
+        sm.sH[2][ty][tx] = sHz;
       }
-      const double2 lHy = from_left(sHy), lHz = from_left(sHz);
-      named_sync(1, NCOMP);  // barrier 3: H^2 sums (and every sE1 read is done)
-      publish_e1();
+      named_sync(1, NCOMP);
       if (own2 && interior) {
-        put(EXY, upd(e1[EXY], C[EXY], C[12 + EXY], sm.sH2[1][ty - 1][tx], sHz));
+        put(EXY, upd(e1[EXY], C[EXY], C[12 + EXY], sm.sH[2][ty - 1][tx], sHz));
         put(EXZ, upd_src(e1[EXZ], C[EXZ], C[12 + EXZ], pH2y, sHy, C[24 + SRC_EXZ]));
-        put(EYX, upd(e1[EYX], C[EYX], C[12 + EYX], lHz, sHz));
+        put(EYX, upd(e1[EYX], C[EYX], C[12 + EYX], sm.sH[2][ty][tx - 1], sHz));
         put(EYZ, upd_src(e1[EYZ], C[EYZ], C[12 + EYZ], pH2x, sHx, C[24 + SRC_EYZ]));
-        put(EZX, upd(e1[EZX], C[EZX], C[12 + EZX], lHy, sHy));
-        put(EZY, upd(e1[EZY], C[EZY], C[12 + EZY], sm.sH2[0][ty - 1][tx], sHx));
+        put(EZX, upd(e1[EZX], C[EZX], C[12 + EZX], sm.sH[1][ty][tx - 1], sHy));
+        put(EZY, upd(e1[EZY], C[EZY], C[12 + EZY], sm.sH[0][ty - 1][tx], sHx));
       }
       pH2x = sHx;
       pH2y = sHy;
-    } else {
-      publish_e1();  // no level-2 reads this iteration
     }
   }
 #undef RD
