@@ -555,7 +555,19 @@ def run_native_multi(P, args, opts, iters, world, rank, local):
     eng.close()
 
     e2e = None
-    if not args.no_e2e:
+    # every local rank pins its slab's 40 arrays on the host: skip the leg if
+    # the node's RAM does not hold all of them (decided identically by all ranks)
+    rank_bytes = 40 * (GRID[0] + 2) * (GRID[1] + 2) * (GRID[2] + 4) * 16
+    local_ranks = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+    avail = host_available_bytes()
+    e2e_skip = (avail and local_ranks * rank_bytes > 0.7 * avail)
+    if e2e_skip:
+        flag = torch.tensor([1], dtype=torch.int32, device="cuda" if backend == "nccl" else "cpu")
+    else:
+        flag = torch.tensor([0], dtype=torch.int32, device="cuda" if backend == "nccl" else "cpu")
+    dist.all_reduce(flag, op=dist.ReduceOp.MAX)
+    e2e_skip = bool(flag.item())
+    if not args.no_e2e and not e2e_skip:
         eng = make_engine()
         host = eng.local_host_problem(P.GEN_RANDOM, SEED)
         for a in host:
@@ -604,6 +616,9 @@ def run_native_multi(P, args, opts, iters, world, rank, local):
                               if peer else
                               "torch.distributed %s batch_isend_irecv after every %d-step pass"
                               % (backend, period)})
+    if e2e_skip:
+        line["e2e"]["skipped"] = ("host RAM: %d local ranks x %.0f GB of pinned slab arrays > 70%% "
+                                  "of %.0f GB available" % (local_ranks, rank_bytes / 1e9, avail / 1e9))
     dist.destroy_process_group()
     return line if rank == 0 else None
 
