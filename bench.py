@@ -271,8 +271,8 @@ def _roofline(P, dims, engine_ran, dev_secs, launches, table=False, iters_total=
         per_launch_s = dev_secs / max(1, iters_total / depth)
     if engine_ran == P.ENGINE_TBLOCK_INPLACE:
         per_launch_s = dev_secs / max(1, iters_total / 2)
-        bytes_launch = 1216.0 * dims.interior_cells()  # 832 B pass + 384 B copy-back
-        kname = "k_tblock_tm<15,6> sub-ranges + k_copy_interior"
+        bytes_launch = 832.0 * dims.interior_cells()  # one pass, outputs shifted into the gap
+        kname = "k_tblock_tm<15,6> sub-ranges (in place)"
     elif engine_ran == P.ENGINE_SPLIT:
         bytes_launch = 512.0 * dims.interior_cells()  # one half-step sweep: 32 x 16 B per cell
         kname = "k_split_h/k_split_e"

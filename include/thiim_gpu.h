@@ -67,10 +67,12 @@ enum {
   THIIM_ENGINE_SPLIT = 1, /* H sweep + E sweep, in place, z-streamed: 1024 B/LUP */
   THIIM_ENGINE_FUSED = 2, /* one z-streamed H->E sweep per step, ping-pong fields: 832 B/LUP */
   THIIM_ENGINE_TBLOCK = 3, /* temporally blocked fused sweep, `time_block` steps per pass */
-  /* TBLOCK on one field set (state that fits in place but not twice): z
-   * sub-ranges of L planes, outputs into spare planes, interior copy-back;
-   * 608 B/LUP.  One whole-z slab; AUTO picks it over SPLIT when >= 8 spare
-   * planes fit.  THIIM_INPLACE_TB=L (env) sets L, 0 disables it under AUTO. */
+  /* TBLOCK on one field set (state that fits in place but not twice): every
+   * field array gets a gap of L + 2 planes; a pass sweeps z sub-ranges of L
+   * planes and stores their outputs L + 2 planes away, alternately up and
+   * down, so nothing is copied back: 416 B/LUP.  One whole-z slab; AUTO picks
+   * it over SPLIT when >= 8 gap planes fit.  THIIM_INPLACE_TB=L (env) sets L,
+   * 0 disables it under AUTO. */
   THIIM_ENGINE_TBLOCK_INPLACE = 4
 };
 

@@ -118,18 +118,31 @@ struct Slab {
   bool maps_seg_ok[6][2] = {};
 
   // TBLOCK in place (THIIM_ENGINE_TBLOCK_INPLACE, one whole-z slab, no second
-  // field set): spare output planes of one z sub-range (12 x ip_L padded
-  // planes) and a two-plane tail per field (see launch_tblock_inplace)
+  // field set): sub-range length; the field arrays carry a gap of ip_L + 2
+  // planes (fstride, see launch_tblock_inplace)
   int ip_L = 0;
-  double2* ip_buf = nullptr;
   // sub-range views only: where the TBLOCK pass stores its outputs (field k at
   // fo_base + k * fo_stride - fo_shift) instead of the other field set
   double2* fo_base = nullptr;
   long long fo_stride = 0, fo_shift = 0;
 
-  double2* field(int set, int k) const { return buf + (size_t)(set * 12 + k) * stride; }
+  // TBLOCK in place (r02): the field arrays get their own stride (nz + 2 + D
+  // planes: the array plus the D-plane gap it oscillates into); views of it
+  // address the coefficients through their own base (cbuf) and tensor maps
+  size_t fstride = 0;        // elements per field array (0: `stride`)
+  double2* cbuf = nullptr;   // views: first coefficient array, plane-shifted like buf
+  TmaMaps cmaps[6];          // views: coefficient maps (tile heights as `maps`)
+  bool cmaps_ok[6] = {false, false, false, false, false, false};
+  TmaMaps cmaps_seg[6][2];
+  bool cmaps_seg_ok[6][2] = {};
+  int ip_pos = 0;            // field planes start at plane ip_pos of their region (0 / D)
+
+  size_t fs() const { return fstride ? fstride : stride; }
+  double2* field(int set, int k) const { return buf + (size_t)(set * 12 + k) * fs(); }
   double2* coeff(int a) const {  // a in 12..39 (FULL layout only)
-    return table ? nullptr : buf + (size_t)(nfield_sets * 12 + (a - 12)) * stride;
+    if (table) return nullptr;
+    if (cbuf) return cbuf + (size_t)(a - 12) * stride;
+    return buf + (size_t)nfield_sets * 12 * fs() + (size_t)(a - 12) * stride;
   }
   int n_arrays() const { return nfield_sets * 12 + (table ? 0 : 28); }
   double2* array(int a) const { return a < 12 ? field(cur, a) : coeff(a); }
@@ -356,15 +369,28 @@ __global__ void k_selftest_cdiv(int n, const double* in, double* out) {
 struct Planes12 {
   double2* p[12];
 };
-__global__ void k_copy_interior(Planes12 dst, Planes12 src, int nplanes, int nx, int ny,
-                                long long px, long long pxy) {
-  // grid: x = rows of one plane (grid-stride), y = plane, z = field; no divisions
+// The x / y ghost ring of `nplanes` consecutive padded planes of the 12 fields,
+// src -> dst (TBLOCK in place: the sweep stores interior cells only, and the
+// ring -- input data, never updated -- must follow the planes it belongs to).
+// grid: x = ring segments (grid-stride), y = plane, z = field
+__global__ void k_copy_ring(Planes12 dst, Planes12 src, int nplanes, int nx, int ny, long long px,
+                            long long pxy) {
   const int k = blockIdx.z, z = blockIdx.y;
-  double2* __restrict__ d = dst.p[k] + (long long)z * pxy + px + 1;
-  const double2* __restrict__ sp = src.p[k] + (long long)z * pxy + px + 1;
-  for (int y = blockIdx.x; y < ny; y += gridDim.x)
-#pragma unroll 4
-    for (int x = threadIdx.x; x < nx; x += blockDim.x) d[(long long)y * px + x] = sp[(long long)y * px + x];
+  double2* __restrict__ d = dst.p[k] + (long long)z * pxy;
+  const double2* __restrict__ sp = src.p[k] + (long long)z * pxy;
+  const long long last = (long long)(ny + 1) * px;
+  const int ncell = 2 * (int)px + 2 * ny;  // rows y = -1, ny; columns x = -1, nx
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ncell; c += gridDim.x * blockDim.x) {
+    long long i;
+    if (c < px) i = c;
+    else if (c < 2 * px) i = last + (c - px);
+    else {
+      const int r = c - 2 * (int)px;  // 0 .. 2 ny - 1
+      const int y = 1 + (r >> 1);
+      i = (long long)y * px + ((r & 1) ? nx + 1 : 0);
+    }
+    d[i] = sp[i];
+  }
 }
 
 __global__ void k_coverage(Grid g, unsigned* cnt, long long cstride, int r0, int r1,
@@ -696,6 +722,13 @@ TmaMaps& tmaps(Slab& s, int by, int width = 32) {
   const int w = map_index(by);
   return width == 32 ? s.maps[w] : s.maps_seg[w][width == 16 ? 0 : 1];
 }
+// coefficient maps: the same maps unless the slab is a view with its own
+// coefficient base (TBLOCK in place)
+TmaMaps& ctmaps(Slab& s, int by, int width = 32) {
+  if (!s.cbuf) return tmaps(s, by, width);
+  const int w = map_index(by);
+  return width == 32 ? s.cmaps[w] : s.cmaps_seg[w][width == 16 ? 0 : 1];
+}
 
 // L2 promotion stays off: 256-B promotion inflated DRAM reads by 7%
 int ensure_tmap(Slab& s, int by, int width = 32) {
@@ -707,23 +740,35 @@ int ensure_tmap(Slab& s, int by, int width = 32) {
   if (ok) return THIIM_OK;
   auto fn = get_encode_fn();
   if (!fn) return fail(THIIM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-  const cuuint64_t dims[4] = {(cuuint64_t)(2 * s.g.px), (cuuint64_t)(s.g.pxy / s.g.px),
-                              (cuuint64_t)(s.g.nz + 2), (cuuint64_t)s.n_arrays()};
-  const cuuint64_t strides[3] = {(cuuint64_t)s.g.px * 16, (cuuint64_t)s.g.pxy * 16,
-                                 (cuuint64_t)s.stride * 16};
   int bw[NBOX] = {32, 31, 31, 30, 30, 29, 28, 27, 26};  // BoxGeom
   for (int b = 0; b < NBOX; ++b) bw[b] = std::max(1, bw[b] - (32 - width));
   int bh[NBOX] = {by, by - 1, by - 2, by - 1, by - 2, by - 3, by - 4, by - 5, by - 6};
   for (int b = 0; b < NBOX; ++b) bh[b] += (32 / width - 1) * (by - 4);  // folded: all segments
-  for (int b = 0; b < NBOX; ++b) {
-    const cuuint32_t box[4] = {(cuuint32_t)(2 * bw[b]), (cuuint32_t)bh[b], 1, 1};
-    const cuuint32_t estr[4] = {1, 1, 1, 1};
-    CUresult r = fn(&tmaps(s, by, width).m[b], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, s.buf, dims,
-                    strides, box,
-                    estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                    CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS)
-      return fail(THIIM_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  // one map set over `narr` arrays of `astride` elements from `base`
+  auto encode = [&](TmaMaps& out, void* base, int narr, size_t astride) -> int {
+    const cuuint64_t dims[4] = {(cuuint64_t)(2 * s.g.px), (cuuint64_t)(s.g.pxy / s.g.px),
+                                (cuuint64_t)(s.g.nz + 2), (cuuint64_t)narr};
+    const cuuint64_t strides[3] = {(cuuint64_t)s.g.px * 16, (cuuint64_t)s.g.pxy * 16,
+                                   (cuuint64_t)astride * 16};
+    for (int b = 0; b < NBOX; ++b) {
+      const cuuint32_t box[4] = {(cuuint32_t)(2 * bw[b]), (cuuint32_t)bh[b], 1, 1};
+      const cuuint32_t estr[4] = {1, 1, 1, 1};
+      CUresult r = fn(&out.m[b], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, base, dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                      CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS)
+        return fail(THIIM_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+    }
+    return THIIM_OK;
+  };
+  int r;
+  if (s.cbuf) {  // view with separate field / coefficient strides (TBLOCK in place)
+    if ((r = encode(tmaps(s, by, width), s.buf, 12 * s.nfield_sets, s.fs()))) return r;
+    if ((r = encode(ctmaps(s, by, width), s.cbuf, 28, s.stride))) return r;
+  } else {
+    if (s.fs() != s.stride)
+      return fail(THIIM_ERR_CONFIG, "internal: field stride differs; the sweep needs a view");
+    if ((r = encode(tmaps(s, by, width), s.buf, s.n_arrays(), s.stride))) return r;
   }
   ok = true;
   return THIIM_OK;
@@ -875,8 +920,9 @@ int launch_tblock2_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches, const Pee
   for (long long it0 = 0; it0 < items; it0 += per_round) {
     ord.item0 = (int)it0;
     const unsigned n = (unsigned)std::min<long long>(per_round, items - it0);
-    kern<<<n, block, smem, s.stream>>>(s.g, A, tmaps(s, BY), tmaps(s, BY, wf ? wf : 32), po,
-                                       cur * 12, nf * 12, zc, tiles_x, n_main, ord);
+    kern<<<n, block, smem, s.stream>>>(s.g, A, tmaps(s, BY), tmaps(s, BY, wf ? wf : 32),
+                                       ctmaps(s, BY), ctmaps(s, BY, wf ? wf : 32), po, cur * 12,
+                                       s.cbuf ? 0 : nf * 12, zc, tiles_x, n_main, ord);
     CK(cudaGetLastError());
     ++*launches;
   }
@@ -991,45 +1037,62 @@ int launch_tblock2(thiim_gpu_ctx* ctx, Slab& s, long long* launches, const PeerO
 }
 
 // TBLOCK without a second field set (BASELINE c3 in the reference layout:
-// 40 arrays fit in HBM, the 52 of ping-pong TBLOCK do not).  The interior is
-// swept as z sub-ranges [a, b) of ip_L planes, in order; each is one deep-slab
-// TBLOCK pass (k_tblock_tm, owned-plane stores) over the view of interior
-// planes [a-1, b+1) plus the plane on either side -- exactly a z-slab whose
-// halos hold the neighbours' current values, here the not yet updated state
-// itself -- storing its two-step outputs into spare planes instead of the
-// other field set.  A later sub-range still reads the two planes below its
-// start, so after sub-range k its planes [a, b-2) are copied back at once and
-// [b-2, b) move to a two-plane tail, copied back once sub-range k+1 has run.
-// Traffic per two steps: one TBLOCK pass (832 B/cell + the ~4 planes each view
-// re-reads) and the 384-B interior copy-back of 12 fields.
+// 40 arrays fit in HBM, the 52 of ping-pong TBLOCK do not).  Each field array
+// has a gap of D = L + 2 planes above it (fstride = nz + 2 + D planes); at
+// rest it sits at the bottom of its region (ip_pos = 0).  A pass sweeps z as
+// sub-ranges [a, b) of L planes; each is one deep-slab TBLOCK pass over the view
+// of interior planes [a-1, b+1) plus the plane on either side (a z-slab whose
+// halos hold the neighbours' current values -- here the not yet updated state
+// itself) that stores its two-step outputs D planes away from its inputs:
+//   even passes shift the array UP into the gap, sub-ranges top-down;
+//   odd passes shift it back DOWN, sub-ranges bottom-up.
+// Outputs of sub-range [a, b) land on padded planes [a+1, b] of the new
+// position, which overlap only inputs of sub-ranges already swept (D = L + 2
+// clears the sub-range's own window [a-1, b+2]), so nothing is copied back:
+// 416 B/LUP plus the ~4 planes every view re-reads.  The sweep stores interior
+// cells only, so the ghost ring of each output plane and the two ghost planes
+// follow with small copies.  A call that ends on an odd pass moves the array
+// back once (one copy), so every other entry point sees the canonical layout.
+static int copy_ring(Slab& s, const Planes12& dst, const Planes12& src, int np, long long* launches) {
+  k_copy_ring<<<dim3(8, np, 12), 256, 0, s.stream>>>(dst, src, np, s.g.nx, s.g.ny, s.g.px, s.g.pxy);
+  CK(cudaGetLastError());
+  ++*launches;
+  return THIIM_OK;
+}
+
+static Planes12 field_planes(const Slab& s, int phys) {
+  Planes12 m;
+  for (int k = 0; k < 12; ++k) m.p[k] = s.field(0, k) + (size_t)phys * s.g.pxy;
+  return m;
+}
+
+static int copy_field_planes(Slab& s, int dst_phys, int src_phys, int np) {
+  const size_t bytes = (size_t)np * s.g.pxy * sizeof(double2);
+  for (int k = 0; k < 12; ++k)
+    CK(cudaMemcpyAsync(s.field(0, k) + (size_t)dst_phys * s.g.pxy,
+                       s.field(0, k) + (size_t)src_phys * s.g.pxy, bytes, cudaMemcpyDeviceToDevice,
+                       s.stream));
+  return THIIM_OK;
+}
+
 static int launch_tblock_inplace(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
-  const int nz = s.g.nz, L = s.ip_L;
+  const int nz = s.g.nz, L = s.ip_L, D = L + 2;
   const long long pxy = s.g.pxy;
-  Planes12 spare, tail;
-  for (int k = 0; k < 12; ++k) {
-    spare.p[k] = s.ip_buf + (size_t)k * L * pxy;
-    tail.p[k] = s.ip_buf + ((size_t)12 * L + 2 * k) * pxy;
-  }
-  auto main_at = [&](int z) {  // padded plane of interior plane z, field set 0
-    Planes12 m;
-    for (int k = 0; k < 12; ++k) m.p[k] = s.field(0, k) + (size_t)(z + 1) * pxy;
-    return m;
-  };
-  auto copy = [&](const Planes12& dst, const Planes12& src, int np) -> int {
-    // 12 x np x up to 64 CTAs of whole rows (full occupancy, 4 loads in flight per thread)
-    const int rows = std::min(s.g.ny, 64);
-    k_copy_interior<<<dim3(rows, np, 12), 256, 0, s.stream>>>(dst, src, np, s.g.nx, s.g.ny,
-                                                              s.g.px, pxy);
-    CK(cudaGetLastError());
-    ++*launches;
-    return THIIM_OK;
-  };
+  const int pin = s.ip_pos, pout = pin == 0 ? D : 0;
+  const bool up = pout > pin;
   int r;
-  for (int a = 0; a < nz; a += L) {
+  // the ghost plane on the side the array moves towards goes first (its new
+  // home is in the gap); the other one last (its new home is dead input)
+  if (up && (r = copy_field_planes(s, pout + nz + 1, pin + nz + 1, 1))) return r;
+  if (!up && (r = copy_field_planes(s, pout, pin, 1))) return r;
+  const int nsub = (nz + L - 1) / L;
+  for (int j = 0; j < nsub; ++j) {
+    const int a = (up ? nsub - 1 - j : j) * L;
     const int b = std::min(nz, a + L);
     const int lo = a > 0 ? a - 1 : 0, hi = b < nz ? b + 1 : nz;
-    Slab v = s;  // view: interior planes [lo, hi) of the same allocation
-    v.buf = s.buf + (size_t)lo * pxy;
+    Slab v = s;  // view: interior planes [lo, hi) of the same field region
+    v.buf = s.buf + (size_t)(pin + lo) * pxy;
+    v.cbuf = s.coeff(12) + (size_t)lo * pxy;
     v.g.nz = hi - lo;
     v.g.halo_lo = lo > 0 ? 1 : 0;
     v.deep = true;
@@ -1039,21 +1102,33 @@ static int launch_tblock_inplace(thiim_gpu_ctx* ctx, Slab& s, long long* launche
     for (auto& row : v.maps_seg_ok)
       for (auto& ok : row) ok = false;
     PeerOut po{};
-    po.st0 = a - lo;  // local plane st0 + j -> spare plane j (global a + j)
+    po.st0 = a - lo;  // owned local planes [st0, st1) = global [a, b)
     po.st1 = b - lo;
-    v.fo_base = s.ip_buf;
-    v.fo_stride = (long long)L * pxy;
-    v.fo_shift = (long long)(po.st0 + 1) * pxy;
+    v.fo_base = s.buf + (size_t)(pout + lo) * pxy;  // the same planes at the new position
+    v.fo_stride = (long long)s.fs();
+    v.fo_shift = 0;
     if ((r = launch_tblock2(ctx, v, launches, po))) return r;
-    if (a > 0 && (r = copy(main_at(a - 2), tail, 2))) return r;  // read by this sub-range
-    const int keep = b < nz ? 2 : 0;
-    if (b - a - keep > 0 && (r = copy(main_at(a), spare, b - a - keep))) return r;
-    if (keep) {
-      Planes12 top = spare;
-      for (auto& q : top.p) q += (size_t)(b - a - 2) * pxy;
-      if ((r = copy(tail, top, 2))) return r;
-    }
+    // the ghost ring of the output planes (padded [a+1, b]) follows them
+    if ((r = copy_ring(s, field_planes(s, pout + a + 1), field_planes(s, pin + a + 1), b - a,
+                       launches)))
+      return r;
   }
+  if (up && (r = copy_field_planes(s, pout, pin, 1))) return r;
+  if (!up && (r = copy_field_planes(s, pout + nz + 1, pin + nz + 1, 1))) return r;
+  s.ip_pos = pout;
+  return THIIM_OK;
+}
+
+// back to the canonical position (ip_pos 0) after a call that ended on an odd
+// pass: planes [D, D + nz + 2) -> [0, nz + 2) in ascending chunks of D planes
+// (each chunk's source and destination are disjoint)
+static int inplace_restore(Slab& s) {
+  if (s.ip_pos == 0) return THIIM_OK;
+  const int D = s.ip_pos, np = s.g.nz + 2;
+  int r;
+  for (int p = 0; p < np; p += D)
+    if ((r = copy_field_planes(s, p, p + D, std::min(D, np - p)))) return r;
+  s.ip_pos = 0;
   return THIIM_OK;
 }
 
@@ -1131,8 +1206,9 @@ double thiim_gpu_balance_model(int engine, int time_block) {
   switch (engine) {
     case THIIM_ENGINE_SPLIT: return 1024.0;
     case THIIM_ENGINE_TBLOCK: return 832.0 / (time_block > 0 ? time_block : 2);
-    // one TBLOCK pass + the 12-field interior copy-back per two steps
-    case THIIM_ENGINE_TBLOCK_INPLACE: return (832.0 + 384.0) / 2;
+    // one TBLOCK pass per two steps, outputs shifted into the gap (no
+    // copy-back; the ghost-ring copies add ~4 / nx of the bytes)
+    case THIIM_ENGINE_TBLOCK_INPLACE: return 832.0 / 2;
     // table coefficient layout: 24 fields x 16 B + 1 B id per HBM pass of time_block steps
     case 100 + THIIM_COEFF_TABLE: return 385.0 / (time_block > 0 ? time_block : 1);
     default: return 832.0;
@@ -1278,13 +1354,43 @@ static int create_impl(const thiim_dims* dims, const thiim_gpu_opts* opts, bool 
     sl.stride = ((size_t)(sl.g.nz + 2) * (size_t)pxy + 15) / 16 * 16;
     ctx->slabs.push_back(sl);
   }
+  if ((want_ip || auto_split) && whole_z && !table) {
+    // TBLOCK in place: every field array gets a gap of D = L + 2 planes above it
+    // (launch_tblock_inplace).  THIIM_INPLACE_TB=L forces the sub-range length
+    // (0: plain split); default the most planes free memory holds, <= 64
+    Slab& sl = ctx->slabs[0];
+    const size_t plane = (size_t)pxy * sizeof(double2);
+    const char* env = std::getenv("THIIM_INPLACE_TB");
+    int L = env ? std::atoi(env) : -1;
+    if (L < 0) {
+      const size_t state = sl.stride * sizeof(double2) * 40, margin = (size_t)768 << 20;
+      const size_t freeb = device_available(sl.device);
+      L = freeb > state + margin
+              ? (int)std::min<size_t>(66, (freeb - state - margin) / (12 * plane)) - 2
+              : 0;
+      if (!want_ip && L < 8) L = 0;  // too short to beat split
+    }
+    L = std::min(L, dims->nz);
+    if (want_ip && !(L >= 2 || (L >= 1 && L == dims->nz))) {
+      delete ctx;
+      return fail(env ? THIIM_ERR_CONFIG : THIIM_ERR_SETUP,
+                  env ? "TBLOCK in place needs sub-ranges of >= 2 planes (THIIM_INPLACE_TB=" +
+                            std::to_string(L) + ")"
+                      : std::string("TBLOCK in place: no device memory for the gap planes"));
+    }
+    if (L >= 2 || (L >= 1 && L == dims->nz)) {
+      sl.ip_L = L;
+      sl.fstride = ((size_t)(sl.g.nz + 2 + L + 2) * (size_t)pxy + 15) / 16 * 16;
+    }
+  }
   for (auto& sl : ctx->slabs) {
     // + tail slack: tile row copies may run past the last padded row; then 256 B
     // for the pass counter of multi-process peer stores
     const size_t tail = (size_t)(34 * (dims->nx + 2) + 256) * sizeof(double2);
-    const size_t state_bytes = (sl.stride * sizeof(double2) * (size_t)sl.n_arrays() + tail + 255) /
-                               256 * 256;
-    const size_t bytes = state_bytes + 256;
+    const size_t state_elems =
+        sl.fs() * 12 * (size_t)sl.nfield_sets + (table ? 0 : sl.stride * 28);
+    const size_t state_bytes = (state_elems * sizeof(double2) + tail + 255) / 256 * 256;
+    size_t bytes = state_bytes + 256;
     sl.counter_offset = (long long)state_bytes;
     cudaError_t e = cudaSetDevice(sl.device);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&sl.stream, cudaStreamNonBlocking);
@@ -1295,6 +1401,16 @@ static int create_impl(const thiim_dims* dims, const thiim_gpu_opts* opts, bool 
       sl.ipc_buf = ipc_alloc;
       e = ipc_alloc ? cudaMalloc(reinterpret_cast<void**>(&sl.buf), bytes)
                     : pool_alloc(reinterpret_cast<void**>(&sl.buf), bytes, sl.device, sl.stream);
+      if (e != cudaSuccess && sl.fstride && !want_ip) {
+        // AUTO: no room for the in-place gap after all -> plain split
+        cudaGetLastError();
+        sl.fstride = 0;
+        sl.ip_L = 0;
+        const size_t sb = (sl.stride * 40 * sizeof(double2) + tail + 255) / 256 * 256;
+        bytes = sb + 256;
+        sl.counter_offset = (long long)sb;
+        e = pool_alloc(reinterpret_cast<void**>(&sl.buf), bytes, sl.device, sl.stream);
+      }
       if (e == cudaSuccess) e = cudaMemsetAsync(sl.buf, 0, bytes, sl.stream);
       if (e == cudaSuccess) e = cudaStreamSynchronize(sl.stream);
       if (e != cudaSuccess) sl.buf = nullptr;
@@ -1322,41 +1438,6 @@ static int create_impl(const thiim_dims* dims, const thiim_gpu_opts* opts, bool 
       cudaGetLastError();
       thiim_gpu_destroy(ctx);
       return fail(THIIM_ERR_SETUP, msg);
-    }
-  }
-  if ((want_ip || auto_split) && whole_z && !table) {
-    // spare planes for TBLOCK in place: THIIM_INPLACE_TB=L forces the sub-range
-    // length (0: plain split); default the most planes free memory holds, <= 64
-    Slab& sl = ctx->slabs[0];
-    const size_t plane = (size_t)pxy * sizeof(double2);
-    const char* env = std::getenv("THIIM_INPLACE_TB");
-    int L = env ? std::atoi(env) : -1;
-    if (L < 0) {
-      const size_t freeb = device_available(sl.device), margin = (size_t)512 << 20;
-      L = freeb > margin ? (int)std::min<size_t>(66, (freeb - margin) / (12 * plane)) - 2 : 0;
-      if (!want_ip && L < 8) L = 0;  // too short to beat split
-    }
-    L = std::min(L, dims->nz);
-    if (want_ip && env && !(L >= 2 || (L >= 1 && L == dims->nz))) {
-      thiim_gpu_destroy(ctx);
-      return fail(THIIM_ERR_CONFIG,
-                  "TBLOCK in place needs sub-ranges of >= 2 planes (THIIM_INPLACE_TB=" +
-                      std::to_string(L) + ")");
-    }
-    if (L >= 2 || (L >= 1 && L == dims->nz)) {
-      cudaSetDevice(sl.device);
-      cudaError_t e = pool_alloc(reinterpret_cast<void**>(&sl.ip_buf), (size_t)12 * (L + 2) * plane,
-                                 sl.device, sl.stream);
-      if (e == cudaSuccess) {
-        sl.ip_L = L;
-      } else {
-        cudaGetLastError();
-        sl.ip_buf = nullptr;
-      }
-    }
-    if (want_ip && !sl.ip_L) {
-      thiim_gpu_destroy(ctx);
-      return fail(THIIM_ERR_SETUP, "TBLOCK in place: no device memory for the spare planes");
     }
   }
   if (n > 1) {
@@ -1582,7 +1663,6 @@ void thiim_gpu_destroy(thiim_gpu_ctx* ctx) {
     if (sl.stream) cudaStreamSynchronize(sl.stream);
     for (auto& p : sl.peer)
       if (p.base) cudaIpcCloseMemHandle(p.base);
-    if (sl.ip_buf) cudaFreeAsync(sl.ip_buf, sl.stream);
     if (sl.buf && sl.ipc_buf) {
       cudaFree(sl.buf);
     } else if (sl.buf) {  // back to the pool; the sync lets the next context reuse it at once
@@ -2083,6 +2163,7 @@ static int step_enqueue(thiim_gpu_ctx* ctx, int steps, long long* launches_out) 
     // TBLOCK in place: two steps per sub-range sweep, an odd remainder split
     for (; n + 2 <= steps; n += 2)
       if ((r = launch_tblock_inplace(ctx, ctx->slabs[0], &launches))) return r;
+    if ((r = inplace_restore(ctx->slabs[0]))) return r;
   }
   for (; n < steps; ++n) {
     if (ctx->engine == THIIM_ENGINE_SPLIT) {

@@ -26,13 +26,17 @@ struct RingProducer {
   using Gm = BoxGeom<BY, W>;
   static_assert(32 % W == 0, "segment width must divide 32");
   Ring<BY, NG>& R;
-  const TmaMaps& maps;
+  const TmaMaps& maps;   // field arrays
+  const TmaMaps& cmaps;  // coefficient arrays (the same maps unless the field
+                         // arrays have their own plane stride: TBLOCK in place)
   int xb, yb;  // interior coordinates of thread (0,0) (of segment 0)
   int gi = 0;
   uint32_t ph = 0;
 
   __device__ RingProducer(Ring<BY, NG>& r, const TmaMaps& m, int xb_, int yb_)
-      : R(r), maps(m), xb(xb_), yb(yb_) {}
+      : R(r), maps(m), cmaps(m), xb(xb_), yb(yb_) {}
+  __device__ RingProducer(Ring<BY, NG>& r, const TmaMaps& m, const TmaMaps& cm, int xb_, int yb_)
+      : R(r), maps(m), cmaps(cm), xb(xb_), yb(yb_) {}
 
   template <int BYTES>
   __device__ __forceinline__ void begin() {
@@ -62,6 +66,17 @@ struct RingProducer {
     tma_load_4d_hint(&R.buf[gi][k][0], &maps.m[B], 2 * (xb + 1 + Gm::x0(B)), yb + 1 + Gm::y0(B), pz,
                      slot, &R.full[gi], pol);
   }
+  // a coefficient array's box (cmaps)
+  template <int B>
+  __device__ __forceinline__ void cbox(int k, int slot, int pz) {
+    tma_load_4d(&R.buf[gi][k][0], &cmaps.m[B], 2 * (xb + 1 + Gm::x0(B)), yb + 1 + Gm::y0(B), pz, slot,
+                &R.full[gi]);
+  }
+  template <int B>
+  __device__ __forceinline__ void cbox(int k, int slot, int pz, uint64_t pol) {
+    tma_load_4d_hint(&R.buf[gi][k][0], &cmaps.m[B], 2 * (xb + 1 + Gm::x0(B)), yb + 1 + Gm::y0(B), pz,
+                     slot, &R.full[gi], pol);
+  }
 };
 
 // Slot bases: field component c of the current set = fb + c; coefficient
@@ -84,9 +99,9 @@ __device__ __forceinline__ void produce_plane_ct(PR& P, int fb, int cb, int z, u
 #define BOXC(B, k, slot, pz) \
   do {                        \
     if (HINT)                 \
-      P.template box<B>(k, slot, pz, pc); \
+      P.template cbox<B>(k, slot, pz, pc); \
     else                      \
-      P.template box<B>(k, slot, pz);     \
+      P.template cbox<B>(k, slot, pz);     \
   } while (0)
   P.template begin_group<BOX_A, 4>();
   BOXF(BOX_A, 0, fb + EXY, p1);
@@ -163,48 +178,48 @@ template <int BH, int BE, class PR>
 __device__ __forceinline__ void produce_levelj_coef_ct(PR& P, int cb, int r, uint64_t pol) {
   const int p0 = r + 1;
   P.template begin_group<BH, 4>();  // Hxy t c, Hyx t c
-  P.template box<BH>(0, cb + HXY, p0, pol);
-  P.template box<BH>(1, cb + 12 + HXY, p0, pol);
-  P.template box<BH>(2, cb + HYX, p0, pol);
-  P.template box<BH>(3, cb + 12 + HYX, p0, pol);
+  P.template cbox<BH>(0, cb + HXY, p0, pol);
+  P.template cbox<BH>(1, cb + 12 + HXY, p0, pol);
+  P.template cbox<BH>(2, cb + HYX, p0, pol);
+  P.template cbox<BH>(3, cb + 12 + HYX, p0, pol);
   P.end();
   P.template begin_group<BH, 3>();  // Hxz t c src
-  P.template box<BH>(0, cb + HXZ, p0, pol);
-  P.template box<BH>(1, cb + 12 + HXZ, p0, pol);
-  P.template box<BH>(2, cb + 24 + SRC_HXZ, p0, pol);
+  P.template cbox<BH>(0, cb + HXZ, p0, pol);
+  P.template cbox<BH>(1, cb + 12 + HXZ, p0, pol);
+  P.template cbox<BH>(2, cb + 24 + SRC_HXZ, p0, pol);
   P.end();
   P.template begin_group<BH, 3>();  // Hyz t c src
-  P.template box<BH>(0, cb + HYZ, p0, pol);
-  P.template box<BH>(1, cb + 12 + HYZ, p0, pol);
-  P.template box<BH>(2, cb + 24 + SRC_HYZ, p0, pol);
+  P.template cbox<BH>(0, cb + HYZ, p0, pol);
+  P.template cbox<BH>(1, cb + 12 + HYZ, p0, pol);
+  P.template cbox<BH>(2, cb + 24 + SRC_HYZ, p0, pol);
   P.end();
   P.template begin_group<BH, 4>();  // Hzx t c, Hzy t c
-  P.template box<BH>(0, cb + HZX, p0, pol);
-  P.template box<BH>(1, cb + 12 + HZX, p0, pol);
-  P.template box<BH>(2, cb + HZY, p0, pol);
-  P.template box<BH>(3, cb + 12 + HZY, p0, pol);
+  P.template cbox<BH>(0, cb + HZX, p0, pol);
+  P.template cbox<BH>(1, cb + 12 + HZX, p0, pol);
+  P.template cbox<BH>(2, cb + HZY, p0, pol);
+  P.template cbox<BH>(3, cb + 12 + HZY, p0, pol);
   P.end();
   P.template begin_group<BE, 4>();  // Exy t c, Eyx t c
-  P.template box<BE>(0, cb + EXY, p0, pol);
-  P.template box<BE>(1, cb + 12 + EXY, p0, pol);
-  P.template box<BE>(2, cb + EYX, p0, pol);
-  P.template box<BE>(3, cb + 12 + EYX, p0, pol);
+  P.template cbox<BE>(0, cb + EXY, p0, pol);
+  P.template cbox<BE>(1, cb + 12 + EXY, p0, pol);
+  P.template cbox<BE>(2, cb + EYX, p0, pol);
+  P.template cbox<BE>(3, cb + 12 + EYX, p0, pol);
   P.end();
   P.template begin_group<BE, 3>();  // Exz t c src
-  P.template box<BE>(0, cb + EXZ, p0, pol);
-  P.template box<BE>(1, cb + 12 + EXZ, p0, pol);
-  P.template box<BE>(2, cb + 24 + SRC_EXZ, p0, pol);
+  P.template cbox<BE>(0, cb + EXZ, p0, pol);
+  P.template cbox<BE>(1, cb + 12 + EXZ, p0, pol);
+  P.template cbox<BE>(2, cb + 24 + SRC_EXZ, p0, pol);
   P.end();
   P.template begin_group<BE, 3>();  // Eyz t c src
-  P.template box<BE>(0, cb + EYZ, p0, pol);
-  P.template box<BE>(1, cb + 12 + EYZ, p0, pol);
-  P.template box<BE>(2, cb + 24 + SRC_EYZ, p0, pol);
+  P.template cbox<BE>(0, cb + EYZ, p0, pol);
+  P.template cbox<BE>(1, cb + 12 + EYZ, p0, pol);
+  P.template cbox<BE>(2, cb + 24 + SRC_EYZ, p0, pol);
   P.end();
   P.template begin_group<BE, 4>();  // Ezx t c, Ezy t c
-  P.template box<BE>(0, cb + EZX, p0, pol);
-  P.template box<BE>(1, cb + 12 + EZX, p0, pol);
-  P.template box<BE>(2, cb + EZY, p0, pol);
-  P.template box<BE>(3, cb + 12 + EZY, p0, pol);
+  P.template cbox<BE>(0, cb + EZX, p0, pol);
+  P.template cbox<BE>(1, cb + 12 + EZX, p0, pol);
+  P.template cbox<BE>(2, cb + EZY, p0, pol);
+  P.template cbox<BE>(3, cb + 12 + EZY, p0, pol);
   P.end();
 }
 

@@ -65,8 +65,9 @@ struct TmSmem {
 // (256 = 9 x 28 + 4: the tenth tile column ran 24 nearly empty CTAs per chunk).
 template <int BY, int NG, bool COUNT, int W, bool DEEP>
 __device__ __forceinline__ void tblock_tm_body(TmSmem<BY, NG>& sm, const Grid& g, const Arrays& A,
-                                               const TmaMaps& maps, const PeerOut& po, int fb, int cb,
-                                               int zc, int chunk, int xb, int yb0) {
+                                               const TmaMaps& maps, const TmaMaps& cmaps,
+                                               const PeerOut& po, int fb, int cb, int zc, int chunk,
+                                               int xb, int yb0) {
   constexpr int NCOMP = 32 * BY;
   constexpr int TY2 = BY - 4;
   constexpr int LAG = 1;
@@ -94,7 +95,10 @@ __device__ __forceinline__ void tblock_tm_body(TmSmem<BY, NG>& sm, const Grid& g
     // ------------------------------------------------------------ producer
     if (tx == 0) {
 #pragma unroll
-      for (int b = 0; b < NBOX; ++b) tma_prefetch_desc(&maps.m[b]);
+      for (int b = 0; b < NBOX; ++b) {
+        tma_prefetch_desc(&maps.m[b]);
+        tma_prefetch_desc(&cmaps.m[b]);
+      }
       // L2 policies: level-1 fields evict_first (read once), level-1
       // coefficients evict_last (level 2 re-reads them one plane later, their
       // last use: evict_first) -- the best of the measured policy sets
@@ -103,7 +107,7 @@ __device__ __forceinline__ void tblock_tm_body(TmSmem<BY, NG>& sm, const Grid& g
 #endif
       const uint64_t pf1 = THIIM_TB_FIELD_POL ? policy_evict_normal() : policy_evict_first(),
                      pc1 = policy_evict_last(), pc2 = policy_evict_first();
-      RingProducer<BY, NG, W> P(sm.ring, maps, xb, yb0);
+      RingProducer<BY, NG, W> P(sm.ring, maps, cmaps, xb, yb0);
       for (int q = qs; q <= qe; ++q) {
         // level 1 keeps coefficients in L2 for level 2 (their last use)
         if (q <= q1) produce_plane_ct<true>(P, fb, cb, q, pf1, pc1);
@@ -497,7 +501,8 @@ __device__ __forceinline__ int band_tile(int t, int tiles_x, const TileOrder& o)
 template <int BY, int NG, bool COUNT = false, int WF = 0, bool DEEP = false>
 __global__ void __launch_bounds__(32 * (BY + 1), 1)
     k_tblock_tm(Grid g, Arrays A, const __grid_constant__ TmaMaps maps,
-                const __grid_constant__ TmaMaps maps_f, const __grid_constant__ PeerOut po, int fb,
+                const __grid_constant__ TmaMaps maps_f, const __grid_constant__ TmaMaps cmaps,
+                const __grid_constant__ TmaMaps cmaps_f, const __grid_constant__ PeerOut po, int fb,
                 int cb, int zc, int tiles_x, int n_main, TileOrder ord) {
   constexpr int TX2 = 28, TY2 = BY - 4;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -514,10 +519,10 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
   const int t = it;
   if (t < n_main) {  // full tiles
     const int b = band_tile(t, tiles_x, ord);
-    tblock_tm_body<BY, NG, COUNT, 32, DEEP>(sm, g, A, maps, po, fb, cb, zc, chunk,
+    tblock_tm_body<BY, NG, COUNT, 32, DEEP>(sm, g, A, maps, cmaps, po, fb, cb, zc, chunk,
                                             (b % tiles_x) * TX2 - 2, (b / tiles_x) * TY2 - 2);
   } else if constexpr (WF > 0) {  // folded remainder column: 32/WF y-tiles per CTA
-    tblock_tm_body<BY, NG, COUNT, WF, DEEP>(sm, g, A, maps_f, po, fb, cb, zc, chunk,
+    tblock_tm_body<BY, NG, COUNT, WF, DEEP>(sm, g, A, maps_f, cmaps_f, po, fb, cb, zc, chunk,
                                             tiles_x * TX2 - 2, (t - n_main) * (32 / WF) * TY2 - 2);
   }
 }

@@ -1,6 +1,6 @@
 """GPU parity of TBLOCK in place (THIIM_ENGINE_TBLOCK_INPLACE): two-step
-sub-range passes on one field set, outputs through spare planes and an interior
-copy-back (thiim_gpu.cu launch_tblock_inplace) -- the engine AUTO picks when
+sub-range passes on one field set whose outputs shift into a gap of L + 2
+planes, alternately up and down (thiim_gpu.cu launch_tblock_inplace) -- the engine AUTO picks when
 the state fits in HBM once but not twice (BASELINE config 3 in the reference
 layout).  Bitwise against the C oracle (step_reference, kernels.cpp:105-113)
 for sub-range lengths that split z raggedly, L = 2 (every plane through the
@@ -45,7 +45,8 @@ def _same(a, b):
                                      ((33, 17, 13), 4), ((20, 9, 9), 8)])
 def test_inplace_matches_oracle(shape, L, monkeypatch):
     s = P.generate_problem(P.GridDims(*shape), P.GEN_RANDOM, seed=5)
-    for steps in (2, 3, 6):
+    # 1, 2, 3 and 4 passes: odd counts end on the shifted position and move back
+    for steps in (2, 3, 4, 6, 8):
         _same(_inplace(s, steps, L, monkeypatch), _oracle(s, steps))
 
 
