@@ -107,3 +107,22 @@ def test_depth3_rejected_where_unsupported():
         P.GpuEngine(P.GridDims(16, 16, 16), P.GpuOptions(time_block=4))
     with pytest.raises(P.ConfigError):
         P.GpuEngine(P.GridDims(16, 16, 16), P.GpuOptions(time_block=3, n_gpus=2, same_device=1))
+
+
+def test_python_tuner_on_a_small_grid():
+    """paper_1510_05218_b200.tune: model-ranked candidates timed, the winner
+    verified bitwise against the fused engine."""
+    r = P.tune(P.GridDims(40, 30, 24), steps=6, min_seconds=0.02, max_trials=4)
+    assert r.winner_verification == "bitwise-equal vs gpu-fused"
+    assert 4 <= len(r.table) <= 5 and all(t["ok"] and t["mlups"] > 0 for t in r.table)
+    assert {t["time_block"] for t in r.table} == {2, 3}
+    best = max(t["mlups"] for t in r.table)
+    won = [t for t in r.table if t["time_block"] == r.best.time_block and
+           t["tile_y"] == r.best.tile_y and t["z_chunk"] == r.best.z_chunk]
+    assert won and won[0]["mlups"] >= 0.98 * best
+    # the winner runs and is bitwise
+    s = P.generate_problem(P.GridDims(40, 30, 24), P.GEN_RANDOM, 2)
+    want = oracle_run(s, 5)
+    got = P.clone_state(s)
+    P.run_gpu(got, 5, r.best)
+    assert_same(got, want)
