@@ -112,10 +112,12 @@ def test_depth3_rejected_where_unsupported():
 def test_python_tuner_on_a_small_grid():
     """paper_1510_05218_b200.tune: model-ranked candidates timed, the winner
     verified bitwise against the fused engine."""
-    r = P.tune(P.GridDims(40, 30, 24), steps=6, min_seconds=0.02, max_trials=4)
+    r = P.tune(P.GridDims(40, 30, 24), steps=6, min_seconds=0.02, max_trials=6)
     assert r.winner_verification == "bitwise-equal vs gpu-fused"
-    assert 4 <= len(r.table) <= 5 and all(t["ok"] and t["mlups"] > 0 for t in r.table)
-    assert {t["time_block"] for t in r.table} == {2, 3}
+    assert 6 <= len(r.table) <= 7 and all(t["ok"] and t["mlups"] > 0 for t in r.table)
+    # the best candidate of every (time block, tile height) is among the trials
+    assert {(t["time_block"], t["tile_y"]) for t in r.table} >= {(2, 15), (2, 14), (2, 12),
+                                                                    (2, 16), (3, 15)}
     best = max(t["mlups"] for t in r.table)
     won = [t for t in r.table if t["time_block"] == r.best.time_block and
            t["tile_y"] == r.best.tile_y and t["z_chunk"] == r.best.z_chunk]
