@@ -39,7 +39,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 SEED = 1
-# BASELINE.json configs; the driver's default bench line is configs[1]
+# BASELINE.json configs; the default bench line is configs[2] (N=1), configs[4] per rank (N>1)
 CONFIGS = {
     "c0": ((64, 64, 64), 50, 0, "configs[0]: 64^3 grid, 50 THIIM iterations"),
     "c1": ((256, 256, 256), 100, 0, "configs[1]: 256x256x256 grid, 100 THIIM iterations"),
@@ -374,6 +374,12 @@ def _line(P, args, world, dims_rank, engine_ran, dev_secs, launches, e2e, clk, e
     }
 
 
+def _device_bytes(device: int) -> int:
+    """Total memory of the GPU (bytes)."""
+    import torch
+    return torch.cuda.get_device_properties(device).total_memory
+
+
 def host_available_bytes() -> int:
     try:
         with open("/proc/meminfo") as f:
@@ -432,11 +438,12 @@ def run_native_single(P, args, opts, iters):
         pinned = host.arrays + out
         for a in pinned:
             P.lib().thiim_gpu_pin_host(a.ctypes.data, a.nbytes)
-        # the stream overlaps problem i's upload with i-1's sweep only when the
-        # device holds >= 2 contexts (52 arrays each with ping-pong fields);
-        # configs[2]/[4] hold one, so there the serial sequence is the API
+        # the stream overlaps problem i's upload with i-1's sweep when the
+        # device holds >= 2 contexts: ping-pong TBLOCK (52 arrays) up to
+        # configs[1]; at configs[2] it holds one, and the library's batch plan
+        # runs two TBLOCK-in-place contexts (40 arrays + a gap each) instead
         stream = None
-        if 2 * 52 * dims.padded_cells() * 16 < 170e9:
+        if 2 * 40 * dims.padded_cells() * 16 < 0.97 * _device_bytes(opts.device):
             # untimed warm-up; 3 problems so the device pool already holds the
             # three contexts the timed call reuses
             P.run_gpu_batch([host] * 3, iters, opts, outputs=[out] * 3)
@@ -446,6 +453,7 @@ def run_native_single(P, args, opts, iters):
                 "api": "run_gpu_batch (thiim_gpu_run_batch), depth %d, one problem per step"
                        % rep.depth,
                 "depth": rep.depth,
+                "engine": rep.engine,
                 "call_ms": round(1e3 * rep.seconds, 1),
                 "device_span_ms": round(1e3 * rep.device_seconds, 1),
                 "device_ms_per_step": {

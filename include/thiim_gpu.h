@@ -207,9 +207,13 @@ int thiim_gpu_compare_fields(thiim_gpu_ctx* ctx, const thiim_c128* const ref_fie
  * Problems are pipelined over `depth` device contexts (<= 0: 3; fewer when
  * device memory holds fewer, stats->depth says how many ran): problem i
  * uploads while i-1 computes and i-2 downloads, each resource in problem
- * order.  Host buffers should be pinned (thiim_gpu_pin_host) for the copies to
- * overlap.  An output may be shared by several problems but must not overlap
- * another problem's inputs (THIIM_ERR_CONFIG).  Blocking; reference layout,
+ * order.  Under THIIM_ENGINE_AUTO, when device memory holds fewer than two
+ * ping-pong TBLOCK contexts but two or more TBLOCK-in-place ones (one field
+ * set each), the batch runs in place whenever overlapping the copies with the
+ * sweeps wins by the library's model (stats->engine, stats->depth).  Host
+ * buffers should be pinned (thiim_gpu_pin_host) for the copies to overlap.
+ * An output may be shared by several problems but must not overlap another
+ * problem's inputs (THIIM_ERR_CONFIG).  Blocking; reference layout,
  * n_gpus = 1. */
 typedef struct {
   double seconds;          /* host wall clock of the whole call, contexts included */

@@ -1259,6 +1259,10 @@ static cudaError_t pool_alloc(void** p, size_t bytes, int dev, cudaStream_t st) 
 
 // Shared by thiim_gpu_create (n_gpus slabs split like the reference's z_slab,
 // reference_engines.cpp:26-30) and thiim_gpu_create_slab (one explicit slab).
+// Longest TBLOCK-in-place sub-range a context created on this thread may take
+// from free memory (run_batch lowers it so that all its contexts fit).
+thread_local int g_ip_max_L = 128;
+
 static int create_impl(const thiim_dims* dims, const thiim_gpu_opts* opts, bool ipc_alloc,
                        const std::vector<std::pair<int, int>>& ranges, thiim_gpu_ctx** out) {
   g_err.clear();
@@ -1357,7 +1361,9 @@ static int create_impl(const thiim_dims* dims, const thiim_gpu_opts* opts, bool 
   if ((want_ip || auto_split) && whole_z && !table) {
     // TBLOCK in place: every field array gets a gap of D = L + 2 planes above it
     // (launch_tblock_inplace).  THIIM_INPLACE_TB=L forces the sub-range length
-    // (0: plain split); default the most planes free memory holds, <= 64
+    // (0: plain split); default the most planes free memory holds, <= 128
+    // (configs[2]: 64 -> 128 planes, 9.63 -> 9.87 GLUP/s; fewer halo re-reads
+    // and round starts per pass)
     Slab& sl = ctx->slabs[0];
     const size_t plane = (size_t)pxy * sizeof(double2);
     const char* env = std::getenv("THIIM_INPLACE_TB");
@@ -1366,7 +1372,7 @@ static int create_impl(const thiim_dims* dims, const thiim_gpu_opts* opts, bool 
       const size_t state = sl.stride * sizeof(double2) * 40, margin = (size_t)768 << 20;
       const size_t freeb = device_available(sl.device);
       L = freeb > state + margin
-              ? (int)std::min<size_t>(66, (freeb - state - margin) / (12 * plane)) - 2
+              ? (int)std::min<size_t>(g_ip_max_L + 2, (freeb - state - margin) / (12 * plane)) - 2
               : 0;
       if (!want_ip && L < 8) L = 0;  // too short to beat split
     }
@@ -2291,6 +2297,53 @@ int thiim_gpu_download_fields_planes(thiim_gpu_ctx* ctx, thiim_c128* const field
 // chains keep each resource in problem order (H2D copies, sweeps, D2H copies),
 // so the PCIe directions and the SMs each work on one problem at a time, and a
 // context is reused only after its previous problem's download (same stream).
+}  // extern "C"
+
+// The engine and pipeline depth a batch under AUTO runs (thiim_gpu_run_batch).
+// Ping-pong TBLOCK holds 52 arrays per context, TBLOCK in place 40 plus a gap
+// of 12 x (L + 2) planes.  When ping-pong fits fewer than two contexts but
+// in place fits two or more, the stream can overlap problem i's PCIe copies
+// with its neighbours' sweeps -- at in place's cost per sweep (measured 1.13x
+// the ping-pong sweep at configs[2]: 2.77 vs 2.45 s).  Per problem:
+//   one ping-pong context:  up + S + down           (serial)
+//   k >= 2 in place:        max(f S, up + down)     (steady state; f = 1.13 at
+//                                                    sub-ranges of 64 planes)
+// with S = LUPs x 416 B / 4.5 TB/s (the sustained TBLOCK rate) and the copies
+// at 50 GB/s (pinned PCIe Gen5 x16, measured 55 up / 52 down).  Returns
+// THIIM_ENGINE_TBLOCK_INPLACE with *depth and the sub-range cap *ip_L set, or
+// THIIM_ENGINE_AUTO (keep the default).
+static int batch_plan(const thiim_dims* dims, int device, int steps, int n_problems, int* depth,
+                      int* ip_L) {
+  const double pxy = (double)(dims->nx + 2) * (dims->ny + 2);
+  const double arr = pxy * (dims->nz + 2) * 16.0, plane = pxy * 16.0;
+  const double margin = 1.0e9;  // >= create's 768 MB reserve + the tails
+  const double freeb = (double)device_available(device);
+  const int n_pp = (int)std::min<double>(*depth, std::floor(freeb / (52 * arr + margin)));
+  if (n_pp >= 2) return THIIM_ENGINE_AUTO;
+  // in-place contexts with the longest sub-range (<= 128, >= 8) they all fit
+  int k = std::min(*depth, n_problems);
+  for (; k >= 2; --k) {
+    const double per = freeb / k - 40 * arr - margin;
+    const int L = (int)std::min<double>(g_ip_max_L + 2.0, std::floor(per / (12 * plane))) - 2;
+    if (L >= std::min(8, dims->nz)) {
+      *ip_L = L;
+      break;
+    }
+  }
+  if (k < 2) return THIIM_ENGINE_AUTO;
+  const double lups = (double)dims->nx * dims->ny * dims->nz * steps;
+  const double S = lups * 416.0 / 4.5e12, up = 40 * arr / 50e9, down = 12 * arr / 50e9;
+  // in place re-reads ~4 halo planes per sub-range view: 1.13x at L = 64
+  const double f = 1.13 * (*ip_L + 4.0) / *ip_L * (64.0 / 68.0);
+  const double t_serial = n_problems * (up + S + down);
+  const double t_stream = up + (n_problems - 1) * std::max(f * S, up + down) + f * S + down;
+  if (n_pp == 1 && t_stream >= t_serial) return THIIM_ENGINE_AUTO;
+  *depth = k;
+  return THIIM_ENGINE_TBLOCK_INPLACE;
+}
+
+extern "C" {
+
 int thiim_gpu_run_batch(const thiim_dims* dims, const thiim_gpu_opts* opts, int n_problems,
                         const thiim_c128* const* inputs, thiim_c128* const* outputs, int steps,
                         int depth, thiim_gpu_batch_stats* stats) {
@@ -2351,6 +2404,17 @@ int thiim_gpu_run_batch(const thiim_dims* dims, const thiim_gpu_opts* opts, int 
       }
   }
   const auto t0 = std::chrono::steady_clock::now();
+  // AUTO with fewer than two ping-pong contexts in device memory: two or more
+  // TBLOCK-in-place contexts (one field set + a gap) when overlapping the PCIe
+  // copies with the sweeps saves more than in place costs (batch_plan)
+  int ip_cap = 0;
+  if (o.engine == THIIM_ENGINE_AUTO && n_problems >= 2 && depth >= 2) {
+    int dplan = depth;
+    if (batch_plan(dims, o.device, steps, n_problems, &dplan, &ip_cap) == THIIM_ENGINE_TBLOCK_INPLACE) {
+      o.engine = THIIM_ENGINE_TBLOCK_INPLACE;
+      depth = dplan;
+    }
+  }
   std::vector<thiim_gpu_ctx*> ctxs(depth, nullptr);
   // per problem: upload, sweep and download brackets
   std::vector<cudaEvent_t> ev((size_t)n_problems * 6, nullptr);
@@ -2367,8 +2431,11 @@ int thiim_gpu_run_batch(const thiim_dims* dims, const thiim_gpu_opts* opts, int 
     return rc;
   };
   int r;
+  const int saved_L = g_ip_max_L;
+  if (ip_cap > 0) g_ip_max_L = ip_cap;
   for (int d = 0; d < depth; ++d)
     if ((r = thiim_gpu_create(dims, &o, &ctxs[d]))) {
+      g_ip_max_L = saved_L;
       // device memory for fewer contexts: a shallower pipeline (depth 1 still
       // runs, one problem at a time); any other failure is an error
       if (d == 0 || r != THIIM_ERR_SETUP) return bail(r);
@@ -2377,6 +2444,7 @@ int thiim_gpu_run_batch(const thiim_dims* dims, const thiim_gpu_opts* opts, int 
       g_err.clear();
       break;
     }
+  g_ip_max_L = saved_L;
   {
     const cudaError_t e = cudaSetDevice(ctxs[0]->slabs[0].device);
     for (auto& x : ev)
@@ -2385,19 +2453,34 @@ int thiim_gpu_run_batch(const thiim_dims* dims, const thiim_gpu_opts* opts, int 
   }
   long long launches = 0;
   auto E = [&](int i, int k) { return ev[(size_t)i * 6 + k]; };
-  for (int i = 0; i < n_problems; ++i) {
+  auto ck = [&](cudaError_t e) { return e == cudaSuccess ? THIIM_OK : fail(THIIM_ERR_CUDA, cudaGetErrorString(e)); };
+  auto enqueue_upload = [&](int i) {
     thiim_gpu_ctx* ctx = ctxs[i % depth];
     cudaStream_t st = ctx->slabs[0].stream;
-    auto ck = [&](cudaError_t e) { return e == cudaSuccess ? THIIM_OK : fail(THIIM_ERR_CUDA, cudaGetErrorString(e)); };
-    if (i > 0 && (r = ck(cudaStreamWaitEvent(st, E(i - 1, 1), 0)))) return bail(r);
-    if ((r = ck(cudaEventRecord(E(i, 0), st)))) return bail(r);
+    int rr;
+    if (i > 0 && (rr = ck(cudaStreamWaitEvent(st, E(i - 1, 1), 0)))) return rr;
+    if ((rr = ck(cudaEventRecord(E(i, 0), st)))) return rr;
     const thiim_c128* const* in = inputs + (size_t)i * 40;
-    if ((r = upload_arrays(ctx, in, 0, 12, 0, false)) || (r = upload_arrays(ctx, in + 12, 12, 12, 0, false)) ||
-        (r = upload_arrays(ctx, in + 24, 24, 12, 0, false)) ||
-        (r = upload_arrays(ctx, in + 36, 36, 4, 0, false)))
-      return bail(r);
+    if ((rr = upload_arrays(ctx, in, 0, 12, 0, false)) || (rr = upload_arrays(ctx, in + 12, 12, 12, 0, false)) ||
+        (rr = upload_arrays(ctx, in + 24, 24, 12, 0, false)) ||
+        (rr = upload_arrays(ctx, in + 36, 36, 4, 0, false)))
+      return rr;
     ctx->loaded = true;
-    if ((r = ck(cudaEventRecord(E(i, 1), st)))) return bail(r);
+    return ck(cudaEventRecord(E(i, 1), st));
+  };
+  // Enqueue order: the uploads of the next depth-1 problems (other contexts)
+  // go in BEFORE problem i's sweep.  A sweep is thousands of launches and the
+  // host blocks in cudaLaunchKernel once the launch queue is full -- until the
+  // sweeps ahead of it have nearly finished -- so an upload enqueued after a
+  // sweep would start only at that sweep's end instead of beside it.  (With
+  // one context every phase shares one stream and keeps problem order.)
+  const int ahead = depth - 1;
+  int uploaded = 0;  // problems whose upload is enqueued
+  for (int i = 0; i < n_problems; ++i) {
+    while (uploaded < n_problems && uploaded <= i + ahead)
+      if ((r = enqueue_upload(uploaded++))) return bail(r);
+    thiim_gpu_ctx* ctx = ctxs[i % depth];
+    cudaStream_t st = ctx->slabs[0].stream;
     if (i > 0 && (r = ck(cudaStreamWaitEvent(st, E(i - 1, 3), 0)))) return bail(r);
     if ((r = ck(cudaEventRecord(E(i, 2), st)))) return bail(r);
     if ((r = step_enqueue(ctx, steps, &launches))) return bail(r);
