@@ -128,3 +128,39 @@ def test_config3_full_workload_inplace_vs_table():
         diff = b.compare_fields(ref)
     assert diff.bitwise_equal, diff
     assert all(np.isfinite(f[n // 2: n // 2 + 4096].view(np.float64)).all() for f in ref)
+
+
+def test_config2_stream_inplace_vs_device_generated():
+    """The e2e stream at configs[2] (bench.py's e2e leg): run_gpu_batch under
+    AUTO holds two TBLOCK-in-place contexts (ping-pong state fits once) and
+    takes its inputs from host memory (the host generator, 87 GB, pinned);
+    its results equal a device-generated (k_generate at full size) ping-pong
+    TBLOCK run bitwise -- which also pins the device generator to the host one
+    on the full grid."""
+    d = P.GridDims(512, 512, 512)
+    n = d.padded_cells()
+    steps = 6  # three passes per problem: ends on an odd pass (array moved back)
+    if host_ram_gb() < 66 * n * 16 / 1e9 + 8:
+        pytest.skip("needs %.0f GB of host RAM" % (66 * n * 16 / 1e9 + 8))
+    ref = [np.empty(n, np.complex128) for _ in range(12)]
+    with P.GpuEngine(d, P.GpuOptions()) as e:
+        e.generate(P.GEN_RANDOM, 1)
+        st = e.step(steps)
+        assert st.engine == P.ENGINE_TBLOCK
+        e.download_fields(ref)
+    P.release_cached(0)
+    host = P.generate_problem(d, P.GEN_RANDOM, 1)
+    out = [np.zeros(n, np.complex128) for _ in range(12)]
+    L = P.lib()
+    bufs = host.arrays + out
+    for a in bufs:
+        assert L.thiim_gpu_pin_host(a.ctypes.data, a.nbytes) == 0
+    try:
+        rep = P.run_gpu_batch([host, host], steps, outputs=[out, out])
+    finally:
+        for a in bufs:
+            L.thiim_gpu_unpin_host(a.ctypes.data)
+    assert rep.engine == "gpu-tblock-inplace" and rep.depth == 2, rep
+    for k in range(12):
+        assert np.array_equal(out[k].view(np.uint64), ref[k].view(np.uint64)), k
+    assert all(np.isfinite(f[n // 2: n // 2 + 4096].view(np.float64)).all() for f in ref)
