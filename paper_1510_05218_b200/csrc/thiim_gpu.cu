@@ -136,6 +136,7 @@ struct Slab {
   TmaMaps cmaps_seg[6][2];
   bool cmaps_seg_ok[6][2] = {};
   int ip_pos = 0;            // field planes start at plane ip_pos of their region (0 / D)
+  unsigned* ring_nz = nullptr;  // in place: some field ghost-ring cell is non-zero (device)
 
   size_t fs() const { return fstride ? fstride : stride; }
   double2* field(int set, int k) const { return buf + (size_t)(set * 12 + k) * fs(); }
@@ -374,7 +375,8 @@ struct Planes12 {
 // ring -- input data, never updated -- must follow the planes it belongs to).
 // grid: x = ring segments (grid-stride), y = plane, z = field
 __global__ void k_copy_ring(Planes12 dst, Planes12 src, int nplanes, int nx, int ny, long long px,
-                            long long pxy) {
+                            long long pxy, const unsigned* nonzero) {
+  if (*nonzero == 0) return;  // every ring cell of the field region is +0.0: nothing moves
   const int k = blockIdx.z, z = blockIdx.y;
   double2* __restrict__ d = dst.p[k] + (long long)z * pxy;
   const double2* __restrict__ sp = src.p[k] + (long long)z * pxy;
@@ -391,6 +393,34 @@ __global__ void k_copy_ring(Planes12 dst, Planes12 src, int nplanes, int nx, int
     }
     d[i] = sp[i];
   }
+}
+
+// *nonzero |= 1 when any x/y ghost-ring cell of planes [0, nplanes) of the 12
+// field arrays is not +0.0 (bitwise).  TBLOCK in place runs it once per call
+// over the whole field region (array + gap): when every ring cell is zero --
+// the device generators' and the usual uploaded states' Dirichlet halo --
+// moving the rings with the array is a no-op and k_copy_ring exits at once.
+__global__ void k_ring_nonzero(Planes12 src, int nplanes, int nx, int ny, long long px,
+                               long long pxy, unsigned* nonzero) {
+  const int k = blockIdx.z;
+  const long long last = (long long)(ny + 1) * px;
+  const int ncell = 2 * (int)px + 2 * ny;
+  bool nz = false;
+  for (int z = blockIdx.y; z < nplanes; z += gridDim.y) {
+    const double2* __restrict__ sp = src.p[k] + (long long)z * pxy;
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ncell; c += gridDim.x * blockDim.x) {
+      long long i;
+      if (c < px) i = c;
+      else if (c < 2 * px) i = last + (c - px);
+      else {
+        const int r = c - 2 * (int)px;
+        i = (long long)(1 + (r >> 1)) * px + ((r & 1) ? nx + 1 : 0);
+      }
+      const double2 v = sp[i];
+      nz |= (__double_as_longlong(v.x) | __double_as_longlong(v.y)) != 0;
+    }
+  }
+  if (__syncthreads_or(nz) && threadIdx.x == 0) atomicOr(nonzero, 1u);
 }
 
 __global__ void k_coverage(Grid g, unsigned* cnt, long long cstride, int r0, int r1,
@@ -1054,7 +1084,8 @@ int launch_tblock2(thiim_gpu_ctx* ctx, Slab& s, long long* launches, const PeerO
 // follow with small copies.  A call that ends on an odd pass moves the array
 // back once (one copy), so every other entry point sees the canonical layout.
 static int copy_ring(Slab& s, const Planes12& dst, const Planes12& src, int np, long long* launches) {
-  k_copy_ring<<<dim3(8, np, 12), 256, 0, s.stream>>>(dst, src, np, s.g.nx, s.g.ny, s.g.px, s.g.pxy);
+  k_copy_ring<<<dim3(8, np, 12), 256, 0, s.stream>>>(dst, src, np, s.g.nx, s.g.ny, s.g.px, s.g.pxy,
+                                                      s.ring_nz);
   CK(cudaGetLastError());
   ++*launches;
   return THIIM_OK;
@@ -1085,10 +1116,13 @@ static int launch_tblock_inplace(thiim_gpu_ctx* ctx, Slab& s, long long* launche
   // home is in the gap); the other one last (its new home is dead input)
   if (up && (r = copy_field_planes(s, pout + nz + 1, pin + nz + 1, 1))) return r;
   if (!up && (r = copy_field_planes(s, pout, pin, 1))) return r;
-  const int nsub = (nz + L - 1) / L;
+  // sub-ranges of equal length Lq <= L (a gap of D = L + 2 >= Lq + 2 planes
+  // still clears each sub-range's window): 512 planes at L = 170 run as 4 x 128,
+  // not 3 x 170 + 2
+  const int nsub = (nz + L - 1) / L, Lq = (nz + nsub - 1) / nsub;
   for (int j = 0; j < nsub; ++j) {
-    const int a = (up ? nsub - 1 - j : j) * L;
-    const int b = std::min(nz, a + L);
+    const int a = (up ? nsub - 1 - j : j) * Lq;
+    const int b = std::min(nz, a + Lq);
     const int lo = a > 0 ? a - 1 : 0, hi = b < nz ? b + 1 : nz;
     Slab v = s;  // view: interior planes [lo, hi) of the same field region
     v.buf = s.buf + (size_t)(pin + lo) * pxy;
@@ -1677,6 +1711,7 @@ void thiim_gpu_destroy(thiim_gpu_ctx* ctx) {
     }
     if (sl.cnt) cudaFree(sl.cnt);
     if (sl.cov_bad) cudaFree(sl.cov_bad);
+    if (sl.ring_nz) cudaFree(sl.ring_nz);
     if (sl.mat) cudaFree(sl.mat);
     if (sl.tab) cudaFree(sl.tab);
     if (sl.ev0) cudaEventDestroy(sl.ev0);
@@ -2167,6 +2202,16 @@ static int step_enqueue(thiim_gpu_ctx* ctx, int steps, long long* launches_out) 
   }
   if (ctx->engine == THIIM_ENGINE_SPLIT && !multi && ctx->slabs[0].ip_L > 0 && !ctx->sanitize) {
     // TBLOCK in place: two steps per sub-range sweep, an odd remainder split
+    Slab& s0 = ctx->slabs[0];
+    if (n + 2 <= steps) {  // do the ghost rings have to move with the array?
+      if (!s0.ring_nz) CK(cudaMalloc(&s0.ring_nz, sizeof(unsigned)));
+      CK(cudaMemsetAsync(s0.ring_nz, 0, sizeof(unsigned), s0.stream));
+      const int np = (int)(s0.fs() / s0.g.pxy);  // array + gap planes
+      k_ring_nonzero<<<dim3(8, std::min(np, 512), 12), 256, 0, s0.stream>>>(
+          field_planes(s0, 0), np, s0.g.nx, s0.g.ny, s0.g.px, s0.g.pxy, s0.ring_nz);
+      CK(cudaGetLastError());
+      ++launches;
+    }
     for (; n + 2 <= steps; n += 2)
       if ((r = launch_tblock_inplace(ctx, ctx->slabs[0], &launches))) return r;
     if ((r = inplace_restore(ctx->slabs[0]))) return r;
