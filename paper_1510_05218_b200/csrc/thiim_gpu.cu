@@ -989,15 +989,32 @@ int launch_tblock_table_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches, cons
   constexpr int TX2 = 28, TY2 = BY - 4;
   const int tiles_x = (s.g.nx + TX2 - 1) / TX2, tiles_y = (s.g.ny + TY2 - 1) / TY2;
   int zc = ctx->opts.z_chunk;
-  if (zc <= 0) zc = tblock_zchunk(s, (long long)tiles_x * tiles_y);
-  const dim3 grid(tiles_x * tiles_y, 1, (s.g.nz + zc - 1) / zc);
+  const int nbt = tiles_x * tiles_y;
+  if (zc <= 0) zc = tblock_zchunk(s, (long long)nbt);
+  const long long items = (long long)nbt * ((s.g.nz + zc - 1) / zc);
+  // rounds of <= one CTA per SM with the tiles in bands, like k_tblock_tm: the
+  // y-neighbours of a round stream the same planes together and share their
+  // overlapping field rows in L2 (schedule 1: one launch, x-fastest)
+  const int sms = sm_count(s.device);
+  const bool one_launch = ctx->opts.schedule == 1;
+  const long long rounds = one_launch ? 1 : (items + sms - 1) / sms;
+  const long long per_round = (items + rounds - 1) / rounds;
+  TileOrder ord;
+  ord.nbt = nbt;
+  ord.tiles_y = tiles_y;
+  ord.band = one_launch ? tiles_x : tblock_band(tiles_x, (int)std::min<long long>(per_round, sms),
+                                                 ctx->opts.band);
   auto kern = s.deep ? (s.cnt ? k_tblock_table<BY, NG, true, true> : k_tblock_table<BY, NG, false, true>)
                      : (s.cnt ? k_tblock_table<BY, NG, true> : k_tblock_table<BY, NG, false>);
-  kern<<<grid, dim3(32, BY + 1), smem, s.stream>>>(
-      s.g, A, T, tmaps(s, BY), po, s.cur * 12, zc, tiles_x);
-  CK(cudaGetLastError());
+  for (long long it0 = 0; it0 < items; it0 += per_round) {
+    ord.item0 = (int)it0;
+    const unsigned n = (unsigned)std::min<long long>(per_round, items - it0);
+    kern<<<n, dim3(32, BY + 1), smem, s.stream>>>(s.g, A, T, tmaps(s, BY), po, s.cur * 12, zc,
+                                                  tiles_x, ord);
+    CK(cudaGetLastError());
+    ++*launches;
+  }
   s.cur ^= 1;
-  ++*launches;
   return THIIM_OK;
 }
 

@@ -21,6 +21,7 @@
 #include "thiim_fused_table.cuh"
 #include "thiim_producer.cuh"
 #include "thiim_ring.cuh"
+#include "thiim_tblock.cuh"
 #include "thiim_tmem.cuh"
 
 namespace thiim_gpu {
@@ -37,7 +38,7 @@ struct TbTableSmem {
 template <int BY, int NG, bool COUNT = false, bool DEEP = false>
 __global__ void __launch_bounds__(32 * (BY + 1), 1)
     k_tblock_table(Grid g, Arrays A, TableGrid T, const __grid_constant__ TmaMaps maps,
-                   const __grid_constant__ PeerOut po, int fb, int zc, int tiles_x) {
+                   const __grid_constant__ PeerOut po, int fb, int zc, int tiles_x, TileOrder ord) {
   constexpr int NCOMP = 32 * BY;
   constexpr int TX2 = 28, TY2 = BY - 4;
   constexpr int LAG = 1;
@@ -45,9 +46,17 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   TbTableSmem<BY, NG>& sm = *reinterpret_cast<TbTableSmem<BY, NG>*>(smem_raw);
   const int tx = threadIdx.x, ty = threadIdx.y;
-  const int btx = blockIdx.x % tiles_x, bty = blockIdx.x / tiles_x;
-  const int xb = btx * TX2 - 2, yb = bty * TY2 - 2;
-  const int z0 = blockIdx.z * zc;
+  // (tile, z-chunk) of this CTA: rounds of <= one CTA per SM, tiles in
+  // vertical bands (TileOrder, thiim_tblock.cuh); the chunk by repeated
+  // subtraction keeps z0 on the uniform datapath
+  int chunk = 0, it = ord.item0 + (int)blockIdx.x;
+  while (it >= ord.nbt) {
+    it -= ord.nbt;
+    ++chunk;
+  }
+  const int b = band_tile(it, tiles_x, ord);
+  const int xb = (b % tiles_x) * TX2 - 2, yb = (b / tiles_x) * TY2 - 2;
+  const int z0 = chunk * zc;
   const int z1 = min(g.nz, z0 + zc);
   const long long pxy = g.pxy;
   const int qs = max(z0 - 1, 0);
