@@ -1,5 +1,6 @@
 """Race stress for the TMA ring's slot release (thiim_ring.cuh): many random
-shapes / seeds / step counts through the fused, TBLOCK and table engines,
+shapes / seeds / step counts through the fused, TBLOCK, TBLOCK-in-place (random
+sub-range lengths) and table engines,
 each compared bitwise with the C oracle.  Prints one JSON line with the
 number of cases and failures.  Test infrastructure: imports oracle/.
 
@@ -24,7 +25,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--seconds", type=float, default=120)
     ap.add_argument("--seed", type=int, default=7)
-    ap.add_argument("--only", default="", help="comma list of fused,tblock,table,table-fused")
+    ap.add_argument("--only", default="", help="comma list of fused,tblock,inplace,table,table-fused")
     a = ap.parse_args()
     rng = np.random.default_rng(a.seed)
     t_end = time.time() + a.seconds
@@ -39,7 +40,9 @@ def main():
         ref = P.generate_problem(d, kind, seed)
         O.c_step((d.nx, d.ny, d.nz), ref.arrays, steps, threads=8)
         runs = [("fused", P.GpuOptions(engine=P.ENGINE_FUSED)),
-                ("tblock", P.GpuOptions(engine=P.ENGINE_TBLOCK))]
+                ("tblock", P.GpuOptions(engine=P.ENGINE_TBLOCK)),
+                ("inplace", P.GpuOptions(engine=P.ENGINE_TBLOCK_INPLACE))]
+        ip_L = int(rng.integers(2, max(3, d.nz + 1)))  # sub-range length of the in-place run
         if layered:
             runs.append(("table", P.GpuOptions(coeff_layout=P.COEFF_TABLE, n_materials=6,
                                                engine=P.ENGINE_TBLOCK)))
@@ -49,6 +52,10 @@ def main():
             runs = [r for r in runs if r[0] in a.only.split(",")]
         for name, o in runs:
             out = P.generate_problem(d, kind, seed)
+            if name == "inplace":
+                os.environ["THIIM_INPLACE_TB"] = str(ip_L)
+            else:
+                os.environ.pop("THIIM_INPLACE_TB", None)
             with P.GpuEngine(d, o) as e:
                 e.generate(kind, seed)
                 e.step(steps)
