@@ -837,12 +837,13 @@ int launch_fused_tma_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
 // ---- TBLOCK (two steps per pass)
 // z-chunks of a TBLOCK launch: each CTA re-does ~2 planes of level-1/level-2
 // work at its start; minimise waves x (planes + 2) over one CTA per SM
-int tblock_zchunk(const Slab& s, long long cols, double overhead = 2.0) {
+int tblock_zchunk(const Slab& s, long long cols, double overhead = 2.0, int span = 0) {
   const long long slots = sm_count(s.device);
+  const int nz = span > 0 ? span : s.g.nz;  // planes the chunks cover
   double best = 1e300;
   int best_c = 1;
-  for (int c = 1; c <= std::max(1, s.g.nz / 8); ++c) {
-    const int planes = (s.g.nz + c - 1) / c;
+  for (int c = 1; c <= std::max(1, nz / 8); ++c) {
+    const int planes = (nz + c - 1) / c;
     const long long waves = (cols * c + slots - 1) / slots;
     const double t = (double)waves * (planes + overhead);
     if (t < best - 1e-9) {
@@ -850,7 +851,7 @@ int tblock_zchunk(const Slab& s, long long cols, double overhead = 2.0) {
       best_c = c;
     }
   }
-  return (s.g.nz + best_c - 1) / best_c;
+  return (nz + best_c - 1) / best_c;
 }
 
 // slot bases of the 4-D tensor maps: current field set, first coefficient
@@ -913,9 +914,12 @@ int launch_tblock2_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches, const Pee
     }
   }
   const int n_main = tiles_x * tiles_y, nbt = n_main + n_fold;
+  // deep slabs / in-place views without folded tiles: chunks cover planes
+  // [0, st1) (level 2 stops below the top halo plane; k_tblock_tm zhi)
+  const int span = s.deep && wf == 0 ? po.st1 : s.g.nz;
   int zc = ctx->opts.z_chunk;
-  if (zc <= 0) zc = tblock_zchunk(s, (long long)nbt);
-  const int nchunks = (s.g.nz + zc - 1) / zc;
+  if (zc <= 0) zc = tblock_zchunk(s, (long long)nbt, 2.0, span);
+  const int nchunks = (span + zc - 1) / zc;
   const long long items = (long long)nbt * nchunks;
   // CTA schedule: rounds of at most one CTA per SM in band order (default), or
   // (schedule 1) one launch of every item in x-fastest order
@@ -990,8 +994,9 @@ int launch_tblock_table_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches, cons
   const int tiles_x = (s.g.nx + TX2 - 1) / TX2, tiles_y = (s.g.ny + TY2 - 1) / TY2;
   int zc = ctx->opts.z_chunk;
   const int nbt = tiles_x * tiles_y;
-  if (zc <= 0) zc = tblock_zchunk(s, (long long)nbt);
-  const long long items = (long long)nbt * ((s.g.nz + zc - 1) / zc);
+  const int span = s.deep ? po.st1 : s.g.nz;  // deep slabs: up to the last owned plane
+  if (zc <= 0) zc = tblock_zchunk(s, (long long)nbt, 2.0, span);
+  const long long items = (long long)nbt * ((span + zc - 1) / zc);
   // rounds of <= one CTA per SM with the tiles in bands, like k_tblock_tm: the
   // y-neighbours of a round stream the same planes together and share their
   // overlapping field rows in L2 (schedule 1: one launch, x-fastest)

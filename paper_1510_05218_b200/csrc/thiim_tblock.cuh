@@ -67,7 +67,7 @@ template <int BY, int NG, bool COUNT, int W, bool DEEP>
 __device__ __forceinline__ void tblock_tm_body(TmSmem<BY, NG>& sm, const Grid& g, const Arrays& A,
                                                const TmaMaps& maps, const TmaMaps& cmaps,
                                                const PeerOut& po, int fb, int cb, int zc, int chunk,
-                                               int xb, int yb0) {
+                                               int zhi, int xb, int yb0) {
   constexpr int NCOMP = 32 * BY;
   constexpr int TY2 = BY - 4;
   constexpr int LAG = 1;
@@ -76,7 +76,7 @@ __device__ __forceinline__ void tblock_tm_body(TmSmem<BY, NG>& sm, const Grid& g
   const int lx = W == 32 ? tx : tx % W, seg = W == 32 ? 0 : tx / W;
   const int yb = yb0 + seg * TY2;
   const int z0 = chunk * zc;
-  const int z1 = min(g.nz, z0 + zc);
+  const int z1 = min(zhi, z0 + zc);
   const long long pxy = g.pxy;
   const int qs = max(z0 - 1, 0);
   const int q1 = min(z1, g.nz - 1);
@@ -517,12 +517,18 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
     ++chunk;
   }
   const int t = it;
+  // deep-halo slabs and in-place views (without folded tiles) end their
+  // chunks at the last owned plane st1 - 1: the plane above is recomputed by
+  // level 1 as halo, but its level-2 outputs are never stored.  (With folded
+  // tiles the extra bound cost registers -- 12 -> 40 B of spills, -1% -- so
+  // those instances sweep to the top as before; launch_tblock2_t matches.)
+  const int zhi = DEEP && WF == 0 ? po.st1 : g.nz;
   if (t < n_main) {  // full tiles
     const int b = band_tile(t, tiles_x, ord);
-    tblock_tm_body<BY, NG, COUNT, 32, DEEP>(sm, g, A, maps, cmaps, po, fb, cb, zc, chunk,
+    tblock_tm_body<BY, NG, COUNT, 32, DEEP>(sm, g, A, maps, cmaps, po, fb, cb, zc, chunk, zhi,
                                             (b % tiles_x) * TX2 - 2, (b / tiles_x) * TY2 - 2);
   } else if constexpr (WF > 0) {  // folded remainder column: 32/WF y-tiles per CTA
-    tblock_tm_body<BY, NG, COUNT, WF, DEEP>(sm, g, A, maps_f, cmaps_f, po, fb, cb, zc, chunk,
+    tblock_tm_body<BY, NG, COUNT, WF, DEEP>(sm, g, A, maps_f, cmaps_f, po, fb, cb, zc, chunk, zhi,
                                             tiles_x * TX2 - 2, (t - n_main) * (32 / WF) * TY2 - 2);
   }
 }

@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
   const int b = band_tile(it, tiles_x, ord);
   const int xb = (b % tiles_x) * TX2 - 2, yb = (b / tiles_x) * TY2 - 2;
   const int z0 = chunk * zc;
-  const int z1 = min(g.nz, z0 + zc);
+  const int z1 = min(DEEP ? po.st1 : g.nz, z0 + zc);  // deep slabs: level 2 stops at st1 - 1
   const long long pxy = g.pxy;
   const int qs = max(z0 - 1, 0);
   const int q1 = min(z1, g.nz - 1);
