@@ -890,9 +890,11 @@ int launch_tblock2_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches, const Pee
     if constexpr (BY == 15) {
       for (auto f : {k_tblock_tm<BY, NG, false, 8>, k_tblock_tm<BY, NG, true, 8>,
                      k_tblock_tm<BY, NG, false, 16>, k_tblock_tm<BY, NG, true, 16>,
-                     k_tblock_tm<BY, NG, false, 0, true>, k_tblock_tm<BY, NG, true, 0, true>,
-                     k_tblock_tm<BY, NG, false, 8, true>, k_tblock_tm<BY, NG, true, 8, true>,
-                     k_tblock_tm<BY, NG, false, 16, true>, k_tblock_tm<BY, NG, true, 16, true>})
+                     k_tblock_tm<BY, NG, false, 0, 1>, k_tblock_tm<BY, NG, true, 0, 1>,
+                     k_tblock_tm<BY, NG, false, 8, 1>, k_tblock_tm<BY, NG, true, 8, 1>,
+                     k_tblock_tm<BY, NG, false, 16, 1>, k_tblock_tm<BY, NG, true, 16, 1>,
+                     k_tblock_tm<BY, NG, false, 0, 2>, k_tblock_tm<BY, NG, false, 8, 2>,
+                     k_tblock_tm<BY, NG, false, 16, 2>})
         CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, tm_smem));
     }
     setup_done(attr_set, s.device);
@@ -914,9 +916,10 @@ int launch_tblock2_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches, const Pee
     }
   }
   const int n_main = tiles_x * tiles_y, nbt = n_main + n_fold;
-  // deep slabs / in-place views without folded tiles: chunks cover planes
+  // in-place views, and deep slabs without folded tiles: chunks cover planes
   // [0, st1) (level 2 stops below the top halo plane; k_tblock_tm zhi)
-  const int span = s.deep && wf == 0 ? po.st1 : s.g.nz;
+  const bool view = s.deep && s.fo_base != nullptr;
+  const int span = view || (s.deep && wf == 0) ? po.st1 : s.g.nz;
   int zc = ctx->opts.z_chunk;
   if (zc <= 0) zc = tblock_zchunk(s, (long long)nbt, 2.0, span);
   const int nchunks = (span + zc - 1) / zc;
@@ -937,13 +940,17 @@ int launch_tblock2_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches, const Pee
   // uninstrumented instances while the sanitizer is on, so every store must be
   // reported missing
   const bool c = s.cnt != nullptr && !std::getenv("THIIM_SANITIZE_UNCOUNTED");
+  if (view && c) return fail(THIIM_ERR_CONFIG, "the sanitizer does not count in-place views");
   auto kern = c ? k_tblock_tm<BY, NG, true> : k_tblock_tm<BY, NG, false>;
   if constexpr (BY == 15) {
-    if (s.deep) {  // owned-plane stores + peer stores (multi-GPU slabs)
-      kern = wf == 8    ? (c ? k_tblock_tm<BY, NG, true, 8, true> : k_tblock_tm<BY, NG, false, 8, true>)
-             : wf == 16 ? (c ? k_tblock_tm<BY, NG, true, 16, true>
-                             : k_tblock_tm<BY, NG, false, 16, true>)
-                        : (c ? k_tblock_tm<BY, NG, true, 0, true> : k_tblock_tm<BY, NG, false, 0, true>);
+    if (view) {  // in-place sub-range view: owned-plane stores only
+      kern = wf == 8 ? k_tblock_tm<BY, NG, false, 8, 2>
+             : wf == 16 ? k_tblock_tm<BY, NG, false, 16, 2> : k_tblock_tm<BY, NG, false, 0, 2>;
+    } else if (s.deep) {  // owned-plane stores + peer stores (multi-GPU slabs)
+      kern = wf == 8    ? (c ? k_tblock_tm<BY, NG, true, 8, 1> : k_tblock_tm<BY, NG, false, 8, 1>)
+             : wf == 16 ? (c ? k_tblock_tm<BY, NG, true, 16, 1>
+                             : k_tblock_tm<BY, NG, false, 16, 1>)
+                        : (c ? k_tblock_tm<BY, NG, true, 0, 1> : k_tblock_tm<BY, NG, false, 0, 1>);
     } else {
       if (wf == 8) kern = c ? k_tblock_tm<BY, NG, true, 8> : k_tblock_tm<BY, NG, false, 8>;
       if (wf == 16) kern = c ? k_tblock_tm<BY, NG, true, 16> : k_tblock_tm<BY, NG, false, 16>;

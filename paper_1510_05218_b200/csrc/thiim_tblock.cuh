@@ -63,7 +63,7 @@ struct TmSmem {
 // tile, stacked in y from yb0 -- the same sweep on narrow tiles, so a remainder
 // column of <= W-4 grid columns costs 32/W times fewer CTAs than full tiles
 // (256 = 9 x 28 + 4: the tenth tile column ran 24 nearly empty CTAs per chunk).
-template <int BY, int NG, bool COUNT, int W, bool DEEP>
+template <int BY, int NG, bool COUNT, int W, int DEEP>
 __device__ __forceinline__ void tblock_tm_body(TmSmem<BY, NG>& sm, const Grid& g, const Arrays& A,
                                                const TmaMaps& maps, const TmaMaps& cmaps,
                                                const PeerOut& po, int fb, int cb, int zc, int chunk,
@@ -322,10 +322,8 @@ __device__ __forceinline__ void tblock_tm_body(TmSmem<BY, NG>& sm, const Grid& g
       // level-2 outputs: owned planes locally, boundary planes also into the
       // neighbours' halos (multi-GPU contexts, peer memory)
       const bool st_ok = r >= po.st0 && r < po.st1;
-      const bool lo_ok = po.lo[0] != nullptr && r >= po.lo_r0 && r < po.lo_r1;
-      const bool hi_ok = po.hi[0] != nullptr && r >= po.hi_r0 && r < po.hi_r1;
       auto put = [&](int comp, const double2 v) {
-        if constexpr (!DEEP) {  // whole-z context: every plane, locally
+        if constexpr (DEEP == 0) {  // whole-z context: every plane, locally
           st_hint(A.fo[comp] + i, v, first);
           mark<COUNT>(A, comp, i);
         } else {
@@ -333,8 +331,12 @@ __device__ __forceinline__ void tblock_tm_body(TmSmem<BY, NG>& sm, const Grid& g
             st_hint(A.fo[comp] + i, v, first);
             mark<COUNT>(A, comp, i);
           }
-          if (lo_ok) st_hint(po.lo[comp] + i + po.lo_shift, v, first);
-          if (hi_ok) st_hint(po.hi[comp] + i + po.hi_shift, v, first);
+          if constexpr (DEEP == 1) {  // multi-GPU slab: boundary planes into the neighbours
+            const bool lo_ok = po.lo[0] != nullptr && r >= po.lo_r0 && r < po.lo_r1;
+            const bool hi_ok = po.hi[0] != nullptr && r >= po.hi_r0 && r < po.hi_r1;
+            if (lo_ok) st_hint(po.lo[comp] + i + po.lo_shift, v, first);
+            if (hi_ok) st_hint(po.hi[comp] + i + po.hi_shift, v, first);
+          }
         }
       };
       const bool plane_ok = r >= 0;
@@ -498,7 +500,10 @@ __device__ __forceinline__ int band_tile(int t, int tiles_x, const TileOrder& o)
   return row * tiles_x + col;
 }
 
-template <int BY, int NG, bool COUNT = false, int WF = 0, bool DEEP = false>
+// DEEP: 0 whole-z context; 1 deep-halo slab of a multi-GPU context (owned
+// planes [st0, st1) stored locally, boundary planes also into the neighbours'
+// halos); 2 sub-range view of TBLOCK in place (owned planes only, no peers)
+template <int BY, int NG, bool COUNT = false, int WF = 0, int DEEP = 0>
 __global__ void __launch_bounds__(32 * (BY + 1), 1)
     k_tblock_tm(Grid g, Arrays A, const __grid_constant__ TmaMaps maps,
                 const __grid_constant__ TmaMaps maps_f, const __grid_constant__ TmaMaps cmaps,
@@ -517,12 +522,13 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
     ++chunk;
   }
   const int t = it;
-  // deep-halo slabs and in-place views (without folded tiles) end their
-  // chunks at the last owned plane st1 - 1: the plane above is recomputed by
-  // level 1 as halo, but its level-2 outputs are never stored.  (With folded
-  // tiles the extra bound cost registers -- 12 -> 40 B of spills, -1% -- so
-  // those instances sweep to the top as before; launch_tblock2_t matches.)
-  const int zhi = DEEP && WF == 0 ? po.st1 : g.nz;
+  // in-place views and deep-halo slabs (the latter without folded tiles) end
+  // their chunks at the last owned plane st1 - 1: the plane above is
+  // recomputed by level 1 as halo, but its level-2 outputs are never stored.
+  // (In the folded deep-slab instances the extra bound cost registers -- 12 ->
+  // 40 B of spills, -1% -- so those sweep to the top as before;
+  // launch_tblock2_t matches.)
+  const int zhi = DEEP == 2 || (DEEP == 1 && WF == 0) ? po.st1 : g.nz;
   if (t < n_main) {  // full tiles
     const int b = band_tile(t, tiles_x, ord);
     tblock_tm_body<BY, NG, COUNT, 32, DEEP>(sm, g, A, maps, cmaps, po, fb, cb, zc, chunk, zhi,
