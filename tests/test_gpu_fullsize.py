@@ -9,9 +9,10 @@
   (k_generate at full size) and, for the reference, inside oracle/_ref (its
   shim's restated generator) -- 87 GB of reference state + 26 GB of downloaded
   fields in host RAM, compared there with compare_states' field loop.
-* configs[2] over all 200 iterations through a size-independent property: two
-  schedules that share nothing but the arithmetic -- TBLOCK (two steps per
-  pass, TMEM hand-off) and fused (one step per pass) -- agree bitwise.
+* configs[2] over all 200 iterations (and configs[4] over all 100) through a
+  size-independent property: two schedules that share nothing but the
+  arithmetic -- TBLOCK (two steps per pass, TMEM hand-off) and fused (one step
+  per pass) -- agree bitwise.
 * configs[3] in the reference layout (174 GB: TBLOCK in place, sub-ranges with
   spare planes) against the table layout (TBLOCK-table, material ids) over all
   200 iterations: bitwise (the two contexts run one after the other).
@@ -103,6 +104,26 @@ def test_config2_full_workload_tblock_vs_fused():
         diff = b.compare_fields(ref)
     assert diff.bitwise_equal, diff
     # not a trivial agreement: the fields moved and stayed finite
+    assert all(np.isfinite(f[n // 2: n // 2 + 4096].view(np.float64)).all() for f in ref)
+
+
+def test_config4_full_workload_tblock_vs_fused():
+    """configs[4] (1024^2 x 128, 100 iterations -- the per-GPU slab of the
+    weak-scaling runs) over the whole workload: TBLOCK (24 rounds per pass) and
+    the fused one-step sweep agree bitwise."""
+    d = P.GridDims(1024, 1024, 128)
+    n = d.padded_cells()
+    ref = [np.empty(n, np.complex128) for _ in range(12)]
+    with P.GpuEngine(d, P.GpuOptions(engine=P.ENGINE_FUSED)) as a:
+        a.generate(P.GEN_RANDOM, 1)
+        a.step(100)
+        a.download_fields(ref)
+    with P.GpuEngine(d, P.GpuOptions(engine=P.ENGINE_TBLOCK)) as b:
+        b.generate(P.GEN_RANDOM, 1)
+        st = b.step(100)
+        assert st.engine == P.ENGINE_TBLOCK
+        diff = b.compare_fields(ref)
+    assert diff.bitwise_equal, diff
     assert all(np.isfinite(f[n // 2: n // 2 + 4096].view(np.float64)).all() for f in ref)
 
 
