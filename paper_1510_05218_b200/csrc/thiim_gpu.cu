@@ -919,7 +919,7 @@ int launch_tblock2_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches, const Pee
   // in-place views, and deep slabs without folded tiles: chunks cover planes
   // [0, st1) (level 2 stops below the top halo plane; k_tblock_tm zhi)
   const bool view = s.deep && s.fo_base != nullptr;
-  const int span = view || (s.deep && wf == 0) ? po.st1 : s.g.nz;
+  const int span = view ? po.st1 - po.st0 : s.deep && wf == 0 ? po.st1 : s.g.nz;
   int zc = ctx->opts.z_chunk;
   if (zc <= 0) zc = tblock_zchunk(s, (long long)nbt, 2.0, span);
   const int nchunks = (span + zc - 1) / zc;

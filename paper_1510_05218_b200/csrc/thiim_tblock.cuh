@@ -67,7 +67,7 @@ template <int BY, int NG, bool COUNT, int W, int DEEP>
 __device__ __forceinline__ void tblock_tm_body(TmSmem<BY, NG>& sm, const Grid& g, const Arrays& A,
                                                const TmaMaps& maps, const TmaMaps& cmaps,
                                                const PeerOut& po, int fb, int cb, int zc, int chunk,
-                                               int zhi, int xb, int yb0) {
+                                               int zlo, int zhi, int xb, int yb0) {
   constexpr int NCOMP = 32 * BY;
   constexpr int TY2 = BY - 4;
   constexpr int LAG = 1;
@@ -75,7 +75,7 @@ __device__ __forceinline__ void tblock_tm_body(TmSmem<BY, NG>& sm, const Grid& g
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int lx = W == 32 ? tx : tx % W, seg = W == 32 ? 0 : tx / W;
   const int yb = yb0 + seg * TY2;
-  const int z0 = chunk * zc;
+  const int z0 = zlo + chunk * zc;
   const int z1 = min(zhi, z0 + zc);
   const long long pxy = g.pxy;
   const int qs = max(z0 - 1, 0);
@@ -326,6 +326,8 @@ __device__ __forceinline__ void tblock_tm_body(TmSmem<BY, NG>& sm, const Grid& g
         if constexpr (DEEP == 0) {  // whole-z context: every plane, locally
           st_hint(A.fo[comp] + i, v, first);
           mark<COUNT>(A, comp, i);
+        } else if constexpr (DEEP == 2) {  // view: chunks cover only [st0, st1)
+          st_hint(A.fo[comp] + i, v, first);
         } else {
           if (st_ok) {
             st_hint(A.fo[comp] + i, v, first);
@@ -529,12 +531,13 @@ __global__ void __launch_bounds__(32 * (BY + 1), 1)
   // 40 B of spills, -1% -- so those sweep to the top as before;
   // launch_tblock2_t matches.)
   const int zhi = DEEP == 2 || (DEEP == 1 && WF == 0) ? po.st1 : g.nz;
+  const int zlo = DEEP == 2 ? po.st0 : 0;
   if (t < n_main) {  // full tiles
     const int b = band_tile(t, tiles_x, ord);
-    tblock_tm_body<BY, NG, COUNT, 32, DEEP>(sm, g, A, maps, cmaps, po, fb, cb, zc, chunk, zhi,
+    tblock_tm_body<BY, NG, COUNT, 32, DEEP>(sm, g, A, maps, cmaps, po, fb, cb, zc, chunk, zlo, zhi,
                                             (b % tiles_x) * TX2 - 2, (b / tiles_x) * TY2 - 2);
   } else if constexpr (WF > 0) {  // folded remainder column: 32/WF y-tiles per CTA
-    tblock_tm_body<BY, NG, COUNT, WF, DEEP>(sm, g, A, maps_f, cmaps_f, po, fb, cb, zc, chunk, zhi,
+    tblock_tm_body<BY, NG, COUNT, WF, DEEP>(sm, g, A, maps_f, cmaps_f, po, fb, cb, zc, chunk, zlo, zhi,
                                             tiles_x * TX2 - 2, (t - n_main) * (32 / WF) * TY2 - 2);
   }
 }
