@@ -2380,10 +2380,12 @@ int thiim_gpu_download_fields_planes(thiim_gpu_ctx* ctx, thiim_c128* const field
 // with its neighbours' sweeps -- at in place's cost per sweep (measured 1.13x
 // the ping-pong sweep at configs[2]: 2.77 vs 2.45 s).  Per problem:
 //   one ping-pong context:  up + S + down           (serial)
-//   k >= 2 in place:        max(f S, up + down)     (steady state; f = 1.13 at
-//                                                    sub-ranges of 64 planes)
+//   k >= 2 in place:        max(f S, up + down)     (steady state; f = 1.04 at
+//                                                    sub-ranges of 128 planes)
 // with S = LUPs x 416 B / 4.5 TB/s (the sustained TBLOCK rate) and the copies
-// at 50 GB/s (pinned PCIe Gen5 x16, measured 55 up / 52 down).  Returns
+// at 50 GB/s (pinned PCIe Gen5 x16, measured 55 up / 52 down).  (Before the
+// view instances of r02t f was 1.13: in place then lost to serial ping-pong
+// beyond ~1,000 iterations per problem at configs[2]; now beyond ~3,000.)  Returns
 // THIIM_ENGINE_TBLOCK_INPLACE with *depth and the sub-range cap *ip_L set, or
 // THIIM_ENGINE_AUTO (keep the default).
 static int batch_plan(const thiim_dims* dims, int device, int steps, int n_problems, int* depth,
@@ -2407,8 +2409,10 @@ static int batch_plan(const thiim_dims* dims, int device, int steps, int n_probl
   if (k < 2) return THIIM_ENGINE_AUTO;
   const double lups = (double)dims->nx * dims->ny * dims->nz * steps;
   const double S = lups * 416.0 / 4.5e12, up = 40 * arr / 50e9, down = 12 * arr / 50e9;
-  // in place re-reads ~4 halo planes per sub-range view: 1.13x at L = 64
-  const double f = 1.13 * (*ip_L + 4.0) / *ip_L * (64.0 / 68.0);
+  // in place: ~2% slower per plane than a whole-z pass plus the halo plane and
+  // prologue of each sub-range view (measured r02t: 10.58 vs 11.0 GLUP/s at
+  // L = 128, configs[2]; 1.04x)
+  const double f = 1.02 * (*ip_L + 2.0) / *ip_L;
   const double t_serial = n_problems * (up + S + down);
   const double t_stream = up + (n_problems - 1) * std::max(f * S, up + down) + f * S + down;
   if (n_pp == 1 && t_stream >= t_serial) return THIIM_ENGINE_AUTO;
