@@ -152,20 +152,24 @@ def test_batch_auto_runs_in_place_when_ping_pong_fits_once():
     import torch
 
     d = P.GridDims(256, 256, 128)
-    steps = 6  # three passes: ends on an odd pass (array moved back)
     ctx_bytes = d.padded_cells() * 16 * 52
     states = [P.generate_problem(d, k, seed=s) for k, s in ((P.GEN_RANDOM, 31), (P.GEN_LAYERED, 32))]
-    want = [oracle_run(s, steps) for s in states]
-    outs = [[np.zeros_like(a) for a in s.fields] for s in states]
     srcs = [states[0], states[1], states[0]]
+    # 6 steps: three passes, ends on an odd pass (array moved back); 7: plus the
+    # split remainder step
+    want = {steps: [oracle_run(s, steps) for s in states] for steps in (6, 7)}
+    outs = {steps: [[np.zeros_like(a) for a in s.fields] for s in states] for steps in (6, 7)}
     P.release_cached(0)
     free, _ = torch.cuda.mem_get_info(0)
     hog = torch.empty(free - int(1.9 * ctx_bytes), dtype=torch.uint8, device="cuda:0")
     try:
-        rep = P.run_gpu_batch(srcs, steps, outputs=[outs[0], outs[1], outs[0]], depth=3)
+        reps = {steps: P.run_gpu_batch(srcs, steps, outputs=[outs[steps][0], outs[steps][1],
+                                                             outs[steps][0]], depth=3)
+                for steps in (6, 7)}
     finally:
         del hog
         torch.cuda.empty_cache()
-    assert rep.engine == "gpu-tblock-inplace" and rep.depth == 2, rep
-    for o, w in zip(outs, want):
-        assert fields_equal(o, w.fields)
+    for steps, rep in reps.items():
+        assert rep.engine == "gpu-tblock-inplace" and rep.depth == 2, rep
+        for o, w in zip(outs[steps], want[steps]):
+            assert fields_equal(o, w.fields), steps
