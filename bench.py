@@ -563,6 +563,25 @@ def run_native_multi(P, args, opts, iters, world, rank, local):
     ordered = getattr(eng, "device_ordered", False)
     eng.close()
 
+    # the same per-rank workload on one GPU (a whole-z context of the rank's
+    # grid, rank 0 alone, device time): the N=1 point of this config's weak
+    # scaling (the N=1 bench line is configs[2]); the driver computes any
+    # efficiency from it
+    n1 = None
+    if not args.no_n1_base:
+        dist.barrier()
+        if rank == 0:
+            e1 = P.GpuEngine(P.GridDims(*GRID), opts)
+            e1.generate(P.GEN_RANDOM, SEED)
+            e1.step(iters)  # warm-up
+            k1 = max(1, min(args.steps, 3))
+            secs1 = sum(e1.step(iters).seconds for _ in range(k1))
+            e1.close()
+            n1 = {"value": round(P.GridDims(*GRID).interior_cells() * iters * k1 / secs1 / 1e6, 2),
+                  "unit": "MLUP/s", "steps": k1,
+                  "what": "the per-rank grid as one whole-z context on one GPU (rank 0, device time)"}
+        dist.barrier()
+
     e2e = None
     # every local rank pins its slab's 40 arrays on the host: skip the leg if
     # the node's RAM does not hold all of them (decided identically by all ranks)
@@ -625,6 +644,8 @@ def run_native_multi(P, args, opts, iters, world, rank, local):
                               if peer else
                               "torch.distributed %s batch_isend_irecv after every %d-step pass"
                               % (backend, period)})
+    if n1:
+        line["config"]["n1_same_workload"] = n1
     if e2e_skip:
         line["e2e"]["skipped"] = ("host RAM: %d local ranks x %.0f GB of pinned slab arrays > 70%% "
                                   "of %.0f GB available" % (local_ranks, rank_bytes / 1e9, avail / 1e9))
@@ -644,6 +665,8 @@ def main():
     ap.add_argument("--device", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-n1-base", action="store_true",
+                    help="N>1: skip the one-GPU run of the per-rank workload")
     ap.add_argument("--tile-y", type=int, default=0)
     ap.add_argument("--z-chunk", type=int, default=0)
     ap.add_argument("--schedule", type=int, default=0,

@@ -42,6 +42,7 @@ def test_bench_two_ranks_one_gpu(peer, iters, check):
     assert check and check[0]["bitwise_equal"], lines
     assert bench and bench[0]["n_gpus"] == 2 and bench[0]["value"] > 0
     cfg = bench[0]["config"]
+    assert cfg["n1_same_workload"]["value"] > 0  # the per-rank grid on one GPU
     if peer == "1":
         assert cfg["exchange"].startswith("peer stores"), cfg
         assert "pass counters" in cfg["exchange"], cfg
