@@ -14,7 +14,10 @@ N>1.  One bench "step" = one full run of that config.
   value   MLUP/s with the problem resident in HBM (device time, CUDA events on
           the launching stream), max over ranks.
   e2e     same metric through the public API, every step's inputs uploaded
-          from pinned host memory and its 12 result fields downloaded.
+          from pinned host memory and its 12 result fields downloaded: the
+          faster of a stream of problems (run_gpu_batch, one problem per step,
+          <= 20; at configs[2] two TBLOCK-in-place contexts so uploads overlap
+          sweeps) and the one-problem call sequence (run_gpu); both reported.
   roofline  dominant kernel vs measured HBM.
   cpu_baseline  the reference's own run_naive (oracle/_ref, compiled from
           /root/reference unmodified) on the host cores, bounded sample.
