@@ -1099,19 +1099,21 @@ int launch_tblock2(thiim_gpu_ctx* ctx, Slab& s, long long* launches, const PeerO
 // 40 arrays fit in HBM, the 52 of ping-pong TBLOCK do not).  Each field array
 // has a gap of D = L + 2 planes above it (fstride = nz + 2 + D planes); at
 // rest it sits at the bottom of its region (ip_pos = 0).  A pass sweeps z as
-// sub-ranges [a, b) of L planes; each is one deep-slab TBLOCK pass over the view
-// of interior planes [a-1, b+1) plus the plane on either side (a z-slab whose
+// sub-ranges [a, b) of L planes; each is one TBLOCK pass over the view of
+// interior planes [a-1, b+1) plus the plane on either side (a z-slab whose
 // halos hold the neighbours' current values -- here the not yet updated state
-// itself) that stores its two-step outputs D planes away from its inputs:
+// itself; k_tblock_tm's view instances, DEEP = 2, sweep only the owned planes
+// [a, b) of it) that stores its two-step outputs D planes away from its inputs:
 //   even passes shift the array UP into the gap, sub-ranges top-down;
 //   odd passes shift it back DOWN, sub-ranges bottom-up.
 // Outputs of sub-range [a, b) land on padded planes [a+1, b] of the new
 // position, which overlap only inputs of sub-ranges already swept (D = L + 2
 // clears the sub-range's own window [a-1, b+2]), so nothing is copied back:
 // 416 B/LUP plus the ~4 planes every view re-reads.  The sweep stores interior
-// cells only, so the ghost ring of each output plane and the two ghost planes
-// follow with small copies.  A call that ends on an odd pass moves the array
-// back once (one copy), so every other entry point sees the canonical layout.
+// cells only, so the ghost ring of each output plane (only when some ring cell
+// is non-zero: k_ring_nonzero) and the two ghost planes follow with small
+// copies.  A call that ends on an odd pass moves the array back once (one
+// copy), so every other entry point sees the canonical layout.
 static int copy_ring(Slab& s, const Planes12& dst, const Planes12& src, int np, long long* launches) {
   k_copy_ring<<<dim3(8, np, 12), 256, 0, s.stream>>>(dst, src, np, s.g.nx, s.g.ny, s.g.px, s.g.pxy,
                                                       s.ring_nz);
