@@ -120,7 +120,8 @@ def test_python_tuner_on_a_small_grid():
                                                                     (2, 16), (3, 15)}
     best = max(t["mlups"] for t in r.table)
     won = [t for t in r.table if t["time_block"] == r.best.time_block and
-           t["tile_y"] == r.best.tile_y and t["z_chunk"] == r.best.z_chunk]
+           t["tile_y"] == r.best.tile_y and t["z_chunk"] == r.best.z_chunk and
+           t["band"] == r.best.band and t["schedule"] == r.best.schedule]
     assert won and won[0]["mlups"] >= 0.98 * best
     # the winner runs and is bitwise
     s = P.generate_problem(P.GridDims(40, 30, 24), P.GEN_RANDOM, 2)
