@@ -164,6 +164,32 @@ void test_batch_matches_run_naive() {
 
 }  // namespace
 
+void test_auto_table_layout() {
+  // coeff_layout = THIIM_COEFF_AUTO_HOST: a piecewise-constant medium (the
+  // layered stack, the vacuum benchmark problem) runs in the compressed TABLE
+  // layout, a random one in the reference layout -- all bitwise run_naive
+  SchemeParams sp;
+  struct Case {
+    ProblemState s;
+    bool table;
+  };
+  std::vector<Case> cases;
+  cases.push_back({random_state(GridDims(40, 33, 24), 5, THIIM_GEN_LAYERED), true});
+  cases.push_back({build_benchmark_problem(GridDims(32, 32, 32), sp), true});
+  cases.push_back({random_state(GridDims(20, 18, 16), 6), false});
+  for (Case& c : cases) {
+    ProblemState a = clone_state(c.s);
+    run_naive(a, 6, 4);
+    GpuOptions o;
+    o.coeff_layout = THIIM_COEFF_AUTO_HOST;
+    const RunReport r = run_gpu(c.s, 6, o);
+    CHECK(compare_states(a, c.s).bitwise_equal);
+    const bool table = r.engine.size() > 6 && r.engine.compare(r.engine.size() - 6, 6, "-table") == 0;
+    CHECK(table == c.table);
+    CHECK(r.balance_model == (c.table ? 192.5 : 416.0));
+  }
+}
+
 int main() {
   const std::vector<std::pair<const char*, std::function<void()>>> cases = {
       {"run_gpu matches run_naive (random states, split + fused)", test_matches_run_naive_random},
@@ -173,6 +199,8 @@ int main() {
       {"single-cell known answer 1.35", test_single_cell_kat},
       {"layered thin-film material", test_layered_material},
       {"run_gpu_batch: stream of problems == run_naive each", test_batch_matches_run_naive},
+      {"coeff_layout AUTO_HOST: compressed table layout for piecewise-constant media",
+       test_auto_table_layout},
   };
   for (const auto& [name, fn] : cases) {
     const int before = g_fail;

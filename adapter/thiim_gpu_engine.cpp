@@ -71,6 +71,33 @@ RunReport run_gpu(ProblemState& state, int steps, const GpuOptions& opts, GpuRun
   thiim_gpu_default_opts(&o);
   apply(opts, o);
 
+  // THIIM_COEFF_AUTO_HOST: piecewise-constant media (<= 16 distinct rows)
+  // run in the compressed TABLE layout, bitwise the same results
+  std::vector<uint8_t> mid;
+  std::vector<thiim_c128> tab;
+  if (opts.coeff_layout == THIIM_COEFF_AUTO_HOST) {
+    const thiim_c128* co[28];
+    for (int i = 0; i < kNumComponents; ++i) {
+      co[i] = reinterpret_cast<const thiim_c128*>(state.coeff_t[i].data());
+      co[12 + i] = reinterpret_cast<const thiim_c128*>(state.coeff_c[i].data());
+    }
+    for (int i = 0; i < kNumSourceComponents; ++i)
+      co[24 + i] = reinterpret_cast<const thiim_c128*>(state.coeff_src[i].data());
+    mid.resize(state.dims.padded_cells());
+    tab.resize(16 * 28);
+    int n = 0;
+    check(thiim_coeff_compress(&d, co, 16, mid.data(), tab.data(), &n), "thiim_coeff_compress");
+    if (n > 0) {
+      o.coeff_layout = THIIM_COEFF_TABLE;
+      o.n_materials = n;
+    } else {
+      mid.clear();
+    }
+  } else {
+    o.coeff_layout = opts.coeff_layout;
+  }
+  const bool packed = !mid.empty();
+
   CtxGuard g;
   check(thiim_gpu_create(&d, &o, &g.ctx), "thiim_gpu_create");
   if (opts.sanitize) check(thiim_gpu_set_sanitize(g.ctx, 1), "thiim_gpu_set_sanitize");
@@ -95,7 +122,10 @@ RunReport run_gpu(ProblemState& state, int steps, const GpuOptions& opts, GpuRun
     s[i] = reinterpret_cast<const thiim_c128*>(state.coeff_src[i].data());
     if (opts.pin_host) pins.pin(state.coeff_src[i].data(), bytes);
   }
-  check(thiim_gpu_upload(g.ctx, f, t, c, s), "thiim_gpu_upload");
+  if (packed)
+    check(thiim_gpu_upload_table(g.ctx, f, mid.data(), tab.data()), "thiim_gpu_upload_table");
+  else
+    check(thiim_gpu_upload(g.ctx, f, t, c, s), "thiim_gpu_upload");
 
   thiim_gpu_stats st{};
   check(thiim_gpu_step(g.ctx, steps, &st), "thiim_gpu_step");
@@ -111,7 +141,7 @@ RunReport run_gpu(ProblemState& state, int steps, const GpuOptions& opts, GpuRun
     out[i] = reinterpret_cast<thiim_c128*>(state.fields[i].data());
   check(thiim_gpu_download_fields(g.ctx, out), "thiim_gpu_download_fields");
 
-  report.engine = engine_name(st.engine);
+  report.engine = std::string(engine_name(st.engine)) + (packed ? "-table" : "");
   report.seconds = st.seconds;
   report.balance_model = st.balance_model;
   if (steps > 0 && st.seconds > 0.0)  // reference_engines.cpp:19-23

@@ -35,12 +35,17 @@ struct GpuOptions {
   int schedule = 0;                // TBLOCK CTA schedule (0 = rounds, 1 = one launch)
   bool sanitize = false;           // exactly-once store coverage check per pass
   bool pin_host = true;            // page-lock the 40 arrays during the copies
+  // coefficient storage on the device: THIIM_COEFF_FULL (the reference
+  // layout) or THIIM_COEFF_AUTO_HOST: compress the state's coefficients on the
+  // host (thiim_coeff_compress) and run the TABLE layout when the medium has
+  // <= 16 distinct coefficient rows (layered stacks), else FULL
+  int coeff_layout = THIIM_COEFF_FULL;
   double hbm_gbs = 0.0;            // if > 0: predicted_mlups = hbm_gbs / balance
 };
 
 // Upload `state`, run `steps` THIIM iterations on the GPU(s), download the 12
 // fields back into `state`.  RunReport: engine "gpu-split|gpu-fused|gpu-tblock|
-// gpu-tblock-inplace",
+// gpu-tblock-inplace" (+ "-table" when the compressed layout ran),
 // threads = #GPUs, seconds = device time of the step loop (CUDA events),
 // mlups = interior*steps/seconds/1e6, balance_model = algorithmic bytes/LUP.
 RunReport run_gpu(ProblemState& state, int steps, const GpuOptions& opts = {});

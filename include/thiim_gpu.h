@@ -109,6 +109,23 @@ typedef struct {
  * 832 B/LUP.  Results are bitwise those of the equivalent FULL problem; the
  * figure is reported separately from the reference-layout roofline. */
 enum { THIIM_COEFF_FULL = 0, THIIM_COEFF_TABLE = 1 };
+/* Not a context layout: host-side adapters (thiim::run_gpu, Python run_gpu)
+ * take it to mean "TABLE when thiim_coeff_compress finds <= 16 rows, else FULL". */
+enum { THIIM_COEFF_AUTO_HOST = 2 };
+
+/* Host-side compression of a reference-layout problem into the TABLE form
+ * (for callers that hold the reference's ProblemState of a piecewise-
+ * constant medium, e.g. the paper's layered thin-film stacks): when the
+ * INTERIOR cells carry at most max_materials (<= 16) distinct coefficient
+ * rows (t x12, c x12, src x4 compared bit for bit), writes material_id
+ * (padded layout, (nx+2)(ny+2)(nz+2) bytes, ghosts 0) and table
+ * [n][28] in order of first appearance along the linear interior index,
+ * and sets *n_materials = n; otherwise *n_materials = 0 (outputs undefined).
+ * Ghost-cell coefficients are never read by any engine and are ignored.
+ * coeffs[k] = ProblemState array 12 + k.  OpenMP over z-planes; no device. */
+int thiim_coeff_compress(const thiim_dims* dims, const thiim_c128* const coeffs[28],
+                         int max_materials, uint8_t* material_id, thiim_c128* table,
+                         int* n_materials);
 
 typedef struct {
   double seconds;          /* device time of the whole step loop (CUDA events) */

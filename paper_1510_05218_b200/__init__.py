@@ -28,7 +28,7 @@ from __future__ import annotations
 import ctypes
 import enum
 import os
-from dataclasses import dataclass, field
+from dataclasses import replace, dataclass, field
 from typing import Tuple, List, Optional
 
 import numpy as np
@@ -39,7 +39,8 @@ __all__ = [
     "COMPONENT_TABLE", "GEN_RANDOM", "GEN_LAYERED", "ENGINE_AUTO", "ENGINE_SPLIT",
     "ENGINE_FUSED", "ENGINE_TBLOCK", "ENGINE_TBLOCK_INPLACE", "GpuOptions", "RunReport", "StateDiff", "GpuEngine",
     "run_gpu", "generate_problem", "compare_states", "balance_model", "lib",
-    "compress_coefficients", "expand_coefficients", "COEFF_FULL", "COEFF_TABLE",
+    "compress_coefficients", "expand_coefficients", "coeff_compress", "COEFF_FULL", "COEFF_TABLE",
+    "COEFF_AUTO",
     "run_gpu_batch", "BatchReport", "release_cached",
 ]
 
@@ -328,6 +329,7 @@ EXPORTED_SYMBOLS = [
     "thiim_gpu_init_materials", "thiim_gpu_selftest_cdiv", "thiim_gpu_slab_export",
     "thiim_gpu_slab_import", "thiim_gpu_slab_detach", "thiim_gpu_run_batch",
     "thiim_gpu_release_cached", "thiim_gpu_enumerate_candidates", "thiim_gpu_tune",
+    "thiim_coeff_compress",
 ]
 
 _LIB = None
@@ -360,6 +362,8 @@ def lib() -> ctypes.CDLL:
     L.thiim_gpu_compare_fields.argtypes = [P, PP, ctypes.POINTER(_Diff)]
     L.thiim_generate_host.argtypes = [ctypes.POINTER(_Dims), ctypes.c_int, ctypes.c_uint64, PP]
     L.thiim_gpu_upload_table.argtypes = [P, PP, P, P]
+    L.thiim_coeff_compress.argtypes = [ctypes.POINTER(_Dims), PP, ctypes.c_int, P, P,
+                                       ctypes.POINTER(ctypes.c_int)]
     L.thiim_gpu_download_table.argtypes = [P, P, P]
     L.thiim_gpu_pin_host.argtypes = [P, ctypes.c_size_t]
     L.thiim_gpu_unpin_host.argtypes = [P]
@@ -406,6 +410,7 @@ GEN_RANDOM = 0
 GEN_LAYERED = 1
 COEFF_FULL = 0
 COEFF_TABLE = 1
+COEFF_AUTO = 2  # run_gpu only (THIIM_COEFF_AUTO_HOST): TABLE for <= 16 coefficient rows, else FULL
 ENGINE_AUTO, ENGINE_SPLIT, ENGINE_FUSED, ENGINE_TBLOCK, ENGINE_TBLOCK_INPLACE = 0, 1, 2, 3, 4
 ENGINE_NAMES = {ENGINE_SPLIT: "gpu-split", ENGINE_FUSED: "gpu-fused", ENGINE_TBLOCK: "gpu-tblock",
                 ENGINE_TBLOCK_INPLACE: "gpu-tblock-inplace"}
@@ -617,6 +622,22 @@ def compress_coefficients(state: ProblemState, max_materials: int = 16):
     return ids.astype(np.uint8).reshape(-1), np.ascontiguousarray(table)
 
 
+def coeff_compress(state: ProblemState, max_materials: int = 16):
+    """Native compression (thiim_coeff_compress) of the interior coefficient
+    rows: (material_id, table) of the THIIM_COEFF_TABLE layout when the medium
+    has at most `max_materials` distinct rows, else None.  Ghost cells' ids are
+    0 (no engine reads their coefficients)."""
+    d = _Dims(state.dims.nx, state.dims.ny, state.dims.nz, state.dims.ghost)
+    mid = np.empty(state.dims.padded_cells(), np.uint8)
+    tab = np.empty((max(1, max_materials), 28), np.complex128)
+    n = ctypes.c_int()
+    _check(lib().thiim_coeff_compress(ctypes.byref(d), _ptrs(state.arrays[12:40]), max_materials,
+                                      mid.ctypes.data, tab.ctypes.data, ctypes.byref(n)))
+    if n.value == 0:
+        return None
+    return mid, np.ascontiguousarray(tab[:n.value])
+
+
 def expand_coefficients(dims: GridDims, material_id: np.ndarray, table: np.ndarray) -> ProblemState:
     """Inverse of compress_coefficients (fields left zero)."""
     s = allocate_state(dims)
@@ -633,11 +654,22 @@ def run_gpu(state: ProblemState, steps: int, opts: Optional[GpuOptions] = None) 
     if steps < 0:
         raise ConfigError("steps must be >= 0")
     opts = opts or GpuOptions()
+    packed = None
+    if opts.coeff_layout == COEFF_AUTO:
+        # piecewise-constant media run in the compressed layout (192.5 instead
+        # of 416 B/LUP with TBLOCK), bitwise the same results
+        packed = coeff_compress(state)
+        opts = replace(opts, coeff_layout=COEFF_TABLE if packed else COEFF_FULL,
+                       n_materials=len(packed[1]) if packed else opts.n_materials)
     with GpuEngine(state.dims, opts) as eng:
-        eng.upload(state)
+        if packed:
+            eng.upload_table(state.fields, packed[0], packed[1])
+        else:
+            eng.upload(state)
         st = eng.step(steps)
         eng.download_fields(state)
-    r = RunReport(engine=ENGINE_NAMES.get(st.engine, "gpu"), dims=state.dims, steps=steps,
+    r = RunReport(engine=ENGINE_NAMES.get(st.engine, "gpu") + ("-table" if packed else ""),
+                  dims=state.dims, steps=steps,
                   steps_executed=steps, threads=st.n_gpus, seconds=st.seconds,
                   balance_model=st.balance_model, kernel_launches=st.kernel_launches)
     if steps > 0 and st.seconds > 0:

@@ -23,6 +23,8 @@
 #include <string>
 #include <vector>
 
+#include <omp.h>
+
 // ring depth (slots) of the default TBLOCK kernel (experiment builds override)
 #ifndef THIIM_TB_NG
 #define THIIM_TB_NG 6
@@ -1350,6 +1352,9 @@ static int create_impl(const thiim_dims* dims, const thiim_gpu_opts* opts, bool 
     return fail(THIIM_ERR_CONFIG,
                 "time_block 3 runs on one whole-z slab in the reference coefficient layout");
   const bool table = o.coeff_layout == THIIM_COEFF_TABLE;
+  if (o.coeff_layout == THIIM_COEFF_AUTO_HOST)
+    return fail(THIIM_ERR_CONFIG, "THIIM_COEFF_AUTO_HOST is resolved by the host adapters "
+                                  "(thiim_coeff_compress), not by a context");
   if (o.coeff_layout != THIIM_COEFF_FULL && !table)
     return fail(THIIM_ERR_CONFIG, "unknown coefficient layout");
   if (table && (o.engine == THIIM_ENGINE_SPLIT || o.engine == THIIM_ENGINE_TBLOCK_INPLACE))
@@ -2763,6 +2768,116 @@ int thiim_generate_host(const thiim_dims* dims, int kind, uint64_t seed,
     return THIIM_ERR_SETUP;
   }
   return thiim_generate_host_planes(dims, kind, seed, 0, dims->nz + 2, arrays);
+}
+
+int thiim_coeff_compress(const thiim_dims* dims, const thiim_c128* const coeffs[28],
+                         int max_materials, uint8_t* material_id, thiim_c128* table,
+                         int* n_materials) {
+  g_err.clear();
+  if (!valid_dims(dims)) return fail(THIIM_ERR_SETUP, "invalid grid dims");
+  if (!coeffs || !material_id || !table || !n_materials) return fail(THIIM_ERR_CONFIG, "null argument");
+  for (int k = 0; k < 28; ++k)
+    if (!coeffs[k]) return fail(THIIM_ERR_CONFIG, "null coefficient array");
+  if (max_materials < 1 || max_materials > kMaxMaterials)
+    return fail(THIIM_ERR_CONFIG, "max_materials must be in 1..16");
+  *n_materials = 0;
+  const long long px = dims->nx + 2, pxy = px * (dims->ny + 2), nz = dims->nz;
+  // a cell's coefficient row: 28 complex values = 56 words, compared bitwise
+  typedef unsigned long long u64;
+  auto word = [&](int k, long long i, int h) -> u64 {
+    u64 w;
+    std::memcpy(&w, reinterpret_cast<const char*>(coeffs[k] + i) + 8 * h, 8);
+    return w;
+  };
+  auto same = [&](long long i, const u64* row) {
+    for (int k = 0; k < 28; ++k)
+      if (word(k, i, 0) != row[2 * k] || word(k, i, 1) != row[2 * k + 1]) return false;
+    return true;
+  };
+  // pass 1: per thread, over a contiguous range of interior planes, the
+  // distinct rows in order of first appearance; material_id holds the local
+  // row index for now
+  int nth = 1;
+#pragma omp parallel
+  {
+#pragma omp single
+    nth = omp_get_num_threads();
+  }
+  nth = (int)std::max<long long>(1, std::min<long long>(nth, nz));
+  std::vector<std::vector<u64>> rows(nth);  // 56 words per row
+  std::vector<int> overflow(nth, 0);
+#pragma omp parallel for schedule(static, 1) num_threads(nth)
+  for (int t = 0; t < nth; ++t) {
+    const long long z0 = 1 + nz * t / nth, z1 = 1 + nz * (t + 1) / nth;
+    std::vector<u64>& R = rows[t];
+    int last = -1;
+    for (long long z = z0; z < z1 && !overflow[t]; ++z)
+      for (long long y = 1; y <= dims->ny && !overflow[t]; ++y) {
+        const long long i0 = z * pxy + y * px;
+        for (long long i = i0 + 1; i <= i0 + dims->nx; ++i) {
+          int id = -1;
+          if (last >= 0 && same(i, &R[56 * (size_t)last])) id = last;
+          for (int r = 0; id < 0 && r < (int)(R.size() / 56); ++r)
+            if (r != last && same(i, &R[56 * (size_t)r])) id = r;
+          if (id < 0) {
+            if ((int)(R.size() / 56) == max_materials) {
+              overflow[t] = 1;
+              break;
+            }
+            id = (int)(R.size() / 56);
+            for (int k = 0; k < 28; ++k) {
+              R.push_back(word(k, i, 0));
+              R.push_back(word(k, i, 1));
+            }
+          }
+          material_id[i] = (uint8_t)id;
+          last = id;
+        }
+      }
+  }
+  for (int t = 0; t < nth; ++t)
+    if (overflow[t]) return THIIM_OK;  // more than max_materials rows: not compressible
+  // merge in plane order: global ids by first appearance along the interior
+  std::vector<u64> G;
+  std::vector<std::vector<uint8_t>> remap(nth);
+  for (int t = 0; t < nth; ++t) {
+    const int nloc = (int)(rows[t].size() / 56);
+    for (int r = 0; r < nloc; ++r) {
+      const u64* row = &rows[t][56 * (size_t)r];
+      int gid = -1;
+      for (int q = 0; gid < 0 && q < (int)(G.size() / 56); ++q)
+        if (std::memcmp(row, &G[56 * (size_t)q], 56 * sizeof(u64)) == 0) gid = q;
+      if (gid < 0) {
+        if ((int)(G.size() / 56) == max_materials) return THIIM_OK;
+        gid = (int)(G.size() / 56);
+        G.insert(G.end(), row, row + 56);
+      }
+      remap[t].push_back((uint8_t)gid);
+    }
+  }
+  // pass 2: local -> global ids; ghost cells 0
+#pragma omp parallel for schedule(static, 1) num_threads(nth)
+  for (int t = 0; t < nth; ++t) {
+    const long long z0 = 1 + nz * t / nth, z1 = 1 + nz * (t + 1) / nth;
+    for (long long z = z0; z < z1; ++z)
+      for (long long y = 1; y <= dims->ny; ++y) {
+        const long long i0 = z * pxy + y * px;
+        for (long long i = i0 + 1; i <= i0 + dims->nx; ++i) material_id[i] = remap[t][material_id[i]];
+      }
+  }
+  std::memset(material_id, 0, (size_t)pxy);  // ghost planes
+  std::memset(material_id + (nz + 1) * pxy, 0, (size_t)pxy);
+#pragma omp parallel for schedule(static) num_threads(nth)
+  for (long long z = 1; z <= nz; ++z) {  // ghost rows and columns
+    uint8_t* m = material_id + z * pxy;
+    std::memset(m, 0, (size_t)px);
+    std::memset(m + (dims->ny + 1) * px, 0, (size_t)px);
+    for (long long y = 1; y <= dims->ny; ++y) m[y * px] = m[y * px + px - 1] = 0;
+  }
+  const int n = (int)(G.size() / 56);
+  std::memcpy(table, G.data(), G.size() * sizeof(u64));
+  *n_materials = n;
+  return THIIM_OK;
 }
 
 int thiim_gpu_pin_host(void* ptr, size_t bytes) {
