@@ -14,6 +14,10 @@
 //   * double (op) complex scales or promotes componentwise.
 // Built with -fmad=false, so no product is fused.  Pinned by
 // tests/test_gpu_materials.py against host libgcc on random and edge operands.
+// Attribution: the division algorithm (Smith 1962, with the scaling guards of
+// GCC's 2021 rework) is the one GCC ships in libgcc2.c (GPL-3.0 with the GCC
+// Runtime Library Exception); cdiv is an independent restatement of that
+// published algorithm in CUDA, not a copy of the libgcc source.
 #pragma once
 
 #include <cfloat>
