@@ -1,5 +1,5 @@
 """Race stress for the TMA ring's slot release (thiim_ring.cuh): many random
-shapes / seeds / step counts through the fused, TBLOCK, TBLOCK-in-place (random
+shapes / seeds / step counts through the fused, TBLOCK (depth 2 and 3), TBLOCK-in-place (random
 sub-range lengths) and table engines,
 each compared bitwise with the C oracle.  Prints one JSON line with the
 number of cases and failures.  Test infrastructure: imports oracle/.
@@ -25,7 +25,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--seconds", type=float, default=120)
     ap.add_argument("--seed", type=int, default=7)
-    ap.add_argument("--only", default="", help="comma list of fused,tblock,inplace,table,table-fused")
+    ap.add_argument("--only", default="", help="comma list of fused,tblock,inplace,tblock3,table,table-fused")
     a = ap.parse_args()
     rng = np.random.default_rng(a.seed)
     t_end = time.time() + a.seconds
@@ -41,7 +41,8 @@ def main():
         O.c_step((d.nx, d.ny, d.nz), ref.arrays, steps, threads=8)
         runs = [("fused", P.GpuOptions(engine=P.ENGINE_FUSED)),
                 ("tblock", P.GpuOptions(engine=P.ENGINE_TBLOCK)),
-                ("inplace", P.GpuOptions(engine=P.ENGINE_TBLOCK_INPLACE))]
+                ("inplace", P.GpuOptions(engine=P.ENGINE_TBLOCK_INPLACE)),
+                ("tblock3", P.GpuOptions(engine=P.ENGINE_TBLOCK, time_block=3))]
         ip_L = int(rng.integers(2, max(3, d.nz + 1)))  # sub-range length of the in-place run
         if layered:
             runs.append(("table", P.GpuOptions(coeff_layout=P.COEFF_TABLE, n_materials=6,
