@@ -1473,10 +1473,14 @@ static int create_impl(const thiim_dims* dims, const thiim_gpu_opts* opts, bool 
     if (e == cudaSuccess) {
       device_pool(sl.device);
       // slab contexts of a multi-process decomposition: cudaMalloc, so that
-      // neighbours in other processes can map the state (thiim_gpu_slab_export)
-      sl.ipc_buf = ipc_alloc;
-      e = ipc_alloc ? cudaMalloc(reinterpret_cast<void**>(&sl.buf), bytes)
-                    : pool_alloc(reinterpret_cast<void**>(&sl.buf), bytes, sl.device, sl.stream);
+      // neighbours in other processes can map the state (thiim_gpu_slab_export).
+      // Slabs of one context on different devices: cudaMalloc as well -- the
+      // neighbours' kernels store into this slab's halos, and
+      // cudaDeviceEnablePeerAccess (below) does not cover memory from a
+      // stream-ordered pool (that would need cudaMemPoolSetAccess per pool)
+      sl.ipc_buf = ipc_alloc || (n > 1 && dev_step != 0);
+      e = sl.ipc_buf ? cudaMalloc(reinterpret_cast<void**>(&sl.buf), bytes)
+                     : pool_alloc(reinterpret_cast<void**>(&sl.buf), bytes, sl.device, sl.stream);
       if (e != cudaSuccess && sl.fstride && !want_ip) {
         // AUTO: no room for the in-place gap after all -> plain split
         cudaGetLastError();
@@ -2225,6 +2229,17 @@ static int step_enqueue(thiim_gpu_ctx* ctx, int steps, long long* launches_out) 
       }
       if (ctx->sanitize && (r = coverage_pass(ctx, true))) return r;
       if (multi && !ctx->peer_stores && (r = exchange_deep(ctx))) return r;
+    }
+    if (ctx->ipc_ordered) {
+      // a pass only waits for the neighbours' PREVIOUS pass; whatever follows
+      // the last one -- the fused remainder step below, a download or the next
+      // upload after the call returns -- needs the halos their LAST pass
+      // stores: the stream ends on their counters reaching this slab's count
+      // (every rank wrote its own counter before it waits: no cycle)
+      Slab& sl = ctx->slabs[0];
+      for (const Slab::Peer& q : sl.peer)
+        if (q.counter && stream_wait_geq(sl.stream, q.counter, sl.passes) != CUDA_SUCCESS)
+          return fail(THIIM_ERR_CUDA, "cuStreamWaitValue64 on a neighbour's pass counter failed");
     }
     for (; n < steps; ++n) {
       if (ctx->peer_stores && multi)

@@ -74,6 +74,26 @@ def test_config4_full_grid_vs_reference():
     _full_grid_vs_reference((1024, 1024, 128), 5)
 
 
+full_length = pytest.mark.skipif(
+    os.environ.get("THIIM_FULL_LENGTH") != "1",
+    reason="THIIM_FULL_LENGTH=1 runs the reference for the whole workload (minutes of CPU time)")
+
+
+@need_ref
+@full_length
+def test_config2_full_length_vs_reference():
+    """configs[2] over all 200 iterations against the reference's run_naive
+    (~4 min on 16 host threads; the round's run is kept under profiles/)."""
+    _full_grid_vs_reference((512, 512, 512), 200)
+
+
+@need_ref
+@full_length
+def test_config4_full_length_vs_reference():
+    """configs[4]'s per-GPU slab over all 100 iterations against run_naive."""
+    _full_grid_vs_reference((1024, 1024, 128), 100)
+
+
 def test_config1_full_workload_vs_reference():
     d = P.GridDims(256, 256, 256)
     s = P.generate_problem(d, P.GEN_RANDOM, seed=1)  # bench.py's problem
