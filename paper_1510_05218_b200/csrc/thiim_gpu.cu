@@ -118,6 +118,8 @@ struct Slab {
   bool maps_ok[6] = {false, false, false, false, false, false};
   TmaMaps maps_seg[6][2];  // the same for 16- / 8-lane segments (folded TBLOCK tiles)
   bool maps_seg_ok[6][2] = {};
+  TmaMaps fmaps[6];  // the one-step (fused) sweeps' maps: no L2 promotion (ensure_tmap)
+  bool fmaps_ok[6] = {false, false, false, false, false, false};
 
   // TBLOCK in place (THIIM_ENGINE_TBLOCK_INPLACE, one whole-z slab, no second
   // field set): sub-range length; the field arrays carry a gap of ip_L + 2
@@ -750,8 +752,9 @@ int map_index(int by) {
 
 // tensor maps for tile height `by` and thread-tile width `width` (32, or a
 // 16 / 8 lane segment of a folded CTA: every box 32 - width columns narrower)
-TmaMaps& tmaps(Slab& s, int by, int width = 32) {
+TmaMaps& tmaps(Slab& s, int by, int width = 32, bool fused = false) {
   const int w = map_index(by);
+  if (fused) return s.fmaps[w];
   return width == 32 ? s.maps[w] : s.maps_seg[w][width == 16 ? 0 : 1];
 }
 // coefficient maps: the same maps unless the slab is a view with its own
@@ -762,13 +765,21 @@ TmaMaps& ctmaps(Slab& s, int by, int width = 32) {
   return width == 32 ? s.cmaps[w] : s.cmaps_seg[w][width == 16 ? 0 : 1];
 }
 
-// L2 promotion stays off: 256-B promotion inflated DRAM reads by 7%
-int ensure_tmap(Slab& s, int by, int width = 32) {
+// L2 promotion (measured, profiles/r02x_l2_promotion.md): the TBLOCK sweeps take
+// 64-B promotion -- box rows start 16 B into a 32-B sector, and fetching the
+// sector pair brings the x-neighbour's overlap along: 3.4% fewer DRAM read bytes
+// per pass at configs[2], +0.2-0.3% on every TBLOCK kernel; 128 B: no change;
+// 256 B: -1% and +7% DRAM reads.  The one-step sweeps (`fused`: their own map
+// set) stay without promotion (64 B: -1.8%).
+int ensure_tmap(Slab& s, int by, int width = 32, bool fused = false) {
   const int w = map_index(by);
   if (w < 0) return fail(THIIM_ERR_CONFIG, "no tensor maps for tile height " + std::to_string(by));
   if (width != 32 && width != 16 && width != 8)
     return fail(THIIM_ERR_CONFIG, "no tensor maps for tile width " + std::to_string(width));
-  bool& ok = width == 32 ? s.maps_ok[w] : s.maps_seg_ok[w][width == 16 ? 0 : 1];
+  if (fused && (width != 32 || s.cbuf))
+    return fail(THIIM_ERR_CONFIG, "internal: the one-step sweeps run full-width tiles, no views");
+  bool& ok = fused ? s.fmaps_ok[w]
+                   : width == 32 ? s.maps_ok[w] : s.maps_seg_ok[w][width == 16 ? 0 : 1];
   if (ok) return THIIM_OK;
   auto fn = get_encode_fn();
   if (!fn) return fail(THIIM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
@@ -782,12 +793,14 @@ int ensure_tmap(Slab& s, int by, int width = 32) {
                                 (cuuint64_t)(s.g.nz + 2), (cuuint64_t)narr};
     const cuuint64_t strides[3] = {(cuuint64_t)s.g.px * 16, (cuuint64_t)s.g.pxy * 16,
                                    (cuuint64_t)astride * 16};
+    const CUtensorMapL2promotion promo =
+        fused ? CU_TENSOR_MAP_L2_PROMOTION_NONE : CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
     for (int b = 0; b < NBOX; ++b) {
       const cuuint32_t box[4] = {(cuuint32_t)(2 * bw[b]), (cuuint32_t)bh[b], 1, 1};
       const cuuint32_t estr[4] = {1, 1, 1, 1};
       CUresult r = fn(&out.m[b], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, base, dims, strides, box, estr,
                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                      CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                      promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
       if (r != CUDA_SUCCESS)
         return fail(THIIM_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
     }
@@ -800,7 +813,7 @@ int ensure_tmap(Slab& s, int by, int width = 32) {
   } else {
     if (s.fs() != s.stride)
       return fail(THIIM_ERR_CONFIG, "internal: field stride differs; the sweep needs a view");
-    if ((r = encode(tmaps(s, by, width), s.buf, s.n_arrays(), s.stride))) return r;
+    if ((r = encode(tmaps(s, by, width, fused), s.buf, s.n_arrays(), s.stride))) return r;
   }
   ok = true;
   return THIIM_OK;
@@ -810,7 +823,7 @@ template <int BY, int NG>
 int launch_fused_tma_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
   const Arrays A = s.arrays(s.cur, s.cur ^ 1);
   const int cur = s.cur, nf = s.nfield_sets;
-  int r = ensure_tmap(s, BY);
+  int r = ensure_tmap(s, BY, 32, true);
   if (r) return r;
   constexpr int TX = 30, TY = BY - 2;
   const size_t smem = sizeof(FusedSmem<BY, NG>);
@@ -829,7 +842,7 @@ int launch_fused_tma_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
   const dim3 grid(tiles_x * tiles_y, 1, (s.g.nz + zc - 1) / zc);
   const dim3 block(32, BY + 1);
   (s.cnt ? k_fused_tma<BY, NG, true> : k_fused_tma<BY, NG, false>)<<<grid, block, smem, s.stream>>>(
-      s.g, A, tmaps(s, BY), zc, tiles_x, cur * 12, nf * 12);
+      s.g, A, tmaps(s, BY, 32, true), zc, tiles_x, cur * 12, nf * 12);
   CK(cudaGetLastError());
   s.cur ^= 1;
   ++*launches;
@@ -1206,10 +1219,10 @@ int launch_fused_table_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
   const int cur = s.cur;
   GroupSeq S;
   seq_table(S, [&](int k) { return cur * 12 + k; });
-  int r = ensure_tmap(s, BY);
+  int r = ensure_tmap(s, BY, 32, true);
   if (r) return r;
   TableMaps maps;
-  maps.f = tmaps(s, BY);
+  maps.f = tmaps(s, BY, 32, true);
   TableGrid T;
   T.mat = s.mat;
   T.mp = s.mp;

@@ -30,6 +30,14 @@ KEYS = [
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM throughput % of peak"),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "achieved occupancy"),
     ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue slots busy"),
+    ("sm__cycles_elapsed.max", "SM cycles elapsed"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "shared-memory wavefronts (LSU: LDS/STS)"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum", "shared-memory load wavefronts"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_st.sum", "shared-memory store wavefronts"),
+    ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "shared-memory bank conflicts"),
+    ("l1tex__data_pipe_lsu_wavefronts.sum", "L1 data-pipe LSU wavefronts"),
+    ("l1tex__throughput.avg.pct_of_peak_sustained_elapsed", "L1/TEX throughput % of peak"),
+    ("l1tex__lsu_writeback_active.avg.pct_of_peak_sustained_elapsed", "LSU writeback % of peak"),
     ("launch__registers_per_thread", "registers/thread"),
     ("launch__shared_mem_per_block_dynamic", "dynamic smem/CTA"),
     ("launch__grid_size", "grid"),
