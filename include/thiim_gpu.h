@@ -328,7 +328,11 @@ int thiim_gpu_slab_info(thiim_gpu_ctx* ctx, thiim_slab_info* info);
  * pass n stores into are done, and their stores into this slab's input halos
  * have landed), and after the pass it writes n (stream memory operations,
  * preceded by a system-scope fence).  So thiim_gpu_step(ctx, k) may advance
- * any even k in one call with no host synchronisation between passes;
+ * any even k in one call with no host synchronisation between passes, and the
+ * call's stream ends on the neighbours' counters reaching this slab's pass
+ * count: when thiim_gpu_step returns, the neighbours' last stores into this
+ * slab's halos have landed (the remainder step, a download or a new upload may
+ * follow);
  * thiim_slab_info.device_ordered says so (0: the stream memory operations were
  * unavailable for the mapped counters, and the caller must barrier all ranks
  * after every 2-step call).  The caller still barriers all ranks once after an
@@ -380,8 +384,11 @@ int thiim_gpu_coverage(thiim_gpu_ctx* ctx, unsigned long long* passes,
 /* Blocks until all work queued on the context's streams has finished. */
 int thiim_gpu_sync(thiim_gpu_ctx* ctx);
 
-/* Contexts take their state from the device's stream-ordered memory pool and
- * give it back on destroy; the pool keeps the pages for the next context
+/* One-GPU contexts take their state from the device's stream-ordered memory pool
+ * and give it back on destroy (slabs that a peer device or process writes into --
+ * n_gpus > 1 on distinct devices, thiim_gpu_create_slab -- are plain cudaMalloc
+ * allocations: peer access and CUDA IPC do not cover pool memory); the pool
+ * keeps the pages for the next context
  * (creating a 14 GB context costs ~2 ms instead of a fresh allocation).  This
  * returns the cached, unused pages of `device`'s pool to the driver, e.g.
  * before another library allocates device memory. */

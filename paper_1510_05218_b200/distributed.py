@@ -270,4 +270,9 @@ def run_distributed(engine, steps: int, exchanger: HaloExchanger) -> dict:
         else:
             sent += exchanger.exchange(engine)
         done += k
+    if getattr(engine, "device_ordered", False) and steps > 0:
+        # every rank's step has returned, i.e. its stream has seen the neighbours'
+        # final counters: from here a rank may destroy its slab (the mapped
+        # counters and halos the neighbours' streams were polling / storing into)
+        exchanger.barrier()
     return {"halo_bytes_sent": sent, "kernel_launches": launches}

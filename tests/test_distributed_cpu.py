@@ -204,8 +204,9 @@ def test_peer_store_protocol_orders_upload_before_first_pass():
 def test_device_ordered_peer_stores_enqueue_all_passes_at_once():
     """Host logic only: with device-side pass counters (device_ordered), the
     2-step passes of a call go to the library in ONE step call -- no host
-    barrier between passes; one barrier on entry, the odd remainder step still
-    exchanges."""
+    barrier between passes; one barrier on entry and one on exit (after it a
+    rank may destroy the slab its neighbours' streams were polling), the odd
+    remainder step still exchanges."""
     calls = []
 
     class Eng:
@@ -226,8 +227,8 @@ def test_device_ordered_peer_stores_enqueue_all_passes_at_once():
             return 8
 
     st = D.run_distributed(Eng(), 9, Ex())
-    assert calls == [("barrier",), ("step", 8), ("step", 1), ("exchange",)]
+    assert calls == [("barrier",), ("step", 8), ("step", 1), ("exchange",), ("barrier",)]
     assert st == {"halo_bytes_sent": 8, "kernel_launches": 5}
     calls.clear()
     D.run_distributed(Eng(), 4, Ex())
-    assert calls == [("barrier",), ("step", 4)]
+    assert calls == [("barrier",), ("step", 4), ("barrier",)]
