@@ -105,6 +105,32 @@ def test_single_process_multi_slab_context(engine, n):
     assert P.compare_states(got, want).bitwise_equal
 
 
+def _gpu_count():
+    import torch
+    return torch.cuda.device_count()
+
+
+@pytest.mark.parametrize("engine,steps", [(P.ENGINE_SPLIT, 3), (P.ENGINE_FUSED, 4),
+                                          (P.ENGINE_TBLOCK, 6), (P.ENGINE_TBLOCK, 7)])
+def test_single_process_context_across_devices(engine, steps):
+    """The same context with its slabs on DISTINCT devices (cuda:0..n-1): kernels
+    of one device store into the neighbours' halos over NVLink peer memory
+    (cudaMalloc slabs + cudaDeviceEnablePeerAccess), passes ordered by stream
+    events.  Runs wherever >= 2 GPUs are visible (the one-GPU boxes of this
+    project skip it; the same-device tests above cover the protocol)."""
+    n = min(_gpu_count(), 4)
+    if n < 2:
+        pytest.skip("needs >= 2 visible GPUs")
+    dims = P.GridDims(72, 50, 12 * n + 5)
+    s = P.generate_problem(dims, P.GEN_RANDOM, 12)
+    want = P.clone_state(s)
+    O.c_step((dims.nx, dims.ny, dims.nz), want.arrays, steps, threads=8)
+    got = P.clone_state(s)
+    r = P.run_gpu(got, steps, P.GpuOptions(engine=engine, n_gpus=n, same_device=0))
+    assert r.threads == n
+    assert P.compare_states(got, want).bitwise_equal
+
+
 @pytest.mark.parametrize("engine,steps", [(P.ENGINE_FUSED, 4), (P.ENGINE_TBLOCK, 4),
                                           (P.ENGINE_TBLOCK, 5)])
 def test_single_process_multi_slab_table_layout(engine, steps):
