@@ -1,6 +1,6 @@
 """Race stress for the TMA ring's slot release (thiim_ring.cuh): many random
 shapes / seeds / step counts through the fused, TBLOCK (depth 2 and 3), TBLOCK-in-place (random
-sub-range lengths) and table engines,
+sub-range lengths), table and multi-slab (peer-store) engines,
 each compared bitwise with the C oracle.  Prints one JSON line with the
 number of cases and failures.  Test infrastructure: imports oracle/.
 
@@ -25,7 +25,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--seconds", type=float, default=120)
     ap.add_argument("--seed", type=int, default=7)
-    ap.add_argument("--only", default="", help="comma list of fused,tblock,inplace,tblock3,table,table-fused")
+    ap.add_argument("--only", default="", help="comma list of fused,tblock,inplace,tblock3,table,table-fused,slabs,slabs-table")
     a = ap.parse_args()
     rng = np.random.default_rng(a.seed)
     t_end = time.time() + a.seconds
@@ -49,6 +49,15 @@ def main():
                                                engine=P.ENGINE_TBLOCK)))
             runs.append(("table-fused", P.GpuOptions(coeff_layout=P.COEFF_TABLE, n_materials=6,
                                                      engine=P.ENGINE_FUSED)))
+        # z-slabs of one context on this device: peer stores into the neighbours'
+        # halos from the TBLOCK kernel, passes ordered by stream events
+        ns = int(rng.integers(2, 4))
+        if d.nz >= 4 * ns:
+            runs.append(("slabs", P.GpuOptions(engine=P.ENGINE_TBLOCK, n_gpus=ns, same_device=1)))
+            if layered:
+                runs.append(("slabs-table", P.GpuOptions(engine=P.ENGINE_TBLOCK, n_gpus=ns,
+                                                         same_device=1, coeff_layout=P.COEFF_TABLE,
+                                                         n_materials=6)))
         if a.only:
             runs = [r for r in runs if r[0] in a.only.split(",")]
         for name, o in runs:
