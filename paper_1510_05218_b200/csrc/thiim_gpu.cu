@@ -850,8 +850,11 @@ int launch_fused_tma_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches) {
 }
 
 // ---- TBLOCK (two steps per pass)
-// z-chunks of a TBLOCK launch: each CTA re-does ~2 planes of level-1/level-2
-// work at its start; minimise waves x (planes + 2) over one CTA per SM
+// z-chunks of a TBLOCK launch: minimise waves x (planes + overhead) over one
+// CTA per SM.  A chunk start re-does ~2 planes of level-1/level-2 work, re-reads
+// their boxes and fills the ring from empty; measured at configs[4] (r02y: one
+// 128-plane chunk in 24 rounds vs two 64-plane chunks in 47, +1.4%) the whole
+// costs the depth-2 kernel ~4.7 plane-iterations, hence its 4.5
 int tblock_zchunk(const Slab& s, long long cols, double overhead = 2.0, int span = 0) {
   const long long slots = sm_count(s.device);
   const int nz = span > 0 ? span : s.g.nz;  // planes the chunks cover
@@ -936,7 +939,7 @@ int launch_tblock2_t(thiim_gpu_ctx* ctx, Slab& s, long long* launches, const Pee
   const bool view = s.deep && s.fo_base != nullptr;
   const int span = view ? po.st1 - po.st0 : s.deep && wf == 0 ? po.st1 : s.g.nz;
   int zc = ctx->opts.z_chunk;
-  if (zc <= 0) zc = tblock_zchunk(s, (long long)nbt, 2.0, span);
+  if (zc <= 0) zc = tblock_zchunk(s, (long long)nbt, 4.5, span);
   const int nchunks = (span + zc - 1) / zc;
   const long long items = (long long)nbt * nchunks;
   // CTA schedule: rounds of at most one CTA per SM in band order (default), or

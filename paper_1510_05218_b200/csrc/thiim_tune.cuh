@@ -212,7 +212,7 @@ int thiim_gpu_tune(const thiim_dims* dims, const thiim_gpu_opts* base, int steps
     double best_t = 1e300;
     int best_c = 1;
     for (int c = 1; c <= std::max(1, dims->nz / 8); ++c) {
-      const double t = (double)((nbt * c + sms - 1) / sms) * ((dims->nz + c - 1) / c + 2.0);
+      const double t = (double)((nbt * c + sms - 1) / sms) * ((dims->nz + c - 1) / c + 4.5);
       if (t < best_t - 1e-9) {
         best_t = t;
         best_c = c;
